@@ -1,0 +1,236 @@
+/*
+ * elixir_b200.h — C-ABI of the B200-native Elixir chunk-memory hot path.
+ *
+ * The reference (`/root/reference/pkg/src/offplan`, "offplan") is a pure-Python
+ * planner/simulator. It specifies the runtime only through contracts:
+ *   - layout:   pack_chunks            (offplan/chunking.py:102-138)
+ *   - trace:    build_chunk_trace      (offplan/chunking.py:149-170)
+ *   - schedule: simulate               (offplan/rcache_sim.py:87-199)
+ *   - memory:   chunk_footprint        (offplan/cost_model.py:147-153)
+ *   - update:   v_g / v_c velocities   (offplan/rcache_sim.py:173-184)
+ * and through the paper's runtime prose (PAPER.md:170-181, :203-206, :221-238,
+ * :276-281). Each entry point below names the reference interface it replaces
+ * or implements. INTEGRATION.md shows the ctypes binding a maintainer adds.
+ *
+ * Conventions
+ *   - Every buffer is caller-owned (torch tensors on the Python side). The
+ *     library never allocates device memory.
+ *   - Every GPU call is asynchronous on the `stream` argument (a cudaStream_t
+ *     passed as void*). Cross-stream ordering is the caller's (events).
+ *   - Return value: ELX_OK (0) or an elx_status error code; a thread-local
+ *     message is available from elx_last_error(). No C++ exception crosses
+ *     the ABI.
+ *   - Element dtypes: ELX_F32, ELX_BF16, ELX_F16.
+ *   - Not thread-safe per stream; one host thread per rank process.
+ */
+#ifndef ELIXIR_B200_H
+#define ELIXIR_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ELX_ABI_VERSION 1
+#define ELX_MAX_WORLD 16
+
+/* Status codes. The split mirrors offplan/errors.py:10-47:
+ * ValidationError family -> 1xx, InfeasibleError family -> 2xx. */
+typedef enum {
+  ELX_OK = 0,
+  ELX_ERR_VALIDATION = 100,        /* errors.py:14  ValidationError        */
+  ELX_ERR_INFEASIBLE = 200,        /* errors.py:30  InfeasibleError        */
+  ELX_ERR_CHUNK_TOO_SMALL = 201,   /* errors.py:34  ChunkTooSmallError     */
+  ELX_ERR_INFEASIBLE_CACHE = 202,  /* errors.py:38  InfeasibleCacheError   */
+  ELX_ERR_CUDA = 300,              /* CUDA runtime failure (no reference analogue) */
+} elx_status;
+
+typedef enum { ELX_F32 = 0, ELX_BF16 = 1, ELX_F16 = 2 } elx_dtype;
+
+/* ---------------------------------------------------------------- misc */
+int32_t elx_abi_version(void);
+const char* elx_last_error(void);
+/* Number of kernels this library launched in this process (all streams).
+ * bench.py reports the delta over its timed region as `gpu_launches`. */
+int64_t elx_launch_count(void);
+
+/* ------------------------------------------------- host: layout + schedule
+ *
+ * elx_layout_pack replaces offplan.pack_chunks (chunking.py:102-138):
+ * greedy in-order packing of `n` parameters (numel[i], already in the
+ * packing order of partition_multiuse, chunking.py:82-99) into chunks of
+ * `chunk_length` elements; a parameter never straddles two chunks.
+ * Outputs: chunk_of[i], offset[i] (element offset inside the chunk), and
+ * *n_chunks. Errors: chunk_length < 1 -> ELX_ERR_VALIDATION;
+ * numel[i] > chunk_length -> ELX_ERR_CHUNK_TOO_SMALL (message names i). */
+int elx_layout_pack(const int64_t* numel, int32_t n, int64_t chunk_length,
+                    int32_t* chunk_of, int64_t* offset, int32_t* n_chunks);
+
+/* One runtime event of the rCache program. Walk positions 0..F-1 are the
+ * forward nodes, F..2F-1 the mirrored backward nodes (chunking.py:165). */
+typedef enum { ELX_EV_GATHER = 0, ELX_EV_REDUCE = 1 } elx_event_kind;
+
+typedef struct {
+  int32_t kind;       /* elx_event_kind                                    */
+  int32_t pos;        /* walk position at which the event is due           */
+  int32_t chunk;      /* chunk id                                          */
+  int32_t block;      /* rCache block the chunk occupies                   */
+  int32_t victim;     /* chunk evicted from `block` (-1 = block was free)  */
+  int32_t issue_pos;  /* earliest walk position the gather may be issued
+                         at (prefetch); == pos if none   */
+} elx_event;
+
+/* Counter block with the field meaning of offplan.SimReport
+ * (rcache_sim.py:65-84); byte fields are derived by the caller as
+ * units * compute_bytes * chunk_length exactly as rcache_sim.py:186-199. */
+typedef struct {
+  int64_t gather_ops;
+  int64_t replaced_ops;      /* gathers of a chunk already gathered once   */
+  int64_t reduce_ops;
+  int64_t c2g_units;         /* gathers of CPU-home chunks                 */
+  int64_t g2c_units;         /* reduces of CPU-home chunks                 */
+  int64_t peak_rcache_blocks;
+  int64_t working_set;       /* chunking.py:173-177                        */
+} elx_sim_counters;
+
+/* elx_schedule replaces offplan.simulate's walk (rcache_sim.py:87-199) and
+ * compiles it into an event program the runtime replays.
+ *   forward nodes in CSR form: node i touches chunks
+ *     node_chunks[node_ptr[i] .. node_ptr[i+1]) ;
+ *   cpu_home[c] != 0 marks chunk c as CPU-homed (Device.CPU);
+ *   events: capacity `events_cap`; *n_events receives the count (the call
+ *     fails with ELX_ERR_VALIDATION if the capacity is too small).
+ * Eviction: farthest next use, ties to the lowest chunk id; chunks are
+ * pinned from their first backward touch until their reduce position.
+ * Errors: ELX_ERR_VALIDATION (bad arguments), ELX_ERR_INFEASIBLE_CACHE
+ * (n_block below the working set, or pinned chunks fill all blocks). */
+int elx_schedule(int32_t n_nodes, const int32_t* node_ptr, const int32_t* node_chunks,
+                 int32_t n_chunks, int32_t n_block, const uint8_t* cpu_home,
+                 elx_event* events, int64_t events_cap, int64_t* n_events,
+                 elx_sim_counters* counters);
+
+/* ------------------------------------------------------- K1 chunk pack
+ * Scatter parameters into a chunk buffer at their layout offsets (and the
+ * reverse), the storage side of pack_chunks (chunking.py:113-131) and of
+ * "we use the gradient to overwrite the data in the parameter chunk"
+ * (PAPER.md:233-236). One call handles any number of members; `members` is
+ * a HOST array (the library batches it into kernel parameters, so no device
+ * table and no host->device copy is needed).
+ *   ext:        external tensor pointer (param, grad, or export target);
+ *               NULL in elx_chunk_pack writes zeros (padding)
+ *   offset:     element offset inside the chunk buffer
+ *   numel:      element count
+ *   ext_dtype:  elx_dtype of ext */
+typedef struct {
+  const void* ext;
+  int64_t offset;
+  int64_t numel;
+  int32_t ext_dtype;
+  int32_t pad_;
+} elx_member;
+
+/* chunk[offset : offset+numel] <- convert(ext) for every member. When
+ * phys_len > used_len the tail [used_len, phys_len) is zero-filled (the
+ * padding of chunking.py:141-146 plus the shard round-up). */
+int elx_chunk_pack(void* chunk, int32_t chunk_dtype, int64_t phys_len, int64_t used_len,
+                   const elx_member* members, int32_t n, void* stream);
+/* ext <- convert(chunk[offset : offset+numel]) for every member. */
+int elx_chunk_unpack(const void* chunk, int32_t chunk_dtype, const elx_member* members,
+                     int32_t n, void* stream);
+
+/* ------------------------------------------------------- K2 chunk fetch
+ * All-gather of one chunk's N rank shards into an rCache block
+ * ("we gather them into rCache before compute operators"):
+ *   block[r*shard_len + i] = shards[r][i],  r < world, i < shard_len.
+ * shards[] are host-array entries holding device pointers: local buffers, or
+ * peer buffers mapped over NVLink (symmetric memory), read in-kernel.
+ * shard_len must be a multiple of 8 elements. dtype is BF16 or F16. */
+int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t world,
+              int32_t dtype, void* stream);
+
+/* ----------------------------------------------------- K3 grad release
+ * Reduce-scatter of one chunk's gradients into this rank's fp32 grad shard,
+ * fused with loss-scale unscale, fp32 cast, the sum-of-squares partial and
+ * the overflow flag (rcache_sim.py:160-167 fires it at
+ * reduce_after[c]):
+ *   g[i] = (sum_{r=0..world-1, in order} float(src[r][i])) * inv_scale
+ *   step_scalars[0] += sum_i g[i]^2   (fp64)
+ *   step_scalars[1]  = 1.0 if any g[i] is not finite
+ * src[r] points at rank r's copy of THIS rank's segment (peer block + rank*S,
+ * or a local all-to-all staging buffer). n = valid elements (padding
+ * excluded). dtype is BF16 or F16. step_scalars is a DEVICE double[2]. */
+int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t world,
+                int32_t dtype, float inv_scale, double* step_scalars, void* stream);
+
+/* ------------------------------------------------------ K4 chunk Adam
+ * Fused mixed-precision AdamW over fp32 master/m/v shards with the fp32
+ * grad shard, writing the new compute-precision parameter shard
+ * (GPU-home update rate v_g,
+ * rcache_sim.py:176-184). Arithmetic follows torch.optim.AdamW's
+ * single-tensor path (see oracle/arith.py). The clip coefficient
+ * min(1, max_norm/(sqrt(step_scalars[0]) + 1e-6)) and the overflow skip
+ * (step_scalars[1] != 0 -> no state change; the compute shard is restored
+ * from the master) are evaluated on the device: no host synchronisation.
+ * `segs` is a DEVICE array of nseg records; tile0 is the running prefix of
+ * ceil(n / ELX_ADAM_TILE) over the preceding records. */
+#define ELX_ADAM_TILE 4096
+typedef struct {
+  float* p32;
+  float* m;
+  float* v;
+  const float* g;
+  void* p16;
+  int64_t n;
+  int64_t tile0;
+  int64_t pad_;
+} elx_adam_seg;
+
+typedef struct {
+  double lr;
+  double beta1;
+  double beta2;
+  double eps;
+  double weight_decay;
+  double max_norm;  /* <= 0 disables clipping */
+  int32_t p16_dtype; /* ELX_BF16 or ELX_F16 */
+  int32_t pad_;
+} elx_adam_hp;
+
+int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const elx_adam_hp* hp,
+             int64_t step, const double* step_scalars, void* stream);
+
+/* ------------------------------------------------ K5 step finalisation
+ * Device-side: out[0] = sqrt(step_scalars[0]) (grad norm), out[1] = clip
+ * coefficient, out[2] = step_scalars[1] (found_inf). For host reporting; the
+ * Adam kernels compute the same values themselves. */
+int elx_norm_finalize(const double* step_scalars, double max_norm, double* out3, void* stream);
+/* step_scalars[0..1] <- 0 */
+int elx_step_reset(double* step_scalars, void* stream);
+
+/* ------------------------------------------------------- K6 offload
+ * Pinned-host <-> HBM moves for CPU-home chunks on a side stream, with an
+ * optional completion event (rcache_sim.py:156-157, 165-166: c2g on each
+ * gather, g2c on each reduce of a CPU-home chunk). Copy engine, no SMs. */
+int elx_copy_h2d(void* dst_dev, const void* src_host, int64_t bytes, void* stream, void* event);
+int elx_copy_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream, void* event);
+
+/* Host Adam for CPU-home optimizer shards (update rate v_c,
+ * rcache_sim.py:176-184): same arithmetic as elx_adam, OpenMP over
+ * `threads` host threads. All pointers are host pointers; step_scalars is a
+ * HOST double[2] (already all-reduced). */
+typedef struct {
+  float* p32;
+  float* m;
+  float* v;
+  const float* g;
+  void* p16;
+  int64_t n;
+} elx_cpu_seg;
+int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_adam_hp* hp, int64_t step,
+                 const double* step_scalars, int32_t threads);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ELIXIR_B200_H */

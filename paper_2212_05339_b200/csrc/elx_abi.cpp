@@ -1,0 +1,30 @@
+// ABI plumbing: version, thread-local error text, launch counter.
+#include "elx_internal.h"
+
+namespace elx {
+
+static thread_local std::string t_error;
+std::atomic<int64_t> g_launches{0};
+
+void set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_error = buf;
+}
+
+void clear_error() { t_error.clear(); }
+
+}  // namespace elx
+
+extern "C" {
+
+int32_t elx_abi_version(void) { return ELX_ABI_VERSION; }
+
+const char* elx_last_error(void) { return elx::t_error.c_str(); }
+
+int64_t elx_launch_count(void) { return elx::g_launches.load(std::memory_order_relaxed); }
+
+}  // extern "C"

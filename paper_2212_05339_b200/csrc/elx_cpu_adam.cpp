@@ -1,0 +1,103 @@
+// Host-side AdamW for CPU-home optimizer shards (the v_c update of
+// rcache_sim.py:176-184 and search.py:153-159). It runs next to the GPU
+// update (the "hybrid optimizer") and must produce the same bits as
+// elx_adam, so this file is built with -ffp-contract=off and without
+// -ffast-math: every float operation below is one IEEE-754 rounding.
+#include <cmath>
+#include <cstring>
+
+#include "elx_internal.h"
+
+namespace {
+
+inline uint16_t f32_to_bf16_rne(float x) {
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) return (uint16_t)((u >> 16) | 0x0040u);  // qNaN
+  const uint32_t lsb = (u >> 16) & 1u;
+  u += 0x7fffu + lsb;
+  return (uint16_t)(u >> 16);
+}
+
+// IEEE binary16 round-to-nearest-even from float32.
+inline uint16_t f32_to_f16_rne(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  const uint32_t ax = x & 0x7fffffffu;
+  if (ax >= 0x7f800000u) return (uint16_t)(sign | 0x7c00u | (ax > 0x7f800000u ? 0x200u : 0u));
+  if (ax >= 0x477ff000u) return (uint16_t)(sign | 0x7c00u);  // rounds to inf
+  if (ax < 0x38800000u) {                                     // subnormal / zero in f16
+    if (ax < 0x33000000u) return (uint16_t)sign;              // < half of min subnormal
+    // value = mant * 2^(e-150); f16 subnormal unit is 2^-24, so the f16
+    // mantissa is mant >> (126 - e), rounded to nearest even.
+    const uint32_t e = ax >> 23;
+    const uint32_t mant = (ax & 0x7fffffu) | 0x800000u;
+    const uint32_t shift = 126u - e;  // in [14, 24]
+    uint32_t r = mant >> shift;
+    const uint32_t rem = mant & ((1u << shift) - 1u);
+    const uint32_t half = 1u << (shift - 1);
+    if (rem > half || (rem == half && (r & 1u))) ++r;
+    return (uint16_t)(sign | r);
+  }
+  uint32_t r = ax - 0x38000000u;  // rebias exponent 127 -> 15 (<<23 >>13 later)
+  const uint32_t rem = r & 0x1fffu;
+  r >>= 13;
+  if (rem > 0x1000u || (rem == 0x1000u && (r & 1u))) ++r;
+  return (uint16_t)(sign | r);
+}
+
+}  // namespace
+
+extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_adam_hp* hp, int64_t step,
+                            const double* step_scalars, int32_t threads) {
+  elx::clear_error();
+  if (!hp || !step_scalars || (nseg > 0 && !segs)) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (step < 1) return elx::fail(ELX_ERR_VALIDATION, "step must be >= 1");
+  if (hp->p16_dtype != ELX_BF16 && hp->p16_dtype != ELX_F16)
+    return elx::fail(ELX_ERR_VALIDATION, "p16_dtype must be bf16/f16");
+  const bool skip = step_scalars[1] != 0.0;
+  float coef = 1.f;
+  if (hp->max_norm > 0.0) {
+    const double c = hp->max_norm / (std::sqrt(step_scalars[0]) + 1e-6);
+    coef = c < 1.0 ? (float)c : 1.f;
+  }
+  const double bc1 = 1.0 - std::pow(hp->beta1, (double)step);
+  const double bc2 = 1.0 - std::pow(hp->beta2, (double)step);
+  const float decay = (float)(1.0 - hp->lr * hp->weight_decay);
+  const float omb1 = (float)(1.0 - hp->beta1);
+  const float b2 = (float)hp->beta2;
+  const float omb2 = (float)(1.0 - hp->beta2);
+  const float bc2s = (float)std::sqrt(bc2);
+  const float neg_step = (float)(-(hp->lr / bc1));
+  const float eps = (float)hp->eps;
+  const bool bf16 = hp->p16_dtype == ELX_BF16;
+  if (threads < 1) threads = 1;
+
+  for (int32_t s = 0; s < nseg; ++s) {
+    float* p32 = segs[s].p32;
+    float* m = segs[s].m;
+    float* v = segs[s].v;
+    const float* g = segs[s].g;
+    uint16_t* p16 = static_cast<uint16_t*>(segs[s].p16);
+    const int64_t n = segs[s].n;
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+      float P = p32[i];
+      if (!skip) {
+        float M = m[i], V = v[i];
+        const float G = g[i] * coef;
+        P = P * decay;
+        M = M + omb1 * (G - M);
+        V = V * b2 + (omb2 * G) * G;
+        const float denom = std::sqrt(V) / bc2s + eps;
+        P = P + (neg_step * M) / denom;
+        p32[i] = P;
+        m[i] = M;
+        v[i] = V;
+      }
+      p16[i] = bf16 ? f32_to_bf16_rne(P) : f32_to_f16_rne(P);
+    }
+  }
+  return ELX_OK;
+}

@@ -1,0 +1,648 @@
+// sm_100a kernels of the Elixir chunk-memory hot path (K1-K6).
+//
+// All of them are HBM- (or NVLink-) bound streaming kernels: no tensor cores,
+// 128-bit vectorised coalesced accesses, grid sized in multiples of the SM
+// count, warp-shuffle reductions for the norm. Floating-point arithmetic in
+// K3/K4 uses explicit round-to-nearest intrinsics (and the file is built with
+// --fmad=false) so results are bit-identical to the CPU oracle, which applies
+// the same IEEE-754 float32 operations in the same order.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+
+#include "elx_internal.h"
+
+namespace {
+
+// ----------------------------------------------------------------- helpers
+
+int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!cached[dev]) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    cached[dev] = n > 0 ? n : 148;
+  }
+  return cached[dev];
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  elx::count_launch();
+  return ELX_OK;
+}
+
+__host__ __device__ inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+__device__ __forceinline__ float ld_as_f32(const void* p, int64_t i, int dt) {
+  if (dt == ELX_F32) return static_cast<const float*>(p)[i];
+  if (dt == ELX_BF16) return __bfloat162float(static_cast<const __nv_bfloat16*>(p)[i]);
+  return __half2float(static_cast<const __half*>(p)[i]);
+}
+
+__device__ __forceinline__ void st_from_f32(void* p, int64_t i, int dt, float x) {
+  if (dt == ELX_F32)
+    static_cast<float*>(p)[i] = x;
+  else if (dt == ELX_BF16)
+    static_cast<__nv_bfloat16*>(p)[i] = __float2bfloat16_rn(x);
+  else
+    static_cast<__half*>(p)[i] = __float2half_rn(x);
+}
+
+template <typename T>
+__device__ __forceinline__ float to_f32(T x);
+template <>
+__device__ __forceinline__ float to_f32<__nv_bfloat16>(__nv_bfloat16 x) {
+  return __bfloat162float(x);
+}
+template <>
+__device__ __forceinline__ float to_f32<__half>(__half x) {
+  return __half2float(x);
+}
+
+template <typename T>
+__device__ __forceinline__ T from_f32(float x);
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+template <>
+__device__ __forceinline__ __half from_f32<__half>(float x) {
+  return __float2half_rn(x);
+}
+
+// Streaming loads/stores: bypass L1 allocation; these buffers are touched once.
+__device__ __forceinline__ uint4 ld_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+// Plain (coherent) 128-bit load, used where the source may be a peer
+// mapping written by another GPU during this kernel's lifetime window.
+__device__ __forceinline__ uint4 ld_plain(const uint4* p) { return *p; }
+
+// ================================================================ K1 pack
+constexpr int kPackBatch = 48;
+constexpr int kPackThreads = 256;
+constexpr int64_t kPackTile = kPackThreads * 8 * 2;  // elements per tile
+
+struct PackBatch {
+  const void* ext[kPackBatch];
+  int64_t offset[kPackBatch];
+  int64_t numel[kPackBatch];
+  int64_t tile0[kPackBatch + 1];
+  int32_t ext_dtype[kPackBatch];
+  int32_t n;
+};
+
+// kDir = 0: chunk <- ext (pack); kDir = 1: ext <- chunk (unpack).
+template <int kDir>
+__global__ void __launch_bounds__(kPackThreads) pack_kernel(void* chunk, int chunk_dt,
+                                                            const PackBatch b) {
+  const int64_t ntiles = b.tile0[b.n];
+  const int csz = chunk_dt == ELX_F32 ? 4 : 2;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    int j = 0;
+    while (j + 1 < b.n && b.tile0[j + 1] <= t) ++j;
+    const int64_t base = (t - b.tile0[j]) * kPackTile;
+    const int64_t cnt = min(kPackTile, b.numel[j] - base);
+    const int64_t coff = b.offset[j] + base;
+    const void* ext = b.ext[j];
+    const int edt = b.ext_dtype[j];
+    char* cptr = static_cast<char*>(chunk) + coff * csz;
+    if (ext == nullptr) {  // zero fill (pack only)
+      if (kDir == 0) {
+        for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) st_from_f32(chunk, coff + i, chunk_dt, 0.f);
+      }
+      continue;
+    }
+    const int esz = edt == ELX_F32 ? 4 : 2;
+    const char* eptr = static_cast<const char*>(ext) + base * esz;
+    // Same-dtype, 16B-aligned, whole-vector range: raw 128-bit copies.
+    const int vec_elems = 16 / csz;
+    if (edt == chunk_dt && aligned16(cptr) && aligned16(eptr) && (cnt % vec_elems) == 0) {
+      const int64_t nv = cnt / vec_elems;
+      if (kDir == 0) {
+        const uint4* s = reinterpret_cast<const uint4*>(eptr);
+        uint4* d = reinterpret_cast<uint4*>(cptr);
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = ld_stream(s + i);
+      } else {
+        const uint4* s = reinterpret_cast<const uint4*>(cptr);
+        uint4* d = reinterpret_cast<uint4*>(const_cast<char*>(eptr));
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = ld_stream(s + i);
+      }
+      continue;
+    }
+    // General path: element-wise conversion through float32.
+    for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) {
+      if (kDir == 0) {
+        st_from_f32(chunk, coff + i, chunk_dt, ld_as_f32(ext, base + i, edt));
+      } else {
+        st_from_f32(const_cast<void*>(ext), base + i, edt, ld_as_f32(chunk, coff + i, chunk_dt));
+      }
+    }
+  }
+}
+
+template <int kDir>
+int run_pack(void* chunk, int32_t chunk_dt, const elx_member* members, int32_t n, int64_t zero_from,
+             int64_t zero_to, cudaStream_t st) {
+  // Flatten members (+ optional zero tail) into kernel-parameter batches.
+  PackBatch b{};
+  b.n = 0;
+  b.tile0[0] = 0;
+  auto flush = [&]() -> int {
+    if (b.n == 0) return ELX_OK;
+    const int64_t ntiles = b.tile0[b.n];
+    if (ntiles > 0) {
+      const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 8);
+      pack_kernel<kDir><<<grid, kPackThreads, 0, st>>>(chunk, chunk_dt, b);
+      int rc = check_launch(kDir == 0 ? "elx_chunk_pack" : "elx_chunk_unpack");
+      if (rc) return rc;
+    }
+    b.n = 0;
+    b.tile0[0] = 0;
+    return ELX_OK;
+  };
+  auto add = [&](const void* ext, int64_t off, int64_t numel, int32_t dt) -> int {
+    if (numel <= 0) return ELX_OK;
+    b.ext[b.n] = ext;
+    b.offset[b.n] = off;
+    b.numel[b.n] = numel;
+    b.ext_dtype[b.n] = dt;
+    b.tile0[b.n + 1] = b.tile0[b.n] + (numel + kPackTile - 1) / kPackTile;
+    ++b.n;
+    if (b.n == kPackBatch) return flush();
+    return ELX_OK;
+  };
+  for (int32_t i = 0; i < n; ++i) {
+    const elx_member& m = members[i];
+    if (m.numel < 0 || m.offset < 0)
+      return elx::fail(ELX_ERR_VALIDATION, "member #%d: negative offset/numel", i);
+    if (elx::dtype_size(m.ext_dtype) == 0)
+      return elx::fail(ELX_ERR_VALIDATION, "member #%d: bad dtype %d", i, m.ext_dtype);
+    if (kDir == 1 && m.ext == nullptr)
+      return elx::fail(ELX_ERR_VALIDATION, "member #%d: null target", i);
+    int rc = add(m.ext, m.offset, m.numel, m.ext_dtype);
+    if (rc) return rc;
+  }
+  if (zero_to > zero_from) {
+    int rc = add(nullptr, zero_from, zero_to - zero_from, chunk_dt);
+    if (rc) return rc;
+  }
+  return flush();
+}
+
+// ================================================================ K2 fetch
+struct PtrBatch {
+  const void* p[ELX_MAX_WORLD];
+};
+
+constexpr int kCopyThreads = 256;
+constexpr int kCopyUnroll = 4;
+
+// blockIdx.y = source rank; grid-stride over that rank's 16-byte vectors.
+__global__ void __launch_bounds__(kCopyThreads) fetch_kernel(uint4* block, const PtrBatch src,
+                                                             int64_t shard_vecs) {
+  const int r = blockIdx.y;
+  const uint4* s = static_cast<const uint4*>(src.p[r]);
+  uint4* d = block + (int64_t)r * shard_vecs;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * kCopyUnroll;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kCopyUnroll + threadIdx.x; i0 < shard_vecs;
+       i0 += stride) {
+    uint4 v[kCopyUnroll];
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      if (i < shard_vecs) v[u] = ld_plain(s + i);
+    }
+#pragma unroll
+    for (int u = 0; u < kCopyUnroll; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      if (i < shard_vecs) d[i] = v[u];
+    }
+  }
+}
+
+// ============================================================== K3 release
+constexpr int kRelThreads = 256;
+
+__device__ __forceinline__ void block_reduce_and_publish(double sq, int bad, double* sc) {
+  __shared__ double s_sq[kRelThreads / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) s_sq[warp] = sq;
+  const int any_bad = __syncthreads_or(bad);
+  if (warp == 0) {
+    double x = lane < (int)(blockDim.x >> 5) ? s_sq[lane] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) {
+      if (x != 0.0) atomicAdd(sc, x);
+      if (any_bad) sc[1] = 1.0;
+    }
+  }
+}
+
+// Vector path: each thread-step reduces 8 consecutive elements from every
+// source (one 16-byte load per rank), writes 32 bytes of fp32.
+template <typename T16, int kWorld>
+__global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict__ g, const PtrBatch src,
+                                                              int world_rt, int64_t n, float inv_scale,
+                                                              double* sc) {
+  const int world = kWorld > 0 ? kWorld : world_rt;
+  const int64_t nv = n >> 3;
+  double sq = 0.0;
+  int bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
+    float acc[8];
+    uint4 raw[kWorld > 0 ? kWorld : 1];
+    if (kWorld > 0) {
+#pragma unroll
+      for (int r = 0; r < (kWorld > 0 ? kWorld : 1); ++r)
+        raw[r] = ld_plain(static_cast<const uint4*>(src.p[r]) + i);
+#pragma unroll
+      for (int r = 0; r < (kWorld > 0 ? kWorld : 1); ++r) {
+        const T16* h = reinterpret_cast<const T16*>(&raw[r]);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
+      }
+    } else {
+      for (int r = 0; r < world; ++r) {
+        const uint4 q = ld_plain(static_cast<const uint4*>(src.p[r]) + i);
+        const T16* h = reinterpret_cast<const T16*>(&q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      acc[e] = __fmul_rn(acc[e], inv_scale);
+      bad |= !isfinite(acc[e]);
+      sq += (double)acc[e] * (double)acc[e];
+    }
+    float4* o = reinterpret_cast<float4*>(g + (i << 3));
+    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+  // Scalar tail (n % 8 elements), handled by block 0.
+  if (blockIdx.x == 0) {
+    for (int64_t i = (nv << 3) + threadIdx.x; i < n; i += blockDim.x) {
+      float a = 0.f;
+      for (int r = 0; r < world; ++r) {
+        const float x = to_f32<T16>(static_cast<const T16*>(src.p[r])[i]);
+        a = r == 0 ? x : __fadd_rn(a, x);
+      }
+      a = __fmul_rn(a, inv_scale);
+      bad |= !isfinite(a);
+      sq += (double)a * (double)a;
+      g[i] = a;
+    }
+  }
+  block_reduce_and_publish(sq, bad, sc);
+}
+
+// Unaligned fallback: scalar loads for every element.
+template <typename T16>
+__global__ void __launch_bounds__(kRelThreads) release_kernel_scalar(float* g, const PtrBatch src, int world,
+                                                                     int64_t n, float inv_scale, double* sc) {
+  double sq = 0.0;
+  int bad = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    float a = 0.f;
+    for (int r = 0; r < world; ++r) {
+      const float x = to_f32<T16>(static_cast<const T16*>(src.p[r])[i]);
+      a = r == 0 ? x : __fadd_rn(a, x);
+    }
+    a = __fmul_rn(a, inv_scale);
+    bad |= !isfinite(a);
+    sq += (double)a * (double)a;
+    g[i] = a;
+  }
+  block_reduce_and_publish(sq, bad, sc);
+}
+
+template <typename T16>
+int run_release(float* g, const PtrBatch& pb, int64_t n, int world, float inv_scale, double* sc,
+                cudaStream_t st) {
+  bool vec = aligned16(g);
+  for (int r = 0; r < world; ++r) vec = vec && aligned16(pb.p[r]);
+  const int64_t work = vec ? (n >> 3) : n;
+  const int grid = (int)std::max<int64_t>(
+      1, std::min<int64_t>((work + kRelThreads - 1) / kRelThreads, (int64_t)sm_count() * 8));
+  if (!vec) {
+    release_kernel_scalar<T16><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc);
+  } else {
+    switch (world) {
+      case 1: release_kernel<T16, 1><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
+      case 2: release_kernel<T16, 2><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
+      case 4: release_kernel<T16, 4><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
+      case 8: release_kernel<T16, 8><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
+      default: release_kernel<T16, 0><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
+    }
+  }
+  return check_launch("elx_release");
+}
+
+// ================================================================= K4 Adam
+constexpr int kAdamThreads = 256;
+constexpr int kAdamUnroll = ELX_ADAM_TILE / (kAdamThreads * 4);
+static_assert(kAdamUnroll * kAdamThreads * 4 == ELX_ADAM_TILE, "tile shape");
+
+struct AdamK {
+  float decay;       // 1 - lr*wd
+  float omb1;        // 1 - beta1   (lerp weight)
+  float b2;          // beta2
+  float omb2;        // 1 - beta2
+  float bc2_sqrt;    // sqrt(1 - beta2^step)
+  float neg_step;    // -lr / (1 - beta1^step)
+  float eps;
+  double max_norm;
+};
+
+// One element of the update; every operation is a single IEEE rounding in
+// the order of the oracle (oracle/arith.py: adamw_step).
+__device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float g, float coef,
+                                          const AdamK& k) {
+  g = __fmul_rn(g, coef);
+  p = __fmul_rn(p, k.decay);
+  m = __fadd_rn(m, __fmul_rn(k.omb1, __fsub_rn(g, m)));
+  v = __fadd_rn(__fmul_rn(v, k.b2), __fmul_rn(__fmul_rn(k.omb2, g), g));
+  const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), k.bc2_sqrt), k.eps);
+  p = __fadd_rn(p, __fdiv_rn(__fmul_rn(k.neg_step, m), denom));
+}
+
+__device__ __forceinline__ float clip_coef(const double* sc, double max_norm) {
+  if (!(max_norm > 0.0)) return 1.f;
+  const double c = max_norm / (sqrt(sc[0]) + 1e-6);
+  return c < 1.0 ? (float)c : 1.f;
+}
+
+template <typename T16>
+__device__ __forceinline__ void store4(T16* p16, float a, float b, float c, float d) {
+  // 4 x 16-bit = 8 bytes, one store.
+  union {
+    T16 h[4];
+    uint2 u;
+  } pk;
+  pk.h[0] = from_f32<T16>(a);
+  pk.h[1] = from_f32<T16>(b);
+  pk.h[2] = from_f32<T16>(c);
+  pk.h[3] = from_f32<T16>(d);
+  *reinterpret_cast<uint2*>(p16) = pk.u;
+}
+
+template <typename T16>
+__global__ void __launch_bounds__(kAdamThreads) adam_kernel(const elx_adam_seg* __restrict__ segs, int nseg,
+                                                            int64_t ntiles, const AdamK k,
+                                                            const double* __restrict__ sc) {
+  const bool skip = sc[1] != 0.0;
+  const float coef = clip_coef(sc, k.max_norm);
+  int s = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    while (s + 1 < nseg && segs[s + 1].tile0 <= t) ++s;  // tiles ascend per CTA
+    float* __restrict__ p32 = segs[s].p32;
+    float* __restrict__ m = segs[s].m;
+    float* __restrict__ v = segs[s].v;
+    const float* __restrict__ g = segs[s].g;
+    T16* __restrict__ p16 = static_cast<T16*>(segs[s].p16);
+    const int64_t n = segs[s].n;
+    const int64_t base = (t - segs[s].tile0) * ELX_ADAM_TILE;
+    const int64_t cnt = min((int64_t)ELX_ADAM_TILE, n - base);
+    const bool vec = cnt == ELX_ADAM_TILE && aligned16(p32 + base) && aligned16(m + base) &&
+                     aligned16(v + base) && aligned16(g + base) &&
+                     ((reinterpret_cast<uintptr_t>(p16 + base) & 7u) == 0);
+    if (vec) {
+      float4 P[kAdamUnroll];
+      if (skip) {
+#pragma unroll
+        for (int u = 0; u < kAdamUnroll; ++u)
+          P[u] = reinterpret_cast<const float4*>(p32 + base)[u * kAdamThreads + threadIdx.x];
+#pragma unroll
+        for (int u = 0; u < kAdamUnroll; ++u)
+          store4<T16>(p16 + base + 4 * (u * kAdamThreads + threadIdx.x), P[u].x, P[u].y, P[u].z, P[u].w);
+        continue;
+      }
+      float4 M[kAdamUnroll], V[kAdamUnroll], G[kAdamUnroll];
+#pragma unroll
+      for (int u = 0; u < kAdamUnroll; ++u) {
+        const int64_t j = u * kAdamThreads + threadIdx.x;
+        P[u] = reinterpret_cast<const float4*>(p32 + base)[j];
+        M[u] = reinterpret_cast<const float4*>(m + base)[j];
+        V[u] = reinterpret_cast<const float4*>(v + base)[j];
+        G[u] = ld_stream_f4(reinterpret_cast<const float4*>(g + base) + j);
+      }
+#pragma unroll
+      for (int u = 0; u < kAdamUnroll; ++u) {
+        adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
+        adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
+        adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
+        adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
+        const int64_t j = u * kAdamThreads + threadIdx.x;
+        reinterpret_cast<float4*>(p32 + base)[j] = P[u];
+        reinterpret_cast<float4*>(m + base)[j] = M[u];
+        reinterpret_cast<float4*>(v + base)[j] = V[u];
+        store4<T16>(p16 + base + 4 * j, P[u].x, P[u].y, P[u].z, P[u].w);
+      }
+    } else {
+      for (int64_t i = base + threadIdx.x; i < base + cnt; i += blockDim.x) {
+        float P = p32[i];
+        if (!skip) {
+          float M = m[i], V = v[i];
+          adam_elem(P, M, V, g[i], coef, k);
+          p32[i] = P;
+          m[i] = M;
+          v[i] = V;
+        }
+        p16[i] = from_f32<T16>(P);
+      }
+    }
+  }
+}
+
+__global__ void norm_finalize_kernel(const double* sc, double max_norm, double* out) {
+  const double nrm = sqrt(sc[0]);
+  out[0] = nrm;
+  double c = 1.0;
+  if (max_norm > 0.0) {
+    c = max_norm / (nrm + 1e-6);
+    if (c > 1.0) c = 1.0;
+  }
+  out[1] = (double)(float)c;
+  out[2] = sc[1];
+}
+
+__global__ void step_reset_kernel(double* sc) {
+  sc[0] = 0.0;
+  sc[1] = 0.0;
+}
+
+}  // namespace
+
+// ======================================================================= ABI
+extern "C" {
+
+int elx_chunk_pack(void* chunk, int32_t chunk_dtype, int64_t phys_len, int64_t used_len,
+                   const elx_member* members, int32_t n, void* stream) {
+  elx::clear_error();
+  if (!chunk) return elx::fail(ELX_ERR_VALIDATION, "null chunk");
+  if (elx::dtype_size(chunk_dtype) == 0) return elx::fail(ELX_ERR_VALIDATION, "bad chunk dtype");
+  if (n < 0 || (n > 0 && !members)) return elx::fail(ELX_ERR_VALIDATION, "bad member table");
+  if (used_len < 0 || phys_len < used_len)
+    return elx::fail(ELX_ERR_VALIDATION, "need 0 <= used_len <= phys_len");
+  for (int32_t i = 0; i < n; ++i)
+    if (members[i].offset + members[i].numel > phys_len)
+      return elx::fail(ELX_ERR_VALIDATION, "member #%d [%lld, +%lld) exceeds chunk length %lld", i,
+                       (long long)members[i].offset, (long long)members[i].numel, (long long)phys_len);
+  return run_pack<0>(chunk, chunk_dtype, members, n, used_len, phys_len, (cudaStream_t)stream);
+}
+
+int elx_chunk_unpack(const void* chunk, int32_t chunk_dtype, const elx_member* members, int32_t n,
+                     void* stream) {
+  elx::clear_error();
+  if (!chunk) return elx::fail(ELX_ERR_VALIDATION, "null chunk");
+  if (elx::dtype_size(chunk_dtype) == 0) return elx::fail(ELX_ERR_VALIDATION, "bad chunk dtype");
+  if (n < 0 || (n > 0 && !members)) return elx::fail(ELX_ERR_VALIDATION, "bad member table");
+  return run_pack<1>(const_cast<void*>(chunk), chunk_dtype, members, n, 0, 0, (cudaStream_t)stream);
+}
+
+int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t world, int32_t dtype,
+              void* stream) {
+  elx::clear_error();
+  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "fetch dtype must be bf16/f16");
+  if (shard_len < 0 || (shard_len % 8) != 0)
+    return elx::fail(ELX_ERR_VALIDATION, "shard_len %lld must be a non-negative multiple of 8",
+                     (long long)shard_len);
+  if (!block || !shards) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (!aligned16(block)) return elx::fail(ELX_ERR_VALIDATION, "block must be 16-byte aligned");
+  PtrBatch pb{};
+  for (int r = 0; r < world; ++r) {
+    if (!shards[r] || !aligned16(shards[r]))
+      return elx::fail(ELX_ERR_VALIDATION, "shard %d null or not 16-byte aligned", r);
+    pb.p[r] = shards[r];
+  }
+  if (shard_len == 0) return ELX_OK;
+  const int64_t vecs = shard_len / 8;
+  const int64_t per_cta = (int64_t)kCopyThreads * kCopyUnroll;
+  const int gx = (int)std::max<int64_t>(
+      1, std::min<int64_t>((vecs + per_cta - 1) / per_cta, std::max<int64_t>(1, (int64_t)sm_count() * 8 / world)));
+  fetch_kernel<<<dim3(gx, world), kCopyThreads, 0, (cudaStream_t)stream>>>(static_cast<uint4*>(block), pb,
+                                                                             vecs);
+  return check_launch("elx_fetch");
+}
+
+int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t world, int32_t dtype,
+                float inv_scale, double* step_scalars, void* stream) {
+  elx::clear_error();
+  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (!grad_shard || !src || !step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (n < 0) return elx::fail(ELX_ERR_VALIDATION, "negative length");
+  PtrBatch pb{};
+  for (int r = 0; r < world; ++r) {
+    if (!src[r]) return elx::fail(ELX_ERR_VALIDATION, "source %d is null", r);
+    pb.p[r] = src[r];
+  }
+  if (n == 0) return ELX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == ELX_BF16) return run_release<__nv_bfloat16>(grad_shard, pb, n, world, inv_scale, step_scalars, st);
+  if (dtype == ELX_F16) return run_release<__half>(grad_shard, pb, n, world, inv_scale, step_scalars, st);
+  return elx::fail(ELX_ERR_VALIDATION, "release dtype must be bf16/f16");
+}
+
+int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const elx_adam_hp* hp, int64_t step,
+             const double* step_scalars, void* stream) {
+  elx::clear_error();
+  if (!hp || !step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (nseg < 0 || ntiles < 0 || (nseg > 0 && !segs_dev)) return elx::fail(ELX_ERR_VALIDATION, "bad segment table");
+  if (step < 1) return elx::fail(ELX_ERR_VALIDATION, "step must be >= 1");
+  if (!(hp->lr >= 0) || !(hp->eps > 0) || !(hp->beta1 >= 0 && hp->beta1 < 1) || !(hp->beta2 >= 0 && hp->beta2 < 1))
+    return elx::fail(ELX_ERR_VALIDATION, "invalid Adam hyper-parameters");
+  if (nseg == 0 || ntiles == 0) return ELX_OK;
+  AdamK k;
+  const double bc1 = 1.0 - std::pow(hp->beta1, (double)step);
+  const double bc2 = 1.0 - std::pow(hp->beta2, (double)step);
+  k.decay = (float)(1.0 - hp->lr * hp->weight_decay);
+  k.omb1 = (float)(1.0 - hp->beta1);
+  k.b2 = (float)hp->beta2;
+  k.omb2 = (float)(1.0 - hp->beta2);
+  k.bc2_sqrt = (float)std::sqrt(bc2);
+  k.neg_step = (float)(-(hp->lr / bc1));
+  k.eps = (float)hp->eps;
+  k.max_norm = hp->max_norm;
+  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 4);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (hp->p16_dtype == ELX_BF16)
+    adam_kernel<__nv_bfloat16><<<grid, kAdamThreads, 0, st>>>(segs_dev, nseg, ntiles, k, step_scalars);
+  else if (hp->p16_dtype == ELX_F16)
+    adam_kernel<__half><<<grid, kAdamThreads, 0, st>>>(segs_dev, nseg, ntiles, k, step_scalars);
+  else
+    return elx::fail(ELX_ERR_VALIDATION, "p16_dtype must be bf16/f16");
+  return check_launch("elx_adam");
+}
+
+int elx_norm_finalize(const double* step_scalars, double max_norm, double* out3, void* stream) {
+  elx::clear_error();
+  if (!step_scalars || !out3) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  norm_finalize_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_scalars, max_norm, out3);
+  return check_launch("elx_norm_finalize");
+}
+
+int elx_step_reset(double* step_scalars, void* stream) {
+  elx::clear_error();
+  if (!step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  step_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_scalars);
+  return check_launch("elx_step_reset");
+}
+
+int elx_copy_h2d(void* dst_dev, const void* src_host, int64_t bytes, void* stream, void* event) {
+  elx::clear_error();
+  if (bytes < 0 || (bytes > 0 && (!dst_dev || !src_host))) return elx::fail(ELX_ERR_VALIDATION, "bad copy");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (bytes > 0) {
+    cudaError_t e = cudaMemcpyAsync(dst_dev, src_host, (size_t)bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_copy_h2d: %s", cudaGetErrorString(e));
+  }
+  if (event) {
+    cudaError_t e = cudaEventRecord((cudaEvent_t)event, st);
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_copy_h2d event: %s", cudaGetErrorString(e));
+  }
+  return ELX_OK;
+}
+
+int elx_copy_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream, void* event) {
+  elx::clear_error();
+  if (bytes < 0 || (bytes > 0 && (!dst_host || !src_dev))) return elx::fail(ELX_ERR_VALIDATION, "bad copy");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (bytes > 0) {
+    cudaError_t e = cudaMemcpyAsync(dst_host, src_dev, (size_t)bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_copy_d2h: %s", cudaGetErrorString(e));
+  }
+  if (event) {
+    cudaError_t e = cudaEventRecord((cudaEvent_t)event, st);
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_copy_d2h event: %s", cudaGetErrorString(e));
+  }
+  return ELX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,242 @@
+"""GPT-2 training step driven through the chunk runtime (the path's caller).
+
+Every coarse node of the access trace (profiles.py:490-521: wpe embed, one
+node per AC-grouped layer, ln_f, the tied lm_head) is a "wrapped operator"
+(PAPER.md:203-206): before it runs, the ChunkFetcher makes its chunks
+resident; the forward runs without saving activations except each node's
+input (activation checkpointing); the backward walks the
+nodes in reverse (chunking.py:165), recomputes each node with autograd,
+writes the parameter gradients over the parameter data in the chunk
+(K1) and releases chunks at their reduce positions
+(rcache_sim.py:160-167, K3). After the walk HybridAdam updates the shards.
+
+GEMMs/attention are PyTorch (cuBLAS / SDPA); the chunk path is ours.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+import torch.nn.functional as F
+
+from . import kernels
+from .errors import ValidationError
+from .layout import build_chunk_trace, pack_chunks
+from .profiles import coarsen_graph, partition_multiuse, synthesize_transformer_profile
+from .runtime import ChunkFetcher, ChunkManager, HybridAdam, LossScaler
+from .schedule import as_plan
+from .transport import make_transport
+
+
+@dataclass(frozen=True)
+class GPT2Config:
+    hidden: int
+    layers: int
+    heads: int
+    vocab: int = 50257
+    seq_len: int = 1024
+    batch: int = 8
+
+    @property
+    def name(self) -> str:
+        return f"gpt2-h{self.hidden}-l{self.layers}"
+
+
+PRESETS = {  # BASELINE.json configs; Table 7 shapes
+    "gpt2-small": GPT2Config(768, 12, 12),
+    "gpt2-1.3b": GPT2Config(2048, 24, 16),
+    "gpt2-4b": GPT2Config(3072, 32, 24),
+    "gpt2-10b": GPT2Config(4096, 48, 32),
+}
+
+
+def param_shapes(cfg: GPT2Config) -> dict[str, tuple[int, ...]]:
+    h = cfg.hidden
+    shapes = {"wte": (cfg.vocab, h), "wpe": (cfg.seq_len, h), "ln_f.w": (h,), "ln_f.b": (h,)}
+    for i in range(cfg.layers):
+        p = f"h{i}."
+        shapes.update({
+            p + "ln_1.w": (h,), p + "ln_1.b": (h,),
+            p + "attn.qkv.w": (3 * h, h), p + "attn.qkv.b": (3 * h,),
+            p + "attn.proj.w": (h, h), p + "attn.proj.b": (h,),
+            p + "ln_2.w": (h,), p + "ln_2.b": (h,),
+            p + "mlp.fc.w": (4 * h, h), p + "mlp.fc.b": (4 * h,),
+            p + "mlp.proj.w": (h, 4 * h), p + "mlp.proj.b": (h,),
+        })
+    return shapes
+
+
+def init_params(cfg: GPT2Config, device, seed: int = 1234, dtype=torch.bfloat16) -> dict[str, torch.Tensor]:
+    """N(0, 0.02) weights, LN weight 1, biases 0."""
+    g = torch.Generator(device=device)
+    g.manual_seed(seed)
+    out = {}
+    for pid, shp in param_shapes(cfg).items():
+        if pid.endswith(".b"):
+            out[pid] = torch.zeros(shp, dtype=dtype, device=device)
+        elif "ln_" in pid:
+            out[pid] = torch.ones(shp, dtype=dtype, device=device)
+        else:
+            out[pid] = (torch.randn(shp, generator=g, device=device, dtype=torch.float32) * 0.02).to(dtype)
+    return out
+
+
+_LAYER_KEYS = ("ln_1.w", "ln_1.b", "attn.qkv.w", "attn.qkv.b", "attn.proj.w", "attn.proj.b",
+               "ln_2.w", "ln_2.b", "mlp.fc.w", "mlp.fc.b", "mlp.proj.w", "mlp.proj.b")
+
+
+def _block(x, p, heads):
+    B, T, H = x.shape
+    ln1w, ln1b, qkvw, qkvb, projw, projb, ln2w, ln2b, fcw, fcb, mpw, mpb = p
+    h = F.layer_norm(x, (H,), ln1w, ln1b, 1e-5)
+    qkv = F.linear(h, qkvw, qkvb)
+    q, k, v = qkv.view(B, T, 3, heads, H // heads).permute(2, 0, 3, 1, 4).unbind(0)
+    a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
+    x = x + F.linear(a.transpose(1, 2).reshape(B, T, H), projw, projb)
+    h = F.layer_norm(x, (H,), ln2w, ln2b, 1e-5)
+    return x + F.linear(F.gelu(F.linear(h, fcw, fcb), approximate="tanh"), mpw, mpb)
+
+
+class ElixirGPT2:
+    """Public entry point: a chunked GPT-2 trainer on one rank.
+
+    ``plan`` is the reference planner's Plan (object or JSON text) for this
+    model at this world size; ``transport`` defaults to torch.distributed
+    when it is initialised with more than one rank.
+    """
+
+    def __init__(self, cfg: GPT2Config, plan, *, device=None, dtype=torch.bfloat16, seed: int = 1234,
+                 lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.01,
+                 max_norm: float | None = 1.0, loss_scale: float | None = None, transport=None,
+                 prefetch: bool = True, cpu_threads: int | None = None, init: dict | None = None):
+        import torch.distributed as dist
+
+        self.cfg = cfg
+        self.device = torch.device(device if device is not None else "cuda")
+        if transport is None:
+            world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+            transport = make_transport(world)
+        self.transport = transport
+        self.profile = synthesize_transformer_profile(cfg.hidden, cfg.layers, cfg.heads, cfg.vocab,
+                                                      cfg.seq_len, cfg.batch, name=cfg.name)
+        self.access = coarsen_graph(self.profile)
+        _, seq = partition_multiuse(self.profile)
+        plan = as_plan(plan)
+        self.layout = pack_chunks(seq, plan.chunk_length)
+        self.trace = build_chunk_trace(self.access, self.layout)
+        self.shapes = param_shapes(cfg)
+        self.manager = ChunkManager(self.profile, self.layout, plan, shapes=self.shapes, transport=transport,
+                                    device=self.device, dtype=dtype)
+        self.manager.load_params(init if init is not None else init_params(cfg, self.device, seed, dtype))
+        if loss_scale is None:
+            self.scaler = LossScaler(1.0, dynamic=False) if dtype == torch.bfloat16 else LossScaler(65536.0)
+        else:
+            self.scaler = LossScaler(loss_scale, dynamic=False)
+        self.fetcher = ChunkFetcher(self.manager, self.trace, prefetch=prefetch,
+                                    inv_scale=1.0 / self.scaler.scale)
+        self.optimizer = HybridAdam(self.manager, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
+                                    max_norm=max_norm, cpu_threads=cpu_threads)
+        # coarse node -> its chunk parameters, in declaration order
+        order = {p.id: i for i, p in enumerate(self.profile.parameters)}
+        self.node_params = [sorted(node, key=order.__getitem__) for node in self.access.coarse_ops]
+        self.K = len(self.node_params)
+        self.wte = self.manager.shared["wte"]
+        self.last_loss = None
+
+    # -------------------------------------------------------------- nodes
+    def _run_node(self, i: int, x, tokens, targets, params):
+        cfg = self.cfg
+        if i == 0:  # embed: wte (shared) + wpe
+            wpe, wte = params
+            T = tokens.shape[1]
+            return F.embedding(tokens, wte) + wpe[:T]
+        if i == self.K - 1:  # tied lm_head + loss
+            (wte,) = params
+            logits = F.linear(x, wte)
+            return F.cross_entropy(logits.float().view(-1, cfg.vocab), targets.reshape(-1))
+        if i == self.K - 2:  # ln_f
+            w, b = params
+            return F.layer_norm(x, (cfg.hidden,), w, b, 1e-5)
+        return _block(x, params, cfg.heads)
+
+    def _params_of(self, i: int):
+        ps = [self.manager.param(pid) for pid in self.node_params[i]]
+        if i == 0 or i == self.K - 1:
+            ps.append(self.manager.param("wte"))
+        return ps
+
+    # -------------------------------------------------------------- step
+    def train_step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        """One chunked training step; returns the loss as a device scalar."""
+        if tokens.device != self.device:
+            raise ValidationError("tokens must already be on the trainer's device")
+        fx, mgr = self.fetcher, self.manager
+        K = self.K
+        fx.inv_scale = 1.0 / self.scaler.scale
+        fx.begin_step()
+        acts = []
+        x = None
+        with torch.no_grad():
+            for i in range(K):
+                fx.enter(i)
+                acts.append(x)
+                x = self._run_node(i, x, tokens, targets, self._params_of(i))
+                fx.after_compute(i)
+        loss = x
+        grad = torch.full((), self.scaler.scale, dtype=torch.float32, device=self.device)
+        wte_grad_set = False
+        for j in range(K):
+            i = K - 1 - j
+            pos = K + j
+            fx.enter(pos)
+            params = [p.detach().requires_grad_(True) for p in self._params_of(i)]
+            with torch.enable_grad():
+                xin = None if i == 0 else acts[i].detach().requires_grad_(True)
+                out = self._run_node(i, xin, tokens, targets, params)
+                inputs = ([xin] if i > 0 else []) + params
+                grads = torch.autograd.grad(out, inputs, grad_outputs=grad)
+            acts[i] = None
+            if i > 0:
+                grad, pgrads = grads[0], grads[1:]
+            else:
+                pgrads = grads
+            chunk_grads = pgrads[:len(self.node_params[i])]
+            self._write_grads(i, chunk_grads)
+            if i == 0 or i == K - 1:
+                wg = pgrads[-1].reshape(-1)
+                buf = self.wte.grad[:self.wte.numel]
+                if wte_grad_set:
+                    buf.add_(wg)
+                else:
+                    kernels.chunk_pack(self.wte.grad, [(wg, 0)], used_len=self.wte.numel)
+                    wte_grad_set = True
+            fx.after_compute(pos)
+            del grads, pgrads, params, out
+        fx.release_shared(self.wte)
+        done = fx.finish()
+        found_inf, _ = self.optimizer.step(done)
+        self.scaler.update(found_inf)
+        self.last_loss = loss
+        return loss
+
+    def _write_grads(self, i: int, grads) -> None:
+        """Overwrite the node's parameter slots in the chunk with their
+        gradients (Fig. 3): one K1 launch per chunk."""
+        by_chunk: dict[int, list] = {}
+        for pid, g in zip(self.node_params[i], grads):
+            c, off, _ = self.manager.members[pid]
+            by_chunk.setdefault(c, []).append((g.reshape(-1), off))
+        for c, mem in by_chunk.items():
+            st = self.manager.storage(c)
+            kernels.chunk_pack(st, mem, used_len=st.numel())
+
+    # -------------------------------------------------------------- misc
+    @property
+    def n_params(self) -> int:
+        return self.profile.total_elements
+
+    def flops_per_step(self) -> float:
+        """8·M·D (cost_model.py:170-174) for this rank's batch."""
+        return 8.0 * self.n_params * self.cfg.batch * self.cfg.seq_len

@@ -1,0 +1,197 @@
+"""Typed torch-tensor wrappers over the C-ABI (include/elixir_b200.h).
+
+Every function here launches native code from libelixir_b200.so on the
+given (or current) CUDA stream; there is no CPU or PyTorch fallback. Inputs
+are validated for device/dtype/contiguity before the call; the library
+validates sizes and alignment and returns typed errors (_lib.check).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from typing import Sequence
+
+import torch
+
+from . import _lib
+from .errors import ValidationError
+
+_DT = {torch.float32: _lib.F32, torch.bfloat16: _lib.BF16, torch.float16: _lib.F16}
+
+
+def elx_dtype(dt: torch.dtype) -> int:
+    try:
+        return _DT[dt]
+    except KeyError:
+        raise ValidationError(f"unsupported dtype {dt}") from None
+
+
+def _stream(stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def _cuda(t: torch.Tensor, what: str) -> None:
+    if not t.is_cuda:
+        raise ValidationError(f"{what} must be a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValidationError(f"{what} must be contiguous")
+
+
+def chunk_pack(chunk: torch.Tensor, members: Sequence[tuple[torch.Tensor | None, int]],
+               used_len: int | None = None, stream=None) -> None:
+    """K1: chunk[off:off+t.numel()] <- t for (t, off) in members; zero the tail
+    [used_len, chunk.numel()) when used_len is given. A member with t=None and
+    an explicit numel given as (None, off, numel) writes zeros."""
+    lib = _lib.load()
+    _cuda(chunk, "chunk")
+    arr = (_lib.Member * max(1, len(members)))()
+    keep = []
+    for i, m in enumerate(members):
+        if m[0] is None:
+            arr[i].ext, arr[i].offset, arr[i].numel, arr[i].ext_dtype = None, int(m[1]), int(m[2]), elx_dtype(chunk.dtype)
+            continue
+        t = m[0]
+        if not t.is_contiguous():
+            t = t.contiguous()
+        _cuda(t, "member")
+        keep.append(t)
+        arr[i].ext, arr[i].offset, arr[i].numel, arr[i].ext_dtype = t.data_ptr(), int(m[1]), t.numel(), elx_dtype(t.dtype)
+    used = chunk.numel() if used_len is None else int(used_len)
+    rc = lib.elx_chunk_pack(chunk.data_ptr(), elx_dtype(chunk.dtype), chunk.numel(), used,
+                            ctypes.addressof(arr), len(members), _stream(stream))
+    _lib.check(rc, "elx_chunk_pack")
+
+
+def chunk_unpack(chunk: torch.Tensor, members: Sequence[tuple[torch.Tensor, int]], stream=None) -> None:
+    """K1 reverse: t <- chunk[off:off+t.numel()] for (t, off) in members."""
+    lib = _lib.load()
+    _cuda(chunk, "chunk")
+    arr = (_lib.Member * max(1, len(members)))()
+    for i, (t, off) in enumerate(members):
+        _cuda(t, "member")
+        if off + t.numel() > chunk.numel():
+            raise ValidationError("member exceeds chunk")
+        arr[i].ext, arr[i].offset, arr[i].numel, arr[i].ext_dtype = t.data_ptr(), int(off), t.numel(), elx_dtype(t.dtype)
+    rc = lib.elx_chunk_unpack(chunk.data_ptr(), elx_dtype(chunk.dtype), ctypes.addressof(arr),
+                              len(members), _stream(stream))
+    _lib.check(rc, "elx_chunk_unpack")
+
+
+def _ptr_array(ptrs: Sequence[int]):
+    arr = (ctypes.c_void_p * max(1, len(ptrs)))()
+    for i, p in enumerate(ptrs):
+        arr[i] = p
+    return arr
+
+
+def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream=None) -> None:
+    """K2: block[r*S:(r+1)*S] <- shard r (device pointers, local or peer-mapped)."""
+    lib = _lib.load()
+    _cuda(block, "block")
+    if block.numel() < len(shard_ptrs) * shard_len:
+        raise ValidationError("block smaller than world * shard_len")
+    arr = _ptr_array(shard_ptrs)
+    rc = lib.elx_fetch(block.data_ptr(), ctypes.addressof(arr), int(shard_len), len(shard_ptrs),
+                       elx_dtype(block.dtype), _stream(stream))
+    _lib.check(rc, "elx_fetch")
+
+
+def release(grad_shard: torch.Tensor, src_ptrs: Sequence[int], n: int, dtype: torch.dtype,
+            inv_scale: float, step_scalars: torch.Tensor, stream=None) -> None:
+    """K3: grad_shard[:n] = (sum_r src_r[:n] in rank order, fp32) * inv_scale,
+    accumulating sum(g^2) into step_scalars[0] and overflow into step_scalars[1]."""
+    lib = _lib.load()
+    _cuda(grad_shard, "grad_shard")
+    if grad_shard.dtype != torch.float32 or grad_shard.numel() < n:
+        raise ValidationError("grad_shard must be float32 with >= n elements")
+    if step_scalars.dtype != torch.float64 or not step_scalars.is_cuda:
+        raise ValidationError("step_scalars must be a CUDA float64 tensor")
+    arr = _ptr_array(src_ptrs)
+    rc = lib.elx_release(grad_shard.data_ptr(), ctypes.addressof(arr), int(n), len(src_ptrs),
+                         elx_dtype(dtype), float(inv_scale), step_scalars.data_ptr(), _stream(stream))
+    _lib.check(rc, "elx_release")
+
+
+class AdamTable:
+    """Device-resident K4 segment table (built once per plan; static pointers)."""
+
+    def __init__(self, segs: Sequence[tuple[torch.Tensor, torch.Tensor, torch.Tensor, torch.Tensor,
+                                            torch.Tensor, int]], device):
+        host = (_lib.AdamSeg * max(1, len(segs)))()
+        tile = 0
+        self.valid_elements = 0
+        for i, (p32, m, v, g, p16, n) in enumerate(segs):
+            for t in (p32, m, v, g, p16):
+                _cuda(t, "adam segment tensor")
+            host[i].p32, host[i].m, host[i].v = p32.data_ptr(), m.data_ptr(), v.data_ptr()
+            host[i].g, host[i].p16, host[i].n, host[i].tile0 = g.data_ptr(), p16.data_ptr(), int(n), tile
+            tile += -(-int(n) // _lib.ADAM_TILE)
+            self.valid_elements += int(n)
+        self.nseg = len(segs)
+        self.ntiles = tile
+        raw = bytes(host)
+        self.dev = torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)
+        self._keep = [s[:5] for s in segs]
+
+
+def adam(table: AdamTable, hp: dict, step: int, step_scalars: torch.Tensor, p16_dtype: torch.dtype,
+         stream=None) -> None:
+    """K4 over every segment of `table` in one launch."""
+    lib = _lib.load()
+    h = _lib.AdamHP(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"],
+                    hp.get("max_norm", 0.0) or 0.0, elx_dtype(p16_dtype), 0)
+    rc = lib.elx_adam(table.dev.data_ptr(), table.nseg, table.ntiles, ctypes.byref(h), int(step),
+                      step_scalars.data_ptr(), _stream(stream))
+    _lib.check(rc, "elx_adam")
+
+
+def cpu_adam(segs: Sequence[tuple[torch.Tensor, ...]], hp: dict, step: int, scalars_host: Sequence[float],
+             p16_dtype: torch.dtype, threads: int) -> None:
+    """Host AdamW (same bits as K4) over CPU tensors (p32, m, v, g, p16, n)."""
+    lib = _lib.load()
+    arr = (_lib.CpuSeg * max(1, len(segs)))()
+    for i, (p32, m, v, g, p16, n) in enumerate(segs):
+        for t in (p32, m, v, g, p16):
+            if t.is_cuda or not t.is_contiguous():
+                raise ValidationError("cpu_adam needs contiguous host tensors")
+        arr[i].p32, arr[i].m, arr[i].v = p32.data_ptr(), m.data_ptr(), v.data_ptr()
+        arr[i].g, arr[i].p16, arr[i].n = g.data_ptr(), p16.data_ptr(), int(n)
+    h = _lib.AdamHP(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"],
+                    hp.get("max_norm", 0.0) or 0.0, elx_dtype(p16_dtype), 0)
+    sc = (ctypes.c_double * 2)(float(scalars_host[0]), float(scalars_host[1]))
+    rc = lib.elx_cpu_adam(ctypes.addressof(arr), len(segs), ctypes.byref(h), int(step),
+                          ctypes.addressof(sc), int(threads))
+    _lib.check(rc, "elx_cpu_adam")
+
+
+def norm_finalize(step_scalars: torch.Tensor, max_norm: float, out3: torch.Tensor, stream=None) -> None:
+    lib = _lib.load()
+    rc = lib.elx_norm_finalize(step_scalars.data_ptr(), float(max_norm or 0.0), out3.data_ptr(),
+                               _stream(stream))
+    _lib.check(rc, "elx_norm_finalize")
+
+
+def step_reset(step_scalars: torch.Tensor, stream=None) -> None:
+    lib = _lib.load()
+    _lib.check(lib.elx_step_reset(step_scalars.data_ptr(), _stream(stream)), "elx_step_reset")
+
+
+def copy_h2d(dst: torch.Tensor, src_host: torch.Tensor, nbytes: int | None = None, stream=None,
+             event: torch.cuda.Event | None = None) -> None:
+    """K6: pinned host -> HBM on `stream` (copy engine)."""
+    lib = _lib.load()
+    nb = src_host.numel() * src_host.element_size() if nbytes is None else int(nbytes)
+    ev = event.cuda_event if event is not None else None
+    rc = lib.elx_copy_h2d(dst.data_ptr(), src_host.data_ptr(), nb, _stream(stream), ev)
+    _lib.check(rc, "elx_copy_h2d")
+
+
+def copy_d2h(dst_host: torch.Tensor, src: torch.Tensor, nbytes: int | None = None, stream=None,
+             event: torch.cuda.Event | None = None) -> None:
+    """K6: HBM -> pinned host on `stream` (copy engine)."""
+    lib = _lib.load()
+    nb = src.numel() * src.element_size() if nbytes is None else int(nbytes)
+    ev = event.cuda_event if event is not None else None
+    rc = lib.elx_copy_d2h(dst_host.data_ptr(), src.data_ptr(), nb, _stream(stream), ev)
+    _lib.check(rc, "elx_copy_d2h")

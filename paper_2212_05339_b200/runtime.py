@@ -1,0 +1,533 @@
+"""Chunk manager, chunk fetcher and hybrid optimizer — the Elixir runtime.
+
+This is the layer the reference leaves as prose (PAPER.md:170-181 chunks and
+rCache, :203-206 wrapped operators, :221-238 gradient overwrite and the
+paired optimizer chunk, :276-281 prefetch on streams) and whose schedule,
+layout and memory contracts it pins in code (chunking.py:102-170,
+rcache_sim.py:87-199, cost_model.py:147-153, search.py:116-126).
+
+HBM layout per rank (N = world size, S = shard length = ceil(C/N) rounded up
+to 8 elements so every shard starts 16-byte aligned):
+  GPU-home chunks  p16 [G, S] compute dtype   (the rank's parameter shard)
+                   p32/m/v [G, S] fp32        (paired optimizer chunk)
+                   g32 [G, S] fp32            (reduced gradient shard)
+  CPU-home chunks  the same five arrays in pinned host memory
+  rCache           n_block blocks of N*S compute-dtype elements, when N > 1
+                   or some chunk is CPU-homed. At N = 1 a GPU-home chunk's
+                   shard IS the whole chunk and is used in place (its gathers
+                   move no bytes but are still counted, as simulate counts
+                   them).
+  shared params    replicated compute copy + fp32 state shard (ZeRO-2
+                   treatment, search.py:116-126), outside the chunks
+                   (chunking.py:95-98).
+
+All kernels come from libelixir_b200.so (kernels.py); torch is used for
+memory, streams, events and collectives.
+"""
+
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+from typing import Any, Callable, Mapping, Sequence
+
+import numpy as np
+import torch
+
+from . import _lib, kernels
+from .errors import InfeasibleCacheError, ValidationError
+from .schedule import Device, Plan, Schedule, as_plan, compile_schedule, report_from_counters
+from .transport import LocalTransport, make_transport
+
+SHARD_ALIGN = 8  # elements; keeps every shard and rCache segment 16-byte aligned
+
+
+def shard_length(chunk_length: int, world: int) -> int:
+    s = -(-chunk_length // world)
+    return -(-s // SHARD_ALIGN) * SHARD_ALIGN
+
+
+@dataclass
+class _SharedParam:
+    pid: str
+    numel: int
+    shape: tuple[int, ...]
+    shard: int               # Ssh
+    full: torch.Tensor       # replicated compute copy [N*Ssh]
+    grad: torch.Tensor       # replicated compute-dtype grad accumulator [N*Ssh]
+    p16: torch.Tensor        # this rank's compute shard [Ssh] (== full at N=1)
+    p32: torch.Tensor
+    m: torch.Tensor
+    v: torch.Tensor
+    g32: torch.Tensor
+
+    def valid(self, rank: int) -> int:
+        return max(0, min(self.shard, self.numel - rank * self.shard))
+
+
+class ChunkManager:
+    """Owns every chunk shard, optimizer shard and rCache block of one rank.
+
+    API mirrors the reference concepts: chunks of ``layout.chunk_length``
+    elements at the layout's exact member offsets (chunking.py:113-131),
+    homes and rCache size from the Plan (search.py:267-291).
+    """
+
+    def __init__(self, profile: Any, layout: Any, plan: Any, *, shapes: Mapping[str, Sequence[int]] | None = None,
+                 transport=None, device=None, dtype: torch.dtype = torch.bfloat16):
+        self.plan: Plan = as_plan(plan)
+        self.layout = layout
+        self.transport = transport or LocalTransport()
+        self.world = self.transport.world
+        self.rank = self.transport.rank
+        self.device = torch.device(device if device is not None else "cuda")
+        self.dtype = dtype
+        if dtype not in (torch.bfloat16, torch.float16):
+            raise ValidationError("compute dtype must be bfloat16 or float16")
+        if self.plan.chunk_length != layout.chunk_length:
+            raise ValidationError(f"plan chunk_length {self.plan.chunk_length} != layout {layout.chunk_length}")
+        n = layout.n_chunks
+        ids = set(range(n))
+        if set(self.plan.chunk_homes) != ids:
+            # cli.py:255-259: a plan and a profile must pack into the same chunk ids.
+            raise ValidationError(f"plan chunk ids {sorted(self.plan.chunk_homes)[:8]}... do not match the "
+                                  f"layout's {n} chunks")
+        self.n_chunks = n
+        self.C = layout.chunk_length
+        self.S = shard_length(self.C, self.world)
+        self.P = self.S * self.world  # physical block length
+        self.homes = [self.plan.chunk_homes[c] for c in range(n)]
+        self.gpu_ids = [c for c in range(n) if self.homes[c] is Device.GPU]
+        self.cpu_ids = [c for c in range(n) if self.homes[c] is Device.CPU]
+        self.row = {}
+        for i, c in enumerate(self.gpu_ids):
+            self.row[c] = i
+        for i, c in enumerate(self.cpu_ids):
+            self.row[c] = i
+        self.used = [sum(m.numel for m in ch.members) for ch in layout.chunks]
+        self.members = {m.param_id: (ch.id, m.offset, m.numel) for ch in layout.chunks for m in ch.members}
+        shared_ids = [p.id for p in profile.parameters if p.shared]
+        self.shapes = {p.id: (tuple(shapes[p.id]) if shapes and p.id in shapes else (p.numel,))
+                       for p in profile.parameters}
+        for pid, (c, off, numel) in self.members.items():
+            if math.prod(self.shapes[pid]) != numel:
+                raise ValidationError(f"shape {self.shapes[pid]} of '{pid}' does not hold {numel} elements")
+
+        dev, S = self.device, self.S
+        G, H = len(self.gpu_ids), len(self.cpu_ids)
+        f32 = torch.float32
+        # ---- GPU-home arenas
+        self.p16 = torch.zeros(G, S, dtype=dtype, device=dev)  # at N=1, S == P: the whole chunk
+        self.p32 = torch.zeros(G, S, dtype=f32, device=dev)
+        self.m = torch.zeros(G, S, dtype=f32, device=dev)
+        self.v = torch.zeros(G, S, dtype=f32, device=dev)
+        self.g32 = torch.zeros(G, S, dtype=f32, device=dev)
+        # ---- CPU-home arenas (pinned)
+        pin = torch.cuda.is_available()
+        self.h_p16 = torch.zeros(H, S, dtype=dtype, pin_memory=pin)
+        self.h_p32 = torch.zeros(H, S, dtype=f32, pin_memory=pin)
+        self.h_m = torch.zeros(H, S, dtype=f32, pin_memory=pin)
+        self.h_v = torch.zeros(H, S, dtype=f32, pin_memory=pin)
+        self.h_g32 = torch.zeros(H, S, dtype=f32, pin_memory=pin)
+        # ---- rCache blocks and release staging
+        self.alias = self.world == 1
+        need_blocks = self.world > 1 or H > 0
+        nb = self.plan.n_block if need_blocks else 0
+        self.blocks = torch.zeros(nb, self.P, dtype=dtype, device=dev)
+        self.recv = torch.zeros(self.P if self.world > 1 else 0, dtype=dtype, device=dev)
+        self.stage32 = torch.zeros(S if H > 0 else 0, dtype=f32, device=dev)
+        # ---- shared (multi-use) parameters: replicated copy + partitioned state
+        self.shared: dict[str, _SharedParam] = {}
+        for pid in shared_ids:
+            numel = next(p.numel for p in profile.parameters if p.id == pid)
+            ssh = shard_length(numel, self.world)
+            full = torch.zeros(ssh * self.world, dtype=dtype, device=dev)
+            p16 = full[self.rank * ssh:(self.rank + 1) * ssh] if self.world == 1 else torch.zeros(ssh, dtype=dtype, device=dev)
+            self.shared[pid] = _SharedParam(
+                pid, numel, self.shapes[pid], ssh, full, torch.zeros_like(full), p16,
+                torch.zeros(ssh, dtype=f32, device=dev), torch.zeros(ssh, dtype=f32, device=dev),
+                torch.zeros(ssh, dtype=f32, device=dev), torch.zeros(ssh, dtype=f32, device=dev))
+        # step scalars: [0] sum g^2, [1] overflow flag (elx_release / elx_adam)
+        self.step_scalars = torch.zeros(4, dtype=torch.float64, device=dev)
+        self._bound: dict[int, torch.Tensor] = {}   # chunk -> storage it is bound to
+        self._views: dict[str, torch.Tensor] = {}
+
+    # ------------------------------------------------------------ sizes
+    def valid(self, c: int, rank: int | None = None) -> int:
+        """Elements of chunk c that are real parameters inside `rank`'s shard."""
+        r = self.rank if rank is None else rank
+        return max(0, min(self.S, self.used[c] - r * self.S))
+
+    def memory_report(self) -> dict:
+        t = lambda *xs: sum(x.numel() * x.element_size() for x in xs)
+        return {
+            "gpu_chunk_state_bytes": t(self.p16, self.p32, self.m, self.v),
+            "gpu_grad_shard_bytes": t(self.g32),
+            "rcache_bytes": t(self.blocks),
+            "host_chunk_state_bytes": t(self.h_p16, self.h_p32, self.h_m, self.h_v, self.h_g32),
+            "shared_bytes": sum(t(s.full, s.grad, s.p32, s.m, s.v, s.g32) + (0 if self.world == 1 else t(s.p16))
+                                for s in self.shared.values()),
+        }
+
+    # ------------------------------------------------------------ init
+    def load_params(self, tensors: Mapping[str, torch.Tensor]) -> None:
+        """Pack initial parameters into chunks (K1) and seed the fp32 masters."""
+        dev = self.device
+        tmp16 = torch.empty(self.P, dtype=self.dtype, device=dev)
+        tmp32 = torch.empty(self.P, dtype=torch.float32, device=dev)
+        lo, hi = self.rank * self.S, (self.rank + 1) * self.S
+        for ch in self.layout.chunks:
+            mem = []
+            for m in ch.members:
+                t = tensors[m.param_id]
+                if t.numel() != m.numel:
+                    raise ValidationError(f"'{m.param_id}' has {t.numel()} elements, layout says {m.numel}")
+                mem.append((t.detach().to(dev).reshape(-1), m.offset))
+            kernels.chunk_pack(tmp16, mem, used_len=ch.used_elements)
+            kernels.chunk_pack(tmp32, mem, used_len=ch.used_elements)
+            r = self.row[ch.id]
+            if self.homes[ch.id] is Device.GPU:
+                if self.alias:
+                    self.p16[r].copy_(tmp16)
+                else:
+                    self.p16[r].copy_(tmp16[lo:hi])
+                self.p32[r].copy_(tmp32[lo:hi])
+            else:
+                self.h_p16[r].copy_(tmp16[lo:hi])
+                self.h_p32[r].copy_(tmp32[lo:hi])
+        for sp in self.shared.values():
+            t = tensors[sp.pid].detach().to(dev).reshape(-1)
+            kernels.chunk_pack(sp.full, [(t, 0)], used_len=sp.numel)
+            lo_s, hi_s = self.rank * sp.shard, (self.rank + 1) * sp.shard
+            kernels.chunk_pack(sp.p32, [(t[lo_s:min(hi_s, sp.numel)], 0)], used_len=max(0, min(hi_s, sp.numel) - lo_s))
+            if self.world > 1:
+                sp.p16.copy_(sp.full[lo_s:hi_s])
+        torch.cuda.synchronize(dev)
+
+    # ------------------------------------------------------------ views
+    def home_storage(self, c: int) -> torch.Tensor:
+        """N=1 GPU-home chunk storage (used in place)."""
+        return self.p16[self.row[c]]
+
+    def bind(self, c: int, storage: torch.Tensor) -> None:
+        self._bound[c] = storage
+        for m in self.layout.chunks[c].members:
+            self._views[m.param_id] = storage[m.offset:m.offset + m.numel].view(self.shapes[m.param_id])
+
+    def unbind(self, c: int) -> None:
+        self._bound.pop(c, None)
+        for m in self.layout.chunks[c].members:
+            self._views.pop(m.param_id, None)
+
+    def storage(self, c: int) -> torch.Tensor:
+        try:
+            return self._bound[c]
+        except KeyError:
+            raise InfeasibleCacheError(f"chunk {c} is not resident in the rCache") from None
+
+    def param(self, pid: str) -> torch.Tensor:
+        """Current compute-dtype view of a parameter (chunk member or shared)."""
+        v = self._views.get(pid)
+        if v is not None:
+            return v
+        sp = self.shared.get(pid)
+        if sp is not None:
+            return sp.full[:sp.numel].view(sp.shape)
+        raise InfeasibleCacheError(f"parameter '{pid}' is not resident (its chunk was not fetched)")
+
+    # ------------------------------------------------------------ export
+    def master_params(self) -> dict[str, torch.Tensor]:
+        """fp32 master values of this rank's shards, reassembled per parameter
+        for the members this rank owns completely (world 1: all of them)."""
+        out = {}
+        for pid, (c, off, numel) in self.members.items():
+            lo = self.rank * self.S
+            if off < lo or off + numel > lo + self.S:
+                continue
+            r = self.row[c]
+            src = self.p32[r] if self.homes[c] is Device.GPU else self.h_p32[r]
+            out[pid] = src[off - lo:off - lo + numel].view(self.shapes[pid]).clone()
+        return out
+
+
+class ChunkFetcher:
+    """Replays the compiled rCache program: gathers (with Belady victims and
+    one-position prefetch on the comm stream), pins, and releases.
+
+    Live counters carry SimReport's field names and must equal
+    offplan.simulate for the same trace/plan (rcache_sim.py:87-199).
+    """
+
+    def __init__(self, manager: ChunkManager, trace: Any, *, comm_stream: torch.cuda.Stream | None = None,
+                 prefetch: bool = True, inv_scale: float = 1.0):
+        self.mgr = manager
+        self.trace = trace
+        plan = manager.plan
+        self.sched: Schedule = compile_schedule(trace, plan.n_block, plan.chunk_homes, manager.n_chunks)
+        self.n_fwd = self.sched.n_forward
+        self.walk = list(trace.forward) + list(trace.backward)
+        self.comm = comm_stream or torch.cuda.Stream(device=manager.device)
+        self.prefetch = prefetch
+        self.inv_scale = inv_scale
+        ev = self.sched.events
+        W = 2 * self.n_fwd
+        self.due = [[] for _ in range(W)]
+        self.early = [[] for _ in range(W)]
+        self.reduces = [[] for _ in range(W)]
+        for e in ev:
+            rec = (int(e["chunk"]), int(e["block"]), int(e["victim"]), int(e["pos"]))
+            if int(e["kind"]) == _lib.EV_REDUCE:
+                self.reduces[int(e["pos"])].append(rec[0])
+            elif prefetch and int(e["issue_pos"]) < int(e["pos"]):
+                self.early[int(e["issue_pos"])].append(rec)
+            else:
+                self.due[int(e["pos"])].append(rec)
+        self._reset()
+
+    # ------------------------------------------------------------ state
+    def _reset(self) -> None:
+        for c in list(self.mgr._bound):
+            self.mgr.unbind(c)
+        self.block_of: dict[int, int] = {}
+        self.ready: dict[int, torch.cuda.Event] = {}
+        self.last_use: dict[int, torch.cuda.Event] = {}
+        self.gathered: set[int] = set()
+        self.live = dict(gather_ops=0, replaced_ops=0, reduce_ops=0, c2g_units=0, g2c_units=0,
+                         peak_rcache_blocks=0)
+        self.bytes_moved = dict(h2d=0, d2h=0, gather=0, scatter=0)
+        self.pos = 0
+
+    def begin_step(self) -> None:
+        self._reset()
+
+    # ------------------------------------------------------------ walk
+    def enter(self, pos: int) -> None:
+        """Before node `pos` computes: make its chunks resident and bound."""
+        if pos != self.pos:
+            raise ValidationError(f"walk out of order: expected position {self.pos}, got {pos}")
+        for rec in self.due[pos]:
+            self._gather(rec)
+        for rec in self.early[pos]:  # prefetch for pos + 1
+            self._gather(rec)
+        cur = torch.cuda.current_stream(self.mgr.device)
+        for c in self.walk[pos]:
+            if c not in self.block_of:
+                raise InfeasibleCacheError(f"chunk {c} needed at position {pos} is not resident")
+            ev = self.ready.pop(c, None)
+            if ev is not None:
+                cur.wait_event(ev)
+        self.live["peak_rcache_blocks"] = max(self.live["peak_rcache_blocks"], len(self.block_of))
+
+    def after_compute(self, pos: int) -> None:
+        """After node `pos` (and, in backward, its gradient write-back)."""
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.mgr.device))
+        for c in self.walk[pos]:
+            self.last_use[c] = ev
+        if pos >= self.n_fwd:
+            for c in self.reduces[pos]:
+                self._release(c, ev)
+        self.pos = pos + 1
+
+    def finish(self) -> torch.cuda.Event:
+        """End of the walk: every release is enqueued; returns their event."""
+        if self.pos != 2 * self.n_fwd:
+            raise ValidationError(f"walk ended at position {self.pos} of {2 * self.n_fwd}")
+        done = torch.cuda.Event()
+        done.record(self.comm)
+        return done
+
+    def counters(self) -> dict:
+        return dict(self.live)
+
+    def report(self, precision=None, hardware=None):
+        from .profiles import PrecisionSpec
+        return report_from_counters(self.live, self.trace, self.mgr.C, self.mgr.plan.chunk_homes,
+                                    precision or PrecisionSpec(), self.mgr.world, hardware)
+
+    # ------------------------------------------------------------ events
+    def _gather(self, rec) -> None:
+        c, b, victim, pos = rec
+        mgr = self.mgr
+        if victim >= 0:
+            if self.block_of.get(victim) != b:
+                raise InfeasibleCacheError(f"schedule desync: victim {victim} not in block {b}")
+            del self.block_of[victim]
+            mgr.unbind(victim)
+        self.block_of[c] = b
+        self.live["gather_ops"] += 1
+        if c in self.gathered:
+            self.live["replaced_ops"] += 1
+        self.gathered.add(c)
+        cpu = mgr.homes[c] is Device.CPU
+        if cpu:
+            self.live["c2g_units"] += 1
+        if mgr.alias and not cpu:
+            mgr.bind(c, mgr.home_storage(c))  # the shard is the whole chunk: no bytes move
+            return
+        block = mgr.blocks[b]
+        comm = self.comm
+        with torch.cuda.stream(comm):
+            if victim >= 0 and victim in self.last_use:
+                comm.wait_event(self.last_use[victim])
+            seg = block[mgr.rank * mgr.S:(mgr.rank + 1) * mgr.S]
+            if cpu:
+                kernels.copy_h2d(seg, mgr.h_p16[mgr.row[c]], stream=comm)
+                self.bytes_moved["h2d"] += seg.numel() * seg.element_size()
+                if mgr.world > 1:
+                    mgr.transport.gather(block, seg)
+            else:
+                mgr.transport.gather(block, mgr.p16[mgr.row[c]])
+            if mgr.world > 1:
+                self.bytes_moved["gather"] += (mgr.world - 1) * mgr.S * block.element_size()
+            ev = torch.cuda.Event()
+            ev.record(comm)
+        self.ready[c] = ev
+        mgr.bind(c, block)
+
+    def _release(self, c: int, grads_written: torch.cuda.Event) -> None:
+        """Reduce-scatter chunk c's gradients into this rank's fp32 shard (K3)."""
+        mgr = self.mgr
+        n = mgr.valid(c)
+        comm = self.comm
+        storage = mgr.storage(c)
+        self.live["reduce_ops"] += 1
+        cpu = mgr.homes[c] is Device.CPU
+        if cpu:
+            self.live["g2c_units"] += 1
+        with torch.cuda.stream(comm):
+            comm.wait_event(grads_written)
+            if mgr.world == 1:
+                srcs = [storage.data_ptr()]
+            else:
+                mgr.transport.scatter(mgr.recv, storage)
+                self.bytes_moved["scatter"] += (mgr.world - 1) * mgr.S * storage.element_size()
+                es = mgr.recv.element_size()
+                srcs = [mgr.recv.data_ptr() + r * mgr.S * es for r in range(mgr.world)]
+            r = mgr.row[c]
+            target = mgr.g32[r] if not cpu else mgr.stage32
+            if n > 0:
+                kernels.release(target, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
+            if cpu and n > 0:
+                kernels.copy_d2h(mgr.h_g32[r], mgr.stage32, n * 4, stream=comm)
+                self.bytes_moved["d2h"] += n * 4
+
+    def release_shared(self, sp: _SharedParam) -> None:
+        """Release of a shared parameter's gradient (after its last use)."""
+        mgr = self.mgr
+        comm = self.comm
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(mgr.device))
+        with torch.cuda.stream(comm):
+            comm.wait_event(ev)
+            if mgr.world == 1:
+                srcs = [sp.grad.data_ptr()]
+            else:
+                recv = torch.empty_like(sp.grad)
+                mgr.transport.scatter(recv, sp.grad)
+                recv.record_stream(comm)
+                es = recv.element_size()
+                srcs = [recv.data_ptr() + r * sp.shard * es for r in range(mgr.world)]
+            n = sp.valid(mgr.rank)
+            if n > 0:
+                kernels.release(sp.g32, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
+
+
+class HybridAdam:
+    """Chunk-wise fused mixed-precision AdamW: GPU-home shards on the device
+    (K4, update rate v_g), CPU-home shards on host threads (elx_cpu_adam,
+    rate v_c), with global grad-norm clipping and overflow skip
+    (rcache_sim.py:173-184)."""
+
+    def __init__(self, manager: ChunkManager, *, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
+                 weight_decay: float = 0.01, max_norm: float | None = 1.0, cpu_threads: int | None = None):
+        self.mgr = manager
+        self.hp = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
+                       max_norm=max_norm or 0.0)
+        self.step_count = 0
+        self.cpu_threads = cpu_threads or max(1, min(32, len(os.sched_getaffinity(0))))
+        segs = []
+        m = manager
+        for c in m.gpu_ids:
+            r = m.row[c]
+            n = m.valid(c)
+            if n > 0:
+                segs.append((m.p32[r], m.m[r], m.v[r], m.g32[r], m.p16[r], n))
+        for sp in m.shared.values():
+            n = sp.valid(m.rank)
+            if n > 0:
+                segs.append((sp.p32, sp.m, sp.v, sp.g32, sp.p16, n))
+        self.table = kernels.AdamTable(segs, m.device)
+        self.cpu_segs = []
+        for c in m.cpu_ids:
+            r = m.row[c]
+            n = m.valid(c)
+            if n > 0:
+                self.cpu_segs.append((m.h_p32[r], m.h_m[r], m.h_v[r], m.h_g32[r], m.h_p16[r], n))
+        self._host_sc = torch.zeros(4, dtype=torch.float64, pin_memory=torch.cuda.is_available())
+        self.last = dict(found_inf=False, grad_norm=0.0, skipped=0)
+        self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
+        self.time_adam = False
+
+    @property
+    def gpu_elements(self) -> int:
+        return self.table.valid_elements
+
+    def step(self, releases_done: torch.cuda.Event) -> tuple[bool, float]:
+        """All-reduce norm/overflow, then update every shard. Returns
+        (found_inf, grad_norm) — one host sync per step (GradScaler also
+        reads found_inf on the host)."""
+        m = self.mgr
+        dev = m.device
+        cur = torch.cuda.current_stream(dev)
+        cur.wait_event(releases_done)
+        if m.world > 1:
+            m.transport.all_reduce_sum(m.step_scalars[:2])
+        self._host_sc.copy_(m.step_scalars, non_blocking=True)
+        torch.cuda.current_stream(dev).synchronize()
+        sq, inf_flag = float(self._host_sc[0]), float(self._host_sc[1])
+        found_inf = inf_flag != 0.0 or not math.isfinite(sq)
+        step = self.step_count + (0 if found_inf else 1)
+        kstep = max(step, 1)
+        if self.time_adam:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(cur)
+        kernels.adam(self.table, self.hp, kstep, m.step_scalars, m.dtype, stream=cur)
+        if self.time_adam:
+            e1.record(cur)
+            self.adam_events.append((e0, e1))
+        if self.cpu_segs:
+            kernels.cpu_adam(self.cpu_segs, self.hp, kstep, (sq, inf_flag), m.dtype, self.cpu_threads)
+        if m.world > 1:
+            for sp in m.shared.values():
+                m.transport.gather(sp.full, sp.p16)
+        kernels.step_reset(m.step_scalars, stream=cur)
+        if not found_inf:
+            self.step_count = step
+        self.last = dict(found_inf=found_inf, grad_norm=math.sqrt(sq) if math.isfinite(sq) else float("inf"),
+                         skipped=self.last["skipped"] + int(found_inf))
+        return found_inf, self.last["grad_norm"]
+
+
+class LossScaler:
+    """Dynamic loss scale for fp16 (GradScaler convention: halve on overflow,
+    double after `growth_interval` clean steps); bf16 uses a static 1.0."""
+
+    def __init__(self, init_scale: float = 65536.0, growth_interval: int = 2000, dynamic: bool = True):
+        self.scale = float(init_scale)
+        self.growth_interval = growth_interval
+        self.dynamic = dynamic
+        self._good = 0
+
+    def update(self, found_inf: bool) -> None:
+        if not self.dynamic:
+            return
+        if found_inf:
+            self.scale *= 0.5
+            self._good = 0
+        else:
+            self._good += 1
+            if self._good >= self.growth_interval:
+                self.scale *= 2.0
+                self._good = 0

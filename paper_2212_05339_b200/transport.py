@@ -1,0 +1,72 @@
+"""Rank-to-rank data movement for chunk fetch and gradient release.
+
+Two exchange primitives cover the path:
+  * gather  — all-gather of every rank's shard into an rCache block (fetch);
+  * scatter — every rank sends segment r of its block to rank r, so that
+    rank r holds all N copies of ITS segment; the release kernel (K3) then
+    reduces them in fixed rank order in fp32. This is a reduce-scatter whose
+    reduction runs in our kernel, giving rank-order-deterministic fp32
+    results (NCCL's bf16 reduce-scatter accumulates in bf16 and in ring
+    order, which cannot meet the 1e-6 parity bar).
+
+Implementations:
+  LocalTransport   world 1 (nothing moves between ranks);
+  TorchDistTransport  torch.distributed collectives (NCCL over NVLink on the
+                   GPU box; gloo on CPU for the multi-process host tests).
+Collectives are issued under the caller's current stream, so the comm
+stream orders them with the K1-K3 launches around them.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+class LocalTransport:
+    world = 1
+    rank = 0
+
+    def gather(self, block: torch.Tensor, shard: torch.Tensor) -> None:  # pragma: no cover - not used at world 1
+        block[: shard.numel()].copy_(shard)
+
+    def scatter(self, recv: torch.Tensor, block: torch.Tensor) -> None:  # pragma: no cover
+        recv.copy_(block)
+
+    def all_reduce_sum(self, t: torch.Tensor) -> None:
+        return None
+
+    def barrier(self) -> None:
+        return None
+
+
+class TorchDistTransport:
+    def __init__(self, group=None):
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.backend = dist.get_backend(group)
+
+    def gather(self, block: torch.Tensor, shard: torch.Tensor) -> None:
+        """block[r*S:(r+1)*S] <- rank r's shard (S = shard.numel())."""
+        out = block[: self.world * shard.numel()]
+        if self.backend == "gloo":  # gloo has no all_gather_into_tensor
+            dist.all_gather(list(out.chunk(self.world)), shard, group=self.group)
+        else:
+            dist.all_gather_into_tensor(out, shard, group=self.group)
+
+    def scatter(self, recv: torch.Tensor, block: torch.Tensor) -> None:
+        """recv[r*S:(r+1)*S] <- rank r's block[self.rank*S:(self.rank+1)*S]."""
+        dist.all_to_all_single(recv, block[: recv.numel()], group=self.group)
+
+    def all_reduce_sum(self, t: torch.Tensor) -> None:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def barrier(self) -> None:
+        dist.barrier(group=self.group)
+
+
+def make_transport(world_size: int):
+    if world_size == 1:
+        return LocalTransport()
+    return TorchDistTransport()

@@ -1,0 +1,107 @@
+"""The C-ABI library loads and exports every symbol include/elixir_b200.h
+declares; host-side entry points (no GPU needed) behave per the header."""
+
+from __future__ import annotations
+
+import ctypes
+import re
+from pathlib import Path
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import arith
+from paper_2212_05339_b200 import _lib, errors, kernels
+
+HEADER = Path(__file__).resolve().parents[1] / "include" / "elixir_b200.h"
+
+
+def _declared():
+    text = re.sub(r"/\*.*?\*/", "", HEADER.read_text(), flags=re.S)
+    return sorted(set(re.findall(r"\b(elx_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_header_symbols_exported():
+    lib = _lib.load()
+    declared = _declared()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(lib, name), name
+    assert set(declared) == set(_lib.EXPORTED)
+
+
+def test_struct_layouts_match_header():
+    assert ctypes.sizeof(_lib.Event) == 24
+    assert ctypes.sizeof(_lib.SimCounters) == 56
+    assert ctypes.sizeof(_lib.Member) == 32
+    assert ctypes.sizeof(_lib.AdamSeg) == 64
+    assert ctypes.sizeof(_lib.AdamHP) == 56
+    assert ctypes.sizeof(_lib.CpuSeg) == 48
+
+
+def test_abi_version_and_errors():
+    lib = _lib.load()
+    assert lib.elx_abi_version() == 1
+    rc = lib.elx_layout_pack(None, 0, 0, None, None, None)
+    assert rc == _lib.ERR_VALIDATION
+    assert b"chunk_length" in lib.elx_last_error()
+    with pytest.raises(errors.ValidationError):
+        _lib.check(rc)
+
+
+def test_gpu_entry_points_validate_before_launch():
+    """Argument validation happens on the host; no GPU is touched."""
+    lib = _lib.load()
+    assert lib.elx_fetch(None, None, 8, 0, _lib.BF16, None) == _lib.ERR_VALIDATION
+    assert lib.elx_fetch(None, None, 7, 1, _lib.BF16, None) == _lib.ERR_VALIDATION
+    assert lib.elx_release(None, None, 8, 1, _lib.BF16, ctypes.c_float(1.0), None, None) == _lib.ERR_VALIDATION
+    assert lib.elx_adam(None, 1, 1, None, 1, None, None) == _lib.ERR_VALIDATION
+    hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 0.0, _lib.BF16, 0)
+    sc = (ctypes.c_double * 2)()
+    assert lib.elx_adam(None, 1, 1, ctypes.byref(hp), 0, ctypes.addressof(sc), None) == _lib.ERR_VALIDATION
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("skip", [False, True])
+def test_host_adam_bit_exact_vs_oracle(dtype, skip):
+    """elx_cpu_adam (the CPU-home optimizer of the hybrid Adam) == oracle, bit for bit."""
+    rng = np.random.default_rng(3)
+    sizes = [1, 7, 4096, 100_003]
+    segs, refs = [], []
+    sq = 0.0
+    for n in sizes:
+        p = (rng.standard_normal(n) * 0.02).astype(np.float32)
+        m = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+        v = (rng.random(n) * 1e-6).astype(np.float32)
+        g = (rng.standard_normal(n) * 0.3).astype(np.float32)
+        sq += float(np.dot(g.astype(np.float64), g))
+        T = [torch.from_numpy(a.copy()) for a in (p, m, v, g)]
+        p16 = torch.zeros(n, dtype=dtype)
+        segs.append((T[0], T[1], T[2], T[3], p16, n))
+        refs.append((p, m, v, g))
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
+    kernels.cpu_adam(segs, hp, 4, (sq, 1.0 if skip else 0.0), dtype, threads=4)
+    coef = arith.clip_coef(sq, 1.0)
+    name = "bf16" if dtype == torch.bfloat16 else "f16"
+    for (P, M, V, G, P16, n), (p, m, v, g) in zip(segs, refs):
+        rp, rm, rv, r16 = arith.adamw(p, m, v, g, 4, 1e-3, 0.9, 0.999, 1e-8, 0.01, coef, skip, name)
+        assert np.array_equal(P.numpy(), rp)
+        assert np.array_equal(M.numpy(), rm)
+        assert np.array_equal(V.numpy(), rv)
+        assert np.array_equal(P16.view(torch.int16).numpy().view(np.uint16), r16)
+
+
+def test_host_f16_rounding_edge_cases():
+    """elx_cpu_adam's float->half conversion equals numpy's (IEEE RNE), incl.
+    subnormals and overflow (exercised through the skip path, which only
+    converts the master)."""
+    vals = np.array([0.0, -0.0, 1.0, 65504.0, 65519.0, 65520.0, 1e6, -1e6, 6.1e-5, 6.0e-8, 5.96e-8, 2.98e-8,
+                     2.9e-8, 1e-10, 3.0e-5, -4.5e-6, np.inf, -np.inf], np.float32)
+    n = vals.size
+    P = torch.from_numpy(vals.copy())
+    z = torch.zeros(n)
+    p16 = torch.zeros(n, dtype=torch.float16)
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, max_norm=0.0)
+    kernels.cpu_adam([(P, z.clone(), z.clone(), z.clone(), p16, n)], hp, 1, (0.0, 1.0), torch.float16, 1)
+    assert np.array_equal(p16.numpy().view(np.uint16), vals.astype(np.float16).view(np.uint16))

@@ -1,0 +1,258 @@
+"""Parity of the sm_100a kernels (K1-K6), called through the C-ABI, against the
+CPU oracle on the same seeded inputs. Integer/byte work is bit-exact; the
+fp32 release and Adam are also bit-exact (the kernels apply the oracle's
+IEEE operations in the oracle's order), which is stricter than the 1e-6
+relative bar of BASELINE.json."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import arith
+from paper_2212_05339_b200 import _lib, errors, kernels
+
+pytestmark = pytest.mark.gpu
+
+HP = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
+
+
+def _bits(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
+def _name(dt):
+    return "bf16" if dt == torch.bfloat16 else "f16"
+
+
+# ------------------------------------------------------------------ K1 pack
+
+@pytest.mark.parametrize("chunk_dtype", [torch.bfloat16, torch.float32, torch.float16])
+def test_pack_unpack_members_and_padding(cuda, chunk_dtype):
+    g = torch.Generator().manual_seed(0)
+    sizes = [5, 3, 4096, 17, 40000, 1, 8]
+    offs, o = [], 3  # start at an odd offset: exercises the unaligned path too
+    for n in sizes:
+        offs.append(o)
+        o += n
+    used, phys = o, o + 101
+    srcs = [torch.randn(n, generator=g).to(torch.bfloat16) for n in sizes]
+    chunk = torch.full((phys,), 7.0, dtype=chunk_dtype, device=cuda)
+    kernels.chunk_pack(chunk, [(s.to(cuda), off) for s, off in zip(srcs, offs)], used_len=used)
+    ref = np.full(phys, 7.0, np.float32)
+    for s, off in zip(srcs, offs):
+        ref[off:off + s.numel()] = s.float().numpy()
+    ref[used:] = 0.0
+    want = torch.from_numpy(ref).to(chunk_dtype).float().numpy()  # RNE, as the kernel converts
+    assert np.array_equal(chunk.float().cpu().numpy(), want)
+    # unpack back into fresh tensors of the source dtype
+    outs = [torch.empty(n, dtype=torch.bfloat16, device=cuda) for n in sizes]
+    kernels.chunk_unpack(chunk, list(zip(outs, offs)))
+    torch.cuda.synchronize()
+    for s, t in zip(srcs, outs):
+        assert torch.equal(t.cpu(), s.to(chunk_dtype).to(torch.bfloat16))
+
+
+def test_pack_is_bit_exact_gpt2_layout(cuda):
+    """Pack a real layout (GPT-2 tiny) and compare with the oracle's byte image."""
+    from oracle import layout_ref as L
+    params, ops = L.gpt2_records(64, 3, 128, 16)
+    _, seq = L.partition(params, ops)
+    C = 16 * 64 * 4 + 999
+    chunks, _ = L.pack(seq, C)
+    g = torch.Generator().manual_seed(1)
+    vals = {pid: torch.randn(n, generator=g).to(torch.bfloat16) for pid, n in seq}
+    for ch in chunks:
+        phys = C + 5
+        buf = torch.empty(phys, dtype=torch.bfloat16, device=cuda)
+        kernels.chunk_pack(buf, [(vals[p].to(cuda), off) for p, off, _ in ch], used_len=sum(n for *_, n in ch))
+        want = arith.pack(phys, [(_bits(vals[p]), off) for p, off, _ in ch])
+        assert np.array_equal(_bits(buf), want)
+
+
+def test_pack_validation(cuda):
+    buf = torch.zeros(10, dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(errors.ValidationError):
+        kernels.chunk_pack(buf, [(torch.zeros(8, dtype=torch.bfloat16, device=cuda), 5)])
+
+
+# ------------------------------------------------------------------ K2 fetch
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
+@pytest.mark.parametrize("shard", [8, 4096, 1_000_008])
+def test_fetch_gathers_shards_in_rank_order(cuda, world, shard):
+    g = torch.Generator().manual_seed(world * 7 + shard)
+    shards = [torch.randint(-32768, 32767, (shard,), generator=g, dtype=torch.int16).view(torch.bfloat16).to(cuda)
+              for _ in range(world)]
+    block = torch.zeros(world * shard, dtype=torch.bfloat16, device=cuda)
+    kernels.fetch(block, [s.data_ptr() for s in shards], shard)
+    want = arith.gather([_bits(s) for s in shards])
+    assert np.array_equal(_bits(block), want)
+
+
+def test_fetch_rejects_unaligned(cuda):
+    block = torch.zeros(64, dtype=torch.bfloat16, device=cuda)
+    s = torch.zeros(16, dtype=torch.bfloat16, device=cuda)
+    with pytest.raises(errors.ValidationError):
+        kernels.fetch(block, [s.data_ptr()], 7)
+    with pytest.raises(errors.ValidationError):
+        kernels.fetch(block, [s.data_ptr() + 2], 8)
+
+
+# ------------------------------------------------------------------ K3 release
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("world", [1, 2, 3, 4, 5, 8])
+@pytest.mark.parametrize("n", [1, 7, 8, 4103, 1_048_579])
+def test_release_bit_exact(cuda, dtype, world, n):
+    g = torch.Generator().manual_seed(n + world)
+    srcs = [(torch.randn(n, generator=g) * 3.0).to(dtype) for _ in range(world)]
+    dsrc = [s.to(cuda) for s in srcs]
+    out = torch.full((n,), -1.0, device=cuda)
+    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    kernels.release(out, [t.data_ptr() for t in dsrc], n, dtype, 1.0 / 128, sc)
+    torch.cuda.synchronize()
+    wg, wsq, wbad = arith.release([_bits(s) for s in srcs], 1.0 / 128, _name(dtype))
+    assert np.array_equal(out.cpu().numpy(), wg)
+    assert sc[0].item() == pytest.approx(wsq, rel=1e-12)
+    assert sc[1].item() == 0.0 and not wbad
+
+
+def test_release_unaligned_sources_use_scalar_path(cuda):
+    n, world = 10_001, 3
+    g = torch.Generator().manual_seed(5)
+    base = [torch.randn(n + 1, generator=g).to(torch.bfloat16).to(cuda) for _ in range(world)]
+    out = torch.zeros(n, device=cuda)
+    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    kernels.release(out, [b.data_ptr() + 2 for b in base], n, torch.bfloat16, 1.0, sc)
+    wg, wsq, _ = arith.release([_bits(b)[1:] for b in base], 1.0)
+    assert np.array_equal(out.cpu().numpy(), wg)
+    assert sc[0].item() == pytest.approx(wsq, rel=1e-12)
+
+
+def test_release_accumulates_norm_and_flags_overflow(cuda):
+    n = 50_000
+    g = torch.Generator().manual_seed(9)
+    a = torch.randn(n, generator=g).to(torch.bfloat16)
+    b = torch.randn(n, generator=g).to(torch.bfloat16)
+    b[12345] = float("inf")
+    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    out = torch.zeros(n, device=cuda)
+    kernels.release(out, [a.to(cuda).data_ptr()], n, torch.bfloat16, 1.0, sc)
+    first = sc[0].item()
+    bb = b.to(cuda)
+    kernels.release(out, [bb.data_ptr()], n, torch.bfloat16, 1.0, sc)
+    torch.cuda.synchronize()
+    assert sc[1].item() == 1.0
+    assert first == pytest.approx(float((a.double() ** 2).sum()), rel=1e-12)
+    kernels.step_reset(sc)
+    torch.cuda.synchronize()
+    assert sc[0].item() == 0.0 and sc[1].item() == 0.0
+
+
+# ------------------------------------------------------------------ K4 Adam
+
+def _segments(cuda, sizes, seed, misalign=False):
+    rng = np.random.default_rng(seed)
+    host, dev = [], []
+    for n in sizes:
+        p = (rng.standard_normal(n) * 0.02).astype(np.float32)
+        m = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+        v = (rng.random(n) * 1e-6).astype(np.float32)
+        gg = (rng.standard_normal(n) * 0.05).astype(np.float32)
+        host.append([p, m, v, gg])
+        off = 1 if misalign else 0
+        ts = []
+        for a in (p, m, v, gg):
+            t = torch.zeros(n + off, device=cuda)
+            t[off:] = torch.from_numpy(a)
+            ts.append(t[off:])
+        p16 = torch.zeros(n + off, dtype=torch.bfloat16, device=cuda)[off:]
+        dev.append((*ts, p16, n))
+    return host, dev
+
+
+@pytest.mark.parametrize("misalign", [False, True])
+def test_adam_bit_exact_multi_segment_multi_step(cuda, misalign):
+    sizes = [1, 3, 4096, 4097, 12_288, 1_000_003]
+    host, dev = _segments(cuda, sizes, 11, misalign)
+    table = kernels.AdamTable(dev, cuda)
+    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    for step in range(1, 4):
+        sq = float(sum(np.dot(h[3].astype(np.float64), h[3]) for h in host))
+        sc[0] = sq
+        sc[1] = 0.0
+        kernels.adam(table, HP, step, sc, torch.bfloat16)
+        torch.cuda.synchronize()
+        coef = arith.clip_coef(sq, HP["max_norm"])
+        for h, d in zip(host, dev):
+            rp, rm, rv, r16 = arith.adamw(h[0], h[1], h[2], h[3], step, HP["lr"], HP["beta1"], HP["beta2"],
+                                          HP["eps"], HP["weight_decay"], coef)
+            assert np.array_equal(d[0].cpu().numpy(), rp)
+            assert np.array_equal(d[1].cpu().numpy(), rm)
+            assert np.array_equal(d[2].cpu().numpy(), rv)
+            assert np.array_equal(_bits(d[4]), r16)
+            h[0], h[1], h[2] = rp, rm, rv
+
+
+def test_adam_skips_on_overflow_and_restores_compute_copy(cuda):
+    host, dev = _segments(cuda, [5000, 77], 12)
+    for d in dev:
+        d[4].fill_(3.0)  # stale grads in the compute copy
+    table = kernels.AdamTable(dev, cuda)
+    sc = torch.tensor([1.0, 1.0, 0, 0], dtype=torch.float64, device=cuda)
+    kernels.adam(table, HP, 1, sc, torch.bfloat16)
+    torch.cuda.synchronize()
+    for h, d in zip(host, dev):
+        assert np.array_equal(d[0].cpu().numpy(), h[0])
+        assert np.array_equal(d[1].cpu().numpy(), h[1])
+        assert np.array_equal(d[2].cpu().numpy(), h[2])
+        assert np.array_equal(_bits(d[4]), arith.f32_to_bf16_bits(h[0]))
+
+
+def test_adam_f16_output(cuda):
+    host, dev = _segments(cuda, [9999], 13)
+    p16 = torch.zeros(9999, dtype=torch.float16, device=cuda)
+    dev = [(d[0], d[1], d[2], d[3], p16, d[5]) for d in dev]
+    table = kernels.AdamTable(dev, cuda)
+    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    hp = dict(HP, max_norm=0.0)
+    kernels.adam(table, hp, 2, sc, torch.float16)
+    h = host[0]
+    rp, _, _, r16 = arith.adamw(h[0], h[1], h[2], h[3], 2, HP["lr"], HP["beta1"], HP["beta2"], HP["eps"],
+                                HP["weight_decay"], np.float32(1.0), False, "f16")
+    assert np.array_equal(dev[0][0].cpu().numpy(), rp)
+    assert np.array_equal(p16.cpu().numpy().view(np.uint16), r16)
+
+
+def test_norm_finalize(cuda):
+    sc = torch.tensor([16.0, 0.0, 0, 0], dtype=torch.float64, device=cuda)
+    out = torch.zeros(3, dtype=torch.float64, device=cuda)
+    kernels.norm_finalize(sc, 1.0, out)
+    o = out.cpu().tolist()
+    assert o[0] == 4.0
+    assert o[1] == float(np.float32(1.0 / (4.0 + 1e-6)))
+    assert o[2] == 0.0
+
+
+# ------------------------------------------------------------------ K6 copies
+
+def test_offload_copies_round_trip(cuda):
+    n = 3_000_001
+    src = torch.randn(n).to(torch.bfloat16).pin_memory()
+    dev = torch.zeros(n, dtype=torch.bfloat16, device=cuda)
+    back = torch.zeros(n, dtype=torch.bfloat16).pin_memory()
+    side = torch.cuda.Stream()
+    kernels.copy_h2d(dev, src, stream=side)
+    kernels.copy_d2h(back, dev, stream=side)
+    side.synchronize()
+    assert torch.equal(back, src)
+
+
+def test_launch_counter_counts_kernels(cuda):
+    before = _lib.launch_count()
+    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    kernels.step_reset(sc)
+    kernels.step_reset(sc)
+    assert _lib.launch_count() - before == 2

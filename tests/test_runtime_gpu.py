@@ -1,0 +1,188 @@
+"""End-to-end runtime parity on a real GPU: a chunked GPT-2 step through
+ChunkManager / ChunkFetcher / HybridAdam against
+  * the oracle schedule (live fetch/release counters == simulate), and
+  * a plain reference step — standalone parameter tensors, the same per-node
+    recompute, and the CPU oracle's release + AdamW — bit-exact fp32 masters.
+Covers GPU-only plans, partial CPU offload, small rCache (evictions and
+re-gathers), fp16 with loss scaling and an injected overflow."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import arith, layout_ref as L
+from paper_2212_05339_b200 import gpt2
+from paper_2212_05339_b200.gpt2 import ElixirGPT2, GPT2Config
+from paper_2212_05339_b200.schedule import Plan
+
+pytestmark = pytest.mark.gpu
+
+CFG = GPT2Config(hidden=64, layers=4, heads=4, vocab=384, seq_len=32, batch=2)
+HP = dict(lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, max_norm=1.0)
+
+
+def _oracle_layout(cfg, C):
+    params, ops = L.gpt2_records(cfg.hidden, cfg.layers, cfg.vocab, cfg.seq_len)
+    _, seq = L.partition(params, ops)
+    chunks, where = L.pack(seq, C)
+    fwd, _, red = L.chunk_trace(L.coarsen(params, ops), where)
+    return chunks, where, fwd, red
+
+
+def _plans(cfg):
+    h = cfg.hidden
+    C = 4 * h * h + 3 * h * h // 2  # forces layers to straddle chunks
+    chunks, where, fwd, red = _oracle_layout(cfg, C)
+    n = len(chunks)
+    ws = max(len(s) for s in fwd)
+    return [
+        ("all-gpu-max", Plan(C, n, {c: "gpu" for c in range(n)})),
+        ("all-gpu-min", Plan(C, ws, {c: "gpu" for c in range(n)})),
+        ("offload-half", Plan(C, ws + 1, {c: ("cpu" if c % 2 else "gpu") for c in range(n)})),
+        ("offload-all", Plan(C, ws, {c: "cpu" for c in range(n)})),
+    ]
+
+
+def _batch(cfg, dev, seed):
+    g = torch.Generator(device=dev).manual_seed(seed)
+    t = torch.randint(0, cfg.vocab, (cfg.batch, cfg.seq_len + 1), generator=g, device=dev)
+    return t[:, :-1].contiguous(), t[:, 1:].contiguous()
+
+
+class ReferenceStep:
+    """Standalone tensors + the same node functions + the CPU oracle optimizer."""
+
+    def __init__(self, model: ElixirGPT2, init):
+        self.m = model
+        self.p16 = {k: v.clone() for k, v in init.items()}
+        self.master = {k: v.float().cpu().numpy().reshape(-1).copy() for k, v in init.items()}
+        self.mom = {k: np.zeros_like(v) for k, v in self.master.items()}
+        self.vel = {k: np.zeros_like(v) for k, v in self.master.items()}
+        self.t = 0
+
+    def step(self, tokens, targets, scale=1.0):
+        m = self.m
+        K = m.K
+
+        def params(i):
+            ps = [self.p16[p] for p in m.node_params[i]]
+            if i in (0, K - 1):
+                ps.append(self.p16["wte"])
+            return ps
+
+        acts, x = [], None
+        with torch.no_grad():
+            for i in range(K):
+                acts.append(x)
+                x = m._run_node(i, x, tokens, targets, params(i))
+        loss = x
+        grad = torch.full((), scale, dtype=torch.float32, device=tokens.device)
+        grads = {}
+        for i in reversed(range(K)):
+            ps = [p.detach().requires_grad_(True) for p in params(i)]
+            with torch.enable_grad():
+                xin = None if i == 0 else acts[i].detach().requires_grad_(True)
+                out = m._run_node(i, xin, tokens, targets, ps)
+                gs = torch.autograd.grad(out, ([xin] if i else []) + ps, grad_outputs=grad)
+            if i:
+                grad, gs = gs[0], gs[1:]
+            for pid, g in zip(m.node_params[i], gs):
+                grads[pid] = g
+            if i in (0, K - 1):
+                grads["wte"] = gs[-1] if "wte" not in grads else grads["wte"] + gs[-1]
+        # oracle: release (world 1) + norm + AdamW
+        rel, sq, bad = {}, 0.0, False
+        name = "bf16" if m.manager.dtype == torch.bfloat16 else "f16"
+        for pid, g in grads.items():
+            bits = g.detach().reshape(-1).cpu().view(torch.int16).numpy().view(np.uint16)
+            r, s, b = arith.release([bits], 1.0 / scale, name)
+            rel[pid], sq, bad = r, sq + s, bad or b
+        coef = arith.clip_coef(sq, HP["max_norm"])
+        t = self.t if bad else self.t + 1
+        for pid in grads:
+            p, mm, vv, p16 = arith.adamw(self.master[pid], self.mom[pid], self.vel[pid], rel[pid], max(t, 1),
+                                         HP["lr"], HP["betas"][0], HP["betas"][1], HP["eps"], HP["weight_decay"],
+                                         coef, bad, name)
+            self.master[pid], self.mom[pid], self.vel[pid] = p, mm, vv
+            t16 = torch.from_numpy(p16.view(np.int16)).view(self.p16[pid].dtype).view(self.p16[pid].shape)
+            self.p16[pid] = t16.to(tokens.device)
+        self.t = t
+        return loss, bad
+
+
+def _masters(model):
+    out = model.manager.master_params()
+    sp = model.manager.shared["wte"]
+    out["wte"] = sp.p32[:sp.numel].clone()
+    return {k: v.float().cpu().numpy().reshape(-1) for k, v in out.items()}
+
+
+@pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min", "offload-half", "offload-all"])
+def test_counters_equal_simulate(cuda, plan_name):
+    plan = dict(_plans(CFG))[plan_name]
+    model = ElixirGPT2(CFG, plan, device=cuda, **HP)
+    tok, tgt = _batch(CFG, cuda, 0)
+    model.train_step(tok, tgt)
+    torch.cuda.synchronize()
+    chunks, where, fwd, red = _oracle_layout(CFG, plan.chunk_length)
+    cpu = {c for c, d in plan.chunk_homes.items() if d.value == "cpu"}
+    want, _ = L.simulate(fwd, plan.n_block, cpu, red)
+    live = model.fetcher.counters()
+    for k in ("gather_ops", "replaced_ops", "reduce_ops", "c2g_units", "g2c_units"):
+        assert live[k] == want[k], (k, live, want)
+    assert live["peak_rcache_blocks"] == want["peak"]
+
+
+@pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min", "offload-half", "offload-all"])
+def test_step_parity_bit_exact(cuda, plan_name):
+    plan = dict(_plans(CFG))[plan_name]
+    init = gpt2.init_params(CFG, cuda, seed=5)
+    model = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
+    ref = ReferenceStep(model, init)
+    for s in range(3):
+        tok, tgt = _batch(CFG, cuda, s)
+        lo = model.train_step(tok, tgt)
+        lr_, _ = ref.step(tok, tgt)
+        torch.cuda.synchronize()
+        assert lo.item() == lr_.item(), (s, lo.item(), lr_.item())
+        got = _masters(model)
+        for pid, want in ref.master.items():
+            assert np.array_equal(got[pid], want), (s, pid, np.abs(got[pid] - want).max())
+
+
+def test_fp16_loss_scale_and_overflow_skip(cuda):
+    plan = dict(_plans(CFG))["offload-half"]
+    init = gpt2.init_params(CFG, cuda, seed=6, dtype=torch.float16)
+    model = ElixirGPT2(CFG, plan, device=cuda, dtype=torch.float16, loss_scale=1024.0,
+                       init={k: v.clone() for k, v in init.items()}, **HP)
+    ref = ReferenceStep(model, init)
+    tok, tgt = _batch(CFG, cuda, 1)
+    model.train_step(tok, tgt)
+    ref.step(tok, tgt, scale=1024.0)
+    # inject an overflow: an absurd loss scale makes the fp16 grads overflow
+    model.scaler.scale = 2.0 ** 60
+    before = _masters(model)
+    model.train_step(tok, tgt)
+    torch.cuda.synchronize()
+    assert model.optimizer.last["found_inf"]
+    after = _masters(model)
+    for k in before:
+        assert np.array_equal(before[k], after[k])
+    # the compute copies were restored from the masters (grads overwrote them)
+    model.scaler.scale = 1024.0
+    lo = model.train_step(tok, tgt)
+    lr_, _ = ref.step(tok, tgt, scale=1024.0)
+    assert lo.item() == lr_.item()
+    got = _masters(model)
+    for pid, want in ref.master.items():
+        assert np.array_equal(got[pid], want), pid
+
+
+def test_loss_decreases_on_fixed_batch(cuda):
+    plan = dict(_plans(CFG))["all-gpu-min"]
+    model = ElixirGPT2(CFG, plan, device=cuda, **HP)
+    tok, tgt = _batch(CFG, cuda, 3)
+    losses = [model.train_step(tok, tgt).item() for _ in range(8)]
+    assert losses[-1] < losses[0] - 0.05, losses
