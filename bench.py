@@ -1,0 +1,457 @@
+"""Benchmark: chunked GPT-2 1.3B training step (BASELINE.json configs[1]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--model gpt2-1.3b] [--sweep]
+
+One process per GPU (torchrun for N > 1, NCCL). Each rank trains GPT-2 with
+a per-rank micro-batch of 8 x 1024 synthetic tokens (weak scaling) through the
+Elixir chunk runtime with the reference planner's plan for N GPUs
+(plans/<model>_n<N>.json, made by offplan.build_plan). Prints ONE JSON line
+(rank 0): samples/s (whole job), the chunk-Adam roofline, per-kernel rates,
+the end-to-end rate through the public API with host buffers, the CPU
+baseline, clocks and the number of our kernel launches.
+
+--impl reference times the CPU path (oracle port: torch-CPU GPT-2 math + the
+C oracle's release/AdamW) on host cores, on a bounded sample, scaled to
+samples/s of the same workload.
+
+--sweep runs the standalone K2/K3/K4 kernels over chunk sizes 4-256 MB
+(BASELINE.json configs[4]) and prints one JSON line per size instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import torch
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "train step samples/sec (GPT-2 chunked, Elixir rCache) + chunk Adam HBM GB/s + fetch/RS bus GB/s"
+ADAM_BYTES_PER_ELEM = 30  # p32,m,v,g32 read (16) + p32,m,v write (12) + bf16 param write (2)
+
+
+def _peaks():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- distributed
+
+def _dist_setup(n_gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    return world, rank, local
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+# ---------------------------------------------------------------- CPU baseline
+
+def cpu_baseline(model_name: str, layers_sample: int = 1, threads: int | None = None):
+    """Oracle-port CPU training step on a bounded sample, scaled to samples/s.
+
+    Sample: ONE sequence (1024 tokens) through `layers_sample` transformer
+    layers (forward + AC recompute + backward, torch CPU fp32) plus the tied
+    lm_head/loss, and the C oracle's release + AdamW over those layers' chunk
+    elements. Scaled: per-layer time x L, optimizer time x (M / sampled
+    elements), giving seconds per sequence of the full model.
+    """
+    import numpy as np
+    from paper_2212_05339_b200.gpt2 import PRESETS, _block
+    import torch.nn.functional as F
+
+    cfg = PRESETS[model_name]
+    cores = len(os.sched_getaffinity(0))
+    threads = threads or cores
+    torch.set_num_threads(threads)
+    h, T, V = cfg.hidden, cfg.seq_len, cfg.vocab
+    g = torch.Generator().manual_seed(0)
+    layer_params = [
+        [torch.ones(h), torch.zeros(h), torch.randn(3 * h, h, generator=g) * 0.02, torch.zeros(3 * h),
+         torch.randn(h, h, generator=g) * 0.02, torch.zeros(h), torch.ones(h), torch.zeros(h),
+         torch.randn(4 * h, h, generator=g) * 0.02, torch.zeros(4 * h), torch.randn(h, 4 * h, generator=g) * 0.02,
+         torch.zeros(h)] for _ in range(layers_sample)]
+    wte = torch.randn(V, h, generator=g) * 0.02
+    x0 = torch.randn(1, T, h, generator=g)
+    tgt = torch.randint(0, V, (1, T), generator=g)
+
+    def layer_pass(ps, x):
+        with torch.no_grad():
+            _block(x, ps, cfg.heads)
+        q = [p.clone().requires_grad_(True) for p in ps]
+        xi = x.clone().requires_grad_(True)
+        out = _block(xi, q, cfg.heads)
+        gr = torch.autograd.grad(out, [xi] + q, torch.ones_like(out))
+        return gr[0]
+
+    t0 = time.perf_counter()
+    x = x0
+    for ps in layer_params:
+        layer_pass(ps, x)
+    t_layers = (time.perf_counter() - t0) / layers_sample
+    t0 = time.perf_counter()
+    w = wte.clone().requires_grad_(True)
+    xi = x0.clone().requires_grad_(True)
+    with torch.no_grad():
+        F.cross_entropy(F.linear(x0, wte).view(-1, V), tgt.view(-1))
+    loss = F.cross_entropy(F.linear(xi, w).view(-1, V), tgt.view(-1))
+    torch.autograd.grad(loss, [xi, w])
+    t_head = time.perf_counter() - t0
+
+    # optimizer: C oracle release (world 1) + AdamW over the sampled layers' elements
+    lib = ctypes.CDLL(str(ROOT / "oracle" / "_build" / "liboracle.so"))
+    lib.oracle_release_bf16.restype = ctypes.c_double
+    lib.oracle_release_bf16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_float, ctypes.c_void_p, ctypes.c_int]
+    lib.oracle_adamw_bf16.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_float,
+                                                             ctypes.c_int, ctypes.c_int]
+    n = layers_sample * (12 * h * h + 13 * h)
+    gb = np.zeros(n, np.uint16)
+    p = np.full(n, 0.01, np.float32)
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    g32 = np.zeros(n, np.float32)
+    p16 = np.zeros(n, np.uint16)
+    ptrs = (ctypes.c_void_p * 1)(gb.ctypes.data)
+    bad = ctypes.c_int(0)
+    k = np.array([1 - 1e-5, 0.1, 0.999, 0.001, 0.0316, -0.01, 1e-8], np.float32)
+    t0 = time.perf_counter()
+    lib.oracle_release_bf16(g32.ctypes.data, ptrs, 1, n, ctypes.c_float(1.0), ctypes.byref(bad), threads)
+    lib.oracle_adamw_bf16(p.ctypes.data, m.ctypes.data, v.ctypes.data, g32.ctypes.data, p16.ctypes.data, n,
+                          k.ctypes.data, ctypes.c_float(1.0), 0, threads)
+    t_opt = time.perf_counter() - t0
+    total = 12 * h * h * cfg.layers + 13 * h * cfg.layers + V * h + T * h + 2 * h
+    sec_per_seq = t_head + cfg.layers * t_layers + t_opt * total / n
+    return {
+        "value": 1.0 / sec_per_seq,
+        "unit": "samples/s",
+        "cores": threads,
+        "kind": "port",
+        "sample": (f"1 sequence x {T} tokens through {layers_sample} of {cfg.layers} layers + tied lm_head "
+                   f"(torch CPU fp32, fwd+recompute+bwd) and C-oracle release+AdamW over {n} elements; "
+                   f"scaled to the full {total}-parameter model"),
+        "seconds_measured": round(t_layers * layers_sample + t_head + t_opt, 3),
+        "breakdown_s_per_seq": {"layers": cfg.layers * t_layers, "head": t_head, "optimizer": t_opt * total / n},
+    }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(args.model)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    value = statistics.median(vals)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"{args.model} chunked training step (CPU oracle port)", "model": args.model,
+                   "seq_len": 1024, "per_rank_batch": 8},
+        "cpu_baseline": {**{k: cb[k] for k in ("kind", "cores", "sample")}, "value": value, "unit": "samples/s"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+# ---------------------------------------------------------------- GPU arm
+
+def run_ours(args):
+    from paper_2212_05339_b200 import _lib
+    from paper_2212_05339_b200.gpt2 import PRESETS, ElixirGPT2
+
+    world, rank, local = _dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
+    cfg = PRESETS[args.model]
+    plan_path = ROOT / "plans" / f"{args.model}_n{world}.json"
+    plan_text = plan_path.read_text()
+    model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234)
+    B, T = cfg.batch, cfg.seq_len
+    gen = torch.Generator(device=dev).manual_seed(1234 + rank)
+    ids = torch.randint(0, cfg.vocab, (B, T + 1), generator=gen, device=dev)
+    tok, tgt = ids[:, :-1].contiguous(), ids[:, 1:].contiguous()
+
+    for _ in range(args.warmup):
+        model.train_step(tok, tgt)
+    _barrier(world)
+
+    # ---- device-resident timed region
+    opt = model.optimizer
+    opt.time_adam = True
+    opt.adam_events.clear()
+    model.fetcher.time_release = True
+    model.fetcher.release_events.clear()
+    cur = torch.cuda.current_stream(dev)
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        _barrier(world)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cur)
+        for _ in range(args.steps):
+            model.train_step(tok, tgt)
+        e1.record(cur)
+        torch.cuda.synchronize(dev)
+    launches = _lib.launch_count() - l0
+    ms = e0.elapsed_time(e1)
+    ms = _max_over_ranks(ms, world)
+    adam_ms = [a.elapsed_time(b) for a, b in opt.adam_events]
+    rel = [(a.elapsed_time(b), n) for a, b, n in model.fetcher.release_events]
+    opt.time_adam = False
+    model.fetcher.time_release = False
+    loss = float(model.last_loss)
+
+    # ---- end to end through the public API with host buffers
+    host_ids = torch.randint(0, cfg.vocab, (B, T + 1), generator=torch.Generator().manual_seed(99 + rank)).pin_memory()
+    dev_ids = torch.empty_like(host_ids, device=dev)
+    loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+    _barrier(world)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(cur)
+    for _ in range(args.steps):
+        dev_ids.copy_(host_ids, non_blocking=True)
+        lo = model.train_step(dev_ids[:, :-1], dev_ids[:, 1:])
+        loss_host.copy_(lo.reshape(1), non_blocking=True)
+        cur.synchronize()
+    f1.record(cur)
+    torch.cuda.synchronize(dev)
+    e2e_ms = _max_over_ranks(f0.elapsed_time(f1), world)
+
+    if rank != 0:
+        return
+    peak, peak_src = _peaks()
+    adam_elems = opt.gpu_elements
+    adam_avg = statistics.mean(adam_ms) if adam_ms else float("nan")
+    adam_gbs = ADAM_BYTES_PER_ELEM * adam_elems / (adam_avg * 1e-3) / 1e9
+    rel_ms = sum(r for r, _ in rel) / max(1, args.steps)
+    rel_elems = sum(n for _, n in rel) / max(1, args.steps)
+    es = 2  # bf16
+    rel_local_bytes = rel_elems * (es * world + 4)
+    traffic = None
+    tp = ROOT / "profiles" / "adam_ncu_traffic.json"
+    if tp.exists():
+        try:
+            t = json.loads(tp.read_text())
+            if t.get("valid_elements") == adam_elems:
+                traffic = t["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
+    samples = world * B * args.steps
+    value = samples / (ms * 1e-3)
+    cpu = cpu_baseline(args.model) if (world == 1 and not args.no_cpu) else None
+    flops = model.flops_per_step()
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16",
+        "data": "synthetic (uniform tokens, N(0,0.02) init, seed 1234+rank)",
+        "config": {
+            "workload": f"{args.model} chunked training step, plan {plan_path.name} (offplan.build_plan)",
+            "model": args.model, "global_batch": world * B, "per_rank_batch": B, "seq_len": T,
+            "parallelism": f"elixir-chunk-dp{world}", "chunk_length": model.layout.chunk_length,
+            "n_chunks": model.layout.n_chunks, "n_block": model.manager.plan.n_block,
+            "l2": "working set (>20 GB of chunk/optimizer state per step) far exceeds the 126 MB L2; no flush needed",
+        },
+        "tflops_per_gpu": flops / (ms / args.steps * 1e-3) / 1e12,
+        "final_loss": loss,
+        "kernels": {
+            "chunk_adam": {"ms_per_launch": adam_avg, "valid_elements": adam_elems, "hbm_gbs": adam_gbs,
+                           "launches_timed": len(adam_ms)},
+            "release": {"ms_per_step": rel_ms, "elements_per_step": rel_elems,
+                        "local_hbm_gbs": rel_local_bytes / (rel_ms * 1e-3) / 1e9 if rel_ms else None,
+                        "bus_gbs": (None if world == 1 else
+                                    (world - 1) / world * 2 * rel_elems * world / (rel_ms * 1e-3) / 1e9)},
+            "fetch": {"note": "N=1: GPU-home chunk shards are used in place (zero-copy gathers)"
+                      if world == 1 else "NCCL all_gather_into_tensor on the comm stream"},
+        },
+        "roofline": {"bound": "hbm", "kernel": "elx_adam (K4)", "achieved": adam_gbs, "peak": peak,
+                     "peak_source": peak_src, "unit": "GB/s", "frac": adam_gbs / peak, "traffic": traffic,
+                     "algorithmic_bytes_per_launch": ADAM_BYTES_PER_ELEM * adam_elems},
+        "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s",
+                "h2d_bytes_per_step": host_ids.numel() * host_ids.element_size(),
+                "d2h_bytes_per_step": loss_host.numel() * loss_host.element_size(),
+                "api": "ElixirGPT2.train_step on tokens copied from pinned host memory, loss read back"},
+        "gpu_launches": launches,
+        "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- kernel sweep
+
+def run_sweep(args):
+    """configs[4]: K2 fetch / K3 release / K4 Adam over chunk sizes 4-256 MB.
+    One GPU: the N 'ranks' of fetch/release are N local buffers (HBM-bound
+    here; on NVLink the same kernels read peer-mapped pointers)."""
+    from paper_2212_05339_b200 import kernels
+    dev = torch.device("cuda", 0)
+    peak, src = _peaks()
+    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    out = []
+
+    def timeit(fn, reps=10):
+        ts = []
+        for i in range(reps + 3):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            torch.cuda.synchronize()
+            if i >= 3:
+                ts.append(a.elapsed_time(b))
+        return statistics.median(ts)
+
+    for mb in (4, 8, 16, 32, 64, 128, 256):
+        C = mb * 2 ** 20 // 2
+        for world in (1, 2, 4, 8):
+            S = -(-C // world)
+            S = -(-S // 8) * 8
+            shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(world)]
+            block = torch.empty(world * S, dtype=torch.bfloat16, device=dev)
+            g32 = torch.empty(S, device=dev)
+            sc = torch.zeros(4, dtype=torch.float64, device=dev)
+            t_f = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S))
+            t_r = timeit(lambda: kernels.release(g32, [s.data_ptr() for s in shards], S, torch.bfloat16, 1.0, sc))
+            p32, m, v = (torch.zeros(S, device=dev) for _ in range(3))
+            p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+            tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
+            sc.zero_()
+            hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=0.0)
+            t_a = timeit(lambda: kernels.adam(tab, hp, 1, sc, torch.bfloat16))
+            rec = {"chunk_mb": mb, "world": world, "shard_elems": S,
+                   "fetch": {"ms": t_f, "hbm_gbs": 2 * 2 * world * S / (t_f * 1e-3) / 1e9},
+                   "release": {"ms": t_r, "hbm_gbs": (2 * world * S + 4 * S) / (t_r * 1e-3) / 1e9},
+                   "adam": {"ms": t_a, "hbm_gbs": 30 * S / (t_a * 1e-3) / 1e9,
+                            "frac": 30 * S / (t_a * 1e-3) / 1e9 / peak}}
+            out.append(rec)
+            print(json.dumps(rec), flush=True)
+            del shards, block, g32, p32, m, v, p16
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--model", default="gpt2-1.3b")
+    ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    if args.warmup < 3 and not args.sweep and args.impl == "ours":
+        print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    elif args.sweep:
+        run_sweep(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -270,6 +270,8 @@ class ChunkFetcher:
         self.comm = comm_stream or torch.cuda.Stream(device=manager.device)
         self.prefetch = prefetch
         self.inv_scale = inv_scale
+        self.time_release = False     # bench: CUDA events around each release
+        self.release_events: list = []
         ev = self.sched.events
         W = 2 * self.n_fwd
         self.due = [[] for _ in range(W)]
@@ -398,6 +400,9 @@ class ChunkFetcher:
             self.live["g2c_units"] += 1
         with torch.cuda.stream(comm):
             comm.wait_event(grads_written)
+            if self.time_release:
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record(comm)
             if mgr.world == 1:
                 srcs = [storage.data_ptr()]
             else:
@@ -409,6 +414,9 @@ class ChunkFetcher:
             target = mgr.g32[r] if not cpu else mgr.stage32
             if n > 0:
                 kernels.release(target, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
+            if self.time_release:
+                t1.record(comm)
+                self.release_events.append((t0, t1, n))
             if cpu and n > 0:
                 kernels.copy_d2h(mgr.h_g32[r], mgr.stage32, n * 4, stream=comm)
                 self.bytes_moved["d2h"] += n * 4

@@ -59,7 +59,7 @@ def test_pack_is_bit_exact_gpt2_layout(cuda):
     from oracle import layout_ref as L
     params, ops = L.gpt2_records(64, 3, 128, 16)
     _, seq = L.partition(params, ops)
-    C = 16 * 64 * 4 + 999
+    C = 4 * 64 * 64 + 999
     chunks, _ = L.pack(seq, C)
     g = torch.Generator().manual_seed(1)
     vals = {pid: torch.randn(n, generator=g).to(torch.bfloat16) for pid, n in seq}
