@@ -257,7 +257,7 @@ def run_ours(args):
     world, rank, local = _dist_setup(args.gpus)
     dev = torch.device("cuda", local)
     cfg = PRESETS[args.model]
-    plan_path = ROOT / "plans" / f"{args.model}_n{world}.json"
+    plan_path = ROOT / "plans" / (args.plan.format(n=world) if args.plan else f"{args.model}_n{world}.json")
     plan_text = plan_path.read_text()
     model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234)
     B, T = cfg.batch, cfg.seq_len
@@ -332,6 +332,10 @@ def run_ours(args):
     samples = world * B * args.steps
     value = samples / (ms * 1e-3)
     cpu = cpu_baseline(args.model) if (world == 1 and not args.no_cpu) else None
+    homes = model.manager.homes
+    offload = {"cpu_home_chunks": len(model.manager.cpu_ids), "gpu_home_chunks": len(model.manager.gpu_ids),
+               "bytes_moved_per_step": {k: v for k, v in model.fetcher.bytes_moved.items()},
+               "sim_counters": model.fetcher.counters()}
     flops = model.flops_per_step()
     line = {
         "metric": METRIC,
@@ -372,6 +376,7 @@ def run_ours(args):
                 "h2d_bytes_per_step": host_ids.numel() * host_ids.element_size(),
                 "d2h_bytes_per_step": loss_host.numel() * loss_host.element_size(),
                 "api": "ElixirGPT2.train_step on tokens copied from pinned host memory, loss read back"},
+        "chunk_runtime": offload,
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
         "clocks": clk.summary(),
@@ -441,6 +446,8 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="gpt2-1.3b")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
+                    "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     args = ap.parse_args()
     if args.warmup < 3 and not args.sweep and args.impl == "ours":

@@ -12,6 +12,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 
 #include "elx_internal.h"
@@ -262,51 +263,64 @@ __device__ __forceinline__ void block_reduce_and_publish(double sq, int bad, dou
   }
 }
 
-// Vector path: each thread-step reduces 8 consecutive elements from every
-// source (one 16-byte load per rank), writes 32 bytes of fp32.
-template <typename T16, int kWorld>
+// Vector path: a thread-step reduces 4 consecutive elements from every source
+// (one 8-byte load per rank) and writes one 16-byte float4, so a warp's loads
+// AND stores are each fully contiguous (256 B / 512 B). kU steps per thread are
+// loaded before any is reduced: kU * world loads in flight per thread
+// (kWorld = 0: runtime world, one step at a time).
+template <typename T16, int kWorld, int kU>
 __global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict__ g, const PtrBatch src,
                                                               int world_rt, int64_t n, float inv_scale,
                                                               double* sc) {
+  constexpr int kR = kWorld > 0 ? kWorld : 1;
   const int world = kWorld > 0 ? kWorld : world_rt;
-  const int64_t nv = n >> 3;
+  const int64_t nv = n >> 2;
   double sq = 0.0;
   int bad = 0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nv; i += stride) {
-    float acc[8];
-    uint4 raw[kWorld > 0 ? kWorld : 1];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * kU;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kU + threadIdx.x; i0 < nv; i0 += stride) {
+    uint2 raw[kU][kR];
     if (kWorld > 0) {
 #pragma unroll
-      for (int r = 0; r < (kWorld > 0 ? kWorld : 1); ++r)
-        raw[r] = ld_plain(static_cast<const uint4*>(src.p[r]) + i);
+      for (int u = 0; u < kU; ++u) {
+        const int64_t i = i0 + (int64_t)u * blockDim.x;
 #pragma unroll
-      for (int r = 0; r < (kWorld > 0 ? kWorld : 1); ++r) {
-        const T16* h = reinterpret_cast<const T16*>(&raw[r]);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
-      }
-    } else {
-      for (int r = 0; r < world; ++r) {
-        const uint4 q = ld_plain(static_cast<const uint4*>(src.p[r]) + i);
-        const T16* h = reinterpret_cast<const T16*>(&q);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
+        for (int r = 0; r < kR; ++r)
+          if (i < nv) raw[u][r] = static_cast<const uint2*>(src.p[r])[i];
       }
     }
 #pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      acc[e] = __fmul_rn(acc[e], inv_scale);
-      bad |= !isfinite(acc[e]);
-      sq += (double)acc[e] * (double)acc[e];
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      if (i >= nv) break;
+      float acc[4];
+      if (kWorld > 0) {
+#pragma unroll
+        for (int r = 0; r < kR; ++r) {
+          const T16* h = reinterpret_cast<const T16*>(&raw[u][r]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
+        }
+      } else {
+        for (int r = 0; r < world; ++r) {
+          const uint2 q = static_cast<const uint2*>(src.p[r])[i];
+          const T16* h = reinterpret_cast<const T16*>(&q);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
+        }
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        acc[e] = __fmul_rn(acc[e], inv_scale);
+        bad |= !isfinite(acc[e]);
+        sq += (double)acc[e] * (double)acc[e];
+      }
+      reinterpret_cast<float4*>(g)[i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     }
-    float4* o = reinterpret_cast<float4*>(g + (i << 3));
-    o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-    o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
   }
-  // Scalar tail (n % 8 elements), handled by block 0.
+  // Scalar tail (n % 4 elements), handled by block 0.
   if (blockIdx.x == 0) {
-    for (int64_t i = (nv << 3) + threadIdx.x; i < n; i += blockDim.x) {
+    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) {
       float a = 0.f;
       for (int r = 0; r < world; ++r) {
         const float x = to_f32<T16>(static_cast<const T16*>(src.p[r])[i]);
@@ -346,19 +360,34 @@ template <typename T16>
 int run_release(float* g, const PtrBatch& pb, int64_t n, int world, float inv_scale, double* sc,
                 cudaStream_t st) {
   bool vec = aligned16(g);
-  for (int r = 0; r < world; ++r) vec = vec && aligned16(pb.p[r]);
-  const int64_t work = vec ? (n >> 3) : n;
-  const int grid = (int)std::max<int64_t>(
-      1, std::min<int64_t>((work + kRelThreads - 1) / kRelThreads, (int64_t)sm_count() * 8));
+  for (int r = 0; r < world; ++r) vec = vec && ((reinterpret_cast<uintptr_t>(pb.p[r]) & 7u) == 0);
+  auto go = [&](auto kern, int64_t work) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int grid = (int)std::max<int64_t>(
+        1, std::min<int64_t>((work + kRelThreads - 1) / kRelThreads, (int64_t)sm_count() * per_sm));
+    kern<<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc);
+  };
+  const int64_t nv = n >> 2;
   if (!vec) {
-    release_kernel_scalar<T16><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc);
+    go(release_kernel_scalar<T16>, n);
   } else {
+    static int variant = [] {
+      const char* e = getenv("ELX_REL_VARIANT");
+      return e ? atoi(e) : 0;
+    }();
     switch (world) {
-      case 1: release_kernel<T16, 1><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
-      case 2: release_kernel<T16, 2><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
-      case 4: release_kernel<T16, 4><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
-      case 8: release_kernel<T16, 8><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
-      default: release_kernel<T16, 0><<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc); break;
+      case 1:
+        // U=8 measured best at world 1 (profiles/r01_kernel_variants.md)
+        if (variant == 1) go(release_kernel<T16, 1, 2>, nv / 2);
+        else if (variant == 2) go(release_kernel<T16, 1, 4>, nv / 4);
+        else go(release_kernel<T16, 1, 8>, nv / 8);
+        break;
+      case 2: go(release_kernel<T16, 2, 2>, nv / 2); break;
+      case 4: go(release_kernel<T16, 4, 2>, nv / 2); break;
+      case 8: go(release_kernel<T16, 8, 1>, nv); break;
+      default: go(release_kernel<T16, 0, 1>, nv); break;
     }
   }
   return check_launch("elx_release");
@@ -412,10 +441,15 @@ __device__ __forceinline__ void store4(T16* p16, float a, float b, float c, floa
   *reinterpret_cast<uint2*>(p16) = pk.u;
 }
 
-template <typename T16>
-__global__ void __launch_bounds__(kAdamThreads) adam_kernel(const elx_adam_seg* __restrict__ segs, int nseg,
-                                                            int64_t ntiles, const AdamK k,
-                                                            const double* __restrict__ sc) {
+// One CTA iteration covers one ELX_ADAM_TILE tile as (4 / kU) passes of kU
+// float4 vectors per thread per stream; kU trades registers (occupancy)
+// against loads in flight. kMinBlocks is the __launch_bounds__ occupancy.
+template <typename T16, int kU, int kMinBlocks>
+__global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
+    adam_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k,
+                const double* __restrict__ sc) {
+  constexpr int kPasses = kAdamUnroll / kU;
+  static_assert(kPasses * kU == kAdamUnroll, "unroll must divide the tile");
   const bool skip = sc[1] != 0.0;
   const float coef = clip_coef(sc, k.max_norm);
   int s = 0;
@@ -433,36 +467,39 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(const elx_adam_seg* 
                      aligned16(v + base) && aligned16(g + base) &&
                      ((reinterpret_cast<uintptr_t>(p16 + base) & 7u) == 0);
     if (vec) {
-      float4 P[kAdamUnroll];
-      if (skip) {
+#pragma unroll 1
+      for (int pass = 0; pass < kPasses; ++pass) {
+        const int64_t j0 = (int64_t)pass * kU * kAdamThreads + threadIdx.x;
+        float4 P[kU];
+        if (skip) {
 #pragma unroll
-        for (int u = 0; u < kAdamUnroll; ++u)
-          P[u] = reinterpret_cast<const float4*>(p32 + base)[u * kAdamThreads + threadIdx.x];
+          for (int u = 0; u < kU; ++u) P[u] = reinterpret_cast<const float4*>(p32 + base)[j0 + u * kAdamThreads];
 #pragma unroll
-        for (int u = 0; u < kAdamUnroll; ++u)
-          store4<T16>(p16 + base + 4 * (u * kAdamThreads + threadIdx.x), P[u].x, P[u].y, P[u].z, P[u].w);
-        continue;
-      }
-      float4 M[kAdamUnroll], V[kAdamUnroll], G[kAdamUnroll];
+          for (int u = 0; u < kU; ++u)
+            store4<T16>(p16 + base + 4 * (j0 + u * kAdamThreads), P[u].x, P[u].y, P[u].z, P[u].w);
+          continue;
+        }
+        float4 M[kU], V[kU], G[kU];
 #pragma unroll
-      for (int u = 0; u < kAdamUnroll; ++u) {
-        const int64_t j = u * kAdamThreads + threadIdx.x;
-        P[u] = reinterpret_cast<const float4*>(p32 + base)[j];
-        M[u] = reinterpret_cast<const float4*>(m + base)[j];
-        V[u] = reinterpret_cast<const float4*>(v + base)[j];
-        G[u] = ld_stream_f4(reinterpret_cast<const float4*>(g + base) + j);
-      }
+        for (int u = 0; u < kU; ++u) {
+          const int64_t j = j0 + u * kAdamThreads;
+          P[u] = reinterpret_cast<const float4*>(p32 + base)[j];
+          M[u] = reinterpret_cast<const float4*>(m + base)[j];
+          V[u] = reinterpret_cast<const float4*>(v + base)[j];
+          G[u] = ld_stream_f4(reinterpret_cast<const float4*>(g + base) + j);
+        }
 #pragma unroll
-      for (int u = 0; u < kAdamUnroll; ++u) {
-        adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
-        adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
-        adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
-        adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
-        const int64_t j = u * kAdamThreads + threadIdx.x;
-        reinterpret_cast<float4*>(p32 + base)[j] = P[u];
-        reinterpret_cast<float4*>(m + base)[j] = M[u];
-        reinterpret_cast<float4*>(v + base)[j] = V[u];
-        store4<T16>(p16 + base + 4 * j, P[u].x, P[u].y, P[u].z, P[u].w);
+        for (int u = 0; u < kU; ++u) {
+          adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
+          adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
+          adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
+          adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
+          const int64_t j = j0 + u * kAdamThreads;
+          reinterpret_cast<float4*>(p32 + base)[j] = P[u];
+          reinterpret_cast<float4*>(m + base)[j] = M[u];
+          reinterpret_cast<float4*>(v + base)[j] = V[u];
+          store4<T16>(p16 + base + 4 * j, P[u].x, P[u].y, P[u].z, P[u].w);
+        }
       }
     } else {
       for (int64_t i = base + threadIdx.x; i < base + cnt; i += blockDim.x) {
@@ -477,6 +514,28 @@ __global__ void __launch_bounds__(kAdamThreads) adam_kernel(const elx_adam_seg* 
         p16[i] = from_f32<T16>(P);
       }
     }
+  }
+}
+
+// Variant table: (unroll, min blocks per SM). Default chosen from the
+// measured sweep (profiles/); ELX_ADAM_VARIANT overrides for experiments.
+template <typename T16>
+int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
+                cudaStream_t st) {
+  auto go = [&](auto kern) -> int {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAdamThreads, 0);
+    if (per_sm < 1) per_sm = 1;
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * per_sm);
+    kern<<<grid, kAdamThreads, 0, st>>>(segs, nseg, ntiles, k, sc);
+    return check_launch("elx_adam");
+  };
+  switch (variant) {
+    case 1: return go(adam_kernel<T16, 4, 2>);
+    case 2: return go(adam_kernel<T16, 4, 3>);
+    case 3: return go(adam_kernel<T16, 2, 4>);
+    case 4: return go(adam_kernel<T16, 1, 6>);
+    default: return go(adam_kernel<T16, 2, 3>);
   }
 }
 
@@ -590,15 +649,14 @@ int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const e
   k.neg_step = (float)(-(hp->lr / bc1));
   k.eps = (float)hp->eps;
   k.max_norm = hp->max_norm;
-  const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * 4);
+  static int variant = [] {
+    const char* e = getenv("ELX_ADAM_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
   cudaStream_t st = (cudaStream_t)stream;
-  if (hp->p16_dtype == ELX_BF16)
-    adam_kernel<__nv_bfloat16><<<grid, kAdamThreads, 0, st>>>(segs_dev, nseg, ntiles, k, step_scalars);
-  else if (hp->p16_dtype == ELX_F16)
-    adam_kernel<__half><<<grid, kAdamThreads, 0, st>>>(segs_dev, nseg, ntiles, k, step_scalars);
-  else
-    return elx::fail(ELX_ERR_VALIDATION, "p16_dtype must be bf16/f16");
-  return check_launch("elx_adam");
+  if (hp->p16_dtype == ELX_BF16) return launch_adam<__nv_bfloat16>(variant, segs_dev, nseg, ntiles, k, step_scalars, st);
+  if (hp->p16_dtype == ELX_F16) return launch_adam<__half>(variant, segs_dev, nseg, ntiles, k, step_scalars, st);
+  return elx::fail(ELX_ERR_VALIDATION, "p16_dtype must be bf16/f16");
 }
 
 int elx_norm_finalize(const double* step_scalars, double max_norm, double* out3, void* stream) {

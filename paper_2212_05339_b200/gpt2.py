@@ -43,6 +43,14 @@ class GPT2Config:
     def name(self) -> str:
         return f"gpt2-h{self.hidden}-l{self.layers}"
 
+    @property
+    def vocab_padded(self) -> int:
+        """Vocab rounded up to 64 rows for the lm_head GEMMs only: an odd
+        leading dimension (50257) forces cuBLAS onto align-1 kernels (3x
+        slower on the lm_head). The parameter keeps vocab*hidden elements;
+        the pad rows are zero and receive no update."""
+        return -(-self.vocab // 64) * 64
+
 
 PRESETS = {  # BASELINE.json configs; PAPER.md Table 7 shapes
     "gpt2-small": GPT2Config(768, 12, 12),
@@ -128,7 +136,8 @@ class ElixirGPT2:
         self.trace = build_chunk_trace(self.access, self.layout)
         self.shapes = param_shapes(cfg)
         self.manager = ChunkManager(self.profile, self.layout, plan, shapes=self.shapes, transport=transport,
-                                    device=self.device, dtype=dtype)
+                                    device=self.device, dtype=dtype,
+                                    shared_padded={"wte": (cfg.vocab_padded, cfg.hidden)})
         self.manager.load_params(init if init is not None else init_params(cfg, self.device, seed, dtype))
         if loss_scale is None:
             self.scaler = LossScaler(1.0, dynamic=False) if dtype == torch.bfloat16 else LossScaler(65536.0)
@@ -152,10 +161,10 @@ class ElixirGPT2:
             wpe, wte = params
             T = tokens.shape[1]
             return F.embedding(tokens, wte) + wpe[:T]
-        if i == self.K - 1:  # tied lm_head + loss
+        if i == self.K - 1:  # tied lm_head + loss (wte viewed with padded vocab rows)
             (wte,) = params
-            logits = F.linear(x, wte)
-            return F.cross_entropy(logits.float().view(-1, cfg.vocab), targets.reshape(-1))
+            logits = F.linear(x, wte)[..., :cfg.vocab]
+            return F.cross_entropy(logits.float().reshape(-1, cfg.vocab), targets.reshape(-1))
         if i == self.K - 2:  # ln_f
             w, b = params
             return F.layer_norm(x, (cfg.hidden,), w, b, 1e-5)
@@ -164,7 +173,7 @@ class ElixirGPT2:
     def _params_of(self, i: int):
         ps = [self.manager.param(pid) for pid in self.node_params[i]]
         if i == 0 or i == self.K - 1:
-            ps.append(self.manager.param("wte"))
+            ps.append(self.manager.padded_param("wte", (self.cfg.vocab_padded, self.cfg.hidden)))
         return ps
 
     # -------------------------------------------------------------- step
@@ -182,9 +191,10 @@ class ElixirGPT2:
             for i in range(K):
                 fx.enter(i)
                 acts.append(x)
-                x = self._run_node(i, x, tokens, targets, self._params_of(i))
+                if i < K - 1:  # the head's loss comes from its backward recompute
+                    x = self._run_node(i, x, tokens, targets, self._params_of(i))
                 fx.after_compute(i)
-        loss = x
+        loss = None
         grad = torch.full((), self.scaler.scale, dtype=torch.float32, device=self.device)
         wte_grad_set = False
         for j in range(K):
@@ -197,6 +207,8 @@ class ElixirGPT2:
                 out = self._run_node(i, xin, tokens, targets, params)
                 inputs = ([xin] if i > 0 else []) + params
                 grads = torch.autograd.grad(out, inputs, grad_outputs=grad)
+            if i == K - 1:
+                loss = out.detach()
             acts[i] = None
             if i > 0:
                 grad, pgrads = grads[0], grads[1:]
@@ -205,7 +217,7 @@ class ElixirGPT2:
             chunk_grads = pgrads[:len(self.node_params[i])]
             self._write_grads(i, chunk_grads)
             if i == 0 or i == K - 1:
-                wg = pgrads[-1].reshape(-1)
+                wg = pgrads[-1].reshape(-1)[:self.wte.numel]
                 buf = self.wte.grad[:self.wte.numel]
                 if wte_grad_set:
                     buf.add_(wg)

@@ -75,7 +75,8 @@ class ChunkManager:
     """
 
     def __init__(self, profile: Any, layout: Any, plan: Any, *, shapes: Mapping[str, Sequence[int]] | None = None,
-                 transport=None, device=None, dtype: torch.dtype = torch.bfloat16):
+                 transport=None, device=None, dtype: torch.dtype = torch.bfloat16,
+                 shared_padded: Mapping[str, Sequence[int]] | None = None):
         self.plan: Plan = as_plan(plan)
         self.layout = layout
         self.transport = transport or LocalTransport()
@@ -142,10 +143,15 @@ class ChunkManager:
         for pid in shared_ids:
             numel = next(p.numel for p in profile.parameters if p.id == pid)
             ssh = shard_length(numel, self.world)
-            full = torch.zeros(ssh * self.world, dtype=dtype, device=dev)
+            # The compute copy may be over-allocated so the model can view it
+            # with padded rows (e.g. vocab rounded up for aligned GEMMs); the
+            # pad is never written (Adam touches valid elements only).
+            pad_shape = tuple(shared_padded[pid]) if shared_padded and pid in shared_padded else None
+            full_len = max(ssh * self.world, math.prod(pad_shape) if pad_shape else 0)
+            full = torch.zeros(full_len, dtype=dtype, device=dev)
             p16 = full[self.rank * ssh:(self.rank + 1) * ssh] if self.world == 1 else torch.zeros(ssh, dtype=dtype, device=dev)
             self.shared[pid] = _SharedParam(
-                pid, numel, self.shapes[pid], ssh, full, torch.zeros_like(full), p16,
+                pid, numel, self.shapes[pid], ssh, full, torch.zeros(ssh * self.world, dtype=dtype, device=dev), p16,
                 torch.zeros(ssh, dtype=f32, device=dev), torch.zeros(ssh, dtype=f32, device=dev),
                 torch.zeros(ssh, dtype=f32, device=dev), torch.zeros(ssh, dtype=f32, device=dev))
         # step scalars: [0] sum g^2, [1] overflow flag (elx_release / elx_adam)
@@ -235,6 +241,14 @@ class ChunkManager:
         if sp is not None:
             return sp.full[:sp.numel].view(sp.shape)
         raise InfeasibleCacheError(f"parameter '{pid}' is not resident (its chunk was not fetched)")
+
+    def padded_param(self, pid: str, shape: Sequence[int]) -> torch.Tensor:
+        """A shared parameter viewed with zero padding (see shared_padded)."""
+        sp = self.shared[pid]
+        n = math.prod(shape)
+        if n > sp.full.numel():
+            raise ValidationError(f"padded view {tuple(shape)} exceeds the allocation of '{pid}'")
+        return sp.full[:n].view(tuple(shape))
 
     # ------------------------------------------------------------ export
     def master_params(self) -> dict[str, torch.Tensor]:
@@ -509,7 +523,7 @@ class HybridAdam:
             kernels.cpu_adam(self.cpu_segs, self.hp, kstep, (sq, inf_flag), m.dtype, self.cpu_threads)
         if m.world > 1:
             for sp in m.shared.values():
-                m.transport.gather(sp.full, sp.p16)
+                m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
         kernels.step_reset(m.step_scalars, stream=cur)
         if not found_inf:
             self.step_count = step

@@ -19,7 +19,7 @@ from paper_2212_05339_b200.schedule import Plan
 
 pytestmark = pytest.mark.gpu
 
-CFG = GPT2Config(hidden=64, layers=4, heads=4, vocab=384, seq_len=32, batch=2)
+CFG = GPT2Config(hidden=64, layers=4, heads=4, vocab=389, seq_len=32, batch=2)  # odd vocab: padded view
 HP = dict(lr=1e-3, betas=(0.9, 0.999), eps=1e-8, weight_decay=0.01, max_norm=1.0)
 
 
@@ -66,10 +66,14 @@ class ReferenceStep:
         m = self.m
         K = m.K
 
-        def params(i):
+        cfg = m.cfg
+        wpad = torch.zeros(cfg.vocab_padded, cfg.hidden, dtype=self.p16["wte"].dtype, device=tokens.device)
+        wpad[:cfg.vocab] = self.p16["wte"]
+
+        def params(i):  # same padded-vocab view of wte as the runtime uses
             ps = [self.p16[p] for p in m.node_params[i]]
             if i in (0, K - 1):
-                ps.append(self.p16["wte"])
+                ps.append(wpad)
             return ps
 
         acts, x = [], None
@@ -91,7 +95,8 @@ class ReferenceStep:
             for pid, g in zip(m.node_params[i], gs):
                 grads[pid] = g
             if i in (0, K - 1):
-                grads["wte"] = gs[-1] if "wte" not in grads else grads["wte"] + gs[-1]
+                gw = gs[-1][:cfg.vocab]
+                grads["wte"] = gw if "wte" not in grads else grads["wte"] + gw
         # oracle: release (world 1) + norm + AdamW
         rel, sq, bad = {}, 0.0, False
         name = "bf16" if m.manager.dtype == torch.bfloat16 else "f16"
