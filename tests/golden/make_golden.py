@@ -205,8 +205,13 @@ def make_adamw():
 
 def make_plans(ref):
     PLANS.mkdir(exist_ok=True)
-    hw = b200_placeholder_hw(ref)
-    (PLANS / "hardware_b200_placeholder.json").write_text(ref.serialize_hardware_profile(hw))
+    measured = PLANS / "hardware_b200_measured.json"
+    if measured.exists():  # written by scripts/profile_hw.py on the B200 box (§8f row 2)
+        hw = ref.load_hardware_profile(measured.read_text())
+        print("planning with", measured.name)
+    else:
+        hw = b200_placeholder_hw(ref)
+        (PLANS / "hardware_b200_placeholder.json").write_text(ref.serialize_hardware_profile(hw))
 
     def hw_n(n):
         return ref.HardwareProfile(n, hw.gpu_capacity_bytes, {k: hw.rates(k) for k in range(1, n + 1)})
