@@ -184,7 +184,7 @@ class ElixirGPT2:
         fx, mgr = self.fetcher, self.manager
         K = self.K
         fx.inv_scale = 1.0 / self.scaler.scale
-        fx.begin_step()
+        fx.begin_step(after=self.optimizer.done_event)
         acts = []
         x = None
         with torch.no_grad():

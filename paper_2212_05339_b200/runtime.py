@@ -118,8 +118,13 @@ class ChunkManager:
         dev, S = self.device, self.S
         G, H = len(self.gpu_ids), len(self.cpu_ids)
         f32 = torch.float32
+        # In-kernel NVLink path: shards and rCache blocks live in symmetric
+        # memory so K2/K3 read peers' buffers directly (transport.alloc).
+        self.p2p = bool(getattr(self.transport, "p2p", False)) and self.world > 1
+        peer_alloc = (lambda shape: self.transport.alloc(shape, dtype, dev)) if self.p2p else \
+            (lambda shape: torch.zeros(shape, dtype=dtype, device=dev))
         # ---- GPU-home arenas
-        self.p16 = torch.zeros(G, S, dtype=dtype, device=dev)  # at N=1, S == P: the whole chunk
+        self.p16 = peer_alloc((G, S))  # at N=1, S == P: the whole chunk
         self.p32 = torch.zeros(G, S, dtype=f32, device=dev)
         self.m = torch.zeros(G, S, dtype=f32, device=dev)
         self.v = torch.zeros(G, S, dtype=f32, device=dev)
@@ -135,7 +140,10 @@ class ChunkManager:
         self.alias = self.world == 1
         need_blocks = self.world > 1 or H > 0
         nb = self.plan.n_block if need_blocks else 0
-        self.blocks = torch.zeros(nb, self.P, dtype=dtype, device=dev)
+        self.blocks = peer_alloc((nb, self.P))
+        # peer base pointers of the same tensors on every rank (P2P only)
+        self.peer_p16 = self.transport.peer_ptrs(self.p16) if self.p2p else None
+        self.peer_blocks = self.transport.peer_ptrs(self.blocks) if self.p2p else None
         self.recv = torch.zeros(self.P if self.world > 1 else 0, dtype=dtype, device=dev)
         self.stage32 = torch.zeros(S if H > 0 else 0, dtype=f32, device=dev)
         # ---- shared (multi-use) parameters: replicated copy + partitioned state
@@ -314,8 +322,16 @@ class ChunkFetcher:
         self.bytes_moved = dict(h2d=0, d2h=0, gather=0, scatter=0)
         self.pos = 0
 
-    def begin_step(self) -> None:
+    def begin_step(self, after: torch.cuda.Event | None = None) -> None:
+        """Start a walk. On the P2P path every rank must have finished its
+        previous optimizer step (which rewrote the shards peers will read)
+        before anyone fetches: one device barrier on the comm stream."""
         self._reset()
+        if self.mgr.p2p:
+            with torch.cuda.stream(self.comm):
+                if after is not None:
+                    self.comm.wait_event(after)
+                self.mgr.transport.device_barrier()
 
     # ------------------------------------------------------------ walk
     def enter(self, pos: int) -> None:
@@ -388,7 +404,12 @@ class ChunkFetcher:
             if victim >= 0 and victim in self.last_use:
                 comm.wait_event(self.last_use[victim])
             seg = block[mgr.rank * mgr.S:(mgr.rank + 1) * mgr.S]
-            if cpu:
+            if mgr.p2p and not cpu:
+                # K2 over NVLink: read every rank's shard of c straight from its HBM
+                es = block.element_size()
+                off = mgr.row[c] * mgr.S * es
+                kernels.fetch(block, [p + off for p in mgr.peer_p16], mgr.S, stream=comm)
+            elif cpu:
                 kernels.copy_h2d(seg, mgr.h_p16[mgr.row[c]], stream=comm)
                 self.bytes_moved["h2d"] += seg.numel() * seg.element_size()
                 if mgr.world > 1:
@@ -419,6 +440,15 @@ class ChunkFetcher:
                 t0.record(comm)
             if mgr.world == 1:
                 srcs = [storage.data_ptr()]
+            elif mgr.p2p:
+                # K3 over NVLink: once every rank's gradients are in its copy of
+                # block b, read segment `rank` of all of them in rank order.
+                b = self.block_of[c]
+                es = storage.element_size()
+                off = (b * mgr.P + mgr.rank * mgr.S) * es
+                mgr.transport.device_barrier()
+                srcs = [p + off for p in mgr.peer_blocks]
+                self.bytes_moved["scatter"] += (mgr.world - 1) * mgr.S * es
             else:
                 mgr.transport.scatter(mgr.recv, storage)
                 self.bytes_moved["scatter"] += (mgr.world - 1) * mgr.S * storage.element_size()
@@ -428,6 +458,8 @@ class ChunkFetcher:
             target = mgr.g32[r] if not cpu else mgr.stage32
             if n > 0:
                 kernels.release(target, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
+            if mgr.p2p:
+                mgr.transport.device_barrier()  # peers may reuse block b only after every rank read it
             if self.time_release:
                 t1.record(comm)
                 self.release_events.append((t0, t1, n))
@@ -491,6 +523,7 @@ class HybridAdam:
         self.last = dict(found_inf=False, grad_norm=0.0, skipped=0)
         self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         self.time_adam = False
+        self.done_event: torch.cuda.Event | None = None
 
     @property
     def gpu_elements(self) -> int:
@@ -525,6 +558,8 @@ class HybridAdam:
             for sp in m.shared.values():
                 m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
         kernels.step_reset(m.step_scalars, stream=cur)
+        self.done_event = torch.cuda.Event()
+        self.done_event.record(cur)
         if not found_inf:
             self.step_count = step
         self.last = dict(found_inf=found_inf, grad_norm=math.sqrt(sq) if math.isfinite(sq) else float("inf"),

@@ -66,7 +66,54 @@ class TorchDistTransport:
         dist.barrier(group=self.group)
 
 
-def make_transport(world_size: int):
+class SymmMemTransport(TorchDistTransport):
+    """In-kernel NVLink path: rCache blocks and GPU-home shards are allocated
+    in torch symmetric memory; K2 (fetch) and K3 (release) read peers' HBM
+    through the mapped pointers, ordered by device-side barriers on the comm
+    stream. Collectives not on that path (shared-parameter exchange, scalar
+    all-reduce, CPU-home segments) stay on NCCL."""
+
+    p2p = True
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        import torch.distributed._symmetric_memory as symm
+
+        self.symm = symm
+        self.handles = []
+        self._group = group if group is not None else dist.group.WORLD
+        try:
+            symm.enable_symm_mem_for_group(self._group.group_name)
+        except Exception:  # newer torch enables it implicitly
+            pass
+
+    def alloc(self, shape, dtype, device) -> torch.Tensor:
+        t = self.symm.empty(*shape, dtype=dtype, device=device)
+        t.zero_()
+        return t
+
+    def peer_ptrs(self, t: torch.Tensor) -> list[int]:
+        """Device pointers of `t`'s counterpart on every rank (rank order)."""
+        if t.numel() == 0:
+            return [0] * self.world
+        h = self.symm.rendezvous(t, self._group)
+        self.handles.append(h)
+        base = h.buffer_ptrs[self.rank]
+        off = t.data_ptr() - base
+        return [int(p) + off for p in h.buffer_ptrs]
+
+    def device_barrier(self) -> None:
+        """All ranks' comm streams reach this point before any continues."""
+        self.handles[0].barrier(channel=0)
+
+
+def make_transport(world_size: int, kind: str | None = None):
+    """kind: "nccl" (default) or "p2p" (env ELX_TRANSPORT)."""
+    import os
+
     if world_size == 1:
         return LocalTransport()
+    kind = kind or os.environ.get("ELX_TRANSPORT", "nccl")
+    if kind == "p2p":
+        return SymmMemTransport()
     return TorchDistTransport()

@@ -143,7 +143,29 @@ class LoopbackTransport:
         self.g.barrier.wait()
 
 
-def run_ranks(world: int, fn):
+class LoopbackP2PTransport(LoopbackTransport):
+    """Emulates the symmetric-memory path on one GPU: the 'peer pointers' are
+    the other rank-threads' tensors on the same device, and the device barrier
+    is a stream sync + host barrier (same ordering guarantee, blocking)."""
+
+    p2p = True
+
+    def alloc(self, shape, dtype, device):
+        return torch.zeros(shape, dtype=dtype, device=device)
+
+    def peer_ptrs(self, t):
+        if t.numel() == 0:
+            return [0] * self.world
+        ts = self._publish(t)
+        ptrs = [x.data_ptr() for x in ts]
+        self._done()
+        return ptrs
+
+    def device_barrier(self):
+        self._done()
+
+
+def run_ranks(world: int, fn, p2p: bool = False):
     """Run fn(rank, transport) in `world` threads; re-raise the first error."""
     group = LoopbackGroup(world)
     out, errs = [None] * world, []
@@ -151,7 +173,7 @@ def run_ranks(world: int, fn):
     def body(r):
         try:
             torch.cuda.set_device(0)
-            out[r] = fn(r, LoopbackTransport(group, r))
+            out[r] = fn(r, (LoopbackP2PTransport if p2p else LoopbackTransport)(group, r))
         except BaseException as exc:  # pragma: no cover - surfaced below
             errs.append(exc)
             group.barrier.abort()

@@ -5,7 +5,9 @@ fp32 masters must equal the oracle's (per-rank grads reduced in rank order in
 fp32, clip, AdamW) bit for bit, and every rank's live counters must equal
 simulate. Exercises sharding, rCache gathers with Belady victims and
 prefetch, the all-to-all + K3 release, the shared wte all-gather and the
-N-scalar all-reduce."""
+N-scalar all-reduce. The "p2p" variant runs the in-kernel NVLink path (K2
+reading peers' shards, K3 reading peers' rCache blocks) with the peers'
+buffers emulated by the other rank-threads' tensors on the same GPU."""
 
 from __future__ import annotations
 
@@ -68,9 +70,10 @@ def _rank_masters(model):
     return out
 
 
+@pytest.mark.parametrize("path", ["exchange", "p2p"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kind", ["rcache-max", "rcache-min", "offload"])
-def test_multirank_step_parity(cuda, world, kind):
+def test_multirank_step_parity(cuda, world, kind, path):
     plan, fwd, red = _plan(kind)
     init = gpt2.init_params(CFG, cuda, seed=11)
     cpu = {c for c, d in plan.chunk_homes.items() if d.value == "cpu"}
@@ -89,7 +92,9 @@ def test_multirank_step_parity(cuda, world, kind):
         live = model.fetcher.counters()
         return losses, _rank_masters(model), live, model
 
-    res = run_ranks(world, rank_fn)
+    res = run_ranks(world, rank_fn, p2p=(path == "p2p"))
+    if path == "p2p":
+        assert res[0][3].manager.p2p
     ref = ReferenceStep(res[0][3], init, HP)
     ref_losses = []
     for s in range(steps):
