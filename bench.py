@@ -259,7 +259,8 @@ def run_ours(args):
     cfg = PRESETS[args.model]
     plan_path = ROOT / "plans" / (args.plan.format(n=world) if args.plan else f"{args.model}_n{world}.json")
     plan_text = plan_path.read_text()
-    model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234)
+    from paper_2212_05339_b200.transport import make_transport
+    model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234, transport=make_transport(world, args.transport))
     B, T = cfg.batch, cfg.seq_len
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     ids = torch.randint(0, cfg.vocab, (B, T + 1), generator=gen, device=dev)
@@ -353,7 +354,7 @@ def run_ours(args):
         "config": {
             "workload": f"{args.model} chunked training step, plan {plan_path.name} (offplan.build_plan)",
             "model": args.model, "global_batch": world * B, "per_rank_batch": B, "seq_len": T,
-            "parallelism": f"elixir-chunk-dp{world}", "chunk_length": model.layout.chunk_length,
+            "parallelism": f"elixir-chunk-dp{world}", "transport": args.transport if world > 1 else "local", "chunk_length": model.layout.chunk_length,
             "n_chunks": model.layout.n_chunks, "n_block": model.manager.plan.n_block,
             "l2": "working set (>20 GB of chunk/optimizer state per step) far exceeds the 126 MB L2; no flush needed",
         },
@@ -367,7 +368,9 @@ def run_ours(args):
                         "bus_gbs": (None if world == 1 else
                                     (world - 1) / world * 2 * rel_elems * world / (rel_ms * 1e-3) / 1e9)},
             "fetch": {"note": "N=1: GPU-home chunk shards are used in place (zero-copy gathers)"
-                      if world == 1 else "NCCL all_gather_into_tensor on the comm stream"},
+                      if world == 1 else ("K2 reading peers' shards over NVLink (symmetric memory)"
+                                          if args.transport == "p2p" else
+                                          "NCCL all_gather_into_tensor on the comm stream")},
         },
         "roofline": {"bound": "hbm", "kernel": "elx_adam (K4)", "achieved": adam_gbs, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": adam_gbs / peak, "traffic": traffic,
@@ -449,6 +452,8 @@ def main():
     ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
                     "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--transport", choices=["nccl", "p2p"], default=os.environ.get("ELX_TRANSPORT", "nccl"),
+                    help="N>1 fetch/release path: NCCL collectives + K3, or in-kernel NVLink (symmetric memory)")
     args = ap.parse_args()
     if args.warmup < 3 and not args.sweep and args.impl == "ours":
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
