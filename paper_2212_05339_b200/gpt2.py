@@ -118,7 +118,8 @@ class ElixirGPT2:
     def __init__(self, cfg: GPT2Config, plan, *, device=None, dtype=torch.bfloat16, seed: int = 1234,
                  lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.01,
                  max_norm: float | None = 1.0, loss_scale: float | None = None, transport=None,
-                 prefetch: bool = True, cpu_threads: int | None = None, init: dict | None = None):
+                 prefetch: bool = True, cpu_threads: int | None = None, init: dict | None = None,
+                 overlap_update: bool = True):
         import torch.distributed as dist
 
         self.cfg = cfg
@@ -146,7 +147,8 @@ class ElixirGPT2:
         self.fetcher = ChunkFetcher(self.manager, self.trace, prefetch=prefetch,
                                     inv_scale=1.0 / self.scaler.scale)
         self.optimizer = HybridAdam(self.manager, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
-                                    max_norm=max_norm, cpu_threads=cpu_threads)
+                                    max_norm=max_norm, cpu_threads=cpu_threads, overlap=overlap_update)
+        self.fetcher.optimizer = self.optimizer
         # coarse node -> its chunk parameters, in declaration order
         order = {p.id: i for i, p in enumerate(self.profile.parameters)}
         self.node_params = [sorted(node, key=order.__getitem__) for node in self.access.coarse_ops]
@@ -173,6 +175,7 @@ class ElixirGPT2:
     def _params_of(self, i: int):
         ps = [self.manager.param(pid) for pid in self.node_params[i]]
         if i == 0 or i == self.K - 1:
+            self.optimizer.wait_gpu("wte", torch.cuda.current_stream(self.device))
             ps.append(self.manager.padded_param("wte", (self.cfg.vocab_padded, self.cfg.hidden)))
         return ps
 
@@ -185,6 +188,7 @@ class ElixirGPT2:
         K = self.K
         fx.inv_scale = 1.0 / self.scaler.scale
         fx.begin_step(after=self.optimizer.done_event)
+        self.optimizer.wait_gpu("wte", torch.cuda.current_stream(self.device))
         acts = []
         x = None
         with torch.no_grad():
@@ -243,6 +247,11 @@ class ElixirGPT2:
         for c, mem in by_chunk.items():
             st = self.manager.storage(c)
             kernels.chunk_pack(st, mem, used_len=st.numel())
+
+    def synchronize(self) -> None:
+        """Make the current stream wait for every outstanding update (end of
+        a timed region / before reading parameters)."""
+        self.optimizer.synchronize()
 
     # -------------------------------------------------------------- misc
     @property

@@ -29,6 +29,7 @@ from __future__ import annotations
 
 import math
 import os
+import threading
 from dataclasses import dataclass
 from typing import Any, Callable, Mapping, Sequence
 
@@ -294,6 +295,8 @@ class ChunkFetcher:
         self.inv_scale = inv_scale
         self.time_release = False     # bench: CUDA events around each release
         self.release_events: list = []
+        self.optimizer = None         # HybridAdam whose per-chunk updates gate our reads
+        self._fenced = False
         ev = self.sched.events
         W = 2 * self.n_fwd
         self.due = [[] for _ in range(W)]
@@ -321,6 +324,7 @@ class ChunkFetcher:
                          peak_rcache_blocks=0)
         self.bytes_moved = dict(h2d=0, d2h=0, gather=0, scatter=0)
         self.pos = 0
+        self._fenced = False
 
     def begin_step(self, after: torch.cuda.Event | None = None) -> None:
         """Start a walk. On the P2P path every rank must have finished its
@@ -343,12 +347,15 @@ class ChunkFetcher:
         for rec in self.early[pos]:  # prefetch for pos + 1
             self._gather(rec)
         cur = torch.cuda.current_stream(self.mgr.device)
+        opt = self.optimizer
         for c in self.walk[pos]:
             if c not in self.block_of:
                 raise InfeasibleCacheError(f"chunk {c} needed at position {pos} is not resident")
             ev = self.ready.pop(c, None)
             if ev is not None:
                 cur.wait_event(ev)
+            elif opt is not None and self.mgr.alias:
+                opt.wait_gpu(c, cur)  # N=1 in-place chunk: its own update must be done
         self.live["peak_rcache_blocks"] = max(self.live["peak_rcache_blocks"], len(self.block_of))
 
     def after_compute(self, pos: int) -> None:
@@ -400,9 +407,14 @@ class ChunkFetcher:
             return
         block = mgr.blocks[b]
         comm = self.comm
+        opt = self.optimizer
+        if cpu and opt is not None:
+            opt.wait_cpu(c)  # host shard rewritten by the CPU-home update
         with torch.cuda.stream(comm):
             if victim >= 0 and victim in self.last_use:
                 comm.wait_event(self.last_use[victim])
+            if not cpu and opt is not None:
+                opt.wait_gpu(c, comm)
             seg = block[mgr.rank * mgr.S:(mgr.rank + 1) * mgr.S]
             if mgr.p2p and not cpu:
                 # K2 over NVLink: read every rank's shard of c straight from its HBM
@@ -433,8 +445,14 @@ class ChunkFetcher:
         cpu = mgr.homes[c] is Device.CPU
         if cpu:
             self.live["g2c_units"] += 1
+        opt = self.optimizer
+        if cpu and opt is not None:
+            opt.wait_cpu(c)  # previous update still reading the host grad shard
         with torch.cuda.stream(comm):
             comm.wait_event(grads_written)
+            if not self._fenced and opt is not None and opt.done_event is not None:
+                comm.wait_event(opt.done_event)  # g32 / step scalars free again
+                self._fenced = True
             if self.time_release:
                 t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 t0.record(comm)
@@ -475,6 +493,10 @@ class ChunkFetcher:
         ev.record(torch.cuda.current_stream(mgr.device))
         with torch.cuda.stream(comm):
             comm.wait_event(ev)
+            opt = self.optimizer
+            if not self._fenced and opt is not None and opt.done_event is not None:
+                comm.wait_event(opt.done_event)
+                self._fenced = True
             if mgr.world == 1:
                 srcs = [sp.grad.data_ptr()]
             else:
@@ -492,43 +514,89 @@ class HybridAdam:
     """Chunk-wise fused mixed-precision AdamW: GPU-home shards on the device
     (K4, update rate v_g), CPU-home shards on host threads (elx_cpu_adam,
     rate v_c), with global grad-norm clipping and overflow skip
-    (rcache_sim.py:173-184; PAPER.md:107-113, :221-238)."""
+    (rcache_sim.py:173-184; PAPER.md:107-113, :221-238).
+
+    With ``overlap`` (default) the update is issued per chunk in forward-use
+    order — shared parameters first — on an optimizer stream, and the CPU-home
+    update runs on a host thread; the next step's fetch of chunk c waits only
+    for c's own update (events / host flags), so the update of later chunks
+    runs under the next forward's compute.
+    """
 
     def __init__(self, manager: ChunkManager, *, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
-                 weight_decay: float = 0.01, max_norm: float | None = 1.0, cpu_threads: int | None = None):
+                 weight_decay: float = 0.01, max_norm: float | None = 1.0, cpu_threads: int | None = None,
+                 overlap: bool = True):
         self.mgr = manager
         self.hp = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
                        max_norm=max_norm or 0.0)
         self.step_count = 0
         self.cpu_threads = cpu_threads or max(1, min(32, len(os.sched_getaffinity(0))))
-        segs = []
+        self.overlap = overlap
         m = manager
+        # groups in forward-use order: shared params (used by the first node), then chunks by id
+        self.groups: list[tuple[object, kernels.AdamTable]] = []
+        all_segs = []
+        for pid, sp in m.shared.items():
+            n = sp.valid(m.rank)
+            if n > 0:
+                seg = (sp.p32, sp.m, sp.v, sp.g32, sp.p16, n)
+                all_segs.append(seg)
+                self.groups.append((pid, kernels.AdamTable([seg], m.device)))
         for c in m.gpu_ids:
             r = m.row[c]
             n = m.valid(c)
             if n > 0:
-                segs.append((m.p32[r], m.m[r], m.v[r], m.g32[r], m.p16[r], n))
-        for sp in m.shared.values():
-            n = sp.valid(m.rank)
-            if n > 0:
-                segs.append((sp.p32, sp.m, sp.v, sp.g32, sp.p16, n))
-        self.table = kernels.AdamTable(segs, m.device)
-        self.cpu_segs = []
+                seg = (m.p32[r], m.m[r], m.v[r], m.g32[r], m.p16[r], n)
+                all_segs.append(seg)
+                self.groups.append((c, kernels.AdamTable([seg], m.device)))
+        self.table = kernels.AdamTable(all_segs, m.device)  # single-launch form (overlap=False)
+        self.cpu_segs = {}
         for c in m.cpu_ids:
             r = m.row[c]
             n = m.valid(c)
             if n > 0:
-                self.cpu_segs.append((m.h_p32[r], m.h_m[r], m.h_v[r], m.h_g32[r], m.h_p16[r], n))
+                self.cpu_segs[c] = (m.h_p32[r], m.h_m[r], m.h_v[r], m.h_g32[r], m.h_p16[r], n)
+        self.stream = torch.cuda.Stream(device=m.device) if overlap else None
         self._host_sc = torch.zeros(4, dtype=torch.float64, pin_memory=torch.cuda.is_available())
         self.last = dict(found_inf=False, grad_norm=0.0, skipped=0)
         self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         self.time_adam = False
         self.done_event: torch.cuda.Event | None = None
+        self.pending: dict[object, torch.cuda.Event] = {}     # key -> GPU update done
+        self.cpu_ready: dict[int, threading.Event] = {c: threading.Event() for c in self.cpu_segs}
+        for ev in self.cpu_ready.values():
+            ev.set()
+        self._cpu_thread: threading.Thread | None = None
+        self._cpu_error: BaseException | None = None
 
     @property
     def gpu_elements(self) -> int:
         return self.table.valid_elements
 
+    # ------------------------------------------------------------ waits used by the fetcher / model
+    def wait_gpu(self, key, stream: torch.cuda.Stream) -> None:
+        ev = self.pending.get(key)
+        if ev is not None:
+            stream.wait_event(ev)
+
+    def wait_cpu(self, c: int) -> None:
+        ev = self.cpu_ready.get(c)
+        if ev is not None and not ev.is_set():
+            ev.wait()
+        if self._cpu_error is not None:
+            raise self._cpu_error
+
+    def synchronize(self, stream: torch.cuda.Stream | None = None) -> None:
+        """Make `stream` (default: current) wait for every outstanding update."""
+        s = stream or torch.cuda.current_stream(self.mgr.device)
+        if self.done_event is not None:
+            s.wait_event(self.done_event)
+        if self._cpu_thread is not None:
+            self._cpu_thread.join()
+            if self._cpu_error is not None:
+                raise self._cpu_error
+
+    # ------------------------------------------------------------ step
     def step(self, releases_done: torch.cuda.Event) -> tuple[bool, float]:
         """All-reduce norm/overflow, then update every shard. Returns
         (found_inf, grad_norm) — one host sync per step (GradScaler also
@@ -540,31 +608,66 @@ class HybridAdam:
         if m.world > 1:
             m.transport.all_reduce_sum(m.step_scalars[:2])
         self._host_sc.copy_(m.step_scalars, non_blocking=True)
-        torch.cuda.current_stream(dev).synchronize()
+        cur.synchronize()
+        if self._cpu_thread is not None:
+            self._cpu_thread.join()
         sq, inf_flag = float(self._host_sc[0]), float(self._host_sc[1])
         found_inf = inf_flag != 0.0 or not math.isfinite(sq)
         step = self.step_count + (0 if found_inf else 1)
         kstep = max(step, 1)
+        opt = self.stream if self.overlap else cur
+        if opt is not cur:
+            opt.wait_stream(cur)
         if self.time_adam:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(cur)
-        kernels.adam(self.table, self.hp, kstep, m.step_scalars, m.dtype, stream=cur)
-        if self.time_adam:
-            e1.record(cur)
-            self.adam_events.append((e0, e1))
+            e0.record(opt)
+        self.pending = {}
+        with torch.cuda.stream(opt):
+            if self.overlap:
+                for key, table in self.groups:
+                    kernels.adam(table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt)
+                    if key in m.shared and m.world > 1:
+                        sp = m.shared[key]
+                        m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
+                    ev = torch.cuda.Event()
+                    ev.record(opt)
+                    self.pending[key] = ev
+            else:
+                kernels.adam(self.table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt)
+                if m.world > 1:
+                    for sp in m.shared.values():
+                        m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
+            if self.time_adam:
+                e1.record(opt)
+                self.adam_events.append((e0, e1))
+            kernels.step_reset(m.step_scalars, stream=opt)
+            self.done_event = torch.cuda.Event()
+            self.done_event.record(opt)
         if self.cpu_segs:
-            kernels.cpu_adam(self.cpu_segs, self.hp, kstep, (sq, inf_flag), m.dtype, self.cpu_threads)
-        if m.world > 1:
-            for sp in m.shared.values():
-                m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
-        kernels.step_reset(m.step_scalars, stream=cur)
-        self.done_event = torch.cuda.Event()
-        self.done_event.record(cur)
+            for ev in self.cpu_ready.values():
+                ev.clear()
+            args = (kstep, (sq, inf_flag))
+            if self.overlap:
+                self._cpu_thread = threading.Thread(target=self._cpu_update, args=args, daemon=True)
+                self._cpu_thread.start()
+            else:
+                self._cpu_update(*args)
         if not found_inf:
             self.step_count = step
         self.last = dict(found_inf=found_inf, grad_norm=math.sqrt(sq) if math.isfinite(sq) else float("inf"),
                          skipped=self.last["skipped"] + int(found_inf))
         return found_inf, self.last["grad_norm"]
+
+    def _cpu_update(self, kstep: int, scalars) -> None:
+        """CPU-home shards in forward order, flagging each chunk when done."""
+        try:
+            for c in sorted(self.cpu_segs):
+                kernels.cpu_adam([self.cpu_segs[c]], self.hp, kstep, scalars, self.mgr.dtype, self.cpu_threads)
+                self.cpu_ready[c].set()
+        except BaseException as exc:  # surfaced by wait_cpu / synchronize
+            self._cpu_error = exc
+            for ev in self.cpu_ready.values():
+                ev.set()
 
 
 class LossScaler:

@@ -70,10 +70,11 @@ def _rank_masters(model):
     return out
 
 
+@pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("path", ["exchange", "p2p"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kind", ["rcache-max", "rcache-min", "offload"])
-def test_multirank_step_parity(cuda, world, kind, path):
+def test_multirank_step_parity(cuda, world, kind, path, overlap):
     plan, fwd, red = _plan(kind)
     init = gpt2.init_params(CFG, cuda, seed=11)
     cpu = {c for c, d in plan.chunk_homes.items() if d.value == "cpu"}
@@ -81,13 +82,14 @@ def test_multirank_step_parity(cuda, world, kind, path):
     steps = 2
 
     def rank_fn(r, transport):
-        model = ElixirGPT2(CFG, plan, device=cuda, transport=transport,
+        model = ElixirGPT2(CFG, plan, device=cuda, transport=transport, overlap_update=overlap,
                            init={k: v.clone() for k, v in init.items()}, **HP)
         assert model.manager.S == shard_length(plan.chunk_length, world)
         losses = []
         for s in range(steps):
             tok, tgt = _batches(world, s, cuda)[r]
             losses.append(model.train_step(tok, tgt).item())
+        model.synchronize()
         torch.cuda.synchronize()
         live = model.fetcher.counters()
         return losses, _rank_masters(model), live, model

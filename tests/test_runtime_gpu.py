@@ -118,6 +118,8 @@ class ReferenceStep:
 
 
 def _masters(model):
+    model.synchronize()
+    torch.cuda.synchronize()
     out = model.manager.master_params()
     sp = model.manager.shared["wte"]
     out["wte"] = sp.p32[:sp.numel].clone()
@@ -140,11 +142,13 @@ def test_counters_equal_simulate(cuda, plan_name):
     assert live["peak_rcache_blocks"] == want["peak"]
 
 
+@pytest.mark.parametrize("overlap", [True, False])
 @pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min", "offload-half", "offload-all"])
-def test_step_parity_bit_exact(cuda, plan_name):
+def test_step_parity_bit_exact(cuda, plan_name, overlap):
     plan = dict(_plans(CFG))[plan_name]
     init = gpt2.init_params(CFG, cuda, seed=5)
-    model = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
+    model = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()},
+                       overlap_update=overlap, **HP)
     ref = ReferenceStep(model, init)
     for s in range(3):
         tok, tgt = _batch(CFG, cuda, s)
