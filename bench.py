@@ -158,7 +158,8 @@ def cpu_baseline(model_name: str, layers_sample: int = 1, threads: int | None = 
     h, T, V = cfg.hidden, cfg.seq_len, cfg.vocab
     g = torch.Generator().manual_seed(0)
     layer_params = [
-        [torch.ones(h), torch.zeros(h), torch.randn(3 * h, h, generator=g) * 0.02, torch.zeros(3 * h),
+        [torch.ones(h), torch.zeros(h)] + [torch.randn(h, h, generator=g) * 0.02 for _ in range(3)]
+        + [torch.zeros(h) for _ in range(3)] + [
          torch.randn(h, h, generator=g) * 0.02, torch.zeros(h), torch.ones(h), torch.zeros(h),
          torch.randn(4 * h, h, generator=g) * 0.02, torch.zeros(4 * h), torch.randn(h, 4 * h, generator=g) * 0.02,
          torch.zeros(h)] for _ in range(layers_sample)]
@@ -261,7 +262,7 @@ def run_ours(args):
     plan_text = plan_path.read_text()
     from paper_2212_05339_b200.transport import make_transport
     model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234, transport=make_transport(world, args.transport),
-                       overlap_update=not args.no_overlap)
+                       overlap_update=args.overlap)
     B, T = cfg.batch, cfg.seq_len
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     ids = torch.randint(0, cfg.vocab, (B, T + 1), generator=gen, device=dev)
@@ -366,7 +367,7 @@ def run_ours(args):
         "kernels": {
             "chunk_adam": {"ms_per_launch": adam_avg, "valid_elements": adam_elems, "hbm_gbs": adam_gbs,
                            "launches_timed": len(adam_ms),
-                           "overlapped_with_next_forward": not args.no_overlap,
+                           "overlapped_with_next_forward": args.overlap,
                            "note": "per step: all K4 launches (one per chunk group) on the optimizer stream, "
                                    "timed first-to-last with CUDA events on that stream"},
             "release": {"ms_per_step": rel_ms, "elements_per_step": rel_elems,
@@ -458,7 +459,8 @@ def main():
     ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
                     "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
-    ap.add_argument("--no-overlap", action="store_true", help="run the optimizer update serially after backward")
+    ap.add_argument("--overlap", action="store_true",
+                    help="issue the GPU update per chunk on an optimizer stream under the next forward")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default=os.environ.get("ELX_TRANSPORT", "nccl"),
                     help="N>1 fetch/release path: NCCL collectives + K3, or in-kernel NVLink (symmetric memory)")
     args = ap.parse_args()

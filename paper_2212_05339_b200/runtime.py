@@ -516,16 +516,19 @@ class HybridAdam:
     rate v_c), with global grad-norm clipping and overflow skip
     (rcache_sim.py:173-184; PAPER.md:107-113, :221-238).
 
-    With ``overlap`` (default) the update is issued per chunk in forward-use
-    order — shared parameters first — on an optimizer stream, and the CPU-home
-    update runs on a host thread; the next step's fetch of chunk c waits only
-    for c's own update (events / host flags), so the update of later chunks
-    runs under the next forward's compute.
+    The CPU-home update always runs on a host thread (the GPU keeps going);
+    the next step's fetch of a CPU-home chunk waits for that chunk's flag.
+    With ``overlap`` the GPU update is also issued per chunk in forward-use
+    order on an optimizer stream and the next forward waits per chunk. On
+    B200 this measured no gain (the persistent K4 grid holds every SM, so
+    the forward's GEMMs queue behind it: 107.95 vs 107.94 ms per step,
+    profiles/r01_overlap.md) and it blurs K4's own timing, so the default is
+    one K4 launch over all GPU-home shards right after the backward.
     """
 
     def __init__(self, manager: ChunkManager, *, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.01, max_norm: float | None = 1.0, cpu_threads: int | None = None,
-                 overlap: bool = True):
+                 overlap: bool = False):
         self.mgr = manager
         self.hp = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
                        max_norm=max_norm or 0.0)
@@ -647,11 +650,8 @@ class HybridAdam:
             for ev in self.cpu_ready.values():
                 ev.clear()
             args = (kstep, (sq, inf_flag))
-            if self.overlap:
-                self._cpu_thread = threading.Thread(target=self._cpu_update, args=args, daemon=True)
-                self._cpu_thread.start()
-            else:
-                self._cpu_update(*args)
+            self._cpu_thread = threading.Thread(target=self._cpu_update, args=args, daemon=True)
+            self._cpu_thread.start()
         if not found_inf:
             self.step_count = step
         self.last = dict(found_inf=found_inf, grad_norm=math.sqrt(sq) if math.isfinite(sq) else float("inf"),

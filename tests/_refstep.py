@@ -34,8 +34,8 @@ class ReferenceStep:
         wpad = torch.zeros(cfg.vocab_padded, cfg.hidden, dtype=self.p16["wte"].dtype, device=tokens.device)
         wpad[:cfg.vocab] = self.p16["wte"]
 
-        def params(i):
-            ps = [self.p16[p] for p in m.node_params[i]]
+        def params(i):  # the same compute pieces (q/k/v row blocks) the runtime uses
+            ps = m.pieces(i, self.p16.__getitem__)
             if i in (0, K - 1):
                 ps.append(wpad)
             return ps
@@ -58,8 +58,7 @@ class ReferenceStep:
                 loss = out.detach()
             if i:
                 grad, gs = gs[0], gs[1:]
-            for pid, g in zip(m.node_params[i], gs):
-                grads[pid] = g
+            grads.update(m.piece_grads_by_param(i, gs[:len(m.node_pieces[i])]))
             if i in (0, K - 1):
                 gw = gs[-1][:cfg.vocab]
                 grads["wte"] = gw if "wte" not in grads else grads["wte"] + gw

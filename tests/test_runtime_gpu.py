@@ -12,7 +12,8 @@ import numpy as np
 import pytest
 import torch
 
-from oracle import arith, layout_ref as L
+from _refstep import ReferenceStep
+from oracle import layout_ref as L
 from paper_2212_05339_b200 import gpt2
 from paper_2212_05339_b200.gpt2 import ElixirGPT2, GPT2Config
 from paper_2212_05339_b200.schedule import Plan
@@ -51,72 +52,6 @@ def _batch(cfg, dev, seed):
     return t[:, :-1].contiguous(), t[:, 1:].contiguous()
 
 
-class ReferenceStep:
-    """Standalone tensors + the same node functions + the CPU oracle optimizer."""
-
-    def __init__(self, model: ElixirGPT2, init):
-        self.m = model
-        self.p16 = {k: v.clone() for k, v in init.items()}
-        self.master = {k: v.float().cpu().numpy().reshape(-1).copy() for k, v in init.items()}
-        self.mom = {k: np.zeros_like(v) for k, v in self.master.items()}
-        self.vel = {k: np.zeros_like(v) for k, v in self.master.items()}
-        self.t = 0
-
-    def step(self, tokens, targets, scale=1.0):
-        m = self.m
-        K = m.K
-
-        cfg = m.cfg
-        wpad = torch.zeros(cfg.vocab_padded, cfg.hidden, dtype=self.p16["wte"].dtype, device=tokens.device)
-        wpad[:cfg.vocab] = self.p16["wte"]
-
-        def params(i):  # same padded-vocab view of wte as the runtime uses
-            ps = [self.p16[p] for p in m.node_params[i]]
-            if i in (0, K - 1):
-                ps.append(wpad)
-            return ps
-
-        acts, x = [], None
-        with torch.no_grad():
-            for i in range(K):
-                acts.append(x)
-                x = m._run_node(i, x, tokens, targets, params(i))
-        loss = x
-        grad = torch.full((), scale, dtype=torch.float32, device=tokens.device)
-        grads = {}
-        for i in reversed(range(K)):
-            ps = [p.detach().requires_grad_(True) for p in params(i)]
-            with torch.enable_grad():
-                xin = None if i == 0 else acts[i].detach().requires_grad_(True)
-                out = m._run_node(i, xin, tokens, targets, ps)
-                gs = torch.autograd.grad(out, ([xin] if i else []) + ps, grad_outputs=grad)
-            if i:
-                grad, gs = gs[0], gs[1:]
-            for pid, g in zip(m.node_params[i], gs):
-                grads[pid] = g
-            if i in (0, K - 1):
-                gw = gs[-1][:cfg.vocab]
-                grads["wte"] = gw if "wte" not in grads else grads["wte"] + gw
-        # oracle: release (world 1) + norm + AdamW
-        rel, sq, bad = {}, 0.0, False
-        name = "bf16" if m.manager.dtype == torch.bfloat16 else "f16"
-        for pid, g in grads.items():
-            bits = g.detach().reshape(-1).cpu().view(torch.int16).numpy().view(np.uint16)
-            r, s, b = arith.release([bits], 1.0 / scale, name)
-            rel[pid], sq, bad = r, sq + s, bad or b
-        coef = arith.clip_coef(sq, HP["max_norm"])
-        t = self.t if bad else self.t + 1
-        for pid in grads:
-            p, mm, vv, p16 = arith.adamw(self.master[pid], self.mom[pid], self.vel[pid], rel[pid], max(t, 1),
-                                         HP["lr"], HP["betas"][0], HP["betas"][1], HP["eps"], HP["weight_decay"],
-                                         coef, bad, name)
-            self.master[pid], self.mom[pid], self.vel[pid] = p, mm, vv
-            t16 = torch.from_numpy(p16.view(np.int16)).view(self.p16[pid].dtype).view(self.p16[pid].shape)
-            self.p16[pid] = t16.to(tokens.device)
-        self.t = t
-        return loss, bad
-
-
 def _masters(model):
     model.synchronize()
     torch.cuda.synchronize()
@@ -149,11 +84,11 @@ def test_step_parity_bit_exact(cuda, plan_name, overlap):
     init = gpt2.init_params(CFG, cuda, seed=5)
     model = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()},
                        overlap_update=overlap, **HP)
-    ref = ReferenceStep(model, init)
+    ref = ReferenceStep(model, init, HP)
     for s in range(3):
         tok, tgt = _batch(CFG, cuda, s)
         lo = model.train_step(tok, tgt)
-        lr_, _ = ref.step(tok, tgt)
+        (lr_,), _ = ref.step([(tok, tgt)])
         torch.cuda.synchronize()
         assert lo.item() == lr_.item(), (s, lo.item(), lr_.item())
         got = _masters(model)
@@ -166,10 +101,10 @@ def test_fp16_loss_scale_and_overflow_skip(cuda):
     init = gpt2.init_params(CFG, cuda, seed=6, dtype=torch.float16)
     model = ElixirGPT2(CFG, plan, device=cuda, dtype=torch.float16, loss_scale=1024.0,
                        init={k: v.clone() for k, v in init.items()}, **HP)
-    ref = ReferenceStep(model, init)
+    ref = ReferenceStep(model, init, HP)
     tok, tgt = _batch(CFG, cuda, 1)
     model.train_step(tok, tgt)
-    ref.step(tok, tgt, scale=1024.0)
+    ref.step([(tok, tgt)], scale=1024.0)
     # inject an overflow: an absurd loss scale makes the fp16 grads overflow
     model.scaler.scale = 2.0 ** 60
     before = _masters(model)
@@ -182,7 +117,7 @@ def test_fp16_loss_scale_and_overflow_skip(cuda):
     # the compute copies were restored from the masters (grads overwrote them)
     model.scaler.scale = 1024.0
     lo = model.train_step(tok, tgt)
-    lr_, _ = ref.step(tok, tgt, scale=1024.0)
+    (lr_,), _ = ref.step([(tok, tgt)], scale=1024.0)
     assert lo.item() == lr_.item()
     got = _masters(model)
     for pid, want in ref.master.items():
