@@ -3,21 +3,13 @@
 // update (the "hybrid optimizer") and must produce the same bits as
 // elx_adam, so this file is built with -ffp-contract=off and without
 // -ffast-math: every float operation below is one IEEE-754 rounding.
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 
 #include "elx_internal.h"
 
 namespace {
-
-inline uint16_t f32_to_bf16_rne(float x) {
-  uint32_t u;
-  std::memcpy(&u, &x, 4);
-  if ((u & 0x7f800000u) == 0x7f800000u && (u & 0x007fffffu)) return (uint16_t)((u >> 16) | 0x0040u);  // qNaN
-  const uint32_t lsb = (u >> 16) & 1u;
-  u += 0x7fffu + lsb;
-  return (uint16_t)(u >> 16);
-}
 
 // IEEE binary16 round-to-nearest-even from float32.
 inline uint16_t f32_to_f16_rne(float f) {
@@ -47,6 +39,47 @@ inline uint16_t f32_to_f16_rne(float f) {
   return (uint16_t)(sign | r);
 }
 
+struct HostK {
+  float coef, decay, omb1, b2, omb2, bc2s, neg_step, eps;
+};
+
+// The bf16 path is written branch-free so the compiler vectorises it; the
+// clones cover AVX-512 / AVX2 / baseline x86-64 hosts (the GPU box's CPU is
+// not known at build time). IEEE sqrt/div only (-fno-math-errno lets sqrtf
+// vectorise; -ffp-contract=off keeps each operation separately rounded).
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void adam_bf16_range(float* __restrict p32, float* __restrict m, float* __restrict v, const float* __restrict g,
+                     uint16_t* __restrict p16, int64_t n, HostK k) {
+  for (int64_t i = 0; i < n; ++i) {
+    const float G = g[i] * k.coef;
+    float P = p32[i] * k.decay;
+    const float Mo = m[i];
+    const float M = Mo + k.omb1 * (G - Mo);
+    const float V = v[i] * k.b2 + (k.omb2 * G) * G;
+    const float denom = std::sqrt(V) / k.bc2s + k.eps;
+    P = P + (k.neg_step * M) / denom;
+    p32[i] = P;
+    m[i] = M;
+    v[i] = V;
+    uint32_t u;
+    std::memcpy(&u, &P, 4);
+    const uint32_t rne = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    const uint32_t qnan = (u >> 16) | 0x40u;
+    p16[i] = (uint16_t)(((u & 0x7fffffffu) > 0x7f800000u) ? qnan : rne);
+  }
+}
+
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void restore_bf16_range(const float* __restrict p32, uint16_t* __restrict p16, int64_t n) {
+  for (int64_t i = 0; i < n; ++i) {
+    uint32_t u;
+    std::memcpy(&u, &p32[i], 4);
+    const uint32_t rne = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    const uint32_t qnan = (u >> 16) | 0x40u;
+    p16[i] = (uint16_t)(((u & 0x7fffffffu) > 0x7f800000u) ? qnan : rne);
+  }
+}
+
 }  // namespace
 
 extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_adam_hp* hp, int64_t step,
@@ -74,6 +107,8 @@ extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_ada
   const bool bf16 = hp->p16_dtype == ELX_BF16;
   if (threads < 1) threads = 1;
 
+  const HostK hk{coef, decay, omb1, b2, omb2, bc2s, neg_step, eps};
+  constexpr int64_t kBlock = 1 << 16;  // elements per OpenMP work item
   for (int32_t s = 0; s < nseg; ++s) {
     float* p32 = segs[s].p32;
     float* m = segs[s].m;
@@ -81,6 +116,18 @@ extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_ada
     const float* g = segs[s].g;
     uint16_t* p16 = static_cast<uint16_t*>(segs[s].p16);
     const int64_t n = segs[s].n;
+    const int64_t nb = (n + kBlock - 1) / kBlock;
+    if (bf16) {
+#pragma omp parallel for num_threads(threads) schedule(static)
+      for (int64_t b = 0; b < nb; ++b) {
+        const int64_t lo = b * kBlock, cnt = std::min(kBlock, n - lo);
+        if (skip)
+          restore_bf16_range(p32 + lo, p16 + lo, cnt);
+        else
+          adam_bf16_range(p32 + lo, m + lo, v + lo, g + lo, p16 + lo, cnt, hk);
+      }
+      continue;
+    }
 #pragma omp parallel for num_threads(threads) schedule(static)
     for (int64_t i = 0; i < n; ++i) {
       float P = p32[i];
@@ -96,7 +143,7 @@ extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_ada
         m[i] = M;
         v[i] = V;
       }
-      p16[i] = bf16 ? f32_to_bf16_rne(P) : f32_to_f16_rne(P);
+      p16[i] = f32_to_f16_rne(P);
     }
   }
   return ELX_OK;
