@@ -517,6 +517,195 @@ __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
   }
 }
 
+// ---------------------------------------------------------------- K4 (TMA)
+// Persistent, warp-specialised variant: one producer warp streams each
+// tile's four fp32 input arrays (p32, m, v, g; 4 x 8 KB) into a shared-memory
+// stage with cp.async.bulk (TMA bulk copies, SASS UBLKCP) completing on an
+// mbarrier; eight consumer warps update from shared memory and store the
+// results (p32, m, v fp32 + the compute-dtype parameter) with 128-bit
+// coalesced stores. kStages tiles are in flight per CTA, so DRAM reads never
+// wait on the arithmetic. Partial or misaligned tiles (segment tails) are
+// handled by the consumers straight from global memory.
+constexpr int kTmaTile = 2048;                 // elements per tile
+constexpr int kTmaConsumers = 256;             // 8 warps x 32 lanes; 8 elements each
+constexpr int kTmaThreads = kTmaConsumers + 32;
+constexpr int kTmaStageBytes = 4 * kTmaTile * 4;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct TileRef {
+  int seg;
+  int64_t base;
+  int64_t cnt;
+  bool tma;
+};
+
+// Tiles are enumerated as (segment-table tile of ELX_ADAM_TILE elements, sub-tile
+// of kTmaTile); producer and consumers walk the same sequence.
+constexpr int kTmaSub = ELX_ADAM_TILE / kTmaTile;
+static_assert(kTmaSub * kTmaTile == ELX_ADAM_TILE, "sub-tiling");
+
+__device__ __forceinline__ TileRef locate(const elx_adam_seg* segs, int nseg, int& s, int64_t t, int sub) {
+  while (s + 1 < nseg && segs[s + 1].tile0 <= t) ++s;
+  TileRef r;
+  r.seg = s;
+  r.base = (t - segs[s].tile0) * ELX_ADAM_TILE + (int64_t)sub * kTmaTile;
+  r.cnt = min((int64_t)kTmaTile, segs[s].n - r.base);
+  r.tma = r.cnt == kTmaTile && aligned16(segs[s].p32 + r.base) && aligned16(segs[s].m + r.base) &&
+          aligned16(segs[s].v + r.base) && aligned16(segs[s].g + r.base) &&
+          ((reinterpret_cast<uintptr_t>(static_cast<char*>(segs[s].p16) + 2 * r.base) & 7u) == 0);
+  return r;
+}
+
+template <typename T16, int kStages>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    adam_tma_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k,
+                    const double* __restrict__ sc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage_base = reinterpret_cast<float*>(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kTmaConsumers / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const bool skip = sc[1] != 0.0;
+  const float coef = clip_coef(sc, k.max_norm);
+
+  if (warp == kTmaConsumers / 32) {  // ---------------- producer warp
+    if (lane == 0) {
+      int s = 0;
+      int64_t q = 0;  // TMA tiles issued
+      for (int64_t tt = blockIdx.x; tt < ntiles * kTmaSub; tt += gridDim.x) {
+        const TileRef r = locate(segs, nseg, s, tt / kTmaSub, (int)(tt % kTmaSub));
+        if (!r.tma) continue;
+        const int st = (int)(q % kStages);
+        const uint32_t ph = (uint32_t)((q / kStages) & 1);
+        mbar_wait(&empty[st], ph ^ 1u);
+        float* dst = stage_base + (size_t)st * (kTmaStageBytes / 4);
+        mbar_expect_tx(&full[st], kTmaStageBytes);
+        const elx_adam_seg& sg = segs[r.seg];
+        tma_load_1d(dst, sg.p32 + r.base, kTmaTile * 4, &full[st]);
+        tma_load_1d(dst + kTmaTile, sg.m + r.base, kTmaTile * 4, &full[st]);
+        tma_load_1d(dst + 2 * kTmaTile, sg.v + r.base, kTmaTile * 4, &full[st]);
+        tma_load_1d(dst + 3 * kTmaTile, sg.g + r.base, kTmaTile * 4, &full[st]);
+        ++q;
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumer warps
+  int s = 0;
+  int64_t q = 0;
+  for (int64_t tt = blockIdx.x; tt < ntiles * kTmaSub; tt += gridDim.x) {
+    const TileRef r = locate(segs, nseg, s, tt / kTmaSub, (int)(tt % kTmaSub));
+    if (r.cnt <= 0) continue;
+    const elx_adam_seg& sg = segs[r.seg];
+    float* __restrict__ p32 = sg.p32 + r.base;
+    float* __restrict__ m = sg.m + r.base;
+    float* __restrict__ v = sg.v + r.base;
+    T16* __restrict__ p16 = static_cast<T16*>(sg.p16) + r.base;
+    if (!r.tma) {  // tail / misaligned tile: straight from global memory
+      const float* g = sg.g + r.base;
+      for (int64_t i = threadIdx.x; i < r.cnt; i += kTmaConsumers) {
+        float P = p32[i];
+        if (!skip) {
+          float M = m[i], V = v[i];
+          adam_elem(P, M, V, g[i], coef, k);
+          p32[i] = P;
+          m[i] = M;
+          v[i] = V;
+        }
+        p16[i] = from_f32<T16>(P);
+      }
+      continue;
+    }
+    const int st = (int)(q % kStages);
+    const uint32_t ph = (uint32_t)((q / kStages) & 1);
+    ++q;
+    mbar_wait(&full[st], ph);
+    const float* src = stage_base + (size_t)st * (kTmaStageBytes / 4);
+    float4 P[2], M[2], V[2], G[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = u * kTmaConsumers + threadIdx.x;  // float4 index within the tile
+      P[u] = reinterpret_cast<const float4*>(src)[j];
+      M[u] = reinterpret_cast<const float4*>(src + kTmaTile)[j];
+      V[u] = reinterpret_cast<const float4*>(src + 2 * kTmaTile)[j];
+      G[u] = reinterpret_cast<const float4*>(src + 3 * kTmaTile)[j];
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);  // stage may be refilled: operands are in registers
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = u * kTmaConsumers + threadIdx.x;
+      if (!skip) {
+        adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
+        adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
+        adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
+        adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
+        reinterpret_cast<float4*>(p32)[j] = P[u];
+        reinterpret_cast<float4*>(m)[j] = M[u];
+        reinterpret_cast<float4*>(v)[j] = V[u];
+      }
+      store4<T16>(p16 + 4 * j, P[u].x, P[u].y, P[u].z, P[u].w);
+    }
+  }
+}
+
+template <typename T16, int kStages>
+int launch_adam_tma(const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
+                    cudaStream_t st) {
+  const int smem = kStages * kTmaStageBytes;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(adam_tma_kernel<T16, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_tma_kernel<T16, kStages>, kTmaThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int grid = (int)std::min<int64_t>(ntiles * kTmaSub, (int64_t)sm_count() * per_sm);
+  adam_tma_kernel<T16, kStages><<<grid, kTmaThreads, smem, st>>>(segs, nseg, ntiles, k, sc);
+  return check_launch("elx_adam (tma)");
+}
+
 // Variant table: (unroll, min blocks per SM). Default chosen from the
 // measured sweep (profiles/); ELX_ADAM_VARIANT overrides for experiments.
 template <typename T16>
@@ -531,6 +720,9 @@ int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles,
     return check_launch("elx_adam");
   };
   switch (variant) {
+    case 5: return launch_adam_tma<T16, 4>(segs, nseg, ntiles, k, sc, st);
+    case 6: return launch_adam_tma<T16, 6>(segs, nseg, ntiles, k, sc, st);
+    case 7: return launch_adam_tma<T16, 3>(segs, nseg, ntiles, k, sc, st);
     case 1: return go(adam_kernel<T16, 4, 2>);
     case 2: return go(adam_kernel<T16, 4, 3>);
     case 3: return go(adam_kernel<T16, 2, 4>);

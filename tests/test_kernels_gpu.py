@@ -256,3 +256,60 @@ def test_launch_counter_counts_kernels(cuda):
     kernels.step_reset(sc)
     kernels.step_reset(sc)
     assert _lib.launch_count() - before == 2
+
+
+_VARIANT_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+from oracle import arith
+from paper_2212_05339_b200 import kernels
+dev = torch.device('cuda:0')
+rng = np.random.default_rng(21)
+sizes = [1, 3, 2048, 4096, 4097, 6143, 12288, 300_001]
+host, segs = [], []
+for n in sizes:
+    arrs = [(rng.standard_normal(n) * s).astype(np.float32) for s in (0.02, 1e-3, 1e-3, 0.05)]
+    arrs[2] = np.abs(arrs[2]) * 1e-3
+    host.append(arrs)
+    off = 1 if n == 4097 else 0   # one misaligned segment -> global-memory tile path
+    ts = []
+    for a in arrs:
+        t = torch.zeros(n + off, device=dev); t[off:] = torch.from_numpy(a); ts.append(t[off:])
+    segs.append((*ts, torch.zeros(n, dtype=torch.bfloat16, device=dev), n))
+tab = kernels.AdamTable(segs, dev)
+hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
+sc = torch.zeros(4, dtype=torch.float64, device=dev)
+for step in (1, 2):
+    sq = float(sum(np.dot(h[3].astype(np.float64), h[3]) for h in host))
+    sc[0] = sq
+    kernels.adam(tab, hp, step, sc, torch.bfloat16)
+    torch.cuda.synchronize()
+    coef = arith.clip_coef(sq, 1.0)
+    for h, d in zip(host, segs):
+        rp, rm, rv, r16 = arith.adamw(h[0], h[1], h[2], h[3], step, 1e-3, 0.9, 0.999, 1e-8, 0.01, coef)
+        assert np.array_equal(d[0].cpu().numpy(), rp) and np.array_equal(d[1].cpu().numpy(), rm)
+        assert np.array_equal(d[2].cpu().numpy(), rv)
+        assert np.array_equal(d[4].cpu().view(torch.int16).numpy().view(np.uint16), r16)
+        h[0], h[1], h[2] = rp, rm, rv
+sc[1] = 1.0
+kernels.adam(tab, hp, 3, sc, torch.bfloat16)
+torch.cuda.synchronize()
+for h, d in zip(host, segs):
+    assert np.array_equal(d[0].cpu().numpy(), h[0])
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("variant", [0, 1, 3, 5, 6, 7])
+def test_adam_variants_bit_exact(cuda, variant):
+    """Every K4 variant (incl. the TMA-staged ones, 5-7) is bit-exact vs the oracle."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    env = dict(os.environ, ELX_ADAM_VARIANT=str(variant))
+    out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
