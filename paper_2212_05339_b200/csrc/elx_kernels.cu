@@ -706,8 +706,9 @@ int launch_adam_tma(const elx_adam_seg* segs, int nseg, int64_t ntiles, const Ad
   return check_launch("elx_adam (tma)");
 }
 
-// Variant table: (unroll, min blocks per SM). Default chosen from the
-// measured sweep (profiles/); ELX_ADAM_VARIANT overrides for experiments.
+// Variant table: 0/7 TMA-staged (default), 5/6 TMA with 4/6 stages, 8 and 1-4
+// register-staged (unroll, min blocks per SM). Default chosen from the measured
+// sweep (profiles/r01_kernel_variants.md); ELX_ADAM_VARIANT overrides.
 template <typename T16>
 int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
                 cudaStream_t st) {
@@ -722,12 +723,13 @@ int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles,
   switch (variant) {
     case 5: return launch_adam_tma<T16, 4>(segs, nseg, ntiles, k, sc, st);
     case 6: return launch_adam_tma<T16, 6>(segs, nseg, ntiles, k, sc, st);
-    case 7: return launch_adam_tma<T16, 3>(segs, nseg, ntiles, k, sc, st);
+    case 8: return go(adam_kernel<T16, 2, 3>);
     case 1: return go(adam_kernel<T16, 4, 2>);
     case 2: return go(adam_kernel<T16, 4, 3>);
     case 3: return go(adam_kernel<T16, 2, 4>);
     case 4: return go(adam_kernel<T16, 1, 6>);
-    default: return go(adam_kernel<T16, 2, 3>);
+    default:  // 0 / 7: TMA-staged, 3 stages x 32 KB, 2 CTAs per SM (profiles/r01_kernel_variants.md)
+      return launch_adam_tma<T16, 3>(segs, nseg, ntiles, k, sc, st);
   }
 }
 
