@@ -369,6 +369,11 @@ class ChunkFetcher:
                 self._release(c, ev)
         self.pos = pos + 1
 
+    # names used by SURVEY.md §8b for the reference runtime's chunk-fetcher
+    def fetch(self, pos: int) -> None:
+        """Make the chunks of walk position `pos` resident (alias of enter)."""
+        self.enter(pos)
+
     def finish(self) -> torch.cuda.Event:
         """End of the walk: every release is enqueued; returns their event."""
         if self.pos != 2 * self.n_fwd:
@@ -599,15 +604,56 @@ class HybridAdam:
             if self._cpu_error is not None:
                 raise self._cpu_error
 
+    # ------------------------------------------------------------ checkpoint
+    def state_dict(self) -> dict:
+        """This rank's fp32 master / m / v shards (GPU-home, CPU-home, shared)
+        and the step count — the complete training state of the chunk path."""
+        self.synchronize()
+        torch.cuda.synchronize(self.mgr.device)
+        m = self.mgr
+        out = {"step": self.step_count, "world": m.world, "rank": m.rank, "chunk_length": m.C,
+               "gpu": {k: getattr(m, k).cpu().clone() for k in ("p32", "m", "v")},
+               "cpu": {k: getattr(m, "h_" + k).clone() for k in ("p32", "m", "v")},
+               "shared": {pid: {k: getattr(sp, k).cpu().clone() for k in ("p32", "m", "v")}
+                          for pid, sp in m.shared.items()}}
+        return out
+
+    def load_state_dict(self, state: dict) -> None:
+        """Restore masters/moments and rebuild every compute-dtype copy from
+        the masters (K4's skip path: p16 <- round(p32); host: elx_cpu_adam)."""
+        m = self.mgr
+        if state["world"] != m.world or state["rank"] != m.rank or state["chunk_length"] != m.C:
+            raise ValidationError("checkpoint was written for a different world/rank/chunk length")
+        self.synchronize()
+        for k in ("p32", "m", "v"):
+            getattr(m, k).copy_(state["gpu"][k])
+            getattr(m, "h_" + k).copy_(state["cpu"][k])
+            for pid, sp in m.shared.items():
+                getattr(sp, k).copy_(state["shared"][pid][k])
+        self.step_count = int(state["step"])
+        sc = torch.tensor([0.0, 1.0, 0.0, 0.0], dtype=torch.float64, device=m.device)  # "skip": restore only
+        kernels.adam(self.table, self.hp, max(1, self.step_count), sc, m.dtype)
+        if self.cpu_segs:
+            kernels.cpu_adam(list(self.cpu_segs.values()), self.hp, max(1, self.step_count), (0.0, 1.0), m.dtype,
+                             self.cpu_threads)
+        if m.world > 1:
+            for sp in m.shared.values():
+                m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
+        torch.cuda.synchronize(m.device)
+
     # ------------------------------------------------------------ step
-    def step(self, releases_done: torch.cuda.Event) -> tuple[bool, float]:
+    def step(self, releases_done: torch.cuda.Event | None = None) -> tuple[bool, float]:
         """All-reduce norm/overflow, then update every shard. Returns
         (found_inf, grad_norm) — one host sync per step (GradScaler also
-        reads found_inf on the host)."""
+        reads found_inf on the host). `releases_done` is the event
+        ChunkFetcher.finish() returns (None: synchronise the device)."""
         m = self.mgr
         dev = m.device
         cur = torch.cuda.current_stream(dev)
-        cur.wait_event(releases_done)
+        if releases_done is None:
+            torch.cuda.synchronize(dev)
+        else:
+            cur.wait_event(releases_done)
         if m.world > 1:
             m.transport.all_reduce_sum(m.step_scalars[:2])
         self._host_sc.copy_(m.step_scalars, non_blocking=True)

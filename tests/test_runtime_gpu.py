@@ -130,3 +130,23 @@ def test_loss_decreases_on_fixed_batch(cuda):
     tok, tgt = _batch(CFG, cuda, 3)
     losses = [model.train_step(tok, tgt).item() for _ in range(8)]
     assert losses[-1] < losses[0] - 0.05, losses
+
+
+def test_checkpoint_round_trip(cuda):
+    """state_dict / load_state_dict restore masters, moments, step and the
+    compute copies: a restored trainer continues bit-identically."""
+    plan = dict(_plans(CFG))["offload-half"]
+    init = gpt2.init_params(CFG, cuda, seed=8)
+    a = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
+    tok, tgt = _batch(CFG, cuda, 4)
+    a.train_step(tok, tgt)
+    a.train_step(tok, tgt)
+    st = a.optimizer.state_dict()
+    b = ElixirGPT2(CFG, plan, device=cuda, init=gpt2.init_params(CFG, cuda, seed=99), **HP)
+    b.optimizer.load_state_dict(st)
+    la = a.train_step(tok, tgt).item()
+    lb = b.train_step(tok, tgt).item()
+    assert la == lb
+    ma, mb = _masters(a), _masters(b)
+    for k in ma:
+        assert np.array_equal(ma[k], mb[k]), k
