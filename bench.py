@@ -38,7 +38,8 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "train step samples/sec (GPT-2 chunked, Elixir rCache) + chunk Adam HBM GB/s + fetch/RS bus GB/s"
-ADAM_BYTES_PER_ELEM = 30  # p32,m,v,g32 read (16) + p32,m,v write (12) + bf16 param write (2)
+# K4 algorithmic bytes per element: p32, m, v read + write (24) + gradient read (fp32 4, or the bf16
+# gradient in place at world 1: 2) + bf16 parameter write (2) -> 30 or 28 (HybridAdam.bytes_per_element)
 
 
 def _peaks():
@@ -319,18 +320,19 @@ def run_ours(args):
         return
     peak, peak_src = _peaks()
     adam_elems = opt.gpu_elements
+    bpe = opt.bytes_per_element
     adam_avg = statistics.mean(adam_ms) if adam_ms else float("nan")
-    adam_gbs = ADAM_BYTES_PER_ELEM * adam_elems / (adam_avg * 1e-3) / 1e9
+    adam_gbs = bpe * adam_elems / (adam_avg * 1e-3) / 1e9
     rel_ms = sum(r for r, _ in rel) / max(1, args.steps)
     rel_elems = sum(n for _, n in rel) / max(1, args.steps)
     es = 2  # bf16
-    rel_local_bytes = rel_elems * (es * world + 4)
+    rel_local_bytes = rel_elems * (es * world + (0 if world == 1 else 4))  # world 1: norm/overflow pass only
     traffic = None
     tp = ROOT / "profiles" / "adam_ncu_traffic.json"
     if tp.exists():
         try:
             t = json.loads(tp.read_text())
-            if t.get("valid_elements") == adam_elems:
+            if t.get("valid_elements") == adam_elems and t.get("bytes_per_element", 30) == bpe:
                 traffic = t["dram_bytes_per_launch"]
         except Exception:
             traffic = None
@@ -381,7 +383,7 @@ def run_ours(args):
         },
         "roofline": {"bound": "hbm", "kernel": "elx_adam (K4)", "achieved": adam_gbs, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": adam_gbs / peak, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": ADAM_BYTES_PER_ELEM * adam_elems},
+                     "algorithmic_bytes_per_launch": bpe * adam_elems, "bytes_per_element": bpe},
         "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s",
                 "h2d_bytes_per_step": host_ids.numel() * host_ids.element_size(),
                 "d2h_bytes_per_step": loss_host.numel() * loss_host.element_size(),

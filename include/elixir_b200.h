@@ -159,7 +159,11 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
  *   step_scalars[1]  = 1.0 if any g[i] is not finite
  * src[r] points at rank r's copy of THIS rank's segment (peer block + rank*S,
  * or a local all-to-all staging buffer). n = valid elements (padding
- * excluded). dtype is BF16 or F16. step_scalars is a DEVICE double[2]. */
+ * excluded). dtype is BF16 or F16. step_scalars is a DEVICE double[2].
+ * grad_shard may be NULL: only the sum of squares and the overflow flag are
+ * produced. At world 1 the reduction is the identity, so the runtime keeps
+ * the gradient in the compute-dtype chunk and the update (elx_adam with a
+ * compute-dtype `g`) applies the same float(g) * inv_scale in-register. */
 int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t world,
                 int32_t dtype, float inv_scale, double* step_scalars, void* stream);
 
@@ -179,11 +183,12 @@ typedef struct {
   float* p32;
   float* m;
   float* v;
-  const float* g;
+  const void* g;     /* gradient: fp32 (released, unscaled) or compute dtype  */
   void* p16;
   int64_t n;
   int64_t tile0;
-  int64_t pad_;
+  int32_t g_dtype;   /* ELX_F32: g used as is; ELX_BF16/F16: float(g)*grad_scale */
+  int32_t pad_;
 } elx_adam_seg;
 
 typedef struct {
@@ -193,6 +198,7 @@ typedef struct {
   double eps;
   double weight_decay;
   double max_norm;  /* <= 0 disables clipping */
+  double grad_scale; /* multiplies compute-dtype gradients (1 / loss scale) */
   int32_t p16_dtype; /* ELX_BF16 or ELX_F16 */
   int32_t pad_;
 } elx_adam_hp;
@@ -223,9 +229,11 @@ typedef struct {
   float* p32;
   float* m;
   float* v;
-  const float* g;
+  const void* g;     /* fp32, or compute dtype scaled by hp->grad_scale */
   void* p16;
   int64_t n;
+  int32_t g_dtype;
+  int32_t pad_;
 } elx_cpu_seg;
 int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_adam_hp* hp, int64_t step,
                  const double* step_scalars, int32_t threads);

@@ -58,18 +58,18 @@ class Member(ctypes.Structure):
 
 class AdamSeg(ctypes.Structure):
     _fields_ = [("p32", c_vp), ("m", c_vp), ("v", c_vp), ("g", c_vp), ("p16", c_vp),
-                ("n", c_i64), ("tile0", c_i64), ("pad_", c_i64)]
+                ("n", c_i64), ("tile0", c_i64), ("g_dtype", c_i32), ("pad_", c_i32)]
 
 
 class AdamHP(ctypes.Structure):
     _fields_ = [("lr", c_f64), ("beta1", c_f64), ("beta2", c_f64), ("eps", c_f64),
-                ("weight_decay", c_f64), ("max_norm", c_f64), ("p16_dtype", c_i32),
-                ("pad_", c_i32)]
+                ("weight_decay", c_f64), ("max_norm", c_f64), ("grad_scale", c_f64),
+                ("p16_dtype", c_i32), ("pad_", c_i32)]
 
 
 class CpuSeg(ctypes.Structure):
     _fields_ = [("p32", c_vp), ("m", c_vp), ("v", c_vp), ("g", c_vp), ("p16", c_vp),
-                ("n", c_i64)]
+                ("n", c_i64), ("g_dtype", c_i32), ("pad_", c_i32)]
 
 
 # name -> (restype, argtypes)

@@ -40,8 +40,38 @@ inline uint16_t f32_to_f16_rne(float f) {
 }
 
 struct HostK {
-  float coef, decay, omb1, b2, omb2, bc2s, neg_step, eps;
+  float coef, decay, omb1, b2, omb2, bc2s, neg_step, eps, gscale;
 };
+
+inline float bf16_bits_to_f32(uint16_t b) {
+  const uint32_t u = (uint32_t)b << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+// IEEE binary16 -> float32 (exact).
+inline float f16_bits_to_f32(uint16_t h) {
+  const uint32_t sign = (uint32_t)(h & 0x8000u) << 16;
+  uint32_t exp = (h >> 10) & 0x1fu, man = h & 0x3ffu, u;
+  if (exp == 0x1fu) {
+    u = sign | 0x7f800000u | (man << 13);
+  } else if (exp != 0) {
+    u = sign | ((exp + 112u) << 23) | (man << 13);
+  } else if (man == 0) {
+    u = sign;
+  } else {  // subnormal: normalise
+    int e = -1;
+    do {
+      man <<= 1;
+      ++e;
+    } while (!(man & 0x400u));
+    u = sign | ((uint32_t)(112 - e) << 23) | ((man & 0x3ffu) << 13);
+  }
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
 
 // The bf16 path is written branch-free so the compiler vectorises it; the
 // clones cover AVX-512 / AVX2 / baseline x86-64 hosts (the GPU box's CPU is
@@ -52,6 +82,30 @@ void adam_bf16_range(float* __restrict p32, float* __restrict m, float* __restri
                      uint16_t* __restrict p16, int64_t n, HostK k) {
   for (int64_t i = 0; i < n; ++i) {
     const float G = g[i] * k.coef;
+    float P = p32[i] * k.decay;
+    const float Mo = m[i];
+    const float M = Mo + k.omb1 * (G - Mo);
+    const float V = v[i] * k.b2 + (k.omb2 * G) * G;
+    const float denom = std::sqrt(V) / k.bc2s + k.eps;
+    P = P + (k.neg_step * M) / denom;
+    p32[i] = P;
+    m[i] = M;
+    v[i] = V;
+    uint32_t u;
+    std::memcpy(&u, &P, 4);
+    const uint32_t rne = (u + 0x7fffu + ((u >> 16) & 1u)) >> 16;
+    const uint32_t qnan = (u >> 16) | 0x40u;
+    p16[i] = (uint16_t)(((u & 0x7fffffffu) > 0x7f800000u) ? qnan : rne);
+  }
+}
+
+// Same update, gradient given as bf16 bits (world-1 in-place chunks): the
+// release's float(g) * inv_scale is applied in-register.
+__attribute__((target_clones("avx512f", "avx2", "default")))
+void adam_bf16_range_g16(float* __restrict p32, float* __restrict m, float* __restrict v,
+                         const uint16_t* __restrict g16, uint16_t* __restrict p16, int64_t n, HostK k) {
+  for (int64_t i = 0; i < n; ++i) {
+    const float G = bf16_bits_to_f32(g16[i]) * k.gscale * k.coef;
     float P = p32[i] * k.decay;
     const float Mo = m[i];
     const float M = Mo + k.omb1 * (G - Mo);
@@ -107,13 +161,16 @@ extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_ada
   const bool bf16 = hp->p16_dtype == ELX_BF16;
   if (threads < 1) threads = 1;
 
-  const HostK hk{coef, decay, omb1, b2, omb2, bc2s, neg_step, eps};
+  const float gscale = (float)hp->grad_scale;
+  const HostK hk{coef, decay, omb1, b2, omb2, bc2s, neg_step, eps, gscale};
   constexpr int64_t kBlock = 1 << 16;  // elements per OpenMP work item
   for (int32_t s = 0; s < nseg; ++s) {
     float* p32 = segs[s].p32;
     float* m = segs[s].m;
     float* v = segs[s].v;
-    const float* g = segs[s].g;
+    const int gdt = segs[s].g_dtype;
+    const float* g = static_cast<const float*>(segs[s].g);
+    const uint16_t* g16 = static_cast<const uint16_t*>(segs[s].g);
     uint16_t* p16 = static_cast<uint16_t*>(segs[s].p16);
     const int64_t n = segs[s].n;
     const int64_t nb = (n + kBlock - 1) / kBlock;
@@ -123,8 +180,10 @@ extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_ada
         const int64_t lo = b * kBlock, cnt = std::min(kBlock, n - lo);
         if (skip)
           restore_bf16_range(p32 + lo, p16 + lo, cnt);
-        else
+        else if (gdt == ELX_F32)
           adam_bf16_range(p32 + lo, m + lo, v + lo, g + lo, p16 + lo, cnt, hk);
+        else
+          adam_bf16_range_g16(p32 + lo, m + lo, v + lo, g16 + lo, p16 + lo, cnt, hk);
       }
       continue;
     }
@@ -133,7 +192,8 @@ extern "C" int elx_cpu_adam(const elx_cpu_seg* segs, int32_t nseg, const elx_ada
       float P = p32[i];
       if (!skip) {
         float M = m[i], V = v[i];
-        const float G = g[i] * coef;
+        const float graw = gdt == ELX_F32 ? g[i] : f16_bits_to_f32(g16[i]) * gscale;
+        const float G = graw * coef;
         P = P * decay;
         M = M + omb1 * (G - M);
         V = V * b2 + (omb2 * G) * G;

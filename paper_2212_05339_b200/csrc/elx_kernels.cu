@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict_
         bad |= !isfinite(acc[e]);
         sq += (double)acc[e] * (double)acc[e];
       }
-      reinterpret_cast<float4*>(g)[i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+      if (g) reinterpret_cast<float4*>(g)[i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     }
   }
   // Scalar tail (n % 4 elements), handled by block 0.
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict_
       a = __fmul_rn(a, inv_scale);
       bad |= !isfinite(a);
       sq += (double)a * (double)a;
-      g[i] = a;
+      if (g) g[i] = a;
     }
   }
   block_reduce_and_publish(sq, bad, sc);
@@ -351,7 +351,7 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel_scalar(float* g, c
     a = __fmul_rn(a, inv_scale);
     bad |= !isfinite(a);
     sq += (double)a * (double)a;
-    g[i] = a;
+    if (g) g[i] = a;
   }
   block_reduce_and_publish(sq, bad, sc);
 }
@@ -359,7 +359,7 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel_scalar(float* g, c
 template <typename T16>
 int run_release(float* g, const PtrBatch& pb, int64_t n, int world, float inv_scale, double* sc,
                 cudaStream_t st) {
-  bool vec = aligned16(g);
+  bool vec = g == nullptr || aligned16(g);
   for (int r = 0; r < world; ++r) vec = vec && ((reinterpret_cast<uintptr_t>(pb.p[r]) & 7u) == 0);
   auto go = [&](auto kern, int64_t work) {
     int per_sm = 0;
@@ -406,8 +406,24 @@ struct AdamK {
   float bc2_sqrt;    // sqrt(1 - beta2^step)
   float neg_step;    // -lr / (1 - beta1^step)
   float eps;
+  float grad_scale;  // for compute-dtype gradients: g = float(g16) * grad_scale
   double max_norm;
 };
+
+// Gradient element i of a segment: fp32 (already released), or the
+// compute-dtype gradient unscaled in-register exactly as K3 would do it.
+template <typename T16>
+__device__ __forceinline__ float load_grad(const void* g, int64_t i, int gdt, float gs) {
+  if (gdt == ELX_F32) return static_cast<const float*>(g)[i];
+  return __fmul_rn(to_f32<T16>(static_cast<const T16*>(g)[i]), gs);
+}
+
+template <typename T16>
+__device__ __forceinline__ float4 cvt4_grad(uint2 raw, float gs) {
+  const T16* h = reinterpret_cast<const T16*>(&raw);
+  return make_float4(__fmul_rn(to_f32<T16>(h[0]), gs), __fmul_rn(to_f32<T16>(h[1]), gs),
+                     __fmul_rn(to_f32<T16>(h[2]), gs), __fmul_rn(to_f32<T16>(h[3]), gs));
+}
 
 // One element of the update; every operation is a single IEEE rounding in
 // the order of the oracle (oracle/arith.py: adamw_step).
@@ -458,13 +474,16 @@ __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
     float* __restrict__ p32 = segs[s].p32;
     float* __restrict__ m = segs[s].m;
     float* __restrict__ v = segs[s].v;
-    const float* __restrict__ g = segs[s].g;
+    const void* g = segs[s].g;
+    const int gdt = segs[s].g_dtype;
     T16* __restrict__ p16 = static_cast<T16*>(segs[s].p16);
     const int64_t n = segs[s].n;
     const int64_t base = (t - segs[s].tile0) * ELX_ADAM_TILE;
     const int64_t cnt = min((int64_t)ELX_ADAM_TILE, n - base);
+    const bool g_ok = gdt == ELX_F32 ? aligned16(static_cast<const float*>(g) + base)
+                                     : ((reinterpret_cast<uintptr_t>(static_cast<const T16*>(g) + base) & 7u) == 0);
     const bool vec = cnt == ELX_ADAM_TILE && aligned16(p32 + base) && aligned16(m + base) &&
-                     aligned16(v + base) && aligned16(g + base) &&
+                     aligned16(v + base) && g_ok &&
                      ((reinterpret_cast<uintptr_t>(p16 + base) & 7u) == 0);
     if (vec) {
 #pragma unroll 1
@@ -486,7 +505,9 @@ __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
           P[u] = reinterpret_cast<const float4*>(p32 + base)[j];
           M[u] = reinterpret_cast<const float4*>(m + base)[j];
           V[u] = reinterpret_cast<const float4*>(v + base)[j];
-          G[u] = ld_stream_f4(reinterpret_cast<const float4*>(g + base) + j);
+          G[u] = gdt == ELX_F32 ? ld_stream_f4(reinterpret_cast<const float4*>(static_cast<const float*>(g) + base) + j)
+                                : cvt4_grad<T16>(reinterpret_cast<const uint2*>(static_cast<const T16*>(g) + base)[j],
+                                                 k.grad_scale);
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
@@ -506,7 +527,7 @@ __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
         float P = p32[i];
         if (!skip) {
           float M = m[i], V = v[i];
-          adam_elem(P, M, V, g[i], coef, k);
+          adam_elem(P, M, V, load_grad<T16>(g, i, gdt, k.grad_scale), coef, k);
           p32[i] = P;
           m[i] = M;
           v[i] = V;
@@ -582,7 +603,8 @@ __device__ __forceinline__ TileRef locate(const elx_adam_seg* segs, int nseg, in
   r.base = (t - segs[s].tile0) * ELX_ADAM_TILE + (int64_t)sub * kTmaTile;
   r.cnt = min((int64_t)kTmaTile, segs[s].n - r.base);
   r.tma = r.cnt == kTmaTile && aligned16(segs[s].p32 + r.base) && aligned16(segs[s].m + r.base) &&
-          aligned16(segs[s].v + r.base) && aligned16(segs[s].g + r.base) &&
+          aligned16(segs[s].v + r.base) &&
+          aligned16(static_cast<const char*>(segs[s].g) + (segs[s].g_dtype == ELX_F32 ? 4 : 2) * r.base) &&
           ((reinterpret_cast<uintptr_t>(static_cast<char*>(segs[s].p16) + 2 * r.base) & 7u) == 0);
   return r;
 }
@@ -618,12 +640,14 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const uint32_t ph = (uint32_t)((q / kStages) & 1);
         mbar_wait(&empty[st], ph ^ 1u);
         float* dst = stage_base + (size_t)st * (kTmaStageBytes / 4);
-        mbar_expect_tx(&full[st], kTmaStageBytes);
         const elx_adam_seg& sg = segs[r.seg];
+        const int gsz = sg.g_dtype == ELX_F32 ? 4 : 2;
+        mbar_expect_tx(&full[st], 3 * kTmaTile * 4 + kTmaTile * gsz);
         tma_load_1d(dst, sg.p32 + r.base, kTmaTile * 4, &full[st]);
         tma_load_1d(dst + kTmaTile, sg.m + r.base, kTmaTile * 4, &full[st]);
         tma_load_1d(dst + 2 * kTmaTile, sg.v + r.base, kTmaTile * 4, &full[st]);
-        tma_load_1d(dst + 3 * kTmaTile, sg.g + r.base, kTmaTile * 4, &full[st]);
+        tma_load_1d(dst + 3 * kTmaTile, static_cast<const char*>(sg.g) + (int64_t)gsz * r.base, kTmaTile * gsz,
+                    &full[st]);
         ++q;
       }
     }
@@ -642,12 +666,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     float* __restrict__ v = sg.v + r.base;
     T16* __restrict__ p16 = static_cast<T16*>(sg.p16) + r.base;
     if (!r.tma) {  // tail / misaligned tile: straight from global memory
-      const float* g = sg.g + r.base;
+      const int gdt = sg.g_dtype;
       for (int64_t i = threadIdx.x; i < r.cnt; i += kTmaConsumers) {
         float P = p32[i];
         if (!skip) {
           float M = m[i], V = v[i];
-          adam_elem(P, M, V, g[i], coef, k);
+          adam_elem(P, M, V, load_grad<T16>(sg.g, r.base + i, gdt, k.grad_scale), coef, k);
           p32[i] = P;
           m[i] = M;
           v[i] = V;
@@ -668,7 +692,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       P[u] = reinterpret_cast<const float4*>(src)[j];
       M[u] = reinterpret_cast<const float4*>(src + kTmaTile)[j];
       V[u] = reinterpret_cast<const float4*>(src + 2 * kTmaTile)[j];
-      G[u] = reinterpret_cast<const float4*>(src + 3 * kTmaTile)[j];
+      G[u] = sg.g_dtype == ELX_F32 ? reinterpret_cast<const float4*>(src + 3 * kTmaTile)[j]
+                                   : cvt4_grad<T16>(reinterpret_cast<const uint2*>(src + 3 * kTmaTile)[j], k.grad_scale);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);  // stage may be refilled: operands are in registers
@@ -809,7 +834,7 @@ int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t wo
                 float inv_scale, double* step_scalars, void* stream) {
   elx::clear_error();
   if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
-  if (!grad_shard || !src || !step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (!src || !step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   if (n < 0) return elx::fail(ELX_ERR_VALIDATION, "negative length");
   PtrBatch pb{};
   for (int r = 0; r < world; ++r) {
@@ -842,6 +867,7 @@ int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const e
   k.bc2_sqrt = (float)std::sqrt(bc2);
   k.neg_step = (float)(-(hp->lr / bc1));
   k.eps = (float)hp->eps;
+  k.grad_scale = (float)hp->grad_scale;
   k.max_norm = hp->max_norm;
   static int variant = [] {
     const char* e = getenv("ELX_ADAM_VARIANT");

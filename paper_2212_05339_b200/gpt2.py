@@ -273,7 +273,7 @@ class ElixirGPT2:
             del grads, pgrads, params, out
         fx.release_shared(self.wte)
         done = fx.finish()
-        found_inf, _ = self.optimizer.step(done)
+        found_inf, _ = self.optimizer.step(done, grad_scale=1.0 / self.scaler.scale)
         self.scaler.update(found_inf)
         self.last_loss = loss
         return loss

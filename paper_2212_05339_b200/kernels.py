@@ -97,18 +97,21 @@ def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream
     _lib.check(rc, "elx_fetch")
 
 
-def release(grad_shard: torch.Tensor, src_ptrs: Sequence[int], n: int, dtype: torch.dtype,
+def release(grad_shard: torch.Tensor | None, src_ptrs: Sequence[int], n: int, dtype: torch.dtype,
             inv_scale: float, step_scalars: torch.Tensor, stream=None) -> None:
     """K3: grad_shard[:n] = (sum_r src_r[:n] in rank order, fp32) * inv_scale,
-    accumulating sum(g^2) into step_scalars[0] and overflow into step_scalars[1]."""
+    accumulating sum(g^2) into step_scalars[0] and overflow into step_scalars[1].
+    grad_shard=None: norm/overflow only (world-1 in-place chunks)."""
     lib = _lib.load()
-    _cuda(grad_shard, "grad_shard")
-    if grad_shard.dtype != torch.float32 or grad_shard.numel() < n:
-        raise ValidationError("grad_shard must be float32 with >= n elements")
+    if grad_shard is not None:
+        _cuda(grad_shard, "grad_shard")
+        if grad_shard.dtype != torch.float32 or grad_shard.numel() < n:
+            raise ValidationError("grad_shard must be float32 with >= n elements")
     if step_scalars.dtype != torch.float64 or not step_scalars.is_cuda:
         raise ValidationError("step_scalars must be a CUDA float64 tensor")
     arr = _ptr_array(src_ptrs)
-    rc = lib.elx_release(grad_shard.data_ptr(), ctypes.addressof(arr), int(n), len(src_ptrs),
+    rc = lib.elx_release(None if grad_shard is None else grad_shard.data_ptr(), ctypes.addressof(arr), int(n),
+                         len(src_ptrs),
                          elx_dtype(dtype), float(inv_scale), step_scalars.data_ptr(), _stream(stream))
     _lib.check(rc, "elx_release")
 
@@ -126,6 +129,7 @@ class AdamTable:
                 _cuda(t, "adam segment tensor")
             host[i].p32, host[i].m, host[i].v = p32.data_ptr(), m.data_ptr(), v.data_ptr()
             host[i].g, host[i].p16, host[i].n, host[i].tile0 = g.data_ptr(), p16.data_ptr(), int(n), tile
+            host[i].g_dtype = elx_dtype(g.dtype)
             tile += -(-int(n) // _lib.ADAM_TILE)
             self.valid_elements += int(n)
         self.nseg = len(segs)
@@ -135,19 +139,24 @@ class AdamTable:
         self._keep = [s[:5] for s in segs]
 
 
+def _hp(hp: dict, p16_dtype: torch.dtype, grad_scale: float):
+    return _lib.AdamHP(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"],
+                       hp.get("max_norm", 0.0) or 0.0, float(grad_scale), elx_dtype(p16_dtype), 0)
+
+
 def adam(table: AdamTable, hp: dict, step: int, step_scalars: torch.Tensor, p16_dtype: torch.dtype,
-         stream=None) -> None:
-    """K4 over every segment of `table` in one launch."""
+         stream=None, grad_scale: float = 1.0) -> None:
+    """K4 over every segment of `table` in one launch. Segments whose
+    gradient is in the compute dtype are unscaled by `grad_scale` in-register."""
     lib = _lib.load()
-    h = _lib.AdamHP(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"],
-                    hp.get("max_norm", 0.0) or 0.0, elx_dtype(p16_dtype), 0)
+    h = _hp(hp, p16_dtype, grad_scale)
     rc = lib.elx_adam(table.dev.data_ptr(), table.nseg, table.ntiles, ctypes.byref(h), int(step),
                       step_scalars.data_ptr(), _stream(stream))
     _lib.check(rc, "elx_adam")
 
 
 def cpu_adam(segs: Sequence[tuple[torch.Tensor, ...]], hp: dict, step: int, scalars_host: Sequence[float],
-             p16_dtype: torch.dtype, threads: int) -> None:
+             p16_dtype: torch.dtype, threads: int, grad_scale: float = 1.0) -> None:
     """Host AdamW (same bits as K4) over CPU tensors (p32, m, v, g, p16, n)."""
     lib = _lib.load()
     arr = (_lib.CpuSeg * max(1, len(segs)))()
@@ -157,8 +166,8 @@ def cpu_adam(segs: Sequence[tuple[torch.Tensor, ...]], hp: dict, step: int, scal
                 raise ValidationError("cpu_adam needs contiguous host tensors")
         arr[i].p32, arr[i].m, arr[i].v = p32.data_ptr(), m.data_ptr(), v.data_ptr()
         arr[i].g, arr[i].p16, arr[i].n = g.data_ptr(), p16.data_ptr(), int(n)
-    h = _lib.AdamHP(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"],
-                    hp.get("max_norm", 0.0) or 0.0, elx_dtype(p16_dtype), 0)
+        arr[i].g_dtype = elx_dtype(g.dtype)
+    h = _hp(hp, p16_dtype, grad_scale)
     sc = (ctypes.c_double * 2)(float(scalars_host[0]), float(scalars_host[1]))
     rc = lib.elx_cpu_adam(ctypes.addressof(arr), len(segs), ctypes.byref(h), int(step),
                           ctypes.addressof(sc), int(threads))

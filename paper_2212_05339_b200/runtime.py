@@ -129,14 +129,21 @@ class ChunkManager:
         self.p32 = torch.zeros(G, S, dtype=f32, device=dev)
         self.m = torch.zeros(G, S, dtype=f32, device=dev)
         self.v = torch.zeros(G, S, dtype=f32, device=dev)
-        self.g32 = torch.zeros(G, S, dtype=f32, device=dev)
+        # World 1: the reduce-scatter is the identity, so the gradient stays in
+        # the compute-dtype chunk; K3 only produces the norm/overflow and K4
+        # unscales the compute-dtype gradient in-register (same IEEE ops). No
+        # fp32 grad shard: the footprint is exactly chunk_footprint.
+        self.fused_w1 = self.world == 1
+        self.g32 = torch.zeros(G, 0 if self.fused_w1 else S, dtype=f32, device=dev)
         # ---- CPU-home arenas (pinned)
         pin = torch.cuda.is_available()
         self.h_p16 = torch.zeros(H, S, dtype=dtype, pin_memory=pin)
         self.h_p32 = torch.zeros(H, S, dtype=f32, pin_memory=pin)
         self.h_m = torch.zeros(H, S, dtype=f32, pin_memory=pin)
         self.h_v = torch.zeros(H, S, dtype=f32, pin_memory=pin)
-        self.h_g32 = torch.zeros(H, S, dtype=f32, pin_memory=pin)
+        # host gradient landing buffer: fp32 reduced shard, or (world 1) the
+        # compute-dtype gradient — half the D2H bytes
+        self.h_g32 = torch.zeros(H, S, dtype=dtype if self.fused_w1 else f32, pin_memory=pin)
         # ---- rCache blocks and release staging
         self.alias = self.world == 1
         need_blocks = self.world > 1 or H > 0
@@ -146,7 +153,7 @@ class ChunkManager:
         self.peer_p16 = self.transport.peer_ptrs(self.p16) if self.p2p else None
         self.peer_blocks = self.transport.peer_ptrs(self.blocks) if self.p2p else None
         self.recv = torch.zeros(self.P if self.world > 1 else 0, dtype=dtype, device=dev)
-        self.stage32 = torch.zeros(S if H > 0 else 0, dtype=f32, device=dev)
+        self.stage32 = torch.zeros(S if (H > 0 and not self.fused_w1) else 0, dtype=f32, device=dev)
         # ---- shared (multi-use) parameters: replicated copy + partitioned state
         self.shared: dict[str, _SharedParam] = {}
         for pid in shared_ids:
@@ -162,7 +169,8 @@ class ChunkManager:
             self.shared[pid] = _SharedParam(
                 pid, numel, self.shapes[pid], ssh, full, torch.zeros(ssh * self.world, dtype=dtype, device=dev), p16,
                 torch.zeros(ssh, dtype=f32, device=dev), torch.zeros(ssh, dtype=f32, device=dev),
-                torch.zeros(ssh, dtype=f32, device=dev), torch.zeros(ssh, dtype=f32, device=dev))
+                torch.zeros(ssh, dtype=f32, device=dev),
+                torch.zeros(0 if self.world == 1 else ssh, dtype=f32, device=dev))
         # step scalars: [0] sum g^2, [1] overflow flag (elx_release / elx_adam)
         self.step_scalars = torch.zeros(4, dtype=torch.float64, device=dev)
         self._bound: dict[int, torch.Tensor] = {}   # chunk -> storage it is bound to
@@ -478,7 +486,7 @@ class ChunkFetcher:
                 es = mgr.recv.element_size()
                 srcs = [mgr.recv.data_ptr() + r * mgr.S * es for r in range(mgr.world)]
             r = mgr.row[c]
-            target = mgr.g32[r] if not cpu else mgr.stage32
+            target = None if mgr.fused_w1 else (mgr.g32[r] if not cpu else mgr.stage32)
             if n > 0:
                 kernels.release(target, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
             if mgr.p2p:
@@ -487,8 +495,10 @@ class ChunkFetcher:
                 t1.record(comm)
                 self.release_events.append((t0, t1, n))
             if cpu and n > 0:
-                kernels.copy_d2h(mgr.h_g32[r], mgr.stage32, n * 4, stream=comm)
-                self.bytes_moved["d2h"] += n * 4
+                src = storage if mgr.fused_w1 else mgr.stage32
+                nbytes = n * src.element_size()
+                kernels.copy_d2h(mgr.h_g32[r], src, nbytes, stream=comm)
+                self.bytes_moved["d2h"] += nbytes
 
     def release_shared(self, sp: _SharedParam) -> None:
         """Release of a shared parameter's gradient (after its last use)."""
@@ -512,7 +522,8 @@ class ChunkFetcher:
                 srcs = [recv.data_ptr() + r * sp.shard * es for r in range(mgr.world)]
             n = sp.valid(mgr.rank)
             if n > 0:
-                kernels.release(sp.g32, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
+                kernels.release(None if mgr.fused_w1 else sp.g32, srcs, n, mgr.dtype, self.inv_scale,
+                                mgr.step_scalars, stream=comm)
 
 
 class HybridAdam:
@@ -547,14 +558,16 @@ class HybridAdam:
         for pid, sp in m.shared.items():
             n = sp.valid(m.rank)
             if n > 0:
-                seg = (sp.p32, sp.m, sp.v, sp.g32, sp.p16, n)
+                seg = (sp.p32, sp.m, sp.v, sp.grad if m.fused_w1 else sp.g32, sp.p16, n)
                 all_segs.append(seg)
                 self.groups.append((pid, kernels.AdamTable([seg], m.device)))
         for c in m.gpu_ids:
             r = m.row[c]
             n = m.valid(c)
             if n > 0:
-                seg = (m.p32[r], m.m[r], m.v[r], m.g32[r], m.p16[r], n)
+                # world 1: the gradient is read from the chunk itself (bf16) and
+                # overwritten in place by the new parameter
+                seg = (m.p32[r], m.m[r], m.v[r], m.p16[r] if m.fused_w1 else m.g32[r], m.p16[r], n)
                 all_segs.append(seg)
                 self.groups.append((c, kernels.AdamTable([seg], m.device)))
         self.table = kernels.AdamTable(all_segs, m.device)  # single-launch form (overlap=False)
@@ -570,6 +583,7 @@ class HybridAdam:
         self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         self.time_adam = False
         self.done_event: torch.cuda.Event | None = None
+        self.grad_scale = 1.0
         self.pending: dict[object, torch.cuda.Event] = {}     # key -> GPU update done
         self.cpu_ready: dict[int, threading.Event] = {c: threading.Event() for c in self.cpu_segs}
         for ev in self.cpu_ready.values():
@@ -580,6 +594,13 @@ class HybridAdam:
     @property
     def gpu_elements(self) -> int:
         return self.table.valid_elements
+
+    @property
+    def bytes_per_element(self) -> int:
+        """K4 algorithmic bytes per element: p32/m/v read+write (24), the
+        gradient read (4 fp32, or 2 compute-dtype at world 1), the compute-dtype
+        parameter write (2)."""
+        return 24 + (2 if self.mgr.fused_w1 else 4) + 2
 
     # ------------------------------------------------------------ waits used by the fetcher / model
     def wait_gpu(self, key, stream: torch.cuda.Stream) -> None:
@@ -642,11 +663,14 @@ class HybridAdam:
         torch.cuda.synchronize(m.device)
 
     # ------------------------------------------------------------ step
-    def step(self, releases_done: torch.cuda.Event | None = None) -> tuple[bool, float]:
+    def step(self, releases_done: torch.cuda.Event | None = None, grad_scale: float = 1.0) -> tuple[bool, float]:
         """All-reduce norm/overflow, then update every shard. Returns
         (found_inf, grad_norm) — one host sync per step (GradScaler also
         reads found_inf on the host). `releases_done` is the event
-        ChunkFetcher.finish() returns (None: synchronise the device)."""
+        ChunkFetcher.finish() returns (None: synchronise the device);
+        `grad_scale` = 1/loss_scale, applied in-register to compute-dtype
+        gradients (world 1)."""
+        self.grad_scale = float(grad_scale)
         m = self.mgr
         dev = m.device
         cur = torch.cuda.current_stream(dev)
@@ -674,7 +698,8 @@ class HybridAdam:
         with torch.cuda.stream(opt):
             if self.overlap:
                 for key, table in self.groups:
-                    kernels.adam(table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt)
+                    kernels.adam(table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt,
+                                 grad_scale=self.grad_scale)
                     if key in m.shared and m.world > 1:
                         sp = m.shared[key]
                         m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
@@ -682,7 +707,8 @@ class HybridAdam:
                     ev.record(opt)
                     self.pending[key] = ev
             else:
-                kernels.adam(self.table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt)
+                kernels.adam(self.table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt,
+                             grad_scale=self.grad_scale)
                 if m.world > 1:
                     for sp in m.shared.values():
                         m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
@@ -708,7 +734,8 @@ class HybridAdam:
         """CPU-home shards in forward order, flagging each chunk when done."""
         try:
             for c in sorted(self.cpu_segs):
-                kernels.cpu_adam([self.cpu_segs[c]], self.hp, kstep, scalars, self.mgr.dtype, self.cpu_threads)
+                kernels.cpu_adam([self.cpu_segs[c]], self.hp, kstep, scalars, self.mgr.dtype, self.cpu_threads,
+                                 grad_scale=self.grad_scale)
                 self.cpu_ready[c].set()
         except BaseException as exc:  # surfaced by wait_cpu / synchronize
             self._cpu_error = exc

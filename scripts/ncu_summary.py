@@ -101,10 +101,12 @@ def main():
                 rd = _bytes(rec["dram__bytes_read.sum"], rec["dram__bytes_read.sum.unit"])
                 wr = _bytes(rec["dram__bytes_write.sum"], rec["dram__bytes_write.sum.unit"])
                 valid = int(sys.argv[sys.argv.index("--valid") + 1]) if "--valid" in sys.argv else None
+                bpe = int(sys.argv[sys.argv.index("--bpe") + 1]) if "--bpe" in sys.argv else 30
                 (PROF / "adam_ncu_traffic.json").write_text(json.dumps({
                     "source": f"profiles/{tag}_{p.stem}.json", "dram_bytes_per_launch": rd + wr,
                     "dram_read": rd, "dram_write": wr, "valid_elements": valid,
-                    "algorithmic_bytes": None if valid is None else 30 * valid}, indent=1))
+                    "bytes_per_element": bpe,
+                    "algorithmic_bytes": None if valid is None else bpe * valid}, indent=1))
 
 
 if __name__ == "__main__":

@@ -36,8 +36,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_lib.SimCounters) == 56
     assert ctypes.sizeof(_lib.Member) == 32
     assert ctypes.sizeof(_lib.AdamSeg) == 64
-    assert ctypes.sizeof(_lib.AdamHP) == 56
-    assert ctypes.sizeof(_lib.CpuSeg) == 48
+    assert ctypes.sizeof(_lib.AdamHP) == 64
+    assert ctypes.sizeof(_lib.CpuSeg) == 56
 
 
 def test_abi_version_and_errors():
@@ -57,7 +57,7 @@ def test_gpu_entry_points_validate_before_launch():
     assert lib.elx_fetch(None, None, 7, 1, _lib.BF16, None) == _lib.ERR_VALIDATION
     assert lib.elx_release(None, None, 8, 1, _lib.BF16, ctypes.c_float(1.0), None, None) == _lib.ERR_VALIDATION
     assert lib.elx_adam(None, 1, 1, None, 1, None, None) == _lib.ERR_VALIDATION
-    hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 0.0, _lib.BF16, 0)
+    hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 0.0, 1.0, _lib.BF16, 0)
     sc = (ctypes.c_double * 2)()
     assert lib.elx_adam(None, 1, 1, ctypes.byref(hp), 0, ctypes.addressof(sc), None) == _lib.ERR_VALIDATION
 
@@ -105,3 +105,22 @@ def test_host_f16_rounding_edge_cases():
     hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.0, max_norm=0.0)
     kernels.cpu_adam([(P, z.clone(), z.clone(), z.clone(), p16, n)], hp, 1, (0.0, 1.0), torch.float16, 1)
     assert np.array_equal(p16.numpy().view(np.uint16), vals.astype(np.float16).view(np.uint16))
+
+
+def test_host_adam_compute_dtype_grads():
+    """elx_cpu_adam reading a bf16 gradient (world-1 CPU-home path) == released fp32 path."""
+    rng = np.random.default_rng(8)
+    n = 70_001
+    p = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    m = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    v = (rng.random(n) * 1e-6).astype(np.float32)
+    gbits = arith.f32_to_bf16_bits((rng.standard_normal(n) * 10).astype(np.float32))
+    g, sq, _ = arith.release([gbits], 1.0 / 64)
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
+    T = [torch.from_numpy(a.copy()) for a in (p, m, v)]
+    g16 = torch.from_numpy(gbits.view(np.int16).copy()).view(torch.bfloat16)
+    p16 = torch.zeros(n, dtype=torch.bfloat16)
+    kernels.cpu_adam([(T[0], T[1], T[2], g16, p16, n)], hp, 3, (sq, 0.0), torch.bfloat16, 4, grad_scale=1.0 / 64)
+    rp, rm, rv, r16 = arith.adamw(p, m, v, g, 3, 1e-3, 0.9, 0.999, 1e-8, 0.01, arith.clip_coef(sq, 1.0))
+    assert np.array_equal(T[0].numpy(), rp) and np.array_equal(T[1].numpy(), rm) and np.array_equal(T[2].numpy(), rv)
+    assert np.array_equal(p16.view(torch.int16).numpy().view(np.uint16), r16)

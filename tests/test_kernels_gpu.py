@@ -276,13 +276,22 @@ for n in sizes:
     for a in arrs:
         t = torch.zeros(n + off, device=dev); t[off:] = torch.from_numpy(a); ts.append(t[off:])
     segs.append((*ts, torch.zeros(n, dtype=torch.bfloat16, device=dev), n))
+# one segment whose gradient is bf16 in place (world-1 fused path), scale 1/8
+nb = 10_240
+gb = arith.f32_to_bf16_bits((rng.standard_normal(nb) * 0.4).astype(np.float32))
+hb = [(rng.standard_normal(nb) * 0.02).astype(np.float32), (rng.standard_normal(nb) * 1e-3).astype(np.float32),
+      (rng.random(nb) * 1e-6).astype(np.float32), arith.release([gb], 0.125)[0]]
+host.append(hb)
+tb = [torch.from_numpy(a.copy()).to(dev) for a in hb[:3]]
+pb16 = torch.from_numpy(gb.view(np.int16).copy()).view(torch.bfloat16).to(dev)
+segs.append((tb[0], tb[1], tb[2], pb16, pb16, nb))
 tab = kernels.AdamTable(segs, dev)
 hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
 sc = torch.zeros(4, dtype=torch.float64, device=dev)
-for step in (1, 2):
+for step in (1,):
     sq = float(sum(np.dot(h[3].astype(np.float64), h[3]) for h in host))
     sc[0] = sq
-    kernels.adam(tab, hp, step, sc, torch.bfloat16)
+    kernels.adam(tab, hp, step, sc, torch.bfloat16, grad_scale=0.125)
     torch.cuda.synchronize()
     coef = arith.clip_coef(sq, 1.0)
     for h, d in zip(host, segs):
@@ -292,7 +301,7 @@ for step in (1, 2):
         assert np.array_equal(d[4].cpu().view(torch.int16).numpy().view(np.uint16), r16)
         h[0], h[1], h[2] = rp, rm, rv
 sc[1] = 1.0
-kernels.adam(tab, hp, 3, sc, torch.bfloat16)
+kernels.adam(tab, hp, 3, sc, torch.bfloat16, grad_scale=0.125)
 torch.cuda.synchronize()
 for h, d in zip(host, segs):
     assert np.array_equal(d[0].cpu().numpy(), h[0])
@@ -313,3 +322,49 @@ def test_adam_variants_bit_exact(cuda, variant):
     out = subprocess.run([sys.executable, "-c", _VARIANT_SCRIPT, root], env=env, capture_output=True, text=True,
                          timeout=300)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_adam_compute_dtype_grads_equal_released_path(cuda):
+    """World-1 fused path: K4 reading the bf16 gradient in place (unscaled
+    in-register) == K3 release to fp32 + K4, bit for bit; mixed segment kinds."""
+    rng = np.random.default_rng(31)
+    inv_scale = 1.0 / 256
+    sizes = [5, 4096, 9000, 300_000]
+    segs, host = [], []
+    sq = 0.0
+    for j, n in enumerate(sizes):
+        p = (rng.standard_normal(n) * 0.02).astype(np.float32)
+        m = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+        v = (rng.random(n) * 1e-6).astype(np.float32)
+        gbits = arith.f32_to_bf16_bits((rng.standard_normal(n) * 40).astype(np.float32))
+        g, s, _ = arith.release([gbits], inv_scale)
+        sq += s
+        host.append((p, m, v, g))
+        P, M, V = (torch.from_numpy(a.copy()).to(cuda) for a in (p, m, v))
+        p16 = torch.from_numpy(gbits.view(np.int16).copy()).view(torch.bfloat16).to(cuda)
+        if j % 2 == 0:  # in place: gradient read from, and parameter written to, the same bf16 buffer
+            segs.append((P, M, V, p16, p16, n))
+        else:           # released fp32 gradient
+            segs.append((P, M, V, torch.from_numpy(g).to(cuda), torch.empty_like(p16), n))
+    sc = torch.tensor([sq, 0, 0, 0], dtype=torch.float64, device=cuda)
+    # the norm-only release accumulates the same sum of squares
+    sc2 = torch.zeros(4, dtype=torch.float64, device=cuda)
+    for (P, M, V, g, p16, n), (p, m, v, gg) in zip(segs, host):
+        bits = torch.from_numpy(arith.from_f32(gg / np.float32(inv_scale), "bf16").view(np.int16)).view(torch.bfloat16)
+    for j, ((P, M, V, g, p16, n), (p, m, v, gg)) in enumerate(zip(segs, host)):
+        if j % 2 == 0:
+            kernels.release(None, [g.data_ptr()], n, torch.bfloat16, inv_scale, sc2)
+    torch.cuda.synchronize()
+    want_even = sum(float(np.dot(h[3].astype(np.float64), h[3])) for j, h in enumerate(host) if j % 2 == 0)
+    assert sc2[0].item() == pytest.approx(want_even, rel=1e-12)
+    tab = kernels.AdamTable(segs, cuda)
+    kernels.adam(tab, HP, 2, sc, torch.bfloat16, grad_scale=inv_scale)
+    torch.cuda.synchronize()
+    coef = arith.clip_coef(sq, HP["max_norm"])
+    for (P, M, V, g, p16, n), (p, m, v, gg) in zip(segs, host):
+        rp, rm, rv, r16 = arith.adamw(p, m, v, gg, 2, HP["lr"], HP["beta1"], HP["beta2"], HP["eps"],
+                                      HP["weight_decay"], coef)
+        assert np.array_equal(P.cpu().numpy(), rp)
+        assert np.array_equal(M.cpu().numpy(), rm)
+        assert np.array_equal(V.cpu().numpy(), rv)
+        assert np.array_equal(_bits(p16), r16)
