@@ -349,8 +349,6 @@ def test_adam_compute_dtype_grads_equal_released_path(cuda):
     sc = torch.tensor([sq, 0, 0, 0], dtype=torch.float64, device=cuda)
     # the norm-only release accumulates the same sum of squares
     sc2 = torch.zeros(4, dtype=torch.float64, device=cuda)
-    for (P, M, V, g, p16, n), (p, m, v, gg) in zip(segs, host):
-        bits = torch.from_numpy(arith.from_f32(gg / np.float32(inv_scale), "bf16").view(np.int16)).view(torch.bfloat16)
     for j, ((P, M, V, g, p16, n), (p, m, v, gg)) in enumerate(zip(segs, host)):
         if j % 2 == 0:
             kernels.release(None, [g.data_ptr()], n, torch.bfloat16, inv_scale, sc2)
