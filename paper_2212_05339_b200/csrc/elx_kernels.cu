@@ -547,10 +547,9 @@ __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
 // coalesced stores. kStages tiles are in flight per CTA, so DRAM reads never
 // wait on the arithmetic. Partial or misaligned tiles (segment tails) are
 // handled by the consumers straight from global memory.
-constexpr int kTmaTile = 2048;                 // elements per tile
-constexpr int kTmaConsumers = 256;             // 8 warps x 32 lanes; 8 elements each
-constexpr int kTmaThreads = kTmaConsumers + 32;
-constexpr int kTmaStageBytes = 4 * kTmaTile * 4;
+// Shape parameters: kTile elements per tile (one stage = 16*kTile bytes for
+// four fp32 arrays), kCW consumer warps (kTile / (32*kCW) elements per
+// consumer thread, a multiple of 4), kStages stages in flight.
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -592,27 +591,30 @@ struct TileRef {
 };
 
 // Tiles are enumerated as (segment-table tile of ELX_ADAM_TILE elements, sub-tile
-// of kTmaTile); producer and consumers walk the same sequence.
-constexpr int kTmaSub = ELX_ADAM_TILE / kTmaTile;
-static_assert(kTmaSub * kTmaTile == ELX_ADAM_TILE, "sub-tiling");
-
+// of kTile); producer and consumers walk the same sequence.
+template <int kTile>
 __device__ __forceinline__ TileRef locate(const elx_adam_seg* segs, int nseg, int& s, int64_t t, int sub) {
   while (s + 1 < nseg && segs[s + 1].tile0 <= t) ++s;
   TileRef r;
   r.seg = s;
-  r.base = (t - segs[s].tile0) * ELX_ADAM_TILE + (int64_t)sub * kTmaTile;
-  r.cnt = min((int64_t)kTmaTile, segs[s].n - r.base);
-  r.tma = r.cnt == kTmaTile && aligned16(segs[s].p32 + r.base) && aligned16(segs[s].m + r.base) &&
+  r.base = (t - segs[s].tile0) * ELX_ADAM_TILE + (int64_t)sub * kTile;
+  r.cnt = min((int64_t)kTile, segs[s].n - r.base);
+  r.tma = r.cnt == kTile && aligned16(segs[s].p32 + r.base) && aligned16(segs[s].m + r.base) &&
           aligned16(segs[s].v + r.base) &&
           aligned16(static_cast<const char*>(segs[s].g) + (segs[s].g_dtype == ELX_F32 ? 4 : 2) * r.base) &&
           ((reinterpret_cast<uintptr_t>(static_cast<char*>(segs[s].p16) + 2 * r.base) & 7u) == 0);
   return r;
 }
 
-template <typename T16, int kStages>
-__global__ void __launch_bounds__(kTmaThreads, 1)
+template <typename T16, int kStages, int kTile, int kCW>
+__global__ void __launch_bounds__(kCW * 32 + 32, 1)
     adam_tma_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k,
                     const double* __restrict__ sc) {
+  constexpr int kCons = kCW * 32;
+  constexpr int kSub = ELX_ADAM_TILE / kTile;
+  constexpr int kStageBytes = 16 * kTile;
+  constexpr int kU = kTile / (kCons * 4);  // float4 vectors per consumer thread
+  static_assert(kSub * kTile == ELX_ADAM_TILE && kU * kCons * 4 == kTile, "tile shape");
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float* stage_base = reinterpret_cast<float*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kStages];
@@ -621,7 +623,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&full[i], 1);
-      mbar_init(&empty[i], kTmaConsumers / 32);
+      mbar_init(&empty[i], kCons / 32);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -629,24 +631,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   const bool skip = sc[1] != 0.0;
   const float coef = clip_coef(sc, k.max_norm);
 
-  if (warp == kTmaConsumers / 32) {  // ---------------- producer warp
+  if (warp == kCons / 32) {  // ---------------- producer warp
     if (lane == 0) {
       int s = 0;
       int64_t q = 0;  // TMA tiles issued
-      for (int64_t tt = blockIdx.x; tt < ntiles * kTmaSub; tt += gridDim.x) {
-        const TileRef r = locate(segs, nseg, s, tt / kTmaSub, (int)(tt % kTmaSub));
+      for (int64_t tt = blockIdx.x; tt < ntiles * kSub; tt += gridDim.x) {
+        const TileRef r = locate<kTile>(segs, nseg, s, tt / kSub, (int)(tt % kSub));
         if (!r.tma) continue;
         const int st = (int)(q % kStages);
         const uint32_t ph = (uint32_t)((q / kStages) & 1);
         mbar_wait(&empty[st], ph ^ 1u);
-        float* dst = stage_base + (size_t)st * (kTmaStageBytes / 4);
+        float* dst = stage_base + (size_t)st * (kStageBytes / 4);
         const elx_adam_seg& sg = segs[r.seg];
         const int gsz = sg.g_dtype == ELX_F32 ? 4 : 2;
-        mbar_expect_tx(&full[st], 3 * kTmaTile * 4 + kTmaTile * gsz);
-        tma_load_1d(dst, sg.p32 + r.base, kTmaTile * 4, &full[st]);
-        tma_load_1d(dst + kTmaTile, sg.m + r.base, kTmaTile * 4, &full[st]);
-        tma_load_1d(dst + 2 * kTmaTile, sg.v + r.base, kTmaTile * 4, &full[st]);
-        tma_load_1d(dst + 3 * kTmaTile, static_cast<const char*>(sg.g) + (int64_t)gsz * r.base, kTmaTile * gsz,
+        mbar_expect_tx(&full[st], 3 * kTile * 4 + kTile * gsz);
+        tma_load_1d(dst, sg.p32 + r.base, kTile * 4, &full[st]);
+        tma_load_1d(dst + kTile, sg.m + r.base, kTile * 4, &full[st]);
+        tma_load_1d(dst + 2 * kTile, sg.v + r.base, kTile * 4, &full[st]);
+        tma_load_1d(dst + 3 * kTile, static_cast<const char*>(sg.g) + (int64_t)gsz * r.base, kTile * gsz,
                     &full[st]);
         ++q;
       }
@@ -657,8 +659,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   // -------------------------------------------------- consumer warps
   int s = 0;
   int64_t q = 0;
-  for (int64_t tt = blockIdx.x; tt < ntiles * kTmaSub; tt += gridDim.x) {
-    const TileRef r = locate(segs, nseg, s, tt / kTmaSub, (int)(tt % kTmaSub));
+  for (int64_t tt = blockIdx.x; tt < ntiles * kSub; tt += gridDim.x) {
+    const TileRef r = locate<kTile>(segs, nseg, s, tt / kSub, (int)(tt % kSub));
     if (r.cnt <= 0) continue;
     const elx_adam_seg& sg = segs[r.seg];
     float* __restrict__ p32 = sg.p32 + r.base;
@@ -667,7 +669,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     T16* __restrict__ p16 = static_cast<T16*>(sg.p16) + r.base;
     if (!r.tma) {  // tail / misaligned tile: straight from global memory
       const int gdt = sg.g_dtype;
-      for (int64_t i = threadIdx.x; i < r.cnt; i += kTmaConsumers) {
+      for (int64_t i = threadIdx.x; i < r.cnt; i += kCons) {
         float P = p32[i];
         if (!skip) {
           float M = m[i], V = v[i];
@@ -684,22 +686,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const uint32_t ph = (uint32_t)((q / kStages) & 1);
     ++q;
     mbar_wait(&full[st], ph);
-    const float* src = stage_base + (size_t)st * (kTmaStageBytes / 4);
-    float4 P[2], M[2], V[2], G[2];
+    const float* src = stage_base + (size_t)st * (kStageBytes / 4);
+    float4 P[kU], M[kU], V[kU], G[kU];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = u * kTmaConsumers + threadIdx.x;  // float4 index within the tile
+    for (int u = 0; u < kU; ++u) {
+      const int j = u * kCons + threadIdx.x;  // float4 index within the tile
       P[u] = reinterpret_cast<const float4*>(src)[j];
-      M[u] = reinterpret_cast<const float4*>(src + kTmaTile)[j];
-      V[u] = reinterpret_cast<const float4*>(src + 2 * kTmaTile)[j];
-      G[u] = sg.g_dtype == ELX_F32 ? reinterpret_cast<const float4*>(src + 3 * kTmaTile)[j]
-                                   : cvt4_grad<T16>(reinterpret_cast<const uint2*>(src + 3 * kTmaTile)[j], k.grad_scale);
+      M[u] = reinterpret_cast<const float4*>(src + kTile)[j];
+      V[u] = reinterpret_cast<const float4*>(src + 2 * kTile)[j];
+      G[u] = sg.g_dtype == ELX_F32 ? reinterpret_cast<const float4*>(src + 3 * kTile)[j]
+                                   : cvt4_grad<T16>(reinterpret_cast<const uint2*>(src + 3 * kTile)[j], k.grad_scale);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);  // stage may be refilled: operands are in registers
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int j = u * kTmaConsumers + threadIdx.x;
+    for (int u = 0; u < kU; ++u) {
+      const int j = u * kCons + threadIdx.x;
       if (!skip) {
         adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
         adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
@@ -714,20 +716,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
   }
 }
 
-template <typename T16, int kStages>
+template <typename T16, int kStages, int kTile, int kCW>
 int launch_adam_tma(const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
                     cudaStream_t st) {
-  const int smem = kStages * kTmaStageBytes;
+  constexpr int kThreads = kCW * 32 + 32;
+  const int smem = kStages * 16 * kTile;
+  auto kern = adam_tma_kernel<T16, kStages, kTile, kCW>;
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(adam_tma_kernel<T16, kStages>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     configured = true;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, adam_tma_kernel<T16, kStages>, kTmaThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  const int grid = (int)std::min<int64_t>(ntiles * kTmaSub, (int64_t)sm_count() * per_sm);
-  adam_tma_kernel<T16, kStages><<<grid, kTmaThreads, smem, st>>>(segs, nseg, ntiles, k, sc);
+  const int grid = (int)std::min<int64_t>(ntiles * (ELX_ADAM_TILE / kTile), (int64_t)sm_count() * per_sm);
+  kern<<<grid, kThreads, smem, st>>>(segs, nseg, ntiles, k, sc);
   return check_launch("elx_adam (tma)");
 }
 
@@ -746,15 +750,19 @@ int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles,
     return check_launch("elx_adam");
   };
   switch (variant) {
-    case 5: return launch_adam_tma<T16, 4>(segs, nseg, ntiles, k, sc, st);
-    case 6: return launch_adam_tma<T16, 6>(segs, nseg, ntiles, k, sc, st);
+    case 5: return launch_adam_tma<T16, 4, 2048, 8>(segs, nseg, ntiles, k, sc, st);
+    case 6: return launch_adam_tma<T16, 6, 2048, 8>(segs, nseg, ntiles, k, sc, st);
+    case 9: return launch_adam_tma<T16, 3, 2048, 16>(segs, nseg, ntiles, k, sc, st);
+    case 10: return launch_adam_tma<T16, 4, 1024, 8>(segs, nseg, ntiles, k, sc, st);
+    case 11: return launch_adam_tma<T16, 3, 1024, 8>(segs, nseg, ntiles, k, sc, st);
+    case 12: return launch_adam_tma<T16, 4, 2048, 16>(segs, nseg, ntiles, k, sc, st);
     case 8: return go(adam_kernel<T16, 2, 3>);
     case 1: return go(adam_kernel<T16, 4, 2>);
     case 2: return go(adam_kernel<T16, 4, 3>);
     case 3: return go(adam_kernel<T16, 2, 4>);
     case 4: return go(adam_kernel<T16, 1, 6>);
     default:  // 0 / 7: TMA-staged, 3 stages x 32 KB, 2 CTAs per SM (profiles/r01_kernel_variants.md)
-      return launch_adam_tma<T16, 3>(segs, nseg, ntiles, k, sc, st);
+      return launch_adam_tma<T16, 3, 2048, 8>(segs, nseg, ntiles, k, sc, st);
   }
 }
 

@@ -309,7 +309,7 @@ print("ok")
 """
 
 
-@pytest.mark.parametrize("variant", [0, 1, 3, 5, 6, 8])
+@pytest.mark.parametrize("variant", [0, 1, 3, 5, 6, 8, 9, 10, 11, 12])
 def test_adam_variants_bit_exact(cuda, variant):
     """Every K4 variant (incl. the TMA-staged ones, 5-7) is bit-exact vs the oracle."""
     import os
