@@ -54,6 +54,10 @@ const char* elx_last_error(void);
 /* Number of kernels this library launched in this process (all streams).
  * bench.py reports the delta over its timed region as `gpu_launches`. */
 int64_t elx_launch_count(void);
+/* sizeof of the ABI structs, for binding checks: 0 elx_event, 1
+ * elx_sim_counters, 2 elx_member, 3 elx_adam_seg, 4 elx_adam_hp,
+ * 5 elx_cpu_seg; -1 for an unknown id. */
+int64_t elx_sizeof(int32_t which);
 
 /* ------------------------------------------------- host: layout + schedule
  *
@@ -201,8 +205,18 @@ typedef struct {
   double grad_scale; /* multiplies compute-dtype gradients (1 / loss scale) */
   int32_t p16_dtype; /* ELX_BF16 or ELX_F16 */
   int32_t pad_;
+  /* Device step (used when elx_adam's `step` is 0): the step number is
+   * t = step_scalars[2] + 1 (completed, non-skipped steps + 1), read on the
+   * device, and the bias corrections come from caller-owned DEVICE tables
+   * computed on the host in double exactly as the oracle does:
+   * bc1_table[t] = 1 - beta1^t, bc2s_table[t] = (float)sqrt(1 - beta2^t).
+   * This keeps the whole optimizer step free of host synchronisation. */
+  const double* bc1_table;
+  const float* bc2s_table;
+  int64_t table_len;
 } elx_adam_hp;
 
+/* step >= 1: host step number. step == 0: device step (see elx_adam_hp). */
 int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const elx_adam_hp* hp,
              int64_t step, const double* step_scalars, void* stream);
 
@@ -213,6 +227,9 @@ int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const e
 int elx_norm_finalize(const double* step_scalars, double max_norm, double* out3, void* stream);
 /* step_scalars[0..1] <- 0 */
 int elx_step_reset(double* step_scalars, void* stream);
+/* End of an optimizer step on the device: if step_scalars[1] == 0 (no
+ * overflow) step_scalars[2] += 1; then step_scalars[0..1] <- 0. */
+int elx_step_advance(double* step_scalars, void* stream);
 
 /* ------------------------------------------------------- K6 offload
  * Pinned-host <-> HBM moves for CPU-home chunks on a side stream, with an

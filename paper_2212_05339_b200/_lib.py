@@ -64,7 +64,8 @@ class AdamSeg(ctypes.Structure):
 class AdamHP(ctypes.Structure):
     _fields_ = [("lr", c_f64), ("beta1", c_f64), ("beta2", c_f64), ("eps", c_f64),
                 ("weight_decay", c_f64), ("max_norm", c_f64), ("grad_scale", c_f64),
-                ("p16_dtype", c_i32), ("pad_", c_i32)]
+                ("p16_dtype", c_i32), ("pad_", c_i32), ("bc1_table", c_vp), ("bc2s_table", c_vp),
+                ("table_len", c_i64)]
 
 
 class CpuSeg(ctypes.Structure):
@@ -77,6 +78,7 @@ _SIGNATURES = {
     "elx_abi_version": (c_i32, []),
     "elx_last_error": (ctypes.c_char_p, []),
     "elx_launch_count": (c_i64, []),
+    "elx_sizeof": (c_i64, [c_i32]),
     "elx_layout_pack": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "elx_schedule": (ctypes.c_int, [c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_chunk_pack": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_vp, c_i32, c_vp]),
@@ -86,6 +88,7 @@ _SIGNATURES = {
     "elx_adam": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "elx_norm_finalize": (ctypes.c_int, [c_vp, c_f64, c_vp, c_vp]),
     "elx_step_reset": (ctypes.c_int, [c_vp, c_vp]),
+    "elx_step_advance": (ctypes.c_int, [c_vp, c_vp]),
     "elx_copy_h2d": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_copy_d2h": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_cpu_adam": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i32]),
@@ -113,6 +116,10 @@ def load() -> ctypes.CDLL:
         fn.argtypes = args
     if lib.elx_abi_version() != 1:
         raise ExtensionMissingError("libelixir_b200 ABI version mismatch")
+    for i, st in enumerate((Event, SimCounters, Member, AdamSeg, AdamHP, CpuSeg)):
+        if lib.elx_sizeof(i) != ctypes.sizeof(st):
+            raise ExtensionMissingError(f"libelixir_b200 struct {st.__name__} layout mismatch "
+                                        f"({lib.elx_sizeof(i)} != {ctypes.sizeof(st)}): rebuild the library")
     _lib = lib
     return lib
 

@@ -27,4 +27,16 @@ const char* elx_last_error(void) { return elx::t_error.c_str(); }
 
 int64_t elx_launch_count(void) { return elx::g_launches.load(std::memory_order_relaxed); }
 
+int64_t elx_sizeof(int32_t which) {
+  switch (which) {
+    case 0: return (int64_t)sizeof(elx_event);
+    case 1: return (int64_t)sizeof(elx_sim_counters);
+    case 2: return (int64_t)sizeof(elx_member);
+    case 3: return (int64_t)sizeof(elx_adam_seg);
+    case 4: return (int64_t)sizeof(elx_adam_hp);
+    case 5: return (int64_t)sizeof(elx_cpu_seg);
+    default: return -1;
+  }
+}
+
 }  // extern "C"

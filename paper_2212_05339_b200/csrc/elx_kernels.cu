@@ -408,7 +408,26 @@ struct AdamK {
   float eps;
   float grad_scale;  // for compute-dtype gradients: g = float(g16) * grad_scale
   double max_norm;
+  // device step: t = sc[2] + 1, bias corrections from host-computed tables
+  int device_step;
+  double lr;
+  const double* bc1;
+  const float* bc2s;
+  int64_t table_len;
 };
+
+// Resolve the step-dependent constants (host-provided, or from the device
+// step counter and the bias-correction tables).
+__device__ __forceinline__ AdamK resolve_step(const AdamK& k, const double* sc) {
+  AdamK r = k;
+  if (k.device_step) {
+    int64_t t = (int64_t)sc[2] + 1;
+    if (t >= k.table_len) t = k.table_len - 1;  // host keeps the table ahead of the step count
+    r.neg_step = (float)(-(k.lr / k.bc1[t]));
+    r.bc2_sqrt = k.bc2s[t];
+  }
+  return r;
+}
 
 // Gradient element i of a segment: fp32 (already released), or the
 // compute-dtype gradient unscaled in-register exactly as K3 would do it.
@@ -462,12 +481,13 @@ __device__ __forceinline__ void store4(T16* p16, float a, float b, float c, floa
 // against loads in flight. kMinBlocks is the __launch_bounds__ occupancy.
 template <typename T16, int kU, int kMinBlocks>
 __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
-    adam_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k,
+    adam_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k0,
                 const double* __restrict__ sc) {
   constexpr int kPasses = kAdamUnroll / kU;
   static_assert(kPasses * kU == kAdamUnroll, "unroll must divide the tile");
   const bool skip = sc[1] != 0.0;
-  const float coef = clip_coef(sc, k.max_norm);
+  const float coef = clip_coef(sc, k0.max_norm);
+  const AdamK k = resolve_step(k0, sc);
   int s = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     while (s + 1 < nseg && segs[s + 1].tile0 <= t) ++s;  // tiles ascend per CTA
@@ -608,7 +628,7 @@ __device__ __forceinline__ TileRef locate(const elx_adam_seg* segs, int nseg, in
 
 template <typename T16, int kStages, int kTile, int kCW>
 __global__ void __launch_bounds__(kCW * 32 + 32, 1)
-    adam_tma_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k,
+    adam_tma_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k0,
                     const double* __restrict__ sc) {
   constexpr int kCons = kCW * 32;
   constexpr int kSub = ELX_ADAM_TILE / kTile;
@@ -629,7 +649,8 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1)
   }
   __syncthreads();
   const bool skip = sc[1] != 0.0;
-  const float coef = clip_coef(sc, k.max_norm);
+  const float coef = clip_coef(sc, k0.max_norm);
+  const AdamK k = resolve_step(k0, sc);
 
   if (warp == kCons / 32) {  // ---------------- producer warp
     if (lane == 0) {
@@ -783,6 +804,12 @@ __global__ void step_reset_kernel(double* sc) {
   sc[1] = 0.0;
 }
 
+__global__ void step_advance_kernel(double* sc) {
+  if (sc[1] == 0.0) sc[2] += 1.0;
+  sc[0] = 0.0;
+  sc[1] = 0.0;
+}
+
 }  // namespace
 
 // ======================================================================= ABI
@@ -861,13 +888,21 @@ int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const e
   elx::clear_error();
   if (!hp || !step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   if (nseg < 0 || ntiles < 0 || (nseg > 0 && !segs_dev)) return elx::fail(ELX_ERR_VALIDATION, "bad segment table");
-  if (step < 1) return elx::fail(ELX_ERR_VALIDATION, "step must be >= 1");
+  if (step < 0) return elx::fail(ELX_ERR_VALIDATION, "step must be >= 1 (host) or 0 (device step)");
+  if (step == 0 && (!hp->bc1_table || !hp->bc2s_table || hp->table_len < 2))
+    return elx::fail(ELX_ERR_VALIDATION, "device step needs bias-correction tables");
   if (!(hp->lr >= 0) || !(hp->eps > 0) || !(hp->beta1 >= 0 && hp->beta1 < 1) || !(hp->beta2 >= 0 && hp->beta2 < 1))
     return elx::fail(ELX_ERR_VALIDATION, "invalid Adam hyper-parameters");
   if (nseg == 0 || ntiles == 0) return ELX_OK;
   AdamK k;
-  const double bc1 = 1.0 - std::pow(hp->beta1, (double)step);
-  const double bc2 = 1.0 - std::pow(hp->beta2, (double)step);
+  const double hstep = step > 0 ? (double)step : 1.0;
+  const double bc1 = 1.0 - std::pow(hp->beta1, hstep);
+  const double bc2 = 1.0 - std::pow(hp->beta2, hstep);
+  k.device_step = step == 0;
+  k.lr = hp->lr;
+  k.bc1 = hp->bc1_table;
+  k.bc2s = hp->bc2s_table;
+  k.table_len = hp->table_len;
   k.decay = (float)(1.0 - hp->lr * hp->weight_decay);
   k.omb1 = (float)(1.0 - hp->beta1);
   k.b2 = (float)hp->beta2;
@@ -899,6 +934,13 @@ int elx_step_reset(double* step_scalars, void* stream) {
   if (!step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   step_reset_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_scalars);
   return check_launch("elx_step_reset");
+}
+
+int elx_step_advance(double* step_scalars, void* stream) {
+  elx::clear_error();
+  if (!step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  step_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_scalars);
+  return check_launch("elx_step_advance");
 }
 
 int elx_copy_h2d(void* dst_dev, const void* src_host, int64_t bytes, void* stream, void* event) {

@@ -273,8 +273,9 @@ class ElixirGPT2:
             del grads, pgrads, params, out
         fx.release_shared(self.wte)
         done = fx.finish()
-        found_inf, _ = self.optimizer.step(done, grad_scale=1.0 / self.scaler.scale)
-        self.scaler.update(found_inf)
+        stats = self.optimizer.step(done, grad_scale=1.0 / self.scaler.scale)
+        if self.scaler.dynamic:  # fp16: the next step's scale depends on this step's overflow (syncs)
+            self.scaler.update(stats.found_inf)
         self.last_loss = loss
         return loss
 

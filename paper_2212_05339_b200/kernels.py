@@ -139,17 +139,51 @@ class AdamTable:
         self._keep = [s[:5] for s in segs]
 
 
-def _hp(hp: dict, p16_dtype: torch.dtype, grad_scale: float):
-    return _lib.AdamHP(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"],
-                       hp.get("max_norm", 0.0) or 0.0, float(grad_scale), elx_dtype(p16_dtype), 0)
+def _hp(hp: dict, p16_dtype: torch.dtype, grad_scale: float, bias_tables=None):
+    h = _lib.AdamHP(hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"],
+                    hp.get("max_norm", 0.0) or 0.0, float(grad_scale), elx_dtype(p16_dtype), 0)
+    if bias_tables is not None:
+        bc1, bc2s = bias_tables
+        h.bc1_table, h.bc2s_table, h.table_len = bc1.data_ptr(), bc2s.data_ptr(), bc1.numel()
+    return h
+
+
+class BiasTables:
+    """Device tables of Adam's bias corrections for the device-step mode of
+    K4: bc1[t] = 1 - beta1**t (float64), bc2s[t] = float32((1 - beta2**t)**0.5),
+    computed on the host with the oracle's float64 formulas."""
+
+    def __init__(self, beta1: float, beta2: float, device, length: int = 4096):
+        self.beta1, self.beta2, self.device = beta1, beta2, device
+        self.bc1 = self.bc2s = None
+        self._build(length)
+
+    def _build(self, length: int) -> None:
+        import numpy as np
+        t = np.arange(length, dtype=np.float64)
+        bc1 = 1.0 - np.power(self.beta1, t)
+        bc2s = np.power(1.0 - np.power(self.beta2, t), 0.5).astype(np.float32)
+        bc1[0] = 1.0  # t = 0 is never used (steps start at 1); keep it finite
+        bc2s[0] = 1.0
+        self.bc1 = torch.from_numpy(bc1).to(self.device)
+        self.bc2s = torch.from_numpy(bc2s).to(self.device)
+
+    def ensure(self, max_step: int) -> None:
+        if max_step + 2 > self.bc1.numel():
+            self._build(max(2 * self.bc1.numel(), max_step + 2))
+
+    def pair(self):
+        return self.bc1, self.bc2s
 
 
 def adam(table: AdamTable, hp: dict, step: int, step_scalars: torch.Tensor, p16_dtype: torch.dtype,
-         stream=None, grad_scale: float = 1.0) -> None:
+         stream=None, grad_scale: float = 1.0, bias_tables: BiasTables | None = None) -> None:
     """K4 over every segment of `table` in one launch. Segments whose
-    gradient is in the compute dtype are unscaled by `grad_scale` in-register."""
+    gradient is in the compute dtype are unscaled by `grad_scale` in-register.
+    step >= 1: host step; step == 0: device step (step_scalars[2] + 1) with
+    `bias_tables`."""
     lib = _lib.load()
-    h = _hp(hp, p16_dtype, grad_scale)
+    h = _hp(hp, p16_dtype, grad_scale, None if bias_tables is None else bias_tables.pair())
     rc = lib.elx_adam(table.dev.data_ptr(), table.nseg, table.ntiles, ctypes.byref(h), int(step),
                       step_scalars.data_ptr(), _stream(stream))
     _lib.check(rc, "elx_adam")
@@ -184,6 +218,12 @@ def norm_finalize(step_scalars: torch.Tensor, max_norm: float, out3: torch.Tenso
 def step_reset(step_scalars: torch.Tensor, stream=None) -> None:
     lib = _lib.load()
     _lib.check(lib.elx_step_reset(step_scalars.data_ptr(), _stream(stream)), "elx_step_reset")
+
+
+def step_advance(step_scalars: torch.Tensor, stream=None) -> None:
+    """Device-side end of step: count it unless it overflowed; clear Σg²/flag."""
+    lib = _lib.load()
+    _lib.check(lib.elx_step_advance(step_scalars.data_ptr(), _stream(stream)), "elx_step_advance")
 
 
 def copy_h2d(dst: torch.Tensor, src_host: torch.Tensor, nbytes: int | None = None, stream=None,

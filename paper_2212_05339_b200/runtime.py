@@ -526,6 +526,34 @@ class ChunkFetcher:
                                 mgr.step_scalars, stream=comm)
 
 
+class StepStats:
+    """Result of one optimizer step; reading it synchronises with the step's
+    scalar snapshot only (not the whole device)."""
+
+    def __init__(self, host_slot: torch.Tensor, ready: torch.cuda.Event):
+        self._slot, self._ready, self._vals = host_slot, ready, None
+
+    def scalars(self) -> tuple[float, float]:
+        if self._vals is None:
+            self._ready.synchronize()
+            self._vals = (float(self._slot[0]), float(self._slot[1]))
+        return self._vals
+
+    @property
+    def found_inf(self) -> bool:
+        sq, flag = self.scalars()
+        return flag != 0.0 or not math.isfinite(sq)
+
+    @property
+    def grad_norm(self) -> float:
+        sq, _ = self.scalars()
+        return math.sqrt(sq) if math.isfinite(sq) else float("inf")
+
+    def __iter__(self):  # (found_inf, grad_norm) unpacking, as the host-sync API returned
+        yield self.found_inf
+        yield self.grad_norm
+
+
 class HybridAdam:
     """Chunk-wise fused mixed-precision AdamW: GPU-home shards on the device
     (K4, update rate v_g), CPU-home shards on host threads (elx_cpu_adam,
@@ -544,11 +572,10 @@ class HybridAdam:
 
     def __init__(self, manager: ChunkManager, *, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.01, max_norm: float | None = 1.0, cpu_threads: int | None = None,
-                 overlap: bool = False):
+                 overlap: bool = False, device_step: bool = True):
         self.mgr = manager
         self.hp = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
                        max_norm=max_norm or 0.0)
-        self.step_count = 0
         self.cpu_threads = cpu_threads or max(1, min(32, len(os.sched_getaffinity(0))))
         self.overlap = overlap
         m = manager
@@ -578,8 +605,16 @@ class HybridAdam:
             if n > 0:
                 self.cpu_segs[c] = (m.h_p32[r], m.h_m[r], m.h_v[r], m.h_g32[r], m.h_p16[r], n)
         self.stream = torch.cuda.Stream(device=m.device) if overlap else None
-        self._host_sc = torch.zeros(4, dtype=torch.float64, pin_memory=torch.cuda.is_available())
-        self.last = dict(found_inf=False, grad_norm=0.0, skipped=0)
+        pin = torch.cuda.is_available()
+        # ring of pinned snapshots of the step scalars (read lazily by StepStats / the CPU thread)
+        self._host_ring = [torch.zeros(4, dtype=torch.float64, pin_memory=pin) for _ in range(8)]
+        self.device_step = device_step
+        self.tables = kernels.BiasTables(betas[0], betas[1], m.device) if device_step else None
+        self._issued = 0          # step() calls since construction / checkpoint load
+        self._step0 = 0           # completed steps at that point
+        self._host_steps = 0      # host-mode step counter
+        self._cpu_steps = 0       # CPU-home update's own counter (same rule as step_scalars[2])
+        self.last_stats = None
         self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         self.time_adam = False
         self.done_event: torch.cuda.Event | None = None
@@ -626,6 +661,14 @@ class HybridAdam:
                 raise self._cpu_error
 
     # ------------------------------------------------------------ checkpoint
+    @property
+    def step_count(self) -> int:
+        """Completed (non-skipped) optimizer steps — the device counter
+        step_scalars[2] is authoritative (reading it synchronises)."""
+        if not self.device_step:
+            return self._host_steps
+        return int(self.mgr.step_scalars[2].item())
+
     def state_dict(self) -> dict:
         """This rank's fp32 master / m / v shards (GPU-home, CPU-home, shared)
         and the step count — the complete training state of the chunk path."""
@@ -651,25 +694,33 @@ class HybridAdam:
             getattr(m, "h_" + k).copy_(state["cpu"][k])
             for pid, sp in m.shared.items():
                 getattr(sp, k).copy_(state["shared"][pid][k])
-        self.step_count = int(state["step"])
+        steps = int(state["step"])
+        self._host_steps = self._cpu_steps = steps
+        self._issued = 0
+        self._step0 = steps
         sc = torch.tensor([0.0, 1.0, 0.0, 0.0], dtype=torch.float64, device=m.device)  # "skip": restore only
-        kernels.adam(self.table, self.hp, max(1, self.step_count), sc, m.dtype)
+        kernels.adam(self.table, self.hp, max(1, steps), sc, m.dtype)
         if self.cpu_segs:
-            kernels.cpu_adam(list(self.cpu_segs.values()), self.hp, max(1, self.step_count), (0.0, 1.0), m.dtype,
+            kernels.cpu_adam(list(self.cpu_segs.values()), self.hp, max(1, steps), (0.0, 1.0), m.dtype,
                              self.cpu_threads)
         if m.world > 1:
             for sp in m.shared.values():
                 m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
+        m.step_scalars.zero_()
+        m.step_scalars[2] = float(steps)
         torch.cuda.synchronize(m.device)
 
     # ------------------------------------------------------------ step
-    def step(self, releases_done: torch.cuda.Event | None = None, grad_scale: float = 1.0) -> tuple[bool, float]:
-        """All-reduce norm/overflow, then update every shard. Returns
-        (found_inf, grad_norm) — one host sync per step (GradScaler also
-        reads found_inf on the host). `releases_done` is the event
-        ChunkFetcher.finish() returns (None: synchronise the device);
-        `grad_scale` = 1/loss_scale, applied in-register to compute-dtype
-        gradients (world 1)."""
+    def step(self, releases_done: torch.cuda.Event | None = None, grad_scale: float = 1.0) -> "StepStats":
+        """All-reduce norm/overflow, then update every shard.
+
+        Device-step mode (default): no host synchronisation — the overflow
+        skip, the clip coefficient and the step number (step_scalars[2]) are
+        all read on the device, and the bias corrections come from device
+        tables. Returns a StepStats whose found_inf / grad_norm synchronise
+        only when read. `releases_done` is the event ChunkFetcher.finish()
+        returns (None: synchronise the device); `grad_scale` = 1/loss_scale,
+        applied in-register to compute-dtype gradients (world 1)."""
         self.grad_scale = float(grad_scale)
         m = self.mgr
         dev = m.device
@@ -680,17 +731,26 @@ class HybridAdam:
             cur.wait_event(releases_done)
         if m.world > 1:
             m.transport.all_reduce_sum(m.step_scalars[:2])
-        self._host_sc.copy_(m.step_scalars, non_blocking=True)
-        cur.synchronize()
+        slot = self._host_ring[self._issued % len(self._host_ring)]
+        slot.copy_(m.step_scalars, non_blocking=True)
+        snap = torch.cuda.Event()
+        snap.record(cur)
+        stats = StepStats(slot, snap)
+        self._issued += 1
         if self._cpu_thread is not None:
             self._cpu_thread.join()
-        sq, inf_flag = float(self._host_sc[0]), float(self._host_sc[1])
-        found_inf = inf_flag != 0.0 or not math.isfinite(sq)
-        step = self.step_count + (0 if found_inf else 1)
-        kstep = max(step, 1)
+        if self.device_step:
+            self.tables.ensure(self._step0 + self._issued)
+            kstep = 0
+        else:
+            found_inf = stats.found_inf
+            kstep = max(self._host_steps + (0 if found_inf else 1), 1)
+            if not found_inf:
+                self._host_steps += 1
         opt = self.stream if self.overlap else cur
         if opt is not cur:
             opt.wait_stream(cur)
+        tabs = self.tables if self.device_step else None
         if self.time_adam:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(opt)
@@ -699,7 +759,7 @@ class HybridAdam:
             if self.overlap:
                 for key, table in self.groups:
                     kernels.adam(table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt,
-                                 grad_scale=self.grad_scale)
+                                 grad_scale=self.grad_scale, bias_tables=tabs)
                     if key in m.shared and m.world > 1:
                         sp = m.shared[key]
                         m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
@@ -708,35 +768,48 @@ class HybridAdam:
                     self.pending[key] = ev
             else:
                 kernels.adam(self.table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt,
-                             grad_scale=self.grad_scale)
+                             grad_scale=self.grad_scale, bias_tables=tabs)
                 if m.world > 1:
                     for sp in m.shared.values():
                         m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
             if self.time_adam:
                 e1.record(opt)
                 self.adam_events.append((e0, e1))
-            kernels.step_reset(m.step_scalars, stream=opt)
+            if self.device_step:
+                kernels.step_advance(m.step_scalars, stream=opt)
+            else:
+                kernels.step_reset(m.step_scalars, stream=opt)
             self.done_event = torch.cuda.Event()
             self.done_event.record(opt)
         if self.cpu_segs:
             for ev in self.cpu_ready.values():
                 ev.clear()
-            args = (kstep, (sq, inf_flag))
-            self._cpu_thread = threading.Thread(target=self._cpu_update, args=args, daemon=True)
+            self._cpu_thread = threading.Thread(target=self._cpu_update, args=(stats,), daemon=True)
             self._cpu_thread.start()
-        if not found_inf:
-            self.step_count = step
-        self.last = dict(found_inf=found_inf, grad_norm=math.sqrt(sq) if math.isfinite(sq) else float("inf"),
-                         skipped=self.last["skipped"] + int(found_inf))
-        return found_inf, self.last["grad_norm"]
+        self.last_stats = stats
+        return stats
 
-    def _cpu_update(self, kstep: int, scalars) -> None:
-        """CPU-home shards in forward order, flagging each chunk when done."""
+    @property
+    def last(self) -> dict:
+        s = self.last_stats
+        if s is None:
+            return dict(found_inf=False, grad_norm=0.0)
+        return dict(found_inf=s.found_inf, grad_norm=s.grad_norm)
+
+    def _cpu_update(self, stats: "StepStats") -> None:
+        """CPU-home shards in forward order, flagging each chunk when done.
+        Runs on a host thread: it waits for this step's scalars (device ->
+        pinned copy), not the main thread."""
         try:
+            sq, flag = stats.scalars()
+            skip = flag != 0.0 or not math.isfinite(sq)
+            kstep = max(self._cpu_steps + (0 if skip else 1), 1)
             for c in sorted(self.cpu_segs):
-                kernels.cpu_adam([self.cpu_segs[c]], self.hp, kstep, scalars, self.mgr.dtype, self.cpu_threads,
+                kernels.cpu_adam([self.cpu_segs[c]], self.hp, kstep, (sq, flag), self.mgr.dtype, self.cpu_threads,
                                  grad_scale=self.grad_scale)
                 self.cpu_ready[c].set()
+            if not skip:
+                self._cpu_steps += 1
         except BaseException as exc:  # surfaced by wait_cpu / synchronize
             self._cpu_error = exc
             for ev in self.cpu_ready.values():

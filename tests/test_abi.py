@@ -32,12 +32,10 @@ def test_header_symbols_exported():
 
 
 def test_struct_layouts_match_header():
-    assert ctypes.sizeof(_lib.Event) == 24
-    assert ctypes.sizeof(_lib.SimCounters) == 56
-    assert ctypes.sizeof(_lib.Member) == 32
-    assert ctypes.sizeof(_lib.AdamSeg) == 64
-    assert ctypes.sizeof(_lib.AdamHP) == 64
-    assert ctypes.sizeof(_lib.CpuSeg) == 56
+    lib = _lib.load()
+    for i, st in enumerate((_lib.Event, _lib.SimCounters, _lib.Member, _lib.AdamSeg, _lib.AdamHP, _lib.CpuSeg)):
+        assert lib.elx_sizeof(i) == ctypes.sizeof(st), st.__name__
+    assert lib.elx_sizeof(99) == -1
 
 
 def test_abi_version_and_errors():
@@ -124,3 +122,34 @@ def test_host_adam_compute_dtype_grads():
     rp, rm, rv, r16 = arith.adamw(p, m, v, g, 3, 1e-3, 0.9, 0.999, 1e-8, 0.01, arith.clip_coef(sq, 1.0))
     assert np.array_equal(T[0].numpy(), rp) and np.array_equal(T[1].numpy(), rm) and np.array_equal(T[2].numpy(), rv)
     assert np.array_equal(p16.view(torch.int16).numpy().view(np.uint16), r16)
+
+
+def test_missing_extension_fails_loudly(tmp_path):
+    """No CPU fallback: without libelixir_b200.so every hot-path entry raises."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "from paper_2212_05339_b200 import errors, layout, profiles\n"
+        "try:\n"
+        "    layout.pack_chunks((profiles.ParameterSpec('a', 4),), 8)\n"
+        "except errors.ExtensionMissingError as e:\n"
+        "    print('raised', e)\n"
+    ) % str(HEADER.parents[1])
+    env = {"ELX_LIB": str(tmp_path / "missing.so"), "PATH": "/usr/bin:/bin"}
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=120)
+    assert "raised" in out.stdout, out.stderr
+
+
+def test_device_step_bias_tables_equal_oracle_constants():
+    """K4's device-step tables hold exactly the oracle's per-step constants
+    (float64 bias corrections; the same float32 casts)."""
+    for b1, b2, lr in ((0.9, 0.999, 1e-3), (0.8, 0.95, 3e-4)):
+        tab = kernels.BiasTables(b1, b2, "cpu", length=20_001)
+        bc1, bc2s = tab.bc1.numpy(), tab.bc2s.numpy()
+        for t in list(range(1, 300)) + list(range(300, 20_001, 97)):
+            k = arith.adam_consts(t, lr, b1, b2, 1e-8, 0.0)
+            assert np.float32(-(lr / bc1[t])) == k["neg_step"], t
+            assert bc2s[t] == k["bc2_sqrt"], t
+        tab.ensure(50_000)
+        assert tab.bc1.numel() >= 50_002

@@ -366,3 +366,32 @@ def test_adam_compute_dtype_grads_equal_released_path(cuda):
         assert np.array_equal(M.cpu().numpy(), rm)
         assert np.array_equal(V.cpu().numpy(), rv)
         assert np.array_equal(_bits(p16), r16)
+
+
+def test_adam_device_step_equals_host_step(cuda):
+    """K4 device-step mode (step number from step_scalars[2], bias corrections
+    from host-computed device tables) == host-step mode, bit for bit; and
+    elx_step_advance counts only non-overflow steps."""
+    host, dev = _segments(cuda, [4096 * 3 + 5, 77], 41)
+    host2, dev2 = _segments(cuda, [4096 * 3 + 5, 77], 41)
+    ta, tb = kernels.AdamTable(dev, cuda), kernels.AdamTable(dev2, cuda)
+    tabs = kernels.BiasTables(HP["beta1"], HP["beta2"], cuda, length=16)
+    sq = 3.0
+    for t in (1, 2, 3, 7):
+        sa = torch.tensor([sq, 0, 0, 0], dtype=torch.float64, device=cuda)
+        sb = torch.tensor([sq, 0, float(t - 1), 0], dtype=torch.float64, device=cuda)
+        kernels.adam(ta, HP, t, sa, torch.bfloat16)
+        kernels.adam(tb, HP, 0, sb, torch.bfloat16, bias_tables=tabs)
+        torch.cuda.synchronize()
+        for a, b in zip(dev, dev2):
+            for x, y in zip(a[:3], b[:3]):
+                assert torch.equal(x, y), t
+            assert torch.equal(a[4], b[4])
+    sc = torch.tensor([1.0, 0.0, 5.0, 0.0], dtype=torch.float64, device=cuda)
+    kernels.step_advance(sc)
+    torch.cuda.synchronize()
+    assert sc.tolist()[:3] == [0.0, 0.0, 6.0]
+    sc[1] = 1.0
+    kernels.step_advance(sc)
+    torch.cuda.synchronize()
+    assert sc.tolist()[:3] == [0.0, 0.0, 6.0]
