@@ -279,6 +279,8 @@ def run_ours(args):
     opt.adam_events.clear()
     model.fetcher.time_release = True
     model.fetcher.release_events.clear()
+    model.fetcher.copy_events.clear()
+    opt.cpu_wait_s = opt.cpu_update_s = 0.0
     cur = torch.cuda.current_stream(dev)
     l0 = _lib.launch_count()
     with ClockSampler(local) as clk:
@@ -295,6 +297,12 @@ def run_ours(args):
     ms = _max_over_ranks(ms, world)
     adam_ms = [a.elapsed_time(b) for a, b in opt.adam_events]
     rel = [(a.elapsed_time(b), n) for a, b, n in model.fetcher.release_events]
+    copies = {}
+    for kind, a, b, nb in model.fetcher.copy_events:
+        ms_, nb0 = copies.get(kind, (0.0, 0))
+        copies[kind] = (ms_ + a.elapsed_time(b), nb0 + nb)
+    cpu_wait_ms = opt.cpu_wait_s * 1e3 / args.steps
+    cpu_update_ms = opt.cpu_update_s * 1e3 / args.steps
     opt.time_adam = False
     model.fetcher.time_release = False
     loss = float(model.last_loss)
@@ -342,7 +350,11 @@ def run_ours(args):
     homes = model.manager.homes
     offload = {"cpu_home_chunks": len(model.manager.cpu_ids), "gpu_home_chunks": len(model.manager.gpu_ids),
                "bytes_moved_per_step": {k: v for k, v in model.fetcher.bytes_moved.items()},
-               "sim_counters": model.fetcher.counters()}
+               "sim_counters": model.fetcher.counters(),
+               "offload_copies_per_step": {k: {"ms": v[0] / args.steps, "bytes": v[1] / args.steps,
+                                               "gbs": v[1] / (v[0] * 1e-3) / 1e9 if v[0] else None}
+                                           for k, v in copies.items()},
+               "cpu_update_ms_per_step": cpu_update_ms, "host_wait_on_cpu_update_ms_per_step": cpu_wait_ms}
     flops = model.flops_per_step()
     line = {
         "metric": METRIC,

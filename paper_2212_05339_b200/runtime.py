@@ -30,6 +30,7 @@ from __future__ import annotations
 import math
 import os
 import threading
+import time
 from dataclasses import dataclass
 from typing import Any, Callable, Mapping, Sequence
 
@@ -301,8 +302,9 @@ class ChunkFetcher:
         self.comm = comm_stream or torch.cuda.Stream(device=manager.device)
         self.prefetch = prefetch
         self.inv_scale = inv_scale
-        self.time_release = False     # bench: CUDA events around each release
+        self.time_release = False     # bench: CUDA events around each release / offload copy
         self.release_events: list = []
+        self.copy_events: list = []
         self.optimizer = None         # HybridAdam whose per-chunk updates gate our reads
         self._fenced = False
         ev = self.sched.events
@@ -497,7 +499,13 @@ class ChunkFetcher:
             if cpu and n > 0:
                 src = storage if mgr.fused_w1 else mgr.stage32
                 nbytes = n * src.element_size()
+                if self.time_release:
+                    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    c0.record(comm)
                 kernels.copy_d2h(mgr.h_g32[r], src, nbytes, stream=comm)
+                if self.time_release:
+                    c1.record(comm)
+                    self.copy_events.append(("d2h", c0, c1, nbytes))
                 self.bytes_moved["d2h"] += nbytes
 
     def release_shared(self, sp: _SharedParam) -> None:
@@ -615,6 +623,8 @@ class HybridAdam:
         self._host_steps = 0      # host-mode step counter
         self._cpu_steps = 0       # CPU-home update's own counter (same rule as step_scalars[2])
         self.last_stats = None
+        self.cpu_wait_s = 0.0      # host time the runtime blocked on CPU-home updates
+        self.cpu_update_s = 0.0    # host time spent in CPU-home updates (on their thread)
         self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         self.time_adam = False
         self.done_event: torch.cuda.Event | None = None
@@ -646,7 +656,9 @@ class HybridAdam:
     def wait_cpu(self, c: int) -> None:
         ev = self.cpu_ready.get(c)
         if ev is not None and not ev.is_set():
+            t0 = time.perf_counter()
             ev.wait()
+            self.cpu_wait_s += time.perf_counter() - t0
         if self._cpu_error is not None:
             raise self._cpu_error
 
@@ -802,6 +814,7 @@ class HybridAdam:
         pinned copy), not the main thread."""
         try:
             sq, flag = stats.scalars()
+            t0 = time.perf_counter()
             skip = flag != 0.0 or not math.isfinite(sq)
             kstep = max(self._cpu_steps + (0 if skip else 1), 1)
             for c in sorted(self.cpu_segs):
@@ -810,6 +823,7 @@ class HybridAdam:
                 self.cpu_ready[c].set()
             if not skip:
                 self._cpu_steps += 1
+            self.cpu_update_s += time.perf_counter() - t0
         except BaseException as exc:  # surfaced by wait_cpu / synchronize
             self._cpu_error = exc
             for ev in self.cpu_ready.values():
