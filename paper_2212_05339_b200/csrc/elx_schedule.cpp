@@ -128,6 +128,11 @@ extern "C" int elx_schedule(int32_t n_nodes, const int32_t* node_ptr, const int3
     return true;
   };
 
+  // Prefetch horizon: a gather may be issued as soon as (a) its block's
+  // previous owner (the victim) was used for the last time before the
+  // eviction — after its release if it was pinned, since a release happens
+  // at a needed position — and (b) the chunk itself was last evicted.
+  std::vector<int32_t> last_needed(n_chunks, -1), last_evicted(n_chunks, -1);
   std::vector<char> pinned_at_start(n_chunks, 0);
   for (int32_t p = 0; p < W; ++p) {
     const bool backward = p >= n_nodes;
@@ -158,6 +163,7 @@ extern "C" int elx_schedule(int32_t n_nodes, const int32_t* node_ptr, const int3
                            n_block, bpos);
         blk = block_of[victim];
         block_of[victim] = -1;
+        last_evicted[victim] = p;
         resident.erase(std::find(resident.begin(), resident.end(), victim));
       } else {
         blk = free_blocks.back();
@@ -169,11 +175,10 @@ extern "C" int elx_schedule(int32_t n_nodes, const int32_t* node_ptr, const int3
       if (gathered[c]) ++cnt.replaced_ops;
       gathered[c] = 1;
       if (cpu_home[c]) ++cnt.c2g_units;
-      // Prefetch legality: the block can be filled one position early when
-      // its previous owner is neither used nor pinned at that position.
-      int32_t issue = p;
-      if (p > 0 && (victim < 0 || (!in_prev_needed[victim] && !pinned_at_prev_start[victim])))
-        issue = p - 1;
+      int32_t issue = 0;
+      if (victim >= 0) issue = std::max(issue, last_needed[victim] + 1);
+      if (last_evicted[c] >= 0) issue = std::max(issue, last_evicted[c]);
+      issue = std::min(issue, p);
       emit(elx_event{ELX_EV_GATHER, p, c, blk, victim, issue});
     }
     cnt.peak_rcache_blocks = std::max<int64_t>(cnt.peak_rcache_blocks, (int64_t)resident.size());
@@ -192,6 +197,7 @@ extern "C" int elx_schedule(int32_t n_nodes, const int32_t* node_ptr, const int3
     for (int32_t c : needed) {
       in_needed[c] = 0;
       in_prev_needed[c] = 1;
+      last_needed[c] = p;
     }
     prev_needed = needed;
     pinned_at_prev_start = pinned_at_start;

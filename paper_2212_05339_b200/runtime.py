@@ -335,6 +335,7 @@ class ChunkFetcher:
         self.bytes_moved = dict(h2d=0, d2h=0, gather=0, scatter=0)
         self.pos = 0
         self._fenced = False
+        self.deferred: dict[int, list] = {}
 
     def begin_step(self, after: torch.cuda.Event | None = None) -> None:
         """Start a walk. On the P2P path every rank must have finished its
@@ -352,9 +353,16 @@ class ChunkFetcher:
         """Before node `pos` computes: make its chunks resident and bound."""
         if pos != self.pos:
             raise ValidationError(f"walk out of order: expected position {self.pos}, got {pos}")
-        for rec in self.due[pos]:
+        for rec in self.deferred.pop(pos, []) + self.due[pos]:
             self._gather(rec)
-        for rec in self.early[pos]:  # prefetch for pos + 1 (PAPER.md:276-281)
+        opt = self.optimizer
+        for rec in self.early[pos]:  # prefetch (PAPER.md:276-281), up to the schedule's horizon
+            c = rec[0]
+            if (opt is not None and self.mgr.homes[c] is Device.CPU and c in opt.cpu_ready
+                    and not opt.cpu_ready[c].is_set()):
+                # its host update is still running: issue at the due position instead of blocking here
+                self.deferred.setdefault(rec[3], []).append(rec)
+                continue
             self._gather(rec)
         cur = torch.cuda.current_stream(self.mgr.device)
         opt = self.optimizer
@@ -437,7 +445,13 @@ class ChunkFetcher:
                 off = mgr.row[c] * mgr.S * es
                 kernels.fetch(block, [p + off for p in mgr.peer_p16], mgr.S, stream=comm)
             elif cpu:
+                if self.time_release:
+                    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    c0.record(comm)
                 kernels.copy_h2d(seg, mgr.h_p16[mgr.row[c]], stream=comm)
+                if self.time_release:
+                    c1.record(comm)
+                    self.copy_events.append(("h2d", c0, c1, seg.numel() * seg.element_size()))
                 self.bytes_moved["h2d"] += seg.numel() * seg.element_size()
                 if mgr.world > 1:
                     mgr.transport.gather(block, seg)
