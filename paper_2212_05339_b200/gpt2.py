@@ -137,7 +137,7 @@ class ElixirGPT2:
                  lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.01,
                  max_norm: float | None = 1.0, loss_scale: float | None = None, transport=None,
                  prefetch: bool = True, cpu_threads: int | None = None, init: dict | None = None,
-                 overlap_update: bool = False):
+                 overlap_update: bool = False, cpu_update: str = "split"):
         import torch.distributed as dist
 
         self.cfg = cfg
@@ -165,7 +165,8 @@ class ElixirGPT2:
         self.fetcher = ChunkFetcher(self.manager, self.trace, prefetch=prefetch,
                                     inv_scale=1.0 / self.scaler.scale)
         self.optimizer = HybridAdam(self.manager, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
-                                    max_norm=max_norm, cpu_threads=cpu_threads, overlap=overlap_update)
+                                    max_norm=max_norm, cpu_threads=cpu_threads, overlap=overlap_update,
+                                    cpu_update=cpu_update)
         self.fetcher.optimizer = self.optimizer
         # coarse node -> its chunk parameters, in declaration order
         order = {p.id: i for i, p in enumerate(self.profile.parameters)}

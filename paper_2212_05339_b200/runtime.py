@@ -43,6 +43,11 @@ from .schedule import Device, Plan, Schedule, as_plan, compile_schedule, report_
 from .transport import LocalTransport, make_transport
 
 SHARD_ALIGN = 8  # elements; keeps every shard and rCache segment 16-byte aligned
+ELX_TILE = _lib.ADAM_TILE
+# (host update, GPU-streamed update) in elements/s, measured on the B200 box
+# (plans/hardware_b200_measured.json: v_c = 19.5 GB/s of 4-byte elements;
+# pinned PCIe ~55 GB/s each way at 14 B per element and direction).
+DEFAULT_UPDATE_RATES = (19.5e9 / 4, 55e9 / 14)
 
 
 def shard_length(chunk_length: int, world: int) -> int:
@@ -432,7 +437,7 @@ class ChunkFetcher:
         comm = self.comm
         opt = self.optimizer
         if cpu and opt is not None:
-            opt.wait_cpu(c)  # host shard rewritten by the CPU-home update
+            opt.wait_offloaded(c, self.comm)  # host shard rewritten by the CPU-home update
         with torch.cuda.stream(comm):
             if victim >= 0 and victim in self.last_use:
                 comm.wait_event(self.last_use[victim])
@@ -476,7 +481,7 @@ class ChunkFetcher:
             self.live["g2c_units"] += 1
         opt = self.optimizer
         if cpu and opt is not None:
-            opt.wait_cpu(c)  # previous update still reading the host grad shard
+            opt.wait_offloaded(c, self.comm)  # previous update still reading the host grad shard
         with torch.cuda.stream(comm):
             comm.wait_event(grads_written)
             if not self._fenced and opt is not None and opt.done_event is not None:
@@ -594,7 +599,8 @@ class HybridAdam:
 
     def __init__(self, manager: ChunkManager, *, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.01, max_norm: float | None = 1.0, cpu_threads: int | None = None,
-                 overlap: bool = False, device_step: bool = True):
+                 overlap: bool = False, device_step: bool = True, cpu_update: str = "split",
+                 update_rates: tuple[float, float] | None = None, stream_tile: int = 32 * 2 ** 20):
         self.mgr = manager
         self.hp = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
                        max_norm=max_norm or 0.0)
@@ -620,12 +626,30 @@ class HybridAdam:
                 all_segs.append(seg)
                 self.groups.append((c, kernels.AdamTable([seg], m.device)))
         self.table = kernels.AdamTable(all_segs, m.device)  # single-launch form (overlap=False)
-        self.cpu_segs = {}
+        all_cpu = {}
         for c in m.cpu_ids:
             r = m.row[c]
             n = m.valid(c)
             if n > 0:
-                self.cpu_segs[c] = (m.h_p32[r], m.h_m[r], m.h_v[r], m.h_g32[r], m.h_p16[r], n)
+                all_cpu[c] = (m.h_p32[r], m.h_m[r], m.h_v[r], m.h_g32[r], m.h_p16[r], n)
+        # CPU-home updates are split between host threads (elx_cpu_adam, rate
+        # v_c) and a GPU-streamed update (H2D p32/m/v/g -> K4 -> D2H
+        # p32/m/v/p16 over PCIe) by measured rate: chunks in forward order go
+        # to the worker that would finish them first (§8f row 4).
+        host_rate, stream_rate = update_rates or DEFAULT_UPDATE_RATES
+        self.cpu_segs, self.stream_segs = {}, {}
+        t_host = t_stream = 0.0
+        for c in sorted(all_cpu):
+            n = all_cpu[c][5]
+            use_stream = (cpu_update == "stream" or
+                          (cpu_update == "split" and t_stream + n / stream_rate < t_host + n / host_rate))
+            if use_stream:
+                self.stream_segs[c] = all_cpu[c]
+                t_stream += n / stream_rate
+            else:
+                self.cpu_segs[c] = all_cpu[c]
+                t_host += n / host_rate
+        self._init_stream_update(stream_tile)
         self.stream = torch.cuda.Stream(device=m.device) if overlap else None
         pin = torch.cuda.is_available()
         # ring of pinned snapshots of the step scalars (read lazily by StepStats / the CPU thread)
@@ -649,6 +673,81 @@ class HybridAdam:
             ev.set()
         self._cpu_thread: threading.Thread | None = None
         self._cpu_error: BaseException | None = None
+
+    def _init_stream_update(self, tile: int) -> None:
+        m = self.mgr
+        self.xfer_done: dict[int, torch.cuda.Event] = {}
+        self.stream_done: torch.cuda.Event | None = None
+        if not self.stream_segs:
+            return
+        dev = m.device
+        T = min(tile, max(seg[5] for seg in self.stream_segs.values()))
+        T = -(-T // ELX_TILE) * ELX_TILE
+        gdt = m.h_g32.dtype
+        self._slots = [dict(p32=torch.empty(T, device=dev), m=torch.empty(T, device=dev),
+                            v=torch.empty(T, device=dev), g=torch.empty(T, dtype=gdt, device=dev),
+                            p16=torch.empty(T, dtype=m.dtype, device=dev), free=None) for _ in range(2)]
+        self._slot_tables: dict[tuple[int, int], kernels.AdamTable] = {}
+        self._tile = T
+        self.h2d_stream = torch.cuda.Stream(device=dev)
+        self.xfer_stream = torch.cuda.Stream(device=dev)
+        self.sc_stream = torch.zeros(4, dtype=torch.float64, device=dev)
+
+    def _slot_table(self, s: int, cnt: int) -> kernels.AdamTable:
+        key = (s, cnt)
+        if key not in self._slot_tables:
+            sl = self._slots[s]
+            self._slot_tables[key] = kernels.AdamTable(
+                [(sl["p32"][:cnt], sl["m"][:cnt], sl["v"][:cnt], sl["g"][:cnt], sl["p16"][:cnt], cnt)], self.mgr.device)
+        return self._slot_tables[key]
+
+    def _stream_update(self, cur: torch.cuda.Stream, tabs) -> None:
+        """GPU-streamed update of the stream-assigned CPU-home chunks: tiles of
+        T elements double-buffered through two HBM slots; H2D on one stream,
+        K4 + D2H on another, so loads of tile k+1 overlap the update of tile k."""
+        m = self.mgr
+        h2d, xfer = self.h2d_stream, self.xfer_stream
+        h2d.wait_stream(cur)
+        xfer.wait_stream(cur)
+        k = 0
+        for c in sorted(self.stream_segs):
+            p32, mm, vv, g, p16, n = self.stream_segs[c]
+            for a in range(0, n, self._tile):
+                cnt = min(self._tile, n - a)
+                s = k % 2
+                sl = self._slots[s]
+                with torch.cuda.stream(h2d):
+                    if sl["free"] is not None:
+                        h2d.wait_event(sl["free"])
+                    for src, dst in ((p32, sl["p32"]), (mm, sl["m"]), (vv, sl["v"]), (g, sl["g"])):
+                        kernels.copy_h2d(dst, src[a:a + cnt], stream=h2d)
+                    loaded = torch.cuda.Event()
+                    loaded.record(h2d)
+                with torch.cuda.stream(xfer):
+                    xfer.wait_event(loaded)
+                    kernels.adam(self._slot_table(s, cnt), self.hp, 0 if tabs is not None else self._kstep,
+                                 self.sc_stream, m.dtype, stream=xfer, grad_scale=self.grad_scale,
+                                 bias_tables=tabs)
+                    for src, dst in ((sl["p32"], p32), (sl["m"], mm), (sl["v"], vv), (sl["p16"], p16)):
+                        kernels.copy_d2h(dst[a:a + cnt], src, cnt * src.element_size(), stream=xfer)
+                    free = torch.cuda.Event()
+                    free.record(xfer)
+                    sl["free"] = free
+                k += 1
+            ev = torch.cuda.Event()
+            ev.record(xfer)
+            self.xfer_done[c] = ev
+        self.stream_done = torch.cuda.Event()
+        self.stream_done.record(xfer)
+
+    def wait_offloaded(self, c: int, stream: torch.cuda.Stream) -> None:
+        """Before touching chunk c's host shards: its previous update must be done
+        (host flag for host-updated chunks, stream event for streamed ones)."""
+        ev = self.xfer_done.get(c)
+        if ev is not None:
+            stream.wait_event(ev)
+        else:
+            self.wait_cpu(c)
 
     @property
     def gpu_elements(self) -> int:
@@ -681,6 +780,8 @@ class HybridAdam:
         s = stream or torch.cuda.current_stream(self.mgr.device)
         if self.done_event is not None:
             s.wait_event(self.done_event)
+        if self.stream_done is not None:
+            s.wait_event(self.stream_done)
         if self._cpu_thread is not None:
             self._cpu_thread.join()
             if self._cpu_error is not None:
@@ -726,9 +827,9 @@ class HybridAdam:
         self._step0 = steps
         sc = torch.tensor([0.0, 1.0, 0.0, 0.0], dtype=torch.float64, device=m.device)  # "skip": restore only
         kernels.adam(self.table, self.hp, max(1, steps), sc, m.dtype)
-        if self.cpu_segs:
-            kernels.cpu_adam(list(self.cpu_segs.values()), self.hp, max(1, steps), (0.0, 1.0), m.dtype,
-                             self.cpu_threads)
+        host_segs = list(self.cpu_segs.values()) + list(self.stream_segs.values())
+        if host_segs:
+            kernels.cpu_adam(host_segs, self.hp, max(1, steps), (0.0, 1.0), m.dtype, self.cpu_threads)
         if m.world > 1:
             for sp in m.shared.values():
                 m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
@@ -773,6 +874,8 @@ class HybridAdam:
             kstep = max(self._host_steps + (0 if found_inf else 1), 1)
             if not found_inf:
                 self._host_steps += 1
+        if self.stream_segs:
+            self.sc_stream.copy_(m.step_scalars)  # snapshot before the opt stream's step_advance
         opt = self.stream if self.overlap else cur
         if opt is not cur:
             opt.wait_stream(cur)
@@ -807,6 +910,9 @@ class HybridAdam:
                 kernels.step_reset(m.step_scalars, stream=opt)
             self.done_event = torch.cuda.Event()
             self.done_event.record(opt)
+        if self.stream_segs:
+            self._kstep = kstep
+            self._stream_update(cur, tabs)
         if self.cpu_segs:
             for ev in self.cpu_ready.values():
                 ev.clear()

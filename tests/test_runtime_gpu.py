@@ -150,3 +150,31 @@ def test_checkpoint_round_trip(cuda):
     ma, mb = _masters(a), _masters(b)
     for k in ma:
         assert np.array_equal(ma[k], mb[k]), k
+
+
+@pytest.mark.parametrize("cpu_update", ["host", "stream", "split"])
+def test_offloaded_update_modes_bit_exact(cuda, cpu_update):
+    """CPU-home chunks updated on host threads, by the GPU-streamed update
+    (H2D -> K4 -> D2H in double-buffered tiles), or split between them: all
+    bit-exact against the oracle; also across an fp16 overflow skip."""
+    plan = dict(_plans(CFG))["offload-all"]
+    init = gpt2.init_params(CFG, cuda, seed=12)
+    model = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()},
+                       cpu_update=cpu_update, **HP)
+    opt = model.optimizer
+    if cpu_update == "host":
+        assert opt.cpu_segs and not opt.stream_segs
+    elif cpu_update == "stream":
+        assert opt.stream_segs and not opt.cpu_segs
+    else:
+        assert opt.cpu_segs and opt.stream_segs
+    opt._init_stream_update(1000) if opt.stream_segs else None  # tiny tiles: several per chunk, both slots
+    ref = ReferenceStep(model, init, HP)
+    for s in range(3):
+        tok, tgt = _batch(CFG, cuda, 10 + s)
+        lo = model.train_step(tok, tgt)
+        (lr_,), _ = ref.step([(tok, tgt)])
+        assert lo.item() == lr_.item(), s
+        got = _masters(model)
+        for pid, want in ref.master.items():
+            assert np.array_equal(got[pid], want), (s, pid)
