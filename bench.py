@@ -263,7 +263,7 @@ def run_ours(args):
     plan_text = plan_path.read_text()
     from paper_2212_05339_b200.transport import make_transport
     model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234, transport=make_transport(world, args.transport),
-                       overlap_update=args.overlap)
+                       overlap_update=args.overlap, cpu_update=args.cpu_update)
     B, T = cfg.batch, cfg.seq_len
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     ids = torch.randint(0, cfg.vocab, (B, T + 1), generator=gen, device=dev)
@@ -354,7 +354,9 @@ def run_ours(args):
                "offload_copies_per_step": {k: {"ms": v[0] / args.steps, "bytes": v[1] / args.steps,
                                                "gbs": v[1] / (v[0] * 1e-3) / 1e9 if v[0] else None}
                                            for k, v in copies.items()},
-               "cpu_update_ms_per_step": cpu_update_ms, "host_wait_on_cpu_update_ms_per_step": cpu_wait_ms}
+               "cpu_update_ms_per_step": cpu_update_ms, "host_wait_on_cpu_update_ms_per_step": cpu_wait_ms,
+               "cpu_update_mode": args.cpu_update,
+               "host_updated_chunks": sorted(opt.cpu_segs), "stream_updated_chunks": sorted(opt.stream_segs)}
     flops = model.flops_per_step()
     line = {
         "metric": METRIC,
@@ -473,6 +475,8 @@ def main():
     ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
                     "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-update", choices=["split", "host", "stream"], default="split",
+                    help="CPU-home chunk update: host threads, GPU-streamed, or split by measured rate")
     ap.add_argument("--overlap", action="store_true",
                     help="issue the GPU update per chunk on an optimizer stream under the next forward")
     ap.add_argument("--transport", choices=["nccl", "p2p"], default=os.environ.get("ELX_TRANSPORT", "nccl"),

@@ -18,6 +18,16 @@ from .profiles import (AccessTrace, ModelProfile, OperatorNode, ParameterSpec, P
                        partition_multiuse, synthesize_transformer_profile)
 from .schedule import Device, Plan, Schedule, SimReport, compile_schedule, load_plan, simulate
 
+__all__ = [
+    "ChunkTooSmallError", "ElixirCudaError", "ExtensionMissingError", "InfeasibleCacheError", "InfeasibleError",
+    "PlannerError", "ProfileFormatError", "UncommonGraphError", "ValidationError",
+    "Chunk", "ChunkLayout", "ChunkMember", "ChunkTrace", "build_chunk_trace", "pack_chunks", "waste_rate",
+    "working_set_blocks", "AccessTrace", "ModelProfile", "OperatorNode", "ParameterSpec", "PrecisionSpec",
+    "coarsen_graph", "partition_multiuse", "synthesize_transformer_profile", "Device", "Plan", "Schedule",
+    "SimReport", "compile_schedule", "load_plan", "simulate", "ChunkManager", "ChunkFetcher", "HybridAdam",
+    "LossScaler", "ElixirGPT2", "GPT2Config", "PRESETS",
+]
+
 __version__ = "0.1.0"
 
 

@@ -32,15 +32,14 @@ import os
 import threading
 import time
 from dataclasses import dataclass
-from typing import Any, Callable, Mapping, Sequence
+from typing import Any, Mapping, Sequence
 
-import numpy as np
 import torch
 
 from . import _lib, kernels
 from .errors import InfeasibleCacheError, ValidationError
 from .schedule import Device, Plan, Schedule, as_plan, compile_schedule, report_from_counters
-from .transport import LocalTransport, make_transport
+from .transport import LocalTransport
 
 SHARD_ALIGN = 8  # elements; keeps every shard and rCache segment 16-byte aligned
 ELX_TILE = _lib.ADAM_TILE
