@@ -231,6 +231,17 @@ int elx_step_reset(double* step_scalars, void* stream);
  * overflow) step_scalars[2] += 1; then step_scalars[0..1] <- 0. */
 int elx_step_advance(double* step_scalars, void* stream);
 
+/* ------------------------------------------- K7 bias-gradient reduction
+ * out[j] = sum_{i<rows} in[i*cols + j] (fp32 accumulation, deterministic:
+ * fixed row slices reduced in slice order), written in out_dtype. Used by the
+ * wrapped linear operators to write bias gradients straight over the bias
+ * slots of the chunk. `workspace` is a caller-owned DEVICE
+ * float buffer of at least elx_colsum_workspace(rows, cols) elements. in_dtype
+ * is BF16 or F16; cols must be a multiple of 8 and `in` 16-byte aligned. */
+int64_t elx_colsum_workspace(int64_t rows, int64_t cols);
+int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, int64_t rows, int64_t cols,
+               float* workspace, void* stream);
+
 /* ------------------------------------------------------- K6 offload
  * Pinned-host <-> HBM moves for CPU-home chunks on a side stream, with an
  * optional completion event (rcache_sim.py:156-157, 165-166: c2g on each

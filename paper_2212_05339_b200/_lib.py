@@ -89,6 +89,8 @@ _SIGNATURES = {
     "elx_norm_finalize": (ctypes.c_int, [c_vp, c_f64, c_vp, c_vp]),
     "elx_step_reset": (ctypes.c_int, [c_vp, c_vp]),
     "elx_step_advance": (ctypes.c_int, [c_vp, c_vp]),
+    "elx_colsum_workspace": (c_i64, [c_i64, c_i64]),
+    "elx_colsum": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_i64, c_i64, c_vp, c_vp]),
     "elx_copy_h2d": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_copy_d2h": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_cpu_adam": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i32]),

@@ -810,6 +810,59 @@ __global__ void step_advance_kernel(double* sc) {
   sc[1] = 0.0;
 }
 
+
+// ============================================================ K7 colsum
+constexpr int kCsThreads = 256;
+constexpr int kCsCols = kCsThreads * 8;  // columns per CTA (8 per thread, one 16-byte load per row)
+
+int colsum_slices(int64_t rows, int64_t cols) {
+  const int64_t xblocks = (cols + kCsCols - 1) / kCsCols;
+  int64_t s = (2LL * sm_count() * 4 + xblocks - 1) / xblocks;
+  s = std::max<int64_t>(1, std::min<int64_t>(s, (rows + 7) / 8));
+  return (int)s;
+}
+
+template <typename T16>
+__global__ void __launch_bounds__(kCsThreads) colsum_partial_kernel(const T16* __restrict__ in, int64_t rows,
+                                                                    int64_t cols, int slices, float* __restrict__ ws) {
+  const int64_t c0 = ((int64_t)blockIdx.x * kCsThreads + threadIdx.x) * 8;
+  if (c0 >= cols) return;
+  const int64_t per = (rows + slices - 1) / slices;
+  const int64_t r0 = (int64_t)blockIdx.y * per, r1 = min(rows, r0 + per);
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  int64_t r = r0;
+  for (; r + 4 <= r1; r += 4) {  // 4 rows of loads in flight
+    uint4 q[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) q[u] = ld_stream(reinterpret_cast<const uint4*>(in + (r + u) * cols + c0));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const T16* h = reinterpret_cast<const T16*>(&q[u]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], to_f32<T16>(h[e]));
+    }
+  }
+  for (; r < r1; ++r) {
+    const uint4 q = ld_stream(reinterpret_cast<const uint4*>(in + r * cols + c0));
+    const T16* h = reinterpret_cast<const T16*>(&q);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], to_f32<T16>(h[e]));
+  }
+  float4* o = reinterpret_cast<float4*>(ws + (int64_t)blockIdx.y * cols + c0);
+  o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+  o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+}
+
+__global__ void colsum_final_kernel(const float* __restrict__ ws, int slices, int64_t cols, void* out, int out_dt) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += (int64_t)gridDim.x * blockDim.x) {
+    float a = 0.f;
+    for (int s = 0; s < slices; ++s) a = __fadd_rn(a, ws[(int64_t)s * cols + j]);
+    st_from_f32(out, j, out_dt, a);
+  }
+}
+
 }  // namespace
 
 // ======================================================================= ABI
@@ -941,6 +994,36 @@ int elx_step_advance(double* step_scalars, void* stream) {
   if (!step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   step_advance_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(step_scalars);
   return check_launch("elx_step_advance");
+}
+
+int64_t elx_colsum_workspace(int64_t rows, int64_t cols) {
+  if (rows < 1 || cols < 1) return 0;
+  return (int64_t)colsum_slices(rows, cols) * cols;
+}
+
+int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, int64_t rows, int64_t cols,
+               float* workspace, void* stream) {
+  elx::clear_error();
+  if (!out || !in || !workspace) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (rows < 1 || cols < 1 || cols % 8) return elx::fail(ELX_ERR_VALIDATION, "need rows >= 1, cols a multiple of 8");
+  if (!aligned16(in) || !aligned16(workspace)) return elx::fail(ELX_ERR_VALIDATION, "in/workspace not 16-byte aligned");
+  if (elx::dtype_size(out_dtype) == 0) return elx::fail(ELX_ERR_VALIDATION, "bad out dtype");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int slices = colsum_slices(rows, cols);
+  const dim3 grid((unsigned)((cols + kCsCols - 1) / kCsCols), (unsigned)slices);
+  if (in_dtype == ELX_BF16)
+    colsum_partial_kernel<__nv_bfloat16><<<grid, kCsThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), rows,
+                                                                      cols, slices, workspace);
+  else if (in_dtype == ELX_F16)
+    colsum_partial_kernel<__half><<<grid, kCsThreads, 0, st>>>(static_cast<const __half*>(in), rows, cols, slices,
+                                                               workspace);
+  else
+    return elx::fail(ELX_ERR_VALIDATION, "colsum input must be bf16/f16");
+  int rc = check_launch("elx_colsum");
+  if (rc) return rc;
+  const int g2 = (int)std::min<int64_t>((cols + 255) / 256, (int64_t)sm_count() * 4);
+  colsum_final_kernel<<<g2, 256, 0, st>>>(workspace, slices, cols, out, out_dtype);
+  return check_launch("elx_colsum final");
 }
 
 int elx_copy_h2d(void* dst_dev, const void* src_host, int64_t bytes, void* stream, void* event) {

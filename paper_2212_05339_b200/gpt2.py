@@ -113,16 +113,54 @@ def layer_pieces(i: int, h: int) -> list[tuple[str, int, tuple[int, ...]]]:
     return out
 
 
-def _block(x, p, heads):
+class _OverwriteLinear(torch.autograd.Function):
+    """y = x W^T + b (a wrapped operator) whose backward
+    writes dW and db straight into `targets` — at run time the chunk slots of
+    W and b themselves: the gradient overwrites the parameter data
+    (Fig. 3). dX is computed first, while W is intact; dW
+    is a cuBLAS GEMM into the slot, db the deterministic K7 column sum. No
+    separate weight-gradient tensor and no K1 write-back copy exist."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, w_target, b_target):
+        ctx.save_for_backward(x, w)
+        ctx.targets = (w_target, b_target)
+        return F.linear(x, w, b)
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w = ctx.saved_tensors
+        w_t, b_t = ctx.targets
+        gy2 = gy.reshape(-1, gy.shape[-1])
+        gx = torch.mm(gy2, w).view(*gy.shape[:-1], w.shape[1]) if ctx.needs_input_grad[0] else None
+        torch.mm(gy2.t(), x.reshape(-1, x.shape[-1]), out=w_t)
+        kernels.colsum(gy2, b_t)
+        return gx, None, None, None, None
+
+
+# (weight, bias) positions of the six linear operators in a layer's pieces
+_LINEARS = ((2, 5), (3, 6), (4, 7), (8, 9), (12, 13), (14, 15))
+
+
+def _block(x, p, heads, targets=None):
+    """One GPT-2 layer on its 16 compute pieces (layer_pieces order). With
+    `targets` (per-piece gradient destinations) the linear operators write
+    their parameter gradients there during backward."""
     B, T, H = x.shape
     ln1w, ln1b, qw, kw, vw, qb, kb, vb, projw, projb, ln2w, ln2b, fcw, fcb, mpw, mpb = p
     hd = H // heads
+
+    def lin(inp, wi, bi):
+        if targets is None:
+            return F.linear(inp, p[wi], p[bi])
+        return _OverwriteLinear.apply(inp, p[wi], p[bi], targets[wi], targets[bi])
+
     h = F.layer_norm(x, (H,), ln1w, ln1b, 1e-5)
-    q, k, v = (F.linear(h, w, b).view(B, T, heads, hd).transpose(1, 2) for w, b in ((qw, qb), (kw, kb), (vw, vb)))
+    q, k, v = (lin(h, wi, bi).view(B, T, heads, hd).transpose(1, 2) for wi, bi in _LINEARS[:3])
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-    x = x + F.linear(a.transpose(1, 2).reshape(B, T, H), projw, projb)
+    x = x + lin(a.transpose(1, 2).reshape(B, T, H), *_LINEARS[3])
     h = F.layer_norm(x, (H,), ln2w, ln2b, 1e-5)
-    return x + F.linear(F.gelu(F.linear(h, fcw, fcb), approximate="tanh"), mpw, mpb)
+    return x + lin(F.gelu(lin(h, *_LINEARS[4]), approximate="tanh"), *_LINEARS[5])
 
 
 class ElixirGPT2:
@@ -183,7 +221,7 @@ class ElixirGPT2:
         self.last_loss = None
 
     # -------------------------------------------------------------- nodes
-    def _run_node(self, i: int, x, tokens, targets, params):
+    def _run_node(self, i: int, x, tokens, targets, params, grad_targets=None):
         cfg = self.cfg
         if i == 0:  # embed: wte (shared) + wpe
             wpe, wte = params
@@ -196,7 +234,7 @@ class ElixirGPT2:
         if i == self.K - 2:  # ln_f
             w, b = params
             return F.layer_norm(x, (cfg.hidden,), w, b, 1e-5)
-        return _block(x, params, cfg.heads)
+        return _block(x, params, cfg.heads, grad_targets)
 
     def pieces(self, i: int, lookup) -> list:
         """Node i's compute tensors cut from full parameters (lookup(pid))."""
@@ -247,12 +285,15 @@ class ElixirGPT2:
             i = K - 1 - j
             pos = K + j
             fx.enter(pos)
-            params = [p.detach().requires_grad_(True) for p in self._params_of(i)]
+            raw = self._params_of(i)
+            params = [p.detach().requires_grad_(True) for p in raw]
+            layer = 0 < i < K - 2
             with torch.enable_grad():
                 xin = None if i == 0 else acts[i].detach().requires_grad_(True)
-                out = self._run_node(i, xin, tokens, targets, params)
+                # layers: linear gradients land in their chunk slots (raw views) directly
+                out = self._run_node(i, xin, tokens, targets, params, grad_targets=raw if layer else None)
                 inputs = ([xin] if i > 0 else []) + params
-                grads = torch.autograd.grad(out, inputs, grad_outputs=grad)
+                grads = torch.autograd.grad(out, inputs, grad_outputs=grad, allow_unused=layer)
             if i == K - 1:
                 loss = out.detach()
             acts[i] = None
@@ -285,6 +326,8 @@ class ElixirGPT2:
         gradients (Fig. 3): one K1 launch per chunk."""
         by_chunk: dict[int, list] = {}
         for (pid, sub, _), g in zip(self.node_pieces[i], grads):
+            if g is None:  # written in place by the wrapped linear (_OverwriteLinear)
+                continue
             c, off, _ = self.manager.members[pid]
             by_chunk.setdefault(c, []).append((g.reshape(-1), off + sub))
         for c, mem in by_chunk.items():

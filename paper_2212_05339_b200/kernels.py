@@ -244,3 +244,17 @@ def copy_d2h(dst_host: torch.Tensor, src: torch.Tensor, nbytes: int | None = Non
     ev = event.cuda_event if event is not None else None
     rc = lib.elx_copy_d2h(dst_host.data_ptr(), src.data_ptr(), nb, _stream(stream), ev)
     _lib.check(rc, "elx_copy_d2h")
+
+
+def colsum(x2d: torch.Tensor, out: torch.Tensor, stream=None) -> None:
+    """K7: out[j] = sum_i x2d[i, j] (fp32 accumulation, deterministic), written
+    in out's dtype — bias gradients straight into their chunk slots."""
+    lib = _lib.load()
+    _cuda(x2d, "x2d")
+    if x2d.dim() != 2 or out.numel() != x2d.shape[1]:
+        raise ValidationError("colsum needs a 2-D input and out of x2d.shape[1] elements")
+    rows, cols = x2d.shape
+    ws = torch.empty(max(1, lib.elx_colsum_workspace(rows, cols)), dtype=torch.float32, device=x2d.device)
+    rc = lib.elx_colsum(out.data_ptr(), elx_dtype(out.dtype), x2d.data_ptr(), elx_dtype(x2d.dtype), rows, cols,
+                        ws.data_ptr(), _stream(stream))
+    _lib.check(rc, "elx_colsum")

@@ -49,16 +49,24 @@ class ReferenceStep:
         grad = torch.full((), scale, dtype=torch.float32, device=tokens.device)
         grads, loss = {}, None
         for i in reversed(range(K)):
-            ps = [p.detach().requires_grad_(True) for p in params(i)]
+            raw = params(i)
+            ps = [p.detach().requires_grad_(True) for p in raw]
+            layer = 0 < i < K - 2
+            # standalone gradient destinations for the wrapped linears (the runtime
+            # writes into the chunk slots instead)
+            tgt = [torch.empty_like(p) for p in raw] if layer else None
             with torch.enable_grad():
                 xin = None if i == 0 else acts[i].detach().requires_grad_(True)
-                out = m._run_node(i, xin, tokens, targets, ps)
-                gs = torch.autograd.grad(out, ([xin] if i else []) + ps, grad_outputs=grad)
+                out = m._run_node(i, xin, tokens, targets, ps, grad_targets=tgt)
+                gs = torch.autograd.grad(out, ([xin] if i else []) + ps, grad_outputs=grad, allow_unused=layer)
             if i == K - 1:
                 loss = out.detach()
             if i:
                 grad, gs = gs[0], gs[1:]
-            grads.update(m.piece_grads_by_param(i, gs[:len(m.node_pieces[i])]))
+            gs = list(gs[:len(m.node_pieces[i])])
+            if layer:
+                gs = [t if g is None else g for g, t in zip(gs, tgt)]
+            grads.update(m.piece_grads_by_param(i, gs))
             if i in (0, K - 1):
                 gw = gs[-1][:cfg.vocab]
                 grads["wte"] = gw if "wte" not in grads else grads["wte"] + gw

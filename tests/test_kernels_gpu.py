@@ -395,3 +395,31 @@ def test_adam_device_step_equals_host_step(cuda):
     kernels.step_advance(sc)
     torch.cuda.synchronize()
     assert sc.tolist()[:3] == [0.0, 0.0, 6.0]
+
+
+@pytest.mark.parametrize("rows,cols", [(1, 8), (7, 24), (8192, 2048), (1000, 8200), (4096, 6144)])
+def test_colsum_deterministic_and_exact(cuda, rows, cols):
+    """K7 bias-gradient column sum: fp32 accumulation over the library's fixed
+    row slices in order, then the slices in order — reproduced exactly here."""
+    from paper_2212_05339_b200 import _lib
+    rng = np.random.default_rng(rows + cols)
+    bits = arith.f32_to_bf16_bits((rng.standard_normal((rows, cols)) * 0.1).astype(np.float32))
+    x = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).to(cuda)
+    out = torch.empty(cols, dtype=torch.bfloat16, device=cuda)
+    kernels.colsum(x, out)
+    out2 = torch.empty(cols, dtype=torch.float32, device=cuda)
+    kernels.colsum(x, out2)
+    slices = _lib.load().elx_colsum_workspace(rows, cols) // cols
+    per = -(-rows // slices)
+    xf = arith.bf16_bits_to_f32(bits).reshape(rows, cols)
+    parts = []
+    for s in range(slices):
+        acc = np.zeros(cols, np.float32)
+        for r in range(s * per, min(rows, (s + 1) * per)):
+            acc = (acc + xf[r]).astype(np.float32)
+        parts.append(acc)
+    tot = np.zeros(cols, np.float32)
+    for a in parts:
+        tot = (tot + a).astype(np.float32)
+    assert np.array_equal(out2.cpu().numpy(), tot)
+    assert np.array_equal(_bits(out), arith.f32_to_bf16_bits(tot))
