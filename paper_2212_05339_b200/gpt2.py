@@ -123,13 +123,17 @@ class _OverwriteLinear(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, w, b, w_target, b_target):
-        ctx.save_for_backward(x, w)
+        # Held on ctx rather than save_for_backward: every weight of a chunk is
+        # a view of the same storage, so writing one slot's gradient bumps the
+        # shared version counter and would trip autograd's saved-tensor check
+        # for the other (disjoint, still intact) slots.
+        ctx.x, ctx.w = x, w
         ctx.targets = (w_target, b_target)
         return F.linear(x, w, b)
 
     @staticmethod
     def backward(ctx, gy):
-        x, w = ctx.saved_tensors
+        x, w = ctx.x, ctx.w
         w_t, b_t = ctx.targets
         gy2 = gy.reshape(-1, gy.shape[-1])
         gx = torch.mm(gy2, w).view(*gy.shape[:-1], w.shape[1]) if ctx.needs_input_grad[0] else None
