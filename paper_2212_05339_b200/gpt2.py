@@ -123,23 +123,29 @@ class _OverwriteLinear(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, x, w, b, w_target, b_target):
-        # Held on ctx rather than save_for_backward: every weight of a chunk is
-        # a view of the same storage, so writing one slot's gradient bumps the
-        # shared version counter and would trip autograd's saved-tensor check
-        # for the other (disjoint, still intact) slots.
-        ctx.x, ctx.w = x, w
+        ctx.save_for_backward(x, w)
         ctx.targets = (w_target, b_target)
         return F.linear(x, w, b)
 
     @staticmethod
     def backward(ctx, gy):
-        x, w = ctx.x, ctx.w
+        x, w = ctx.saved_tensors
         w_t, b_t = ctx.targets
         gy2 = gy.reshape(-1, gy.shape[-1])
         gx = torch.mm(gy2, w).view(*gy.shape[:-1], w.shape[1]) if ctx.needs_input_grad[0] else None
         torch.mm(gy2.t(), x.reshape(-1, x.shape[-1]), out=w_t)
         kernels.colsum(gy2, b_t)
         return gx, None, None, None, None
+
+
+def _alias(t: torch.Tensor) -> torch.Tensor:
+    """Same storage, own version counter. Gradient targets are aliases of the
+    chunk slots: every parameter of a chunk is a view of ONE storage, so an
+    `out=` write through a plain view would bump the version counter shared by
+    all of them and trip autograd's saved-tensor check for the (disjoint,
+    still intact) parameters other operators saved."""
+    a = torch.empty(0, dtype=t.dtype, device=t.device)
+    return a.set_(t.untyped_storage(), t.storage_offset(), t.size(), t.stride())
 
 
 # (weight, bias) positions of the six linear operators in a layer's pieces
@@ -295,7 +301,8 @@ class ElixirGPT2:
             with torch.enable_grad():
                 xin = None if i == 0 else acts[i].detach().requires_grad_(True)
                 # layers: linear gradients land in their chunk slots (raw views) directly
-                out = self._run_node(i, xin, tokens, targets, params, grad_targets=raw if layer else None)
+                out = self._run_node(i, xin, tokens, targets, params,
+                                     grad_targets=[_alias(t) for t in raw] if layer else None)
                 inputs = ([xin] if i > 0 else []) + params
                 grads = torch.autograd.grad(out, inputs, grad_outputs=grad, allow_unused=layer)
             if i == K - 1:
