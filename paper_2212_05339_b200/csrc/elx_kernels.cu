@@ -812,13 +812,15 @@ __global__ void step_advance_kernel(double* sc) {
 
 
 // ============================================================ K7 colsum
-constexpr int kCsThreads = 256;
+constexpr int kCsThreads = 128;
 constexpr int kCsCols = kCsThreads * 8;  // columns per CTA (8 per thread, one 16-byte load per row)
+constexpr int kCsMaxSlices = 128;
 
 int colsum_slices(int64_t rows, int64_t cols) {
   const int64_t xblocks = (cols + kCsCols - 1) / kCsCols;
-  int64_t s = (2LL * sm_count() * 4 + xblocks - 1) / xblocks;
-  s = std::max<int64_t>(1, std::min<int64_t>(s, (rows + 7) / 8));
+  int64_t s = (4LL * sm_count() + xblocks - 1) / xblocks;           // ~4 CTAs per SM in total
+  s = std::min<int64_t>(s, kCsMaxSlices);
+  s = std::max<int64_t>(1, std::min<int64_t>(s, (rows + 15) / 16));  // >= 16 rows per slice
   return (int)s;
 }
 
@@ -833,12 +835,12 @@ __global__ void __launch_bounds__(kCsThreads) colsum_partial_kernel(const T16* _
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
   int64_t r = r0;
-  for (; r + 4 <= r1; r += 4) {  // 4 rows of loads in flight
-    uint4 q[4];
+  for (; r + 8 <= r1; r += 8) {  // 8 rows of loads in flight
+    uint4 q[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) q[u] = ld_stream(reinterpret_cast<const uint4*>(in + (r + u) * cols + c0));
+    for (int u = 0; u < 8; ++u) q[u] = ld_stream(reinterpret_cast<const uint4*>(in + (r + u) * cols + c0));
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 8; ++u) {
       const T16* h = reinterpret_cast<const T16*>(&q[u]);
 #pragma unroll
       for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], to_f32<T16>(h[e]));
@@ -858,7 +860,15 @@ __global__ void __launch_bounds__(kCsThreads) colsum_partial_kernel(const T16* _
 __global__ void colsum_final_kernel(const float* __restrict__ ws, int slices, int64_t cols, void* out, int out_dt) {
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += (int64_t)gridDim.x * blockDim.x) {
     float a = 0.f;
-    for (int s = 0; s < slices; ++s) a = __fadd_rn(a, ws[(int64_t)s * cols + j]);
+    int s = 0;
+    for (; s + 8 <= slices; s += 8) {  // loads in flight; summed strictly in slice order
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = ws[(int64_t)(s + u) * cols + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a = __fadd_rn(a, v[u]);
+    }
+    for (; s < slices; ++s) a = __fadd_rn(a, ws[(int64_t)s * cols + j]);
     st_from_f32(out, j, out_dt, a);
   }
 }
@@ -1021,8 +1031,8 @@ int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, i
     return elx::fail(ELX_ERR_VALIDATION, "colsum input must be bf16/f16");
   int rc = check_launch("elx_colsum");
   if (rc) return rc;
-  const int g2 = (int)std::min<int64_t>((cols + 255) / 256, (int64_t)sm_count() * 4);
-  colsum_final_kernel<<<g2, 256, 0, st>>>(workspace, slices, cols, out, out_dtype);
+  const int g2 = (int)std::min<int64_t>((cols + 127) / 128, (int64_t)sm_count() * 4);
+  colsum_final_kernel<<<g2, 128, 0, st>>>(workspace, slices, cols, out, out_dtype);
   return check_launch("elx_colsum final");
 }
 
