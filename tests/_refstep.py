@@ -63,12 +63,13 @@ class ReferenceStep:
                 loss = out.detach()
             if i:
                 grad, gs = gs[0], gs[1:]
-            gs = list(gs[:len(m.node_pieces[i])])
+            full = list(gs)
+            pgs = full[:len(m.node_pieces[i])]
             if layer:
-                gs = [t if g is None else g for g, t in zip(gs, tgt)]
-            grads.update(m.piece_grads_by_param(i, gs))
+                pgs = [t if g is None else g for g, t in zip(pgs, tgt)]
+            grads.update(m.piece_grads_by_param(i, pgs))
             if i in (0, K - 1):
-                gw = gs[-1][:cfg.vocab]
+                gw = full[-1][:cfg.vocab]
                 grads["wte"] = gw if "wte" not in grads else grads["wte"] + gw
         return loss, grads
 
