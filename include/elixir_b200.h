@@ -232,13 +232,21 @@ int elx_step_reset(double* step_scalars, void* stream);
 int elx_step_advance(double* step_scalars, void* stream);
 
 /* ------------------------------------------- K7 bias-gradient reduction
- * out[j] = sum_{i<rows} in[i*cols + j] (fp32 accumulation, deterministic:
- * fixed row slices reduced in slice order), written in out_dtype. Used by the
- * wrapped linear operators to write bias gradients straight over the bias
- * slots of the chunk. `workspace` is a caller-owned DEVICE
- * float buffer of at least elx_colsum_workspace(rows, cols) elements. in_dtype
- * is BF16 or F16; cols must be a multiple of 8 and `in` 16-byte aligned. */
+ * out[j] = sum_{i<rows} in[i*cols + j] (fp32 accumulation, deterministic),
+ * written in out_dtype. Used by the wrapped linear operators to write bias
+ * gradients straight over the bias slots of the chunk.
+ * Summation order (elx_colsum_geometry): the rows are cut into `ctas`
+ * contiguous slices of ceil(rows/ctas), each slice into `groups` contiguous
+ * sub-slices of ceil(slice/groups) rows; every sub-slice is summed from 0.0f in
+ * row order, the sub-slices of a slice in order, then the slices in order.
+ * The default kernel is one thread-block cluster per column strip (partials
+ * combined through distributed shared memory) and needs no workspace
+ * (elx_colsum_workspace returns 0 and `workspace` may be NULL); otherwise
+ * `workspace` is a caller-owned DEVICE float buffer of at least
+ * elx_colsum_workspace(rows, cols) elements. in_dtype is BF16 or F16; cols
+ * must be a multiple of 8 and `in` 16-byte aligned. */
 int64_t elx_colsum_workspace(int64_t rows, int64_t cols);
+int elx_colsum_geometry(int64_t rows, int64_t cols, int32_t* ctas, int32_t* groups);
 int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, int64_t rows, int64_t cols,
                float* workspace, void* stream);
 

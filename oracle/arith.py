@@ -107,6 +107,30 @@ def release(srcs, inv_scale: float, dtype: str = "bf16"):
     return g, sq, bool(not np.isfinite(g).all())
 
 
+def colsum_ordered(x: np.ndarray, slices: int, groups: int) -> np.ndarray:
+    """Bias-gradient column sum (K7) in its fixed fp32 order: rows cut into
+    `slices` contiguous slices of ceil(rows/slices) rows, each slice into
+    `groups` contiguous sub-slices of ceil(slice/groups); a sub-slice is
+    summed from 0 in row order, sub-slices in order, then slices in order.
+    (The bias gradient of y = x W^T + b is the column sum of dy; torch's
+    reference computes it as dy.sum(0) with an unspecified order.)"""
+    rows, cols = x.shape
+    per = -(-rows // slices)
+    sub = -(-per // groups)
+    tot = np.zeros(cols, np.float32)
+    for s in range(slices):
+        end = min(rows, (s + 1) * per)
+        cta = np.zeros(cols, np.float32)
+        for w in range(groups):
+            r0 = s * per + w * sub
+            acc = np.zeros(cols, np.float32)
+            for r in range(r0, min(end, r0 + sub)):
+                acc = (acc + x[r]).astype(np.float32)
+            cta = (cta + acc).astype(np.float32)
+        tot = (tot + cta).astype(np.float32)
+    return tot
+
+
 def clip_coef(sq: float, max_norm: float) -> np.float32:
     """clip_grad_norm_ convention: min(1, max_norm / (norm + 1e-6)) (float64 -> float32)."""
     if not max_norm > 0:

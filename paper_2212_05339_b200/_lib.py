@@ -90,6 +90,7 @@ _SIGNATURES = {
     "elx_step_reset": (ctypes.c_int, [c_vp, c_vp]),
     "elx_step_advance": (ctypes.c_int, [c_vp, c_vp]),
     "elx_colsum_workspace": (c_i64, [c_i64, c_i64]),
+    "elx_colsum_geometry": (ctypes.c_int, [c_i64, c_i64, c_vp, c_vp]),
     "elx_colsum": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_i64, c_i64, c_vp, c_vp]),
     "elx_copy_h2d": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_copy_d2h": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),

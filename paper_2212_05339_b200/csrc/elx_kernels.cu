@@ -8,6 +8,7 @@
 // the same IEEE-754 float32 operations in the same order.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -18,6 +19,8 @@
 #include "elx_internal.h"
 
 namespace {
+
+namespace cg = cooperative_groups;
 
 // ----------------------------------------------------------------- helpers
 
@@ -93,6 +96,11 @@ __device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
                : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
                : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
 // Plain (coherent) 128-bit load, used where the source may be a peer
@@ -263,6 +271,63 @@ __device__ __forceinline__ void block_reduce_and_publish(double sq, int bad, dou
   }
 }
 
+// Sum of squares of one fp32 value into an fp64 accumulator. d*d is exact in
+// fp64 (a 24-bit significand squared fits in 53 bits, and the exponent range
+// of a float squared fits fp64's), so one DFMA rounds exactly like the
+// separate multiply + add the oracle performs.
+__device__ __forceinline__ double sq_acc(double sq, float a) {
+  const double d = (double)a;
+  return __fma_rn(d, d, sq);
+}
+
+// Overflow flag from the accumulated sum of squares: a finite float squares
+// to a finite double (<= 1.2e77) and no sum of < 2^60 of them overflows fp64,
+// so sq is non-finite exactly when some element was inf/nan. This replaces a
+// per-element isfinite test (two instructions per element) by one per thread.
+__device__ __forceinline__ int bad_of(double sq) { return !isfinite(sq); }
+
+// World-1 release (norm + overflow only, no gradient written): the gradient
+// stays in the compute-dtype chunk (K4 reads it in place), so this pass reads
+// 2 B/element and produces sum(g^2) and the overflow flag. 16-byte loads (8
+// elements), kU of them in flight per thread, and occupancy held at >= 4 CTAs
+// per SM by the launch bound: the earlier 4-element / 120-register kernel ran
+// at 25% occupancy and 3.4 TB/s (profiles/r02_release.json). kScaleOne skips
+// the multiply by inv_scale == 1 (an exact identity).
+template <typename T16, bool kScaleOne, int kU>
+__global__ void __launch_bounds__(kRelThreads, 4) release_norm_kernel(const uint4* __restrict__ src, int64_t n,
+                                                              float inv_scale, double* sc) {
+  const int64_t nv = n >> 3;
+  double sq = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * kU;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kU + threadIdx.x; i0 < nv; i0 += stride) {
+    uint4 raw[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t i = i0 + (int64_t)u * blockDim.x;
+      raw[u] = i < nv ? ld_stream(src + i) : make_uint4(0, 0, 0, 0);  // zero bits: +0.0, adds nothing
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const T16* h = reinterpret_cast<const T16*>(&raw[u]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float a = to_f32<T16>(h[e]);
+        if (!kScaleOne) a = __fmul_rn(a, inv_scale);
+        sq = sq_acc(sq, a);
+      }
+    }
+  }
+  if (blockIdx.x == 0) {  // scalar tail (n % 8)
+    const T16* s = reinterpret_cast<const T16*>(src);
+    for (int64_t i = (nv << 3) + threadIdx.x; i < n; i += blockDim.x) {
+      float a = to_f32<T16>(s[i]);
+      if (!kScaleOne) a = __fmul_rn(a, inv_scale);
+      sq = sq_acc(sq, a);
+    }
+  }
+  block_reduce_and_publish(sq, bad_of(sq), sc);
+}
+
 // Vector path: a thread-step reduces 4 consecutive elements from every source
 // (one 8-byte load per rank) and writes one 16-byte float4, so a warp's loads
 // AND stores are each fully contiguous (256 B / 512 B). kU steps per thread are
@@ -276,7 +341,6 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict_
   const int world = kWorld > 0 ? kWorld : world_rt;
   const int64_t nv = n >> 2;
   double sq = 0.0;
-  int bad = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * kU;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kU + threadIdx.x; i0 < nv; i0 += stride) {
     uint2 raw[kU][kR];
@@ -312,8 +376,7 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict_
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         acc[e] = __fmul_rn(acc[e], inv_scale);
-        bad |= !isfinite(acc[e]);
-        sq += (double)acc[e] * (double)acc[e];
+        sq = sq_acc(sq, acc[e]);
       }
       if (g) reinterpret_cast<float4*>(g)[i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     }
@@ -327,12 +390,11 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict_
         a = r == 0 ? x : __fadd_rn(a, x);
       }
       a = __fmul_rn(a, inv_scale);
-      bad |= !isfinite(a);
-      sq += (double)a * (double)a;
+      sq = sq_acc(sq, a);
       if (g) g[i] = a;
     }
   }
-  block_reduce_and_publish(sq, bad, sc);
+  block_reduce_and_publish(sq, bad_of(sq), sc);
 }
 
 // Unaligned fallback: scalar loads for every element.
@@ -340,7 +402,6 @@ template <typename T16>
 __global__ void __launch_bounds__(kRelThreads) release_kernel_scalar(float* g, const PtrBatch src, int world,
                                                                      int64_t n, float inv_scale, double* sc) {
   double sq = 0.0;
-  int bad = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
     float a = 0.f;
@@ -349,11 +410,10 @@ __global__ void __launch_bounds__(kRelThreads) release_kernel_scalar(float* g, c
       a = r == 0 ? x : __fadd_rn(a, x);
     }
     a = __fmul_rn(a, inv_scale);
-    bad |= !isfinite(a);
-    sq += (double)a * (double)a;
+    sq = sq_acc(sq, a);
     if (g) g[i] = a;
   }
-  block_reduce_and_publish(sq, bad, sc);
+  block_reduce_and_publish(sq, bad_of(sq), sc);
 }
 
 template <typename T16>
@@ -370,13 +430,27 @@ int run_release(float* g, const PtrBatch& pb, int64_t n, int world, float inv_sc
     kern<<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc);
   };
   const int64_t nv = n >> 2;
+  static int variant = [] {
+    const char* e = getenv("ELX_REL_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  if (world == 1 && g == nullptr && aligned16(pb.p[0]) && variant == 0) {  // norm/overflow only
+    auto go_norm = [&](auto kern, int u) {
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelThreads, 0);
+      if (per_sm < 1) per_sm = 1;
+      const int64_t work = ((n >> 3) + u - 1) / u;
+      const int grid = (int)std::max<int64_t>(
+          1, std::min<int64_t>((work + kRelThreads - 1) / kRelThreads, (int64_t)sm_count() * per_sm));
+      kern<<<grid, kRelThreads, 0, st>>>(static_cast<const uint4*>(pb.p[0]), n, inv_scale, sc);
+    };
+    if (inv_scale == 1.0f) go_norm(release_norm_kernel<T16, true, 4>, 4);
+    else go_norm(release_norm_kernel<T16, false, 4>, 4);
+    return check_launch("elx_release (norm)");
+  }
   if (!vec) {
     go(release_kernel_scalar<T16>, n);
   } else {
-    static int variant = [] {
-      const char* e = getenv("ELX_REL_VARIANT");
-      return e ? atoi(e) : 0;
-    }();
     switch (world) {
       case 1:
         // U=8 measured best at world 1 (profiles/r01_kernel_variants.md)
@@ -873,6 +947,83 @@ __global__ void colsum_final_kernel(const float* __restrict__ ws, int slices, in
   }
 }
 
+// K7, single launch: one thread-block CLUSTER of kCcCluster CTAs per strip of
+// kCcStrip columns. CTA c of the cluster owns rows [c*per_cta, ...), split
+// into kCcWarps contiguous row groups, one per warp; a lane sums 4 columns
+// (one 8-byte load per row, a warp reads 256 contiguous bytes) with kCcU rows
+// of loads in flight. The warps' partials are combined in warp order through
+// shared memory, then CTA 0 of the cluster reads the other CTAs' partials
+// through distributed shared memory in cluster-rank order and writes the
+// result: no workspace, no second launch, and the order of every fp32 add is
+// fixed (tot = fold_c fold_w fold_rows), so the result is deterministic.
+// Replaces the two-kernel partial/final scheme (3.9 ms over 144 calls per
+// GPT-2 1.3B step, profiles/r01f_launches.md).
+constexpr int kCcWarps = 16;
+constexpr int kCcThreads = kCcWarps * 32;
+constexpr int kCcStrip = 128;
+constexpr int kCcCluster = 8;
+constexpr int kCcU = 16;
+
+template <typename T16>
+__global__ void __cluster_dims__(1, kCcCluster, 1) __launch_bounds__(kCcThreads, 1)
+    colsum_cluster_kernel(const T16* __restrict__ in, int64_t rows, int64_t cols, void* out, int out_dt) {
+  __shared__ float part[kCcWarps][kCcStrip];
+  __shared__ float cta_sum[kCcStrip];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = (int)cluster.block_rank();
+  const int64_t col0 = (int64_t)blockIdx.x * kCcStrip;
+  const int64_t cc = col0 + lane * 4;
+  const int64_t per_cta = (rows + kCcCluster - 1) / kCcCluster;
+  const int64_t per_warp = (per_cta + kCcWarps - 1) / kCcWarps;
+  const int64_t cta_end = min(rows, (int64_t)(c + 1) * per_cta);
+  const int64_t r0 = (int64_t)c * per_cta + (int64_t)warp * per_warp;
+  const int64_t r1 = min(cta_end, r0 + per_warp);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  if (cc < cols && r0 < r1) {
+    // byte pointer advanced by a fixed row stride: no 64-bit multiply per load,
+    // which lets ptxas issue all kCcU loads before the first dependent add
+    const char* p = reinterpret_cast<const char*>(in + r0 * cols + cc);
+    const int64_t sb = cols * (int64_t)sizeof(T16);
+    int64_t r = r0;
+    for (; r + kCcU <= r1; r += kCcU) {
+      uint2 q[kCcU];
+#pragma unroll
+      for (int u = 0; u < kCcU; ++u) q[u] = ld_stream_u2(reinterpret_cast<const uint2*>(p + u * sb));
+      p += kCcU * sb;
+#pragma unroll
+      for (int u = 0; u < kCcU; ++u) {
+        const T16* h = reinterpret_cast<const T16*>(&q[u]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(acc[e], to_f32<T16>(h[e]));
+      }
+    }
+    for (; r < r1; ++r, p += sb) {
+      const uint2 q = ld_stream_u2(reinterpret_cast<const uint2*>(p));
+      const T16* h = reinterpret_cast<const T16*>(&q);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(acc[e], to_f32<T16>(h[e]));
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) part[warp][lane * 4 + e] = acc[e];
+  __syncthreads();
+  if (threadIdx.x < kCcStrip) {
+    float a = 0.f;
+#pragma unroll
+    for (int w = 0; w < kCcWarps; ++w) a = __fadd_rn(a, part[w][threadIdx.x]);
+    cta_sum[threadIdx.x] = a;
+  }
+  cluster.sync();
+  if (c == 0 && threadIdx.x < kCcStrip && col0 + threadIdx.x < cols) {
+    float a = 0.f;
+#pragma unroll
+    for (int k = 0; k < kCcCluster; ++k) a = __fadd_rn(a, *cluster.map_shared_rank(&cta_sum[threadIdx.x], k));
+    st_from_f32(out, col0 + threadIdx.x, out_dt, a);
+  }
+  cluster.sync();  // peers' shared memory stays alive until CTA 0 has read it
+}
+
 }  // namespace
 
 // ======================================================================= ABI
@@ -1006,19 +1157,53 @@ int elx_step_advance(double* step_scalars, void* stream) {
   return check_launch("elx_step_advance");
 }
 
+static int colsum_variant() {
+  static int v = [] {
+    const char* e = getenv("ELX_COLSUM_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 int64_t elx_colsum_workspace(int64_t rows, int64_t cols) {
-  if (rows < 1 || cols < 1) return 0;
+  if (rows < 1 || cols < 1 || colsum_variant() == 0) return 0;
   return (int64_t)colsum_slices(rows, cols) * cols;
+}
+
+int elx_colsum_geometry(int64_t rows, int64_t cols, int32_t* ctas, int32_t* groups) {
+  elx::clear_error();
+  if (!ctas || !groups) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (rows < 1 || cols < 1) return elx::fail(ELX_ERR_VALIDATION, "need rows, cols >= 1");
+  if (colsum_variant() == 0) {
+    *ctas = kCcCluster;
+    *groups = kCcWarps;
+  } else {
+    *ctas = colsum_slices(rows, cols);
+    *groups = 1;
+  }
+  return ELX_OK;
 }
 
 int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, int64_t rows, int64_t cols,
                float* workspace, void* stream) {
   elx::clear_error();
-  if (!out || !in || !workspace) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (!out || !in) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   if (rows < 1 || cols < 1 || cols % 8) return elx::fail(ELX_ERR_VALIDATION, "need rows >= 1, cols a multiple of 8");
-  if (!aligned16(in) || !aligned16(workspace)) return elx::fail(ELX_ERR_VALIDATION, "in/workspace not 16-byte aligned");
+  if (!aligned16(in)) return elx::fail(ELX_ERR_VALIDATION, "in not 16-byte aligned");
   if (elx::dtype_size(out_dtype) == 0) return elx::fail(ELX_ERR_VALIDATION, "bad out dtype");
+  if (in_dtype != ELX_BF16 && in_dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "colsum input must be bf16/f16");
   cudaStream_t st = (cudaStream_t)stream;
+  if (colsum_variant() == 0) {
+    const dim3 grid((unsigned)((cols + kCcStrip - 1) / kCcStrip), kCcCluster);
+    if (in_dtype == ELX_BF16)
+      colsum_cluster_kernel<__nv_bfloat16><<<grid, kCcThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), rows,
+                                                                        cols, out, out_dtype);
+    else
+      colsum_cluster_kernel<__half><<<grid, kCcThreads, 0, st>>>(static_cast<const __half*>(in), rows, cols, out,
+                                                                 out_dtype);
+    return check_launch("elx_colsum (cluster)");
+  }
+  if (!workspace || !aligned16(workspace)) return elx::fail(ELX_ERR_VALIDATION, "workspace null or not 16-byte aligned");
   const int slices = colsum_slices(rows, cols);
   const dim3 grid((unsigned)((cols + kCsCols - 1) / kCsCols), (unsigned)slices);
   if (in_dtype == ELX_BF16)

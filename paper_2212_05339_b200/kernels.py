@@ -254,7 +254,16 @@ def colsum(x2d: torch.Tensor, out: torch.Tensor, stream=None) -> None:
     if x2d.dim() != 2 or out.numel() != x2d.shape[1]:
         raise ValidationError("colsum needs a 2-D input and out of x2d.shape[1] elements")
     rows, cols = x2d.shape
-    ws = torch.empty(max(1, lib.elx_colsum_workspace(rows, cols)), dtype=torch.float32, device=x2d.device)
+    nws = lib.elx_colsum_workspace(rows, cols)
+    ws = torch.empty(nws, dtype=torch.float32, device=x2d.device).data_ptr() if nws > 0 else None
     rc = lib.elx_colsum(out.data_ptr(), elx_dtype(out.dtype), x2d.data_ptr(), elx_dtype(x2d.dtype), rows, cols,
-                        ws.data_ptr(), _stream(stream))
+                        ws, _stream(stream))
     _lib.check(rc, "elx_colsum")
+
+
+def colsum_geometry(rows: int, cols: int) -> tuple[int, int]:
+    """(slices, sub-slices per slice) of K7's fixed summation order."""
+    lib = _lib.load()
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(lib.elx_colsum_geometry(int(rows), int(cols), ctypes.byref(a), ctypes.byref(b)), "elx_colsum_geometry")
+    return a.value, b.value

@@ -131,6 +131,38 @@ def test_release_unaligned_sources_use_scalar_path(cuda):
     assert sc[0].item() == pytest.approx(wsq, rel=1e-12)
 
 
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("inv_scale", [1.0, 1.0 / 65536])
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 4103, 1_048_583])
+@pytest.mark.parametrize("bad", [None, "inf", "nan", "-inf"])
+def test_release_norm_only_world1(cuda, dtype, inv_scale, n, bad):
+    """World-1 release with no gradient output (the dedicated norm kernel:
+    16-byte loads, scalar tail, flag derived from the fp64 sum): sum of squares
+    within 1e-12 of the oracle and the overflow flag exact, including a
+    non-finite element in the vector body or the tail."""
+    g = torch.Generator().manual_seed(n)
+    src = (torch.randn(n, generator=g) * 3.0).to(dtype)
+    if bad is not None:
+        src[(n * 7) // 11] = float(bad)
+    d = src.to(cuda)
+    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    kernels.release(None, [d.data_ptr()], n, dtype, inv_scale, sc)
+    torch.cuda.synchronize()
+    _, wsq, wbad = arith.release([_bits(src)], inv_scale, _name(dtype))
+    assert sc[1].item() == (1.0 if wbad else 0.0)
+    assert wbad == (bad is not None)
+    if not wbad:
+        assert sc[0].item() == pytest.approx(wsq, rel=1e-12)
+    # 8-byte aligned but not 16: same answer through the general path
+    if n > 8 and bad is None:
+        buf = torch.zeros(n + 4, dtype=dtype, device=cuda)
+        buf[4:] = d
+        sc2 = torch.zeros(4, dtype=torch.float64, device=cuda)
+        kernels.release(None, [buf.data_ptr() + 8], n, dtype, inv_scale, sc2)
+        torch.cuda.synchronize()
+        assert sc2[0].item() == pytest.approx(wsq, rel=1e-12) and sc2[1].item() == 0.0
+
+
 def test_release_accumulates_norm_and_flags_overflow(cuda):
     n = 50_000
     g = torch.Generator().manual_seed(9)
@@ -399,9 +431,9 @@ def test_adam_device_step_equals_host_step(cuda):
 
 @pytest.mark.parametrize("rows,cols", [(1, 8), (7, 24), (8192, 2048), (1000, 8200), (4096, 6144)])
 def test_colsum_deterministic_and_exact(cuda, rows, cols):
-    """K7 bias-gradient column sum: fp32 accumulation over the library's fixed
-    row slices in order, then the slices in order — reproduced exactly here."""
-    from paper_2212_05339_b200 import _lib
+    """K7 bias-gradient column sum: fp32 accumulation in the library's fixed
+    order (rows within a sub-slice, sub-slices within a slice, slices) —
+    reproduced exactly by the oracle."""
     rng = np.random.default_rng(rows + cols)
     bits = arith.f32_to_bf16_bits((rng.standard_normal((rows, cols)) * 0.1).astype(np.float32))
     x = torch.from_numpy(bits.view(np.int16)).view(torch.bfloat16).to(cuda)
@@ -409,18 +441,9 @@ def test_colsum_deterministic_and_exact(cuda, rows, cols):
     kernels.colsum(x, out)
     out2 = torch.empty(cols, dtype=torch.float32, device=cuda)
     kernels.colsum(x, out2)
-    slices = _lib.load().elx_colsum_workspace(rows, cols) // cols
-    per = -(-rows // slices)
+    slices, groups = kernels.colsum_geometry(rows, cols)
     xf = arith.bf16_bits_to_f32(bits).reshape(rows, cols)
-    parts = []
-    for s in range(slices):
-        acc = np.zeros(cols, np.float32)
-        for r in range(s * per, min(rows, (s + 1) * per)):
-            acc = (acc + xf[r]).astype(np.float32)
-        parts.append(acc)
-    tot = np.zeros(cols, np.float32)
-    for a in parts:
-        tot = (tot + a).astype(np.float32)
+    tot = arith.colsum_ordered(xf, slices, groups)
     assert np.array_equal(out2.cpu().numpy(), tot)
     assert np.array_equal(_bits(out), arith.f32_to_bf16_bits(tot))
 
