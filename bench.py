@@ -107,18 +107,27 @@ class ClockSampler:
 # ---------------------------------------------------------------- distributed
 
 def _dist_setup(n_gpus: int):
+    """One process per GPU over NCCL. When fewer GPUs than ranks are visible
+    (the one-GPU development box), the ranks share device `local % count` and
+    talk over gloo — a functional run of the N>1 code path (sharding, rCache,
+    all-gather / all-to-all + K3, the scalar all-reduce, max-over-ranks
+    timing), flagged `oversubscribed` in the JSON line: not a scaling number."""
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != n_gpus:
         raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}: launch N>1 with torchrun")
+    ndev = max(1, torch.cuda.device_count())
+    shared = world > ndev
+    dev_index = local % ndev
+    torch.cuda.set_device(dev_index)
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(local)
-    return world, rank, local
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+    return world, rank, dev_index, (f"{world} ranks on {ndev} GPU(s) over gloo" if shared else None)
 
 
 def _max_over_ranks(x: float, world: int) -> float:
@@ -256,7 +265,9 @@ def run_ours(args):
     from paper_2212_05339_b200 import _lib
     from paper_2212_05339_b200.gpt2 import PRESETS, ElixirGPT2
 
-    world, rank, local = _dist_setup(args.gpus)
+    world, rank, local, oversub = _dist_setup(args.gpus)
+    if oversub and args.transport == "p2p":
+        raise SystemExit("--transport p2p needs one GPU per rank (symmetric memory refuses a shared device)")
     dev = torch.device("cuda", local)
     cfg = PRESETS[args.model]
     plan_path = ROOT / "plans" / (args.plan.format(n=world) if args.plan else f"{args.model}_n{world}.json")
@@ -377,6 +388,7 @@ def run_ours(args):
             "parallelism": f"elixir-chunk-dp{world}", "transport": args.transport if world > 1 else "local", "chunk_length": model.layout.chunk_length,
             "n_chunks": model.layout.n_chunks, "n_block": model.manager.plan.n_block,
             "l2": "working set (>20 GB of chunk/optimizer state per step) far exceeds the 126 MB L2; no flush needed",
+            **({"oversubscribed": oversub} if oversub else {}),
         },
         "tflops_per_gpu": flops / (ms / args.steps * 1e-3) / 1e12,
         "final_loss": loss,

@@ -229,6 +229,11 @@ def make_plans(ref):
     mib_cands = lambda lo, hi, step: [k * MI for k in range(lo, hi + 1, step)]
     # C1: GPT-2 small, world 1, 32 MB chunks (16 Mi elements), all blocks.
     emit("gpt2-small_n1.json", "gpt2-small", 1, candidates=[16 * MI])
+    # Multi-process runs of the N > 1 path (tests/test_multiprocess_gpu.py: N ranks on one GPU over
+    # gloo): GPT-2 small at 2 and 4 ranks, all blocks, and with a tight budget (n_block 2 of 12: evictions, 5 chunks CPU-home).
+    for n in (2, 4):
+        emit(f"gpt2-small_n{n}.json", "gpt2-small", n, candidates=[16 * MI])
+    emit("gpt2-small_rcache_n2.json", "gpt2-small", 2, candidates=[8 * MI], u_allowed=0.8e9)
     # C2: GPT-2 1.3B searched over Mi-multiple chunk lengths, 1/2/4/8 GPUs.
     for n in (1, 2, 4, 8):
         emit(f"gpt2-1.3b_n{n}.json", "gpt2-1.3b", n, candidates=mib_cands(16, 128, 2))
@@ -237,7 +242,9 @@ def make_plans(ref):
     emit("gpt2-4b_offload_n1.json", "gpt2-4b", 1, u_allowed=30e9, candidates=mib_cands(36, 256, 4))
     emit("gpt2-4b_offload_n2.json", "gpt2-4b", 2, u_allowed=20e9, candidates=mib_cands(36, 256, 4))
     # C4: GPT-2 10B with cached chunks (working set < n_block < n_chunks) and cold chunks on CPU.
-    for n, u in ((1, 20e9), (2, 12e9), (4, 8e9), (8, 8e9)):
+    # n=1: budget 100 GB -> 13 of 24 chunks GPU-home, 11 CPU-home (72 GB of pinned host shard state;
+    # the B200 box has 196 GB of host RAM, which a 20 GB budget's all-CPU plan, ~158 GB pinned, would exhaust).
+    for n, u in ((1, 100e9), (2, 12e9), (4, 8e9), (8, 8e9)):
         emit(f"gpt2-10b_offload_n{n}.json", "gpt2-10b", n, u_allowed=u, candidates=mib_cands(64, 512, 8))
 
 

@@ -1,0 +1,60 @@
+"""One rank of a REAL multi-process run of the N > 1 runtime path (launched by
+tests/test_multiprocess_gpu.py under torch.distributed.run; not a test file).
+
+Every rank shares GPU 0 and talks over torch.distributed's gloo backend with
+CUDA tensors: the same TorchDistTransport code the NCCL path runs (all-gather
+fetch, all-to-all + K3 release, the shared wte exchange, the N-scalar
+all-reduce), in separate processes with separate CUDA contexts. Trains the
+tiny config of tests/test_multirank_gpu.py for two steps and saves this
+rank's losses, fp32 master shards and live counters to <out>/rank<r>.npz.
+
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P tests/mp_worker.py <plan kind> <out dir>
+"""
+
+import json
+import os
+import sys
+from pathlib import Path
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(HERE.parent))
+sys.path.insert(0, str(HERE))
+
+from paper_2212_05339_b200 import gpt2  # noqa: E402
+from paper_2212_05339_b200.gpt2 import ElixirGPT2  # noqa: E402
+from paper_2212_05339_b200.transport import TorchDistTransport  # noqa: E402
+from test_multirank_gpu import CFG, HP, _batches, _plan, _rank_masters  # noqa: E402
+
+
+def main():
+    kind, out = sys.argv[1], Path(sys.argv[2])
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    torch.cuda.set_device(0)
+    dev = torch.device("cuda", 0)
+    dist.init_process_group("gloo")
+    plan, _, _ = _plan(kind)
+    init = gpt2.init_params(CFG, dev, seed=11)
+    model = ElixirGPT2(CFG, plan, device=dev, transport=TorchDistTransport(), init=init, **HP)
+    losses = []
+    for s in range(2):
+        tok, tgt = _batches(world, s, dev)[rank]
+        losses.append(model.train_step(tok, tgt).item())
+    model.synchronize()
+    torch.cuda.synchronize()
+    rec = {"losses": np.array(losses, np.float64), "counters": np.array(json.dumps(model.fetcher.counters()))}
+    for pid, (off, vals) in _rank_masters(model).items():
+        rec[f"off::{pid}"] = np.array(off)
+        rec[f"val::{pid}"] = vals
+    out.mkdir(parents=True, exist_ok=True)
+    np.savez(out / f"rank{rank}.npz", **rec)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
