@@ -403,9 +403,9 @@ def run_ours(args):
                         "bus_gbs": (None if world == 1 else
                                     (world - 1) / world * 2 * rel_elems * world / (rel_ms * 1e-3) / 1e9)},
             "fetch": {"note": "N=1: GPU-home chunk shards are used in place (zero-copy gathers)"
-                      if world == 1 else ("K2 reading peers' shards over NVLink (symmetric memory)"
-                                          if args.transport == "p2p" else
-                                          "NCCL all_gather_into_tensor on the comm stream")},
+                      if world == 1 else {"p2p": "K2 reading peers' shards over NVLink (symmetric memory)",
+                                          "ipc": "K2 reading peers' shards through CUDA-IPC mappings",
+                                          }.get(args.transport, "all_gather_into_tensor on the comm stream")},
         },
         "roofline": {"bound": "hbm", "kernel": "elx_adam (K4)", "achieved": adam_gbs, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": adam_gbs / peak, "traffic": traffic,
@@ -491,8 +491,9 @@ def main():
                     help="CPU-home chunk update: host threads, GPU-streamed, or split by measured rate")
     ap.add_argument("--overlap", action="store_true",
                     help="issue the GPU update per chunk on an optimizer stream under the next forward")
-    ap.add_argument("--transport", choices=["nccl", "p2p"], default=os.environ.get("ELX_TRANSPORT", "nccl"),
-                    help="N>1 fetch/release path: NCCL collectives + K3, or in-kernel NVLink (symmetric memory)")
+    ap.add_argument("--transport", choices=["nccl", "p2p", "ipc"], default=os.environ.get("ELX_TRANSPORT", "nccl"),
+                    help="N>1 fetch/release path: NCCL collectives + K3, or in-kernel P2P with peer pointers from "
+                         "symmetric memory (p2p) or CUDA IPC + our device barrier (ipc)")
     args = ap.parse_args()
     if args.warmup < 3 and not args.sweep and args.impl == "ours":
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)

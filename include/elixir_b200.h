@@ -153,6 +153,23 @@ int elx_chunk_unpack(const void* chunk, int32_t chunk_dtype, const elx_member* m
 int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t world,
               int32_t dtype, void* stream);
 
+/* Stream-ordered barrier across ranks over peer-mapped memory (the ordering
+ * the in-kernel P2P fetch/release needs: every rank's earlier work on its
+ * stream is visible to every peer before any rank's later work starts).
+ * pads[r] is rank r's int32[world] signal pad (DEVICE pointers, local or
+ * peer-mapped via CUDA IPC / symmetric memory, zero-initialised once); epoch
+ * is a caller counter > 0 that increases by one per barrier. One thread
+ * stores `epoch` into pads[p][rank] for every p with system-scope release
+ * semantics, then waits until pads[rank][p] >= epoch for every p
+ * (acquire). A barrier that waits longer than ~20 s traps (the stream's
+ * context reports an error) instead of hanging. */
+int elx_device_barrier(int32_t* const* pads, int32_t world, int32_t rank, int32_t epoch, void* stream);
+
+/* cudaDeviceEnablePeerAccess(peer) from the current device, treating
+ * "already enabled" and peer == current device as success: kernels here can
+ * then dereference peer-mapped (CUDA IPC) pointers into `peer`'s HBM. */
+int elx_enable_peer_access(int32_t peer_device);
+
 /* ----------------------------------------------------- K3 grad release
  * Reduce-scatter of one chunk's gradients into this rank's fp32 grad shard,
  * fused with loss-scale unscale, fp32 cast, the sum-of-squares partial and

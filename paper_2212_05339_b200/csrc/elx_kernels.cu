@@ -250,6 +250,40 @@ __global__ void __launch_bounds__(kCopyThreads) fetch_kernel(uint4* block, const
   }
 }
 
+// ============================================================= barrier
+struct PadBatch {
+  int32_t* p[ELX_MAX_WORLD];
+};
+
+__device__ __forceinline__ void st_release_sys(int32_t* p, int32_t v) {
+  asm volatile("st.release.sys.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// One thread: publish `epoch` into every rank's pad (slot `rank`), then wait
+// for every rank's arrival in our own pad. The system-scope fence orders all
+// of this stream's earlier writes (previous kernels included) before the flag
+// stores; the acquire loads order the peers' writes before everything this
+// stream runs next. Bounded: ~20 s of polling, then trap (a loud error, never
+// a silent hang).
+__global__ void device_barrier_kernel(const PadBatch pads, int world, int rank, int32_t epoch) {
+  __threadfence_system();
+  for (int p = 0; p < world; ++p) st_release_sys(pads.p[p] + rank, epoch);
+  const int32_t* mine = pads.p[rank];
+  const long long t0 = clock64();
+  for (int p = 0; p < world; ++p) {
+    while (ld_acquire_sys(mine + p) < epoch) {
+      __nanosleep(256);
+      if (clock64() - t0 > 40000000000LL) __trap();
+    }
+  }
+  __threadfence_system();
+}
+
 // ============================================================== K3 release
 constexpr int kRelThreads = 256;
 
@@ -1077,6 +1111,39 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
   fetch_kernel<<<dim3(gx, world), kCopyThreads, 0, (cudaStream_t)stream>>>(static_cast<uint4*>(block), pb,
                                                                              vecs);
   return check_launch("elx_fetch");
+}
+
+int elx_enable_peer_access(int32_t peer_device) {
+  elx::clear_error();
+  int cur = 0;
+  cudaGetDevice(&cur);
+  if (peer_device == cur) return ELX_OK;
+  int can = 0;
+  cudaDeviceCanAccessPeer(&can, cur, peer_device);
+  if (!can) return elx::fail(ELX_ERR_CUDA, "device %d cannot access peer %d", cur, peer_device);
+  cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free status
+    return ELX_OK;
+  }
+  if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "enable peer access %d: %s", peer_device, cudaGetErrorString(e));
+  return ELX_OK;
+}
+
+int elx_device_barrier(int32_t* const* pads, int32_t world, int32_t rank, int32_t epoch, void* stream) {
+  elx::clear_error();
+  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (rank < 0 || rank >= world) return elx::fail(ELX_ERR_VALIDATION, "rank %d out of range", rank);
+  if (epoch <= 0) return elx::fail(ELX_ERR_VALIDATION, "epoch must be > 0");
+  if (!pads) return elx::fail(ELX_ERR_VALIDATION, "null pad table");
+  PadBatch pb{};
+  for (int r = 0; r < world; ++r) {
+    if (!pads[r] || (reinterpret_cast<uintptr_t>(pads[r]) & 3u))
+      return elx::fail(ELX_ERR_VALIDATION, "pad %d null or misaligned", r);
+    pb.p[r] = pads[r];
+  }
+  device_barrier_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(pb, world, rank, epoch);
+  return check_launch("elx_device_barrier");
 }
 
 int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t world, int32_t dtype,

@@ -97,6 +97,21 @@ def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream
     _lib.check(rc, "elx_fetch")
 
 
+def enable_peer_access(peer_device: int) -> None:
+    """Let kernels on the current device read/write memory on `peer_device`
+    (NVLink P2P; a no-op when already enabled or when it is this device)."""
+    _lib.check(_lib.load().elx_enable_peer_access(int(peer_device)), "elx_enable_peer_access")
+
+
+def device_barrier(pad_ptrs: Sequence[int], rank: int, epoch: int, stream=None) -> None:
+    """Stream-ordered cross-rank barrier over peer-mapped int32[world] signal
+    pads (pad_ptrs[r] = rank r's pad as a pointer usable on this device)."""
+    lib = _lib.load()
+    arr = _ptr_array(pad_ptrs)
+    rc = lib.elx_device_barrier(ctypes.addressof(arr), len(pad_ptrs), int(rank), int(epoch), _stream(stream))
+    _lib.check(rc, "elx_device_barrier")
+
+
 def release(grad_shard: torch.Tensor | None, src_ptrs: Sequence[int], n: int, dtype: torch.dtype,
             inv_scale: float, step_scalars: torch.Tensor, stream=None) -> None:
     """K3: grad_shard[:n] = (sum_r src_r[:n] in rank order, fp32) * inv_scale,

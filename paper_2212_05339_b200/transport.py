@@ -107,8 +107,65 @@ class SymmMemTransport(TorchDistTransport):
         self.handles[0].barrier(channel=0)
 
 
+class IpcTransport(TorchDistTransport):
+    """The same in-kernel P2P path without symmetric memory: shards and
+    rCache blocks are ordinary device tensors exported with CUDA IPC (torch's
+    CUDA tensor sharing), every rank maps its peers' allocations, and the
+    stream-ordered device barrier is our own kernel (elx_device_barrier) over
+    IPC-mapped int32 signal pads. Works for ranks on different GPUs (peer
+    access over NVLink, enabled explicitly) and for several processes sharing
+    one GPU, which symmetric memory refuses — so the P2P path can run in real
+    separate processes on the one-GPU test box."""
+
+    p2p = True
+
+    def __init__(self, group=None):
+        super().__init__(group)
+        from . import kernels
+
+        self._kernels = kernels
+        self.device = torch.device("cuda", torch.cuda.current_device())
+        self.peers: list[torch.Tensor] = []  # keep the peer mappings alive
+        self.epoch = 0
+        self.pad = torch.zeros(self.world, dtype=torch.int32, device=self.device)
+        self.pad_ptrs = self.peer_ptrs(self.pad)
+
+    def alloc(self, shape, dtype, device) -> torch.Tensor:
+        return torch.zeros(shape, dtype=dtype, device=device)
+
+    def peer_ptrs(self, t: torch.Tensor) -> list[int]:
+        """Device pointers of `t`'s counterpart on every rank (rank order)."""
+        if t.numel() == 0:
+            return [0] * self.world
+        from torch.multiprocessing.reductions import rebuild_cuda_tensor, reduce_tensor
+
+        torch.cuda.current_stream(t.device).synchronize()  # contents initialised before peers map it
+        _, args = reduce_tensor(t)
+        everyone = [None] * self.world
+        dist.all_gather_object(everyone, (t.device.index, args), group=self.group)
+        ptrs = []
+        for r, (dev_index, a) in enumerate(everyone):
+            if r == self.rank:
+                ptrs.append(t.data_ptr())
+                continue
+            if dev_index != t.device.index:
+                self._kernels.enable_peer_access(dev_index)
+            peer = rebuild_cuda_tensor(*a)
+            self.peers.append(peer)
+            ptrs.append(peer.data_ptr())
+        torch.cuda.set_device(t.device)
+        dist.barrier(group=self.group)  # every rank has mapped before anyone frees or reuses
+        return ptrs
+
+    def device_barrier(self) -> None:
+        """All ranks' current streams reach this point before any continues."""
+        self.epoch += 1
+        self._kernels.device_barrier(self.pad_ptrs, self.rank, self.epoch)
+
+
 def make_transport(world_size: int, kind: str | None = None):
-    """kind: "nccl" (default) or "p2p" (env ELX_TRANSPORT)."""
+    """kind: "nccl" (default), "p2p" (symmetric memory) or "ipc" (CUDA IPC
+    peer mappings + our device barrier); env ELX_TRANSPORT."""
     import os
 
     if world_size == 1:
@@ -116,4 +173,6 @@ def make_transport(world_size: int, kind: str | None = None):
     kind = kind or os.environ.get("ELX_TRANSPORT", "nccl")
     if kind == "p2p":
         return SymmMemTransport()
+    if kind == "ipc":
+        return IpcTransport()
     return TorchDistTransport()

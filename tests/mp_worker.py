@@ -9,7 +9,11 @@ tiny config of tests/test_multirank_gpu.py for two steps and saves this
 rank's losses, fp32 master shards and live counters to <out>/rank<r>.npz.
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
-        --master-port P tests/mp_worker.py <plan kind> <out dir>
+        --master-port P tests/mp_worker.py <plan kind> <out dir> [exchange|ipc]
+
+"ipc" runs the in-kernel P2P path instead: K2 reads the peers' shards and K3
+the peers' rCache blocks through CUDA-IPC mappings of the other processes'
+allocations, ordered by elx_device_barrier over IPC-mapped signal pads.
 """
 
 import json
@@ -27,19 +31,22 @@ sys.path.insert(0, str(HERE))
 
 from paper_2212_05339_b200 import gpt2  # noqa: E402
 from paper_2212_05339_b200.gpt2 import ElixirGPT2  # noqa: E402
-from paper_2212_05339_b200.transport import TorchDistTransport  # noqa: E402
+from paper_2212_05339_b200.transport import IpcTransport, TorchDistTransport  # noqa: E402
 from test_multirank_gpu import CFG, HP, _batches, _plan, _rank_masters  # noqa: E402
 
 
 def main():
     kind, out = sys.argv[1], Path(sys.argv[2])
+    path = sys.argv[3] if len(sys.argv) > 3 else "exchange"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     torch.cuda.set_device(0)
     dev = torch.device("cuda", 0)
     dist.init_process_group("gloo")
     plan, _, _ = _plan(kind)
     init = gpt2.init_params(CFG, dev, seed=11)
-    model = ElixirGPT2(CFG, plan, device=dev, transport=TorchDistTransport(), init=init, **HP)
+    transport = IpcTransport() if path == "ipc" else TorchDistTransport()
+    model = ElixirGPT2(CFG, plan, device=dev, transport=transport, init=init, **HP)
+    assert model.manager.p2p == (path == "ipc")
     losses = []
     for s in range(2):
         tok, tgt = _batches(world, s, dev)[rank]

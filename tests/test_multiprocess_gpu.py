@@ -2,7 +2,9 @@
 context per rank, torch.distributed gloo collectives on CUDA tensors), all
 ranks sharing the one GPU of the test box.
 
-1. tests/mp_worker.py trains the tiny config for two steps per rank; its
+1. tests/mp_worker.py trains the tiny config for two steps per rank (over the
+   gloo exchange path, or over the in-kernel P2P path with CUDA-IPC peer
+   mappings and our device barrier); its
    losses, fp32 master shards and live counters must equal the thread
    loopback run of the same config (tests/test_multirank_gpu.py), which is
    itself checked bit for bit against the CPU oracle — so the multi-process
@@ -50,10 +52,14 @@ def _torchrun(world: int, args: list[str], timeout: int = 600) -> subprocess.Com
     return p
 
 
+@pytest.mark.parametrize("path", ["exchange", "ipc"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kind", ["rcache-min", "offload"])
-def test_multiprocess_gloo_equals_loopback(cuda, tmp_path, world, kind):
-    _torchrun(world, ["tests/mp_worker.py", kind, str(tmp_path)])
+def test_multiprocess_gloo_equals_loopback(cuda, tmp_path, world, kind, path):
+    """path "exchange": gloo all-gather / all-to-all + K3. path "ipc": the
+    in-kernel P2P path across processes (CUDA-IPC peer mappings, our device
+    barrier kernel), which symmetric memory cannot run on a shared GPU."""
+    _torchrun(world, ["tests/mp_worker.py", kind, str(tmp_path), path])
     got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
 
     plan, fwd, red = _plan(kind)
@@ -93,10 +99,12 @@ def test_multiprocess_gloo_equals_loopback(cuda, tmp_path, world, kind):
                 np.testing.assert_allclose(vals, ref_vals, rtol=1e-6, atol=0)
 
 
-@pytest.mark.parametrize("plan", ["gpt2-small_n2.json", "gpt2-small_rcache_n2.json"])
-def test_bench_two_ranks_one_gpu(cuda, plan):
+@pytest.mark.parametrize("plan,transport", [("gpt2-small_n2.json", "nccl"), ("gpt2-small_rcache_n2.json", "nccl"),
+                                            ("gpt2-small_rcache_n2.json", "ipc")])
+def test_bench_two_ranks_one_gpu(cuda, plan, transport):
+    """transport "nccl" falls back to gloo on a shared GPU (same TorchDistTransport code)."""
     p = _torchrun(2, ["bench.py", "--gpus", "2", "--model", "gpt2-small", "--plan", plan, "--steps", "2",
-                      "--warmup", "3", "--no-cpu"], timeout=900)
+                      "--warmup", "3", "--no-cpu", "--transport", transport], timeout=900)
     line = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1])
     assert line["n_gpus"] == 2 and line["config"]["global_batch"] == 16
     assert "oversubscribed" in line["config"]
