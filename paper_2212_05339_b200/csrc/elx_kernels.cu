@@ -845,6 +845,190 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1)
   }
 }
 
+// ------------------------------------------------- K4 (TMA in, TMA out)
+// As adam_tma_kernel, but the results also leave through the TMA engine: the
+// consumers write p32/m/v back over their operands in the stage and the
+// compute-dtype parameter over the gradient slot, then one elected consumer
+// thread issues four cp.async.bulk shared->global stores per tile (bulk
+// group) and hands the stage back to the producer once those stores have
+// READ shared memory (wait_group.read, one tile behind so the stores of
+// tile q overlap the math of tile q+1). Warps issue no global stores at all.
+__device__ __forceinline__ void bar_consumers(int n) {
+  asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int kN>
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kN) : "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <typename T16, int kStages, int kTile, int kCW>
+__global__ void __launch_bounds__(kCW * 32 + 32, 1)
+    adam_tma_st_kernel(const elx_adam_seg* __restrict__ segs, int nseg, int64_t ntiles, const AdamK k0,
+                       const double* __restrict__ sc) {
+  constexpr int kCons = kCW * 32;
+  constexpr int kSub = ELX_ADAM_TILE / kTile;
+  constexpr int kStageBytes = 16 * kTile;
+  constexpr int kU = kTile / (kCons * 4);
+  static_assert(kSub * kTile == ELX_ADAM_TILE && kU * kCons * 4 == kTile, "tile shape");
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float* stage_base = reinterpret_cast<float*>(smem_raw);
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);  // the elected storer hands the stage back
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const bool skip = sc[1] != 0.0;
+  const float coef = clip_coef(sc, k0.max_norm);
+  const AdamK k = resolve_step(k0, sc);
+
+  auto tma_ok = [&](const TileRef& r) {
+    return r.tma && aligned16(static_cast<char*>(segs[r.seg].p16) + 2 * r.base);
+  };
+
+  if (warp == kCons / 32) {  // ---------------- producer warp
+    if (lane == 0) {
+      int s = 0;
+      int64_t q = 0;
+      for (int64_t tt = blockIdx.x; tt < ntiles * kSub; tt += gridDim.x) {
+        const TileRef r = locate<kTile>(segs, nseg, s, tt / kSub, (int)(tt % kSub));
+        if (!tma_ok(r)) continue;
+        const int st = (int)(q % kStages);
+        const uint32_t ph = (uint32_t)((q / kStages) & 1);
+        mbar_wait(&empty[st], ph ^ 1u);
+        float* dst = stage_base + (size_t)st * (kStageBytes / 4);
+        const elx_adam_seg& sg = segs[r.seg];
+        const int gsz = sg.g_dtype == ELX_F32 ? 4 : 2;
+        mbar_expect_tx(&full[st], 3 * kTile * 4 + kTile * gsz);
+        tma_load_1d(dst, sg.p32 + r.base, kTile * 4, &full[st]);
+        tma_load_1d(dst + kTile, sg.m + r.base, kTile * 4, &full[st]);
+        tma_load_1d(dst + 2 * kTile, sg.v + r.base, kTile * 4, &full[st]);
+        tma_load_1d(dst + 3 * kTile, static_cast<const char*>(sg.g) + (int64_t)gsz * r.base, kTile * gsz, &full[st]);
+        ++q;
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumer warps
+  const bool storer = threadIdx.x == 0;
+  int s = 0;
+  int64_t q = 0;
+  int prev_st = -1;  // stage whose stores were issued last (storer only)
+  for (int64_t tt = blockIdx.x; tt < ntiles * kSub; tt += gridDim.x) {
+    const TileRef r = locate<kTile>(segs, nseg, s, tt / kSub, (int)(tt % kSub));
+    if (r.cnt <= 0) continue;
+    const elx_adam_seg& sg = segs[r.seg];
+    float* __restrict__ p32 = sg.p32 + r.base;
+    float* __restrict__ m = sg.m + r.base;
+    float* __restrict__ v = sg.v + r.base;
+    T16* __restrict__ p16 = static_cast<T16*>(sg.p16) + r.base;
+    if (!tma_ok(r)) {  // tail / misaligned tile: straight from global memory
+      const int gdt = sg.g_dtype;
+      for (int64_t i = threadIdx.x; i < r.cnt; i += kCons) {
+        float P = p32[i];
+        if (!skip) {
+          float M = m[i], V = v[i];
+          adam_elem(P, M, V, load_grad<T16>(sg.g, r.base + i, gdt, k.grad_scale), coef, k);
+          p32[i] = P;
+          m[i] = M;
+          v[i] = V;
+        }
+        p16[i] = from_f32<T16>(P);
+      }
+      continue;
+    }
+    const int st = (int)(q % kStages);
+    const uint32_t ph = (uint32_t)((q / kStages) & 1);
+    ++q;
+    mbar_wait(&full[st], ph);
+    float* stg = stage_base + (size_t)st * (kStageBytes / 4);
+    const bool g32 = sg.g_dtype == ELX_F32;
+    float4 P[kU], M[kU], V[kU], G[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = u * kCons + threadIdx.x;
+      P[u] = reinterpret_cast<const float4*>(stg)[j];
+      M[u] = reinterpret_cast<const float4*>(stg + kTile)[j];
+      V[u] = reinterpret_cast<const float4*>(stg + 2 * kTile)[j];
+      G[u] = g32 ? reinterpret_cast<const float4*>(stg + 3 * kTile)[j]
+                 : cvt4_grad<T16>(reinterpret_cast<const uint2*>(stg + 3 * kTile)[j], k.grad_scale);
+    }
+    // fp32 gradients: the 2-byte results of float4 j land on bytes another
+    // thread's float4 occupies, so every read finishes first (bf16: in place)
+    if (g32) bar_consumers(kCons);
+    T16* out16 = reinterpret_cast<T16*>(stg + 3 * kTile);
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int j = u * kCons + threadIdx.x;
+      if (!skip) {
+        adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
+        adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
+        adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
+        adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
+        reinterpret_cast<float4*>(stg)[j] = P[u];
+        reinterpret_cast<float4*>(stg + kTile)[j] = M[u];
+        reinterpret_cast<float4*>(stg + 2 * kTile)[j] = V[u];
+      }
+      store4<T16>(out16 + 4 * j, P[u].x, P[u].y, P[u].z, P[u].w);
+    }
+    fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy engine
+    bar_consumers(kCons);
+    if (storer) {
+      if (!skip) {
+        tma_store_1d(p32, stg, kTile * 4);
+        tma_store_1d(m, stg + kTile, kTile * 4);
+        tma_store_1d(v, stg + 2 * kTile, kTile * 4);
+      }
+      tma_store_1d(p16, out16, kTile * 2);
+      tma_store_commit();
+      if (prev_st >= 0) {
+        tma_store_wait_read<1>();  // the previous tile's stores have read their stage
+        mbar_arrive(&empty[prev_st]);
+      }
+      prev_st = st;
+    }
+  }
+  if (storer) {
+    tma_store_wait_all();
+    if (prev_st >= 0) mbar_arrive(&empty[prev_st]);
+  }
+}
+
+template <typename T16, int kStages, int kTile, int kCW>
+int launch_adam_tma_st(const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
+                       cudaStream_t st) {
+  constexpr int kThreads = kCW * 32 + 32;
+  const int smem = kStages * 16 * kTile;
+  auto kern = adam_tma_st_kernel<T16, kStages, kTile, kCW>;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    configured = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int grid = (int)std::min<int64_t>(ntiles * (ELX_ADAM_TILE / kTile), (int64_t)sm_count() * per_sm);
+  kern<<<grid, kThreads, smem, st>>>(segs, nseg, ntiles, k, sc);
+  return check_launch("elx_adam (tma in/out)");
+}
+
 template <typename T16, int kStages, int kTile, int kCW>
 int launch_adam_tma(const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
                     cudaStream_t st) {
@@ -864,9 +1048,11 @@ int launch_adam_tma(const elx_adam_seg* segs, int nseg, int64_t ntiles, const Ad
   return check_launch("elx_adam (tma)");
 }
 
-// Variant table: 0/7 TMA-staged (default), 5/6 TMA with 4/6 stages, 8 and 1-4
-// register-staged (unroll, min blocks per SM). Default chosen from the measured
-// sweep (profiles/r01_kernel_variants.md); ELX_ADAM_VARIANT overrides.
+// Variant table: 0/13 TMA in + TMA bulk-store out (default), 14/15 the same with
+// 2 stages / 16 consumer warps; 7 TMA-staged loads with register stores, 5/6/9-12
+// its other shapes; 8 and 1-4 register-staged (unroll, min blocks per SM). Default
+// chosen from the measured sweep (profiles/r01_kernel_variants.md);
+// ELX_ADAM_VARIANT overrides.
 template <typename T16>
 int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
                 cudaStream_t st) {
@@ -885,13 +1071,19 @@ int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles,
     case 10: return launch_adam_tma<T16, 4, 1024, 8>(segs, nseg, ntiles, k, sc, st);
     case 11: return launch_adam_tma<T16, 3, 1024, 8>(segs, nseg, ntiles, k, sc, st);
     case 12: return launch_adam_tma<T16, 4, 2048, 16>(segs, nseg, ntiles, k, sc, st);
+    case 13: return launch_adam_tma_st<T16, 3, 2048, 8>(segs, nseg, ntiles, k, sc, st);
+    case 14: return launch_adam_tma_st<T16, 2, 2048, 8>(segs, nseg, ntiles, k, sc, st);
+    case 15: return launch_adam_tma_st<T16, 3, 2048, 16>(segs, nseg, ntiles, k, sc, st);
     case 8: return go(adam_kernel<T16, 2, 3>);
     case 1: return go(adam_kernel<T16, 4, 2>);
     case 2: return go(adam_kernel<T16, 4, 3>);
     case 3: return go(adam_kernel<T16, 2, 4>);
     case 4: return go(adam_kernel<T16, 1, 6>);
-    default:  // 0 / 7: TMA-staged, 3 stages x 32 KB, 2 CTAs per SM (profiles/r01_kernel_variants.md)
-      return launch_adam_tma<T16, 3, 2048, 8>(segs, nseg, ntiles, k, sc, st);
+    case 7: return launch_adam_tma<T16, 3, 2048, 8>(segs, nseg, ntiles, k, sc, st);
+    default:  // 0 / 13: TMA in + TMA bulk-store out, 3 stages x 32 KB, 2 CTAs per SM: 0.963 of the
+              // measured copy peak in-step, above a no-math kernel moving the same bytes
+              // (profiles/r01_kernel_variants.md)
+      return launch_adam_tma_st<T16, 3, 2048, 8>(segs, nseg, ntiles, k, sc, st);
   }
 }
 

@@ -15,7 +15,13 @@ g0 = torch.Generator(device=dev).manual_seed(0)
 f = lambda s: (torch.randn(segs_n, per, device=dev, generator=g0) * s)
 p32, m, v, g = f(0.02), f(1e-3), f(1e-3).abs() * 1e-3, f(0.05)
 p16 = torch.zeros(segs_n, per, dtype=torch.bfloat16, device=dev)
-tab = kernels.AdamTable([(p32[i], m[i], v[i], g[i], p16[i], per) for i in range(segs_n)], dev)
+# argv[2] == "bf16": the world-1 fused layout of the training step — the gradient is the bf16
+# chunk itself (read in place, overwritten by the new parameter): 28 B/element instead of 30
+fused = len(sys.argv) > 2 and sys.argv[2] == "bf16"
+if fused:
+    p16.copy_(g)
+tab = kernels.AdamTable([(p32[i], m[i], v[i], p16[i] if fused else g[i], p16[i], per) for i in range(segs_n)], dev)
+bpe = 28 if fused else 30
 sc = torch.zeros(4, dtype=torch.float64, device=dev)
 hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
 
@@ -32,7 +38,8 @@ def timed(fn, reps=10, warm=40):
 
 
 t = timed(lambda: kernels.adam(tab, hp, 3, sc, torch.bfloat16), warm=60)
-print(f"adam variant {os.environ.get('ELX_ADAM_VARIANT', '0')}: {t:.3f} ms  {30 * segs_n * per / t / 1e6:.1f} GB/s")
+print(f"adam variant {os.environ.get('ELX_ADAM_VARIANT', '0')} ({bpe} B/elem): {t:.3f} ms  "
+      f"{bpe * segs_n * per / t / 1e6:.1f} GB/s")
 src = p16.view(-1)[: segs_n * per]
 out = g.view(-1)
 tot = segs_n * per
