@@ -335,6 +335,31 @@ def run_ours(args):
     torch.cuda.synchronize(dev)
     e2e_ms = _max_over_ranks(f0.elapsed_time(f1), world)
 
+    # ---- K3 alone on the step's own chunks (world 1: the norm/overflow pass over every GPU-home
+    # chunk, the same launches as inside the step, with the GPU otherwise idle): the in-step time
+    # above is stretched by the backward GEMMs running concurrently on the compute stream
+    rel_alone = None
+    if world == 1 and model.manager.gpu_ids:
+        from paper_2212_05339_b200 import kernels
+        mgr = model.manager
+        scratch = torch.zeros(4, dtype=torch.float64, device=dev)
+        todo = [(mgr.home_storage(c).data_ptr(), mgr.valid(c)) for c in mgr.gpu_ids if mgr.valid(c) > 0]
+        ts = []
+        for i in range(8):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(cur)
+            for ptr, n in todo:
+                kernels.release(None, [ptr], n, mgr.dtype, 1.0, scratch, stream=cur)
+            b.record(cur)
+            torch.cuda.synchronize(dev)
+            if i >= 3:
+                ts.append(a.elapsed_time(b))
+        ms_alone = statistics.median(ts)
+        n_alone = sum(n for _, n in todo)
+        rel_alone = {"ms": ms_alone, "launches": len(todo), "elements": n_alone,
+                     "hbm_gbs": 2 * n_alone / (ms_alone * 1e-3) / 1e9,
+                     "frac": 2 * n_alone / (ms_alone * 1e-3) / 1e9 / _peaks()[0]}
+
     if rank != 0:
         return
     peak, peak_src = _peaks()
@@ -401,7 +426,9 @@ def run_ours(args):
             "release": {"ms_per_step": rel_ms, "elements_per_step": rel_elems,
                         "local_hbm_gbs": rel_local_bytes / (rel_ms * 1e-3) / 1e9 if rel_ms else None,
                         "bus_gbs": (None if world == 1 else
-                                    (world - 1) / world * 2 * rel_elems * world / (rel_ms * 1e-3) / 1e9)},
+                                    (world - 1) / world * 2 * rel_elems * world / (rel_ms * 1e-3) / 1e9),
+                        "in_step_note": "comm stream, concurrent with the backward's GEMMs",
+                        "alone": rel_alone},
             "fetch": {"note": "N=1: GPU-home chunk shards are used in place (zero-copy gathers)"
                       if world == 1 else {"p2p": "K2 reading peers' shards over NVLink (symmetric memory)",
                                           "ipc": "K2 reading peers' shards through CUDA-IPC mappings",
@@ -432,13 +459,16 @@ def run_sweep(args):
     from paper_2212_05339_b200 import kernels
     dev = torch.device("cuda", 0)
     peak, src = _peaks()
-    flush = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    # L2 flush by READING 256 MB (2x the 126 MB L2): a write-flush (zero_) would leave the L2 full of
+    # dirty lines whose write-back then lands inside the next timed kernel
+    flush = torch.ones(64 * 2 ** 20, dtype=torch.float32, device=dev)
+    flush_sink = torch.empty((), dtype=torch.float32, device=dev)
     out = []
 
     def timeit(fn, reps=10):
         ts = []
         for i in range(reps + 3):
-            flush.zero_()
+            torch.sum(flush, dim=0, out=flush_sink)
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()
@@ -458,6 +488,7 @@ def run_sweep(args):
             g32 = torch.empty(S, device=dev)
             sc = torch.zeros(4, dtype=torch.float64, device=dev)
             t_f = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S))
+            t_fc = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S, engine="ce"))
             t_r = timeit(lambda: kernels.release(g32, [s.data_ptr() for s in shards], S, torch.bfloat16, 1.0, sc))
             p32, m, v = (torch.zeros(S, device=dev) for _ in range(3))
             p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
@@ -467,6 +498,7 @@ def run_sweep(args):
             t_a = timeit(lambda: kernels.adam(tab, hp, 1, sc, torch.bfloat16))
             rec = {"chunk_mb": mb, "world": world, "shard_elems": S,
                    "fetch": {"ms": t_f, "hbm_gbs": 2 * 2 * world * S / (t_f * 1e-3) / 1e9},
+                   "fetch_copy_engine": {"ms": t_fc, "hbm_gbs": 2 * 2 * world * S / (t_fc * 1e-3) / 1e9},
                    "release": {"ms": t_r, "hbm_gbs": (2 * world * S + 4 * S) / (t_r * 1e-3) / 1e9},
                    "adam": {"ms": t_a, "hbm_gbs": 30 * S / (t_a * 1e-3) / 1e9,
                             "frac": 30 * S / (t_a * 1e-3) / 1e9 / peak}}

@@ -153,6 +153,13 @@ int elx_chunk_unpack(const void* chunk, int32_t chunk_dtype, const elx_member* m
 int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t world,
               int32_t dtype, void* stream);
 
+/* K2 on the copy engines instead of SMs: the same gather (same arguments,
+ * same validation, same bytes) as `world` cudaMemcpyAsync calls on `stream`
+ * (peer shards over NVLink through the DMA engines), so a fetch overlapped
+ * with the compute stream's GEMMs takes no SM time from them. */
+int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int32_t world,
+                 int32_t dtype, void* stream);
+
 /* Stream-ordered barrier across ranks over peer-mapped memory (the ordering
  * the in-kernel P2P fetch/release needs: every rank's earlier work on its
  * stream is visible to every peer before any rank's later work starts).

@@ -1305,6 +1305,28 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
   return check_launch("elx_fetch");
 }
 
+int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int32_t world, int32_t dtype,
+                 void* stream) {
+  elx::clear_error();
+  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "fetch dtype must be bf16/f16");
+  if (shard_len < 0 || (shard_len % 8) != 0)
+    return elx::fail(ELX_ERR_VALIDATION, "shard_len %lld must be a non-negative multiple of 8",
+                     (long long)shard_len);
+  if (!block || !shards) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (!aligned16(block)) return elx::fail(ELX_ERR_VALIDATION, "block must be 16-byte aligned");
+  for (int r = 0; r < world; ++r)
+    if (!shards[r] || !aligned16(shards[r]))
+      return elx::fail(ELX_ERR_VALIDATION, "shard %d null or not 16-byte aligned", r);
+  const size_t bytes = (size_t)shard_len * 2;
+  for (int r = 0; r < world && bytes > 0; ++r) {
+    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(block) + r * bytes, shards[r], bytes, cudaMemcpyDefault,
+                                    (cudaStream_t)stream);
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_fetch_ce rank %d: %s", r, cudaGetErrorString(e));
+  }
+  return ELX_OK;
+}
+
 int elx_enable_peer_access(int32_t peer_device) {
   elx::clear_error();
   int cur = 0;

@@ -85,16 +85,21 @@ def _ptr_array(ptrs: Sequence[int]):
     return arr
 
 
-def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream=None) -> None:
-    """K2: block[r*S:(r+1)*S] <- shard r (device pointers, local or peer-mapped)."""
+def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream=None, engine: str = "sm") -> None:
+    """K2: block[r*S:(r+1)*S] <- shard r (device pointers, local or peer-mapped).
+    engine "sm": the fetch kernel; "ce": the copy engines (cudaMemcpyAsync per
+    rank), leaving every SM to the compute stream."""
     lib = _lib.load()
     _cuda(block, "block")
     if block.numel() < len(shard_ptrs) * shard_len:
         raise ValidationError("block smaller than world * shard_len")
+    if engine not in ("sm", "ce"):
+        raise ValidationError(f"fetch engine must be 'sm' or 'ce', not {engine!r}")
     arr = _ptr_array(shard_ptrs)
-    rc = lib.elx_fetch(block.data_ptr(), ctypes.addressof(arr), int(shard_len), len(shard_ptrs),
-                       elx_dtype(block.dtype), _stream(stream))
-    _lib.check(rc, "elx_fetch")
+    fn = lib.elx_fetch if engine == "sm" else lib.elx_fetch_ce
+    rc = fn(block.data_ptr(), ctypes.addressof(arr), int(shard_len), len(shard_ptrs), elx_dtype(block.dtype),
+            _stream(stream))
+    _lib.check(rc, "elx_fetch" if engine == "sm" else "elx_fetch_ce")
 
 
 def enable_peer_access(peer_device: int) -> None:

@@ -447,7 +447,8 @@ class ChunkFetcher:
                 # K2 over NVLink: read every rank's shard of c straight from its HBM
                 es = block.element_size()
                 off = mgr.row[c] * mgr.S * es
-                kernels.fetch(block, [p + off for p in mgr.peer_p16], mgr.S, stream=comm)
+                kernels.fetch(block, [p + off for p in mgr.peer_p16], mgr.S, stream=comm,
+                              engine=getattr(mgr.transport, "fetch_engine", "sm"))
             elif cpu:
                 if self.time_release:
                     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -12,7 +12,12 @@ Two exchange primitives cover the path:
 Implementations:
   LocalTransport   world 1 (nothing moves between ranks);
   TorchDistTransport  torch.distributed collectives (NCCL over NVLink on the
-                   GPU box; gloo on CPU for the multi-process host tests).
+                   GPU box; gloo on CPU for the multi-process host tests);
+  SymmMemTransport   in-kernel P2P: K2/K3 read peers' HBM through torch
+                   symmetric-memory mappings, symmetric-memory barriers;
+  IpcTransport     the same P2P path over CUDA-IPC mappings and our own
+                   device barrier kernel (also runs N processes on one GPU).
+The P2P transports can run K2 on the copy engines (fetch_engine "ce").
 Collectives are issued under the caller's current stream, so the comm
 stream orders them with the K1-K3 launches around them.
 """
@@ -75,10 +80,14 @@ class SymmMemTransport(TorchDistTransport):
 
     p2p = True
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, fetch_engine: str | None = None):
         super().__init__(group)
+        import os
+
         import torch.distributed._symmetric_memory as symm
 
+        # K2 on SMs ("sm", the fetch kernel) or on the copy engines ("ce")
+        self.fetch_engine = fetch_engine or os.environ.get("ELX_FETCH_ENGINE", "sm")
         self.symm = symm
         self.handles = []
         self._group = group if group is not None else dist.group.WORLD
@@ -119,10 +128,13 @@ class IpcTransport(TorchDistTransport):
 
     p2p = True
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, fetch_engine: str | None = None):
         super().__init__(group)
+        import os
+
         from . import kernels
 
+        self.fetch_engine = fetch_engine or os.environ.get("ELX_FETCH_ENGINE", "sm")
         self._kernels = kernels
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.peers: list[torch.Tensor] = []  # keep the peer mappings alive

@@ -9,11 +9,12 @@ tiny config of tests/test_multirank_gpu.py for two steps and saves this
 rank's losses, fp32 master shards and live counters to <out>/rank<r>.npz.
 
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
-        --master-port P tests/mp_worker.py <plan kind> <out dir> [exchange|ipc]
+        --master-port P tests/mp_worker.py <plan kind> <out dir> [exchange|ipc|ipc-ce]
 
 "ipc" runs the in-kernel P2P path instead: K2 reads the peers' shards and K3
 the peers' rCache blocks through CUDA-IPC mappings of the other processes'
-allocations, ordered by elx_device_barrier over IPC-mapped signal pads.
+allocations, ordered by elx_device_barrier over IPC-mapped signal pads;
+"ipc-ce" does the same with K2 on the copy engines (elx_fetch_ce).
 """
 
 import json
@@ -44,9 +45,12 @@ def main():
     dist.init_process_group("gloo")
     plan, _, _ = _plan(kind)
     init = gpt2.init_params(CFG, dev, seed=11)
-    transport = IpcTransport() if path == "ipc" else TorchDistTransport()
+    if path.startswith("ipc"):  # "ipc": K2 kernel, "ipc-ce": K2 on the copy engines
+        transport = IpcTransport(fetch_engine="ce" if path == "ipc-ce" else "sm")
+    else:
+        transport = TorchDistTransport()
     model = ElixirGPT2(CFG, plan, device=dev, transport=transport, init=init, **HP)
-    assert model.manager.p2p == (path == "ipc")
+    assert model.manager.p2p == path.startswith("ipc")
     losses = []
     for s in range(2):
         tok, tgt = _batches(world, s, dev)[rank]

@@ -91,6 +91,21 @@ def test_fetch_gathers_shards_in_rank_order(cuda, world, shard):
     assert np.array_equal(_bits(block), want)
 
 
+@pytest.mark.parametrize("world", [1, 2, 8])
+def test_fetch_copy_engine_equals_kernel(cuda, world):
+    """K2 on the copy engines (elx_fetch_ce) gathers the same bytes as the kernel."""
+    g = torch.Generator().manual_seed(world)
+    shard = 1_000_008
+    shards = [torch.randint(-32768, 32767, (shard,), generator=g, dtype=torch.int16).view(torch.bfloat16).to(cuda)
+              for _ in range(world)]
+    block = torch.zeros(world * shard, dtype=torch.bfloat16, device=cuda)
+    kernels.fetch(block, [s.data_ptr() for s in shards], shard, engine="ce")
+    torch.cuda.synchronize()
+    assert np.array_equal(_bits(block), arith.gather([_bits(s) for s in shards]))
+    with pytest.raises(errors.ValidationError):
+        kernels.fetch(block, [s.data_ptr() + 2 for s in shards], 8, engine="ce")
+
+
 def test_fetch_rejects_unaligned(cuda):
     block = torch.zeros(64, dtype=torch.bfloat16, device=cuda)
     s = torch.zeros(16, dtype=torch.bfloat16, device=cuda)

@@ -52,7 +52,7 @@ def _torchrun(world: int, args: list[str], timeout: int = 600) -> subprocess.Com
     return p
 
 
-@pytest.mark.parametrize("path", ["exchange", "ipc"])
+@pytest.mark.parametrize("path", ["exchange", "ipc", "ipc-ce"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kind", ["rcache-min", "offload"])
 def test_multiprocess_gloo_equals_loopback(cuda, tmp_path, world, kind, path):
