@@ -281,6 +281,33 @@ int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, i
 int elx_copy_h2d(void* dst_dev, const void* src_host, int64_t bytes, void* stream, void* event);
 int elx_copy_d2h(void* dst_host, const void* src_dev, int64_t bytes, void* stream, void* event);
 
+/* ------------------------------------- K8 lm_head softmax cross-entropy
+ * The caller's tied lm_head (the training step that drives the chunk path,
+ * profiles.py:466 — the shared wte used as the output projection), on the
+ * padded bf16 logits [rows, ld] straight out of the GEMM; columns >= vocab
+ * (the pad rows of the padded wte view) are excluded. No fp32 copy of the
+ * logits is made.
+ *   fwd: lse[r] = log(sum_{c<vocab} exp(x[r,c])), loss[r] = lse[r] - x[r,t_r]
+ *        (0 when t_r == ignore_index, NaN when t_r is out of range);
+ *   bwd: in place, x[r,c] <- (exp(x[r,c] - lse[r]) - [c == t_r]) * (*scale)
+ *        for c < vocab and 0 for the pad columns; `scale` is a DEVICE float
+ *        (upstream gradient / counted rows). dtype must be BF16. */
+int elx_xent_fwd(const void* logits, int32_t dtype, int64_t rows, int64_t ld, int64_t vocab, const int64_t* targets,
+                 int64_t ignore_index, float* lse, float* loss, void* stream);
+int elx_xent_bwd(void* logits, int32_t dtype, int64_t rows, int64_t ld, int64_t vocab, const int64_t* targets,
+                 int64_t ignore_index, const float* lse, const float* scale, void* stream);
+
+/* ------------------------------- K9 LayerNorm parameter gradients
+ * The wrapped LayerNorms of the caller write their weight/bias gradients
+ * straight over the parameter slots of the chunk:
+ *   dgamma[j] = sum_r dy[r,j] * (x[r,j] - mean[r]) * rstd[r]
+ *   dbeta[j]  = sum_r dy[r,j]
+ * x, dy: [rows, cols] (BF16/F16, 8-byte aligned, cols % 4 == 0); mean, rstd:
+ * float32 [rows] as torch's native_layer_norm returns them; outputs in dtype.
+ * fp32 accumulation in a fixed order (same cluster shape as K7): deterministic. */
+int elx_ln_param_grad(void* dgamma, void* dbeta, const void* x, const void* dy, const float* mean, const float* rstd,
+                      int32_t dtype, int64_t rows, int64_t cols, void* stream);
+
 /* Host Adam for CPU-home optimizer shards (update rate v_c,
  * rcache_sim.py:176-184): same arithmetic as elx_adam, OpenMP over
  * `threads` host threads. All pointers are host pointers; step_scalars is a

@@ -1,0 +1,326 @@
+// sm_100a kernels of the GPT-2 training step that drives the chunk path (the
+// path's caller): the tied lm_head's softmax cross-entropy
+// (K8). Built WITHOUT --fmad=false (elx_kernels.cu keeps that flag for the
+// bit-exact optimizer arithmetic); parity here is against torch within
+// float32 tolerance, and runtime vs reference step is bit-identical because
+// both call these kernels.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "elx_internal.h"
+
+namespace {
+
+namespace cg = cooperative_groups;
+
+constexpr int kXentThreads = 256;
+
+int check(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  elx::count_launch();
+  return ELX_OK;
+}
+
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+__device__ __forceinline__ float to_f(__half x) { return __half2float(x); }
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+template <>
+__device__ __forceinline__ __half from_f<__half>(float x) {
+  return __float2half_rn(x);
+}
+
+template <typename T16>
+__device__ __forceinline__ void unpack8(const uint4& q, float (&f)[8]) {
+  const T16* h = reinterpret_cast<const T16*>(&q);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) f[e] = to_f(h[e]);
+}
+
+// (max, sum of exp(x - max)) pairs combined exactly as an online softmax.
+__device__ __forceinline__ void lse_merge(float& m, float& s, float m2, float s2) {
+  if (m2 == -INFINITY) return;
+  if (m == -INFINITY) {
+    m = m2;
+    s = s2;
+    return;
+  }
+  if (m2 > m) {
+    s = s * __expf(m - m2) + s2;
+    m = m2;
+  } else {
+    s = s + s2 * __expf(m2 - m);
+  }
+}
+
+// One CTA per row of the padded logits [rows, ld] (bf16; columns >= vocab are
+// the lm_head's pad rows and are excluded): lse[row] = log(sum exp(x)) and
+// loss[row] = lse - x[target] (0 for ignore_index; NaN for an out-of-range
+// target, which then trips the overflow skip instead of a device assert).
+template <typename T16>
+__global__ void __launch_bounds__(kXentThreads) xent_fwd_kernel(const T16* __restrict__ logits, int64_t ld,
+                                                                int64_t vocab, const int64_t* __restrict__ tgt,
+                                                                int64_t ignore, float* __restrict__ lse,
+                                                                float* __restrict__ loss) {
+  const int64_t row = blockIdx.x;
+  const T16* x = logits + row * ld;
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  const int64_t nfull = vocab >> 3;  // vectors entirely inside the vocabulary
+  float m = -INFINITY, s = 0.f;
+  for (int64_t v = threadIdx.x; v < nfull; v += kXentThreads) {
+    float f[8];
+    unpack8<T16>(__ldcs(xv + v), f);
+    float vm = f[0];
+#pragma unroll
+    for (int e = 1; e < 8; ++e) vm = fmaxf(vm, f[e]);
+    float vs = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) vs += __expf(f[e] - vm);
+    lse_merge(m, s, vm, vs);
+  }
+  for (int64_t c = (nfull << 3) + threadIdx.x; c < vocab; c += kXentThreads) {
+    const float f = to_f(x[c]);
+    lse_merge(m, s, f, 1.f);
+  }
+  // warp, then block reduction of the (m, s) pairs
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float m2 = __shfl_xor_sync(0xffffffffu, m, o);
+    const float s2 = __shfl_xor_sync(0xffffffffu, s, o);
+    lse_merge(m, s, m2, s2);
+  }
+  __shared__ float sm[kXentThreads / 32], ss[kXentThreads / 32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sm[warp] = m;
+    ss[warp] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = sm[0], S = ss[0];
+    for (int w = 1; w < kXentThreads / 32; ++w) lse_merge(M, S, sm[w], ss[w]);
+    const float l = M + logf(S);
+    lse[row] = l;
+    const int64_t t = tgt[row];
+    if (t == ignore)
+      loss[row] = 0.f;
+    else if (t < 0 || t >= vocab)
+      loss[row] = NAN;
+    else
+      loss[row] = l - to_f(x[t]);
+  }
+}
+
+// In place over the logits: g = (exp(x - lse) - [col == target]) * scale for
+// col < vocab, 0 for the pad columns; rows with ignore_index get 0. `scale`
+// is a DEVICE float (upstream gradient / number of counted rows), so the
+// loss scale never crosses to the host.
+template <typename T16>
+__global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(T16* __restrict__ logits, int64_t ld,
+                                                                int64_t vocab, const int64_t* __restrict__ tgt,
+                                                                int64_t ignore, const float* __restrict__ lse,
+                                                                const float* __restrict__ scale) {
+  const int64_t row = blockIdx.x;
+  const int64_t t = tgt[row];
+  const float L = lse[row];
+  const float sc = t == ignore ? 0.f : (t < 0 || t >= vocab ? NAN : *scale);
+  uint4* xv = reinterpret_cast<uint4*>(logits + row * ld);
+  const int64_t nvec = ld >> 3;
+  for (int64_t v = threadIdx.x; v < nvec; v += kXentThreads) {
+    float f[8];
+    unpack8<T16>(xv[v], f);
+    union {
+      T16 h[8];
+      uint4 u;
+    } o;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int64_t col = (v << 3) + e;
+      const float p = col < vocab ? __expf(f[e] - L) - (col == t ? 1.f : 0.f) : 0.f;
+      o.h[e] = from_f<T16>(col < vocab ? p * sc : 0.f);
+    }
+    __stcs(xv + v, o.u);
+  }
+}
+
+// ---------------------------------------------------------- K9 LN param grads
+// LayerNorm weight/bias gradients of one wrapped LayerNorm, written straight
+// over the weight/bias slots of the chunk (like K7 for the
+// linear biases): dgamma[j] = sum_r dy[r,j] * (x[r,j] - mean[r]) * rstd[r],
+// dbeta[j] = sum_r dy[r,j]. Same deterministic cluster shape as K7: a cluster
+// of kLnCluster CTAs per 128-column strip, contiguous row ranges per warp,
+// warps combined in order through shared memory, CTAs in cluster-rank order
+// through distributed shared memory. Replaces torch's GammaBetaBackward
+// (73 us per LayerNorm at 8192 x 2048, profiles/r01h_launches.md) and the K1
+// write-back of the LayerNorm gradients.
+constexpr int kLnWarps = 16;
+constexpr int kLnThreads = kLnWarps * 32;
+constexpr int kLnStrip = 128;
+constexpr int kLnCluster = 8;
+constexpr int kLnU = 8;
+
+__device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
+  return r;
+}
+
+template <typename T16>
+__global__ void __cluster_dims__(1, kLnCluster, 1) __launch_bounds__(kLnThreads, 1)
+    ln_param_grad_kernel(const T16* __restrict__ x, const T16* __restrict__ dy, const float* __restrict__ mean,
+                         const float* __restrict__ rstd, int64_t rows, int64_t cols, T16* __restrict__ dgamma,
+                         T16* __restrict__ dbeta) {
+  __shared__ float pg[kLnWarps][kLnStrip], pb[kLnWarps][kLnStrip];
+  __shared__ float cg_sum[kLnStrip], cb_sum[kLnStrip];
+  cg::cluster_group cluster = cg::this_cluster();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = (int)cluster.block_rank();
+  const int64_t col0 = (int64_t)blockIdx.x * kLnStrip;
+  const int64_t cc = col0 + lane * 4;
+  const int64_t per_cta = (rows + kLnCluster - 1) / kLnCluster;
+  const int64_t per_warp = (per_cta + kLnWarps - 1) / kLnWarps;
+  const int64_t cta_end = min(rows, (int64_t)(c + 1) * per_cta);
+  const int64_t r0 = (int64_t)c * per_cta + (int64_t)warp * per_warp;
+  const int64_t r1 = min(cta_end, r0 + per_warp);
+  float ag[4] = {0.f, 0.f, 0.f, 0.f}, ab[4] = {0.f, 0.f, 0.f, 0.f};
+  if (cc < cols && r0 < r1) {
+    const char* px = reinterpret_cast<const char*>(x + r0 * cols + cc);
+    const char* pd = reinterpret_cast<const char*>(dy + r0 * cols + cc);
+    const int64_t sb = cols * (int64_t)sizeof(T16);
+    int64_t r = r0;
+    for (; r < r1; r += kLnU) {
+      const int nu = (int)min((int64_t)kLnU, r1 - r);
+      uint2 qx[kLnU], qd[kLnU];
+      float mu[kLnU], rs[kLnU];
+#pragma unroll
+      for (int u = 0; u < kLnU; ++u) {
+        if (u < nu) {
+          qx[u] = ld_nc_u2(px + u * sb);
+          qd[u] = ld_nc_u2(pd + u * sb);
+          mu[u] = mean[r + u];
+          rs[u] = rstd[r + u];
+        }
+      }
+      px += kLnU * sb;
+      pd += kLnU * sb;
+#pragma unroll
+      for (int u = 0; u < kLnU; ++u) {
+        if (u < nu) {
+          const T16* hx = reinterpret_cast<const T16*>(&qx[u]);
+          const T16* hd = reinterpret_cast<const T16*>(&qd[u]);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float g = to_f(hd[e]);
+            ag[e] += g * ((to_f(hx[e]) - mu[u]) * rs[u]);
+            ab[e] += g;
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    pg[warp][lane * 4 + e] = ag[e];
+    pb[warp][lane * 4 + e] = ab[e];
+  }
+  __syncthreads();
+  if (threadIdx.x < kLnStrip) {
+    float a = 0.f, b = 0.f;
+#pragma unroll
+    for (int w = 0; w < kLnWarps; ++w) {
+      a += pg[w][threadIdx.x];
+      b += pb[w][threadIdx.x];
+    }
+    cg_sum[threadIdx.x] = a;
+    cb_sum[threadIdx.x] = b;
+  }
+  cluster.sync();
+  if (c == 0 && threadIdx.x < kLnStrip && col0 + threadIdx.x < cols) {
+    float a = 0.f, b = 0.f;
+#pragma unroll
+    for (int k = 0; k < kLnCluster; ++k) {
+      a += *cluster.map_shared_rank(&cg_sum[threadIdx.x], k);
+      b += *cluster.map_shared_rank(&cb_sum[threadIdx.x], k);
+    }
+    dgamma[col0 + threadIdx.x] = from_f<T16>(a);
+    dbeta[col0 + threadIdx.x] = from_f<T16>(b);
+  }
+  cluster.sync();  // peers' shared memory stays alive until CTA 0 has read it
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+}  // namespace
+
+extern "C" {
+
+int elx_xent_fwd(const void* logits, int32_t dtype, int64_t rows, int64_t ld, int64_t vocab, const int64_t* targets,
+                 int64_t ignore_index, float* lse, float* loss, void* stream) {
+  elx::clear_error();
+  if (!logits || !targets || !lse || !loss) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "xent logits must be bf16/f16");
+  if (rows < 0 || vocab < 1 || ld < vocab || (ld % 8) != 0)
+    return elx::fail(ELX_ERR_VALIDATION, "need rows >= 0, 1 <= vocab <= ld, ld a multiple of 8");
+  if (!aligned16(logits)) return elx::fail(ELX_ERR_VALIDATION, "logits not 16-byte aligned");
+  if (rows == 0) return ELX_OK;
+  if (rows > 0x7fffffff) return elx::fail(ELX_ERR_VALIDATION, "too many rows");
+  if (dtype == ELX_BF16)
+    xent_fwd_kernel<<<(unsigned)rows, kXentThreads, 0, (cudaStream_t)stream>>>(
+        static_cast<const __nv_bfloat16*>(logits), ld, vocab, targets, ignore_index, lse, loss);
+  else
+    xent_fwd_kernel<<<(unsigned)rows, kXentThreads, 0, (cudaStream_t)stream>>>(
+        static_cast<const __half*>(logits), ld, vocab, targets, ignore_index, lse, loss);
+  return check("elx_xent_fwd");
+}
+
+int elx_xent_bwd(void* logits, int32_t dtype, int64_t rows, int64_t ld, int64_t vocab, const int64_t* targets,
+                 int64_t ignore_index, const float* lse, const float* scale, void* stream) {
+  elx::clear_error();
+  if (!logits || !targets || !lse || !scale) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "xent logits must be bf16/f16");
+  if (rows < 0 || vocab < 1 || ld < vocab || (ld % 8) != 0)
+    return elx::fail(ELX_ERR_VALIDATION, "need rows >= 0, 1 <= vocab <= ld, ld a multiple of 8");
+  if (!aligned16(logits)) return elx::fail(ELX_ERR_VALIDATION, "logits not 16-byte aligned");
+  if (rows == 0) return ELX_OK;
+  if (rows > 0x7fffffff) return elx::fail(ELX_ERR_VALIDATION, "too many rows");
+  if (dtype == ELX_BF16)
+    xent_bwd_kernel<<<(unsigned)rows, kXentThreads, 0, (cudaStream_t)stream>>>(
+        static_cast<__nv_bfloat16*>(logits), ld, vocab, targets, ignore_index, lse, scale);
+  else
+    xent_bwd_kernel<<<(unsigned)rows, kXentThreads, 0, (cudaStream_t)stream>>>(
+        static_cast<__half*>(logits), ld, vocab, targets, ignore_index, lse, scale);
+  return check("elx_xent_bwd");
+}
+
+int elx_ln_param_grad(void* dgamma, void* dbeta, const void* x, const void* dy, const float* mean, const float* rstd,
+                      int32_t dtype, int64_t rows, int64_t cols, void* stream) {
+  elx::clear_error();
+  if (!dgamma || !dbeta || !x || !dy || !mean || !rstd) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "ln grads must be bf16/f16");
+  if (rows < 1 || cols < 1 || (cols % 4) != 0) return elx::fail(ELX_ERR_VALIDATION, "need rows >= 1, cols % 4 == 0");
+  if ((reinterpret_cast<uintptr_t>(x) & 7u) || (reinterpret_cast<uintptr_t>(dy) & 7u))
+    return elx::fail(ELX_ERR_VALIDATION, "x/dy not 8-byte aligned");
+  const dim3 grid((unsigned)((cols + kLnStrip - 1) / kLnStrip), kLnCluster);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == ELX_BF16)
+    ln_param_grad_kernel<__nv_bfloat16><<<grid, kLnThreads, 0, st>>>(
+        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), mean, rstd, rows, cols,
+        static_cast<__nv_bfloat16*>(dgamma), static_cast<__nv_bfloat16*>(dbeta));
+  else
+    ln_param_grad_kernel<__half><<<grid, kLnThreads, 0, st>>>(
+        static_cast<const __half*>(x), static_cast<const __half*>(dy), mean, rstd, rows, cols,
+        static_cast<__half*>(dgamma), static_cast<__half*>(dbeta));
+  return check("elx_ln_param_grad");
+}
+
+}  // extern "C"

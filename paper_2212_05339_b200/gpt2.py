@@ -138,6 +138,29 @@ class _OverwriteLinear(torch.autograd.Function):
         return gx, None, None, None, None
 
 
+class _OverwriteLayerNorm(torch.autograd.Function):
+    """LayerNorm over the last dimension (eps 1e-5) whose backward computes
+    dX with torch's LayerNorm backward (input gradient only) and writes dW/db
+    straight into `targets` (the chunk slots) with the deterministic K9
+    reduction: no GammaBeta kernel, no gradient tensors, no K1 write-back."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, w_target, b_target):
+        y, mean, rstd = torch.native_layer_norm(x, (x.shape[-1],), w, b, 1e-5)
+        ctx.save_for_backward(x, w, b, mean, rstd)
+        ctx.targets = (w_target, b_target)
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        x, w, b, mean, rstd = ctx.saved_tensors
+        H = x.shape[-1]
+        gy = gy.contiguous()
+        gx = torch.ops.aten.native_layer_norm_backward(gy, x, (H,), mean, rstd, w, b, [True, False, False])[0]
+        kernels.ln_param_grad(x.reshape(-1, H), gy.reshape(-1, H), mean.reshape(-1), rstd.reshape(-1), *ctx.targets)
+        return gx, None, None, None, None
+
+
 def _alias(t: torch.Tensor) -> torch.Tensor:
     """Same storage, own version counter. Gradient targets are aliases of the
     chunk slots: every parameter of a chunk is a view of ONE storage, so an
@@ -165,11 +188,16 @@ def _block(x, p, heads, targets=None):
             return F.linear(inp, p[wi], p[bi])
         return _OverwriteLinear.apply(inp, p[wi], p[bi], targets[wi], targets[bi])
 
-    h = F.layer_norm(x, (H,), ln1w, ln1b, 1e-5)
+    def ln(inp, wi, bi):
+        if targets is None:
+            return F.layer_norm(inp, (H,), p[wi], p[bi], 1e-5)
+        return _OverwriteLayerNorm.apply(inp, p[wi], p[bi], targets[wi], targets[bi])
+
+    h = ln(x, 0, 1)
     q, k, v = (lin(h, wi, bi).view(B, T, heads, hd).transpose(1, 2) for wi, bi in _LINEARS[:3])
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
     x = x + lin(a.transpose(1, 2).reshape(B, T, H), *_LINEARS[3])
-    h = F.layer_norm(x, (H,), ln2w, ln2b, 1e-5)
+    h = ln(x, 10, 11)
     return x + lin(F.gelu(lin(h, *_LINEARS[4]), approximate="tanh"), *_LINEARS[5])
 
 
@@ -239,8 +267,10 @@ class ElixirGPT2:
             return F.embedding(tokens, wte) + wpe[:T]
         if i == self.K - 1:  # tied lm_head + loss (wte viewed with padded vocab rows)
             (wte,) = params
-            logits = F.linear(x, wte)[..., :cfg.vocab]
-            return F.cross_entropy(logits.float().reshape(-1, cfg.vocab), targets.reshape(-1))
+            logits = F.linear(x, wte)  # [B, T, vocab_padded] bf16, straight from the GEMM
+            # K8: cross-entropy on the padded bf16 logits (pad columns excluded), gradient written
+            # in place: no sliced fp32 copy of the 0.8 GB logits and no separate softmax kernels
+            return kernels.lm_head_cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1), cfg.vocab)
         if i == self.K - 2:  # ln_f
             w, b = params
             return F.layer_norm(x, (cfg.hidden,), w, b, 1e-5)

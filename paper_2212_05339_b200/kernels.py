@@ -287,3 +287,68 @@ def colsum_geometry(rows: int, cols: int) -> tuple[int, int]:
     a, b = ctypes.c_int32(), ctypes.c_int32()
     _lib.check(lib.elx_colsum_geometry(int(rows), int(cols), ctypes.byref(a), ctypes.byref(b)), "elx_colsum_geometry")
     return a.value, b.value
+
+
+def ln_param_grad(x2d: torch.Tensor, dy2d: torch.Tensor, mean: torch.Tensor, rstd: torch.Tensor,
+                  dgamma: torch.Tensor, dbeta: torch.Tensor, stream=None) -> None:
+    """K9: LayerNorm weight/bias gradients written into dgamma/dbeta (the
+    chunk slots): dgamma = sum_r dy * (x - mean) * rstd, dbeta = sum_r dy
+    (fp32, deterministic order)."""
+    lib = _lib.load()
+    for t, w in ((x2d, "x"), (dy2d, "dy"), (mean, "mean"), (rstd, "rstd")):
+        _cuda(t, w)
+    rows, cols = x2d.shape
+    if dy2d.shape != x2d.shape or dy2d.dtype != x2d.dtype or mean.numel() != rows or rstd.numel() != rows:
+        raise ValidationError("ln_param_grad: x/dy shapes or dtypes differ, or mean/rstd are not one per row")
+    if mean.dtype != torch.float32 or rstd.dtype != torch.float32:
+        raise ValidationError("ln_param_grad: mean/rstd must be float32")
+    if dgamma.numel() != cols or dbeta.numel() != cols or dgamma.dtype != x2d.dtype or dbeta.dtype != x2d.dtype:
+        raise ValidationError("ln_param_grad: dgamma/dbeta must hold `cols` elements of x's dtype")
+    rc = lib.elx_ln_param_grad(dgamma.data_ptr(), dbeta.data_ptr(), x2d.data_ptr(), dy2d.data_ptr(), mean.data_ptr(),
+                               rstd.data_ptr(), elx_dtype(x2d.dtype), rows, cols, _stream(stream))
+    _lib.check(rc, "elx_ln_param_grad")
+
+
+class LMHeadCrossEntropy(torch.autograd.Function):
+    """K8: mean softmax cross-entropy over the padded bf16/f16 lm_head logits
+    [rows, ld] (columns >= vocab excluded), with no fp32 copy of the logits.
+    Forward: per-row log-sum-exp and loss (elx_xent_fwd), mean over counted
+    rows. Backward: the logits buffer is overwritten in place by its gradient
+    (elx_xent_bwd) — the GEMM that produced it does not need it back — scaled
+    on the device by upstream / count. Matches F.cross_entropy(logits[:, :vocab]
+    .float(), targets) within float32 tolerance (tests/test_kernels_gpu.py)."""
+
+    @staticmethod
+    def forward(ctx, logits: torch.Tensor, targets: torch.Tensor, vocab: int, ignore_index: int = -100):
+        lib = _lib.load()
+        _cuda(logits, "logits")
+        if logits.dim() != 2 or logits.dtype not in (torch.bfloat16, torch.float16):
+            raise ValidationError("logits must be a contiguous 2-D bf16/f16 tensor")
+        rows, ld = logits.shape
+        tg = targets.reshape(-1)
+        if tg.numel() != rows or tg.dtype != torch.int64 or not tg.is_cuda:
+            raise ValidationError("targets must be int64 CUDA with one entry per logits row")
+        tg = tg.contiguous()
+        lse = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        loss = torch.empty(rows, dtype=torch.float32, device=logits.device)
+        rc = lib.elx_xent_fwd(logits.data_ptr(), elx_dtype(logits.dtype), rows, ld, int(vocab), tg.data_ptr(), int(ignore_index),
+                              lse.data_ptr(), loss.data_ptr(), _stream(None))
+        _lib.check(rc, "elx_xent_fwd")
+        count = (tg != ignore_index).sum().to(torch.float32)
+        ctx.save_for_backward(logits, tg, lse, count)
+        ctx.vocab, ctx.ignore = int(vocab), int(ignore_index)
+        return loss.sum() / count
+
+    @staticmethod
+    def backward(ctx, g):
+        logits, tg, lse, count = ctx.saved_tensors
+        rows, ld = logits.shape
+        scale = (g.to(torch.float32) / count).reshape(1).contiguous()
+        rc = _lib.load().elx_xent_bwd(logits.data_ptr(), elx_dtype(logits.dtype), rows, ld, ctx.vocab, tg.data_ptr(), ctx.ignore,
+                                      lse.data_ptr(), scale.data_ptr(), _stream(None))
+        _lib.check(rc, "elx_xent_bwd")
+        return logits, None, None, None
+
+
+def lm_head_cross_entropy(logits: torch.Tensor, targets: torch.Tensor, vocab: int, ignore_index: int = -100):
+    return LMHeadCrossEntropy.apply(logits, targets, vocab, ignore_index)

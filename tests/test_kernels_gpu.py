@@ -508,3 +508,76 @@ def test_symmetric_memory_transport_api(cuda):
     out = subprocess.run([sys.executable, "-c", _SYMM_SCRIPT, root, port], capture_output=True, text=True,
                          timeout=300, env=dict(os.environ))
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+# ------------------------------------------------------------------ K8 lm_head cross-entropy
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("rows,vocab,ld", [(1, 8, 8), (7, 389, 448), (64, 50257, 50304), (300, 1000, 1000)])
+def test_lm_head_cross_entropy_matches_torch(cuda, rows, vocab, ld, dtype):
+    """K8 vs torch F.cross_entropy on the fp32 copy of the unpadded bf16 logits:
+    loss within 2e-6 relative, gradient within bf16 rounding (the kernel writes
+    the bf16 gradient in place over the logits); pad columns get 0; an
+    ignore_index row contributes nothing."""
+    g = torch.Generator(device=cuda).manual_seed(rows + vocab)
+    logits = (torch.randn(rows, ld, device=cuda, generator=g) * 3).to(dtype)
+    tgt = torch.randint(0, vocab, (rows,), device=cuda, generator=g)
+    if rows > 2:
+        tgt[1] = -100
+    ref_in = logits[:, :vocab].float().clone().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(ref_in, tgt)
+    ref.backward(torch.tensor(3.0, device=cuda))
+    x = logits.clone().requires_grad_(True)
+    loss = kernels.lm_head_cross_entropy(x, tgt, vocab)
+    (gx,) = torch.autograd.grad(loss, [x], torch.tensor(3.0, device=cuda))
+    torch.cuda.synchronize()
+    assert abs(loss.item() - ref.item()) <= 2e-6 * abs(ref.item())
+    want = ref_in.grad
+    got = gx[:, :vocab].float()
+    # f16 flushes gradients below its subnormal step (6e-8) to zero; bf16 keeps fp32's range
+    atol = 1e-6 * float(want.abs().max()) + (6e-8 if dtype == torch.float16 else 0.0)
+    assert torch.allclose(got, want, rtol=1e-2, atol=atol)
+    assert torch.equal(gx[:, vocab:].float(), torch.zeros_like(gx[:, vocab:].float()))
+    if rows > 2:
+        assert torch.count_nonzero(gx[1]) == 0
+
+
+def test_lm_head_cross_entropy_deterministic(cuda):
+    g = torch.Generator(device=cuda).manual_seed(5)
+    logits = torch.randn(512, 50304, device=cuda, generator=g).to(torch.bfloat16)
+    tgt = torch.randint(0, 50257, (512,), device=cuda, generator=g)
+    outs = []
+    for _ in range(2):
+        x = logits.clone().requires_grad_(True)
+        loss = kernels.lm_head_cross_entropy(x, tgt, 50257)
+        (gx,) = torch.autograd.grad(loss, [x])
+        outs.append((loss.item(), gx.clone()))
+    assert outs[0][0] == outs[1][0] and torch.equal(outs[0][1], outs[1][1])
+
+
+# ------------------------------------------------------------------ K9 LayerNorm parameter gradients
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("rows,cols", [(1, 4), (7, 132), (8192, 2048), (1000, 3072)])
+def test_ln_param_grad_matches_float64(cuda, dtype, rows, cols):
+    """K9 vs a float64 reduction of the same inputs (dgamma = sum dy*(x-mean)*rstd,
+    dbeta = sum dy) within the output dtype's rounding; deterministic."""
+    g = torch.Generator(device=cuda).manual_seed(rows * 3 + cols)
+    x = (torch.randn(rows, cols, device=cuda, generator=g) * 2 + 0.5).to(dtype)
+    w = torch.randn(cols, device=cuda, generator=g).to(dtype)
+    b = torch.randn(cols, device=cuda, generator=g).to(dtype)
+    _, mean, rstd = torch.native_layer_norm(x, (cols,), w, b, 1e-5)
+    dy = torch.randn(rows, cols, device=cuda, generator=g).to(dtype)
+    dg = torch.empty(cols, dtype=dtype, device=cuda)
+    db = torch.empty(cols, dtype=dtype, device=cuda)
+    kernels.ln_param_grad(x, dy, mean.reshape(-1), rstd.reshape(-1), dg, db)
+    xhat = (x.double() - mean.double().reshape(-1, 1)) * rstd.double().reshape(-1, 1)
+    want_g = (dy.double() * xhat).sum(0)
+    want_b = dy.double().sum(0)
+    tol = 2 ** -7 if dtype == torch.bfloat16 else 2 ** -10
+    for got, want in ((dg, want_g), (db, want_b)):
+        err = (got.double() - want).abs()
+        assert bool((err <= tol * want.abs() + 1e-4 * (rows ** 0.5)).all()), float(err.max())
+    dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
+    kernels.ln_param_grad(x, dy, mean.reshape(-1), rstd.reshape(-1), dg2, db2)
+    assert torch.equal(dg, dg2) and torch.equal(db, db2)
