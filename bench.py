@@ -158,7 +158,8 @@ def cpu_baseline(model_name: str, layers_sample: int = 1, threads: int | None = 
     elements), giving seconds per sequence of the full model.
     """
     import numpy as np
-    from paper_2212_05339_b200.gpt2 import PRESETS, _block
+    from oracle.gpt2_ref import block as _block
+    from paper_2212_05339_b200.gpt2 import PRESETS
     import torch.nn.functional as F
 
     cfg = PRESETS[model_name]

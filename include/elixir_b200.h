@@ -308,6 +308,21 @@ int elx_xent_bwd(void* logits, int32_t dtype, int64_t rows, int64_t ld, int64_t 
 int elx_ln_param_grad(void* dgamma, void* dbeta, const void* x, const void* dy, const float* mean, const float* rstd,
                       int32_t dtype, int64_t rows, int64_t cols, void* stream);
 
+/* ------------------------- K10-K12 the GPT-2 layer's row/elementwise ops
+ * LayerNorm over the last dimension of [rows, cols] (BF16/F16, cols % 8 == 0,
+ * cols <= 4096, 16-byte aligned; one warp per row held in registers):
+ *   fwd:    y = (x - mean) * rstd * w + b, mean/rstd float32 [rows] out;
+ *   bwd_dx: dx = rstd * (g - mean(g) - xhat * mean(g * xhat)), g = dy * w
+ *           (the weight/bias gradients are elx_ln_param_grad's).
+ * tanh-GELU over n elements (n % 8 == 0): y = 0.5 x (1 + tanh(sqrt(2/pi)
+ * (x + 0.044715 x^3))) and dx = dy * y'(x). */
+int elx_layer_norm_fwd(void* y, float* mean, float* rstd, const void* x, const void* w, const void* b, int32_t dtype,
+                       int64_t rows, int64_t cols, float eps, void* stream);
+int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w, const float* mean, const float* rstd,
+                          int32_t dtype, int64_t rows, int64_t cols, void* stream);
+int elx_gelu_fwd(void* y, const void* x, int32_t dtype, int64_t n, void* stream);
+int elx_gelu_bwd(void* dx, const void* x, const void* dy, int32_t dtype, int64_t n, void* stream);
+
 /* Host Adam for CPU-home optimizer shards (update rate v_c,
  * rcache_sim.py:176-184): same arithmetic as elx_adam, OpenMP over
  * `threads` host threads. All pointers are host pointers; step_scalars is a

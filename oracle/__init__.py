@@ -23,4 +23,6 @@ Contents
                  (tests/golden/adamw_golden.npz).
   c/elx_oracle.c plain-C restatement of arith.py (OpenMP), used as the timed
                  CPU baseline at full size; cross-checked against arith.py.
+  gpt2_ref.py    the GPT-2 layer in stock torch ops (the CPU baseline's model
+                 math; the product's layer runs our CUDA kernels).
 """

@@ -98,6 +98,10 @@ _SIGNATURES = {
     "elx_xent_fwd": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "elx_xent_bwd": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "elx_ln_param_grad": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i64, c_vp]),
+    "elx_layer_norm_fwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i64, c_f32, c_vp]),
+    "elx_layer_norm_bwd_dx": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i64, c_vp]),
+    "elx_gelu_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i64, c_vp]),
+    "elx_gelu_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp]),
     "elx_copy_h2d": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_copy_d2h": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_cpu_adam": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i32]),

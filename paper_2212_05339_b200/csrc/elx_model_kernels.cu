@@ -9,6 +9,7 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -258,6 +259,223 @@ __global__ void __cluster_dims__(1, kLnCluster, 1) __launch_bounds__(kLnThreads,
   cluster.sync();  // peers' shared memory stays alive until CTA 0 has read it
 }
 
+// ------------------------------------------------- K10/K11 LayerNorm (rows)
+// One warp per row of [rows, cols] (cols % 8 == 0, cols <= 32*8*kV), the row
+// held in registers as 16-byte vectors: mean, then the variance about it
+// (two passes over registers, no Welford drift), rstd = rsqrt(var + eps).
+// Forward writes y and the fp32 mean/rstd the backward (K9 and K11) reads.
+constexpr int kRowWarps = 8;
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T16, int kV>
+__global__ void __launch_bounds__(kRowWarps * 32) ln_fwd_kernel(const T16* __restrict__ x, const T16* __restrict__ w,
+                                                                const T16* __restrict__ b, T16* __restrict__ y,
+                                                                float* __restrict__ mean, float* __restrict__ rstd,
+                                                                int64_t rows, int cols, float eps) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nvec = cols >> 3;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  uint4 q[kV];
+  float s = 0.f;
+#pragma unroll
+  for (int j = 0; j < kV; ++j) {
+    const int v = lane + 32 * j;
+    if (v < nvec) {
+      q[j] = __ldcs(xr + v);
+      float f[8];
+      unpack8<T16>(q[j], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += f[e];
+    }
+  }
+  const float mu = warp_sum(s) / (float)cols;
+  float s2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < kV; ++j) {
+    if (lane + 32 * j < nvec) {
+      float f[8];
+      unpack8<T16>(q[j], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float d = f[e] - mu;
+        s2 += d * d;
+      }
+    }
+  }
+  const float rs = rsqrtf(warp_sum(s2) / (float)cols + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  const uint4* bv = reinterpret_cast<const uint4*>(b);
+#pragma unroll
+  for (int j = 0; j < kV; ++j) {
+    const int v = lane + 32 * j;
+    if (v < nvec) {
+      float f[8], fw[8], fb[8];
+      unpack8<T16>(q[j], f);
+      unpack8<T16>(__ldg(wv + v), fw);
+      unpack8<T16>(__ldg(bv + v), fb);
+      union {
+        T16 h[8];
+        uint4 u;
+      } o;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) o.h[e] = from_f<T16>((f[e] - mu) * rs * fw[e] + fb[e]);
+      yr[v] = o.u;
+    }
+  }
+  if (lane == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+// dx = rstd * (g - mean(g) - xhat * mean(g * xhat)), g = dy * w, xhat = (x - mean) * rstd
+template <typename T16, int kV>
+__global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __restrict__ x, const T16* __restrict__ dy,
+                                                                   const T16* __restrict__ w,
+                                                                   const float* __restrict__ mean,
+                                                                   const float* __restrict__ rstd, T16* __restrict__ dx,
+                                                                   int64_t rows, int cols) {
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  const int nvec = cols >> 3;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  const uint4* dr = reinterpret_cast<const uint4*>(dy + row * cols);
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  const float mu = mean[row], rs = rstd[row];
+  uint4 qx[kV], qd[kV];
+  float c1 = 0.f, c2 = 0.f;
+#pragma unroll
+  for (int j = 0; j < kV; ++j) {
+    const int v = lane + 32 * j;
+    if (v < nvec) {
+      qx[j] = __ldcs(xr + v);
+      qd[j] = __ldcs(dr + v);
+      float fx[8], fd[8], fw[8];
+      unpack8<T16>(qx[j], fx);
+      unpack8<T16>(qd[j], fd);
+      unpack8<T16>(__ldg(wv + v), fw);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float g = fd[e] * fw[e];
+        c1 += g * ((fx[e] - mu) * rs);
+        c2 += g;
+      }
+    }
+  }
+  c1 = warp_sum(c1) / (float)cols;
+  c2 = warp_sum(c2) / (float)cols;
+  uint4* o = reinterpret_cast<uint4*>(dx + row * cols);
+#pragma unroll
+  for (int j = 0; j < kV; ++j) {
+    const int v = lane + 32 * j;
+    if (v < nvec) {
+      float fx[8], fd[8], fw[8];
+      unpack8<T16>(qx[j], fx);
+      unpack8<T16>(qd[j], fd);
+      unpack8<T16>(__ldg(wv + v), fw);
+      union {
+        T16 h[8];
+        uint4 u;
+      } r;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (fx[e] - mu) * rs;
+        r.h[e] = from_f<T16>(rs * (fd[e] * fw[e] - c2 - xh * c1));
+      }
+      o[v] = r.u;
+    }
+  }
+}
+
+// ---------------------------------------------------------- K12 tanh-GELU
+// y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))) and its derivative,
+// 16-byte vectors, grid-stride; tanh via the SFU (tanh.approx.f32, ~2^-11
+// relative), below the bf16 output rounding.
+__device__ __forceinline__ float tanh_fast(float v) {
+  float r;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+constexpr float kGeluBeta = 0.7978845608028654f;   // sqrt(2/pi)
+constexpr float kGeluKappa = 0.044715f;
+
+template <typename T16>
+__global__ void __launch_bounds__(256) gelu_fwd_kernel(const T16* __restrict__ x, T16* __restrict__ y, int64_t nvec) {
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  uint4* yv = reinterpret_cast<uint4*>(y);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    float f[8];
+    unpack8<T16>(__ldcs(xv + i), f);
+    union {
+      T16 h[8];
+      uint4 u;
+    } o;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = f[e];
+      const float t = tanh_fast(kGeluBeta * (v + kGeluKappa * v * v * v));
+      o.h[e] = from_f<T16>(0.5f * v * (1.f + t));
+    }
+    yv[i] = o.u;
+  }
+}
+
+template <typename T16>
+__global__ void __launch_bounds__(256) gelu_bwd_kernel(const T16* __restrict__ x, const T16* __restrict__ dy,
+                                                       T16* __restrict__ dx, int64_t nvec) {
+  const uint4* xv = reinterpret_cast<const uint4*>(x);
+  const uint4* dv = reinterpret_cast<const uint4*>(dy);
+  uint4* ov = reinterpret_cast<uint4*>(dx);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < nvec; i += (int64_t)gridDim.x * blockDim.x) {
+    float f[8], g[8];
+    unpack8<T16>(__ldcs(xv + i), f);
+    unpack8<T16>(__ldcs(dv + i), g);
+    union {
+      T16 h[8];
+      uint4 u;
+    } o;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float v = f[e];
+      const float v2 = v * v;
+      const float t = tanh_fast(kGeluBeta * (v + kGeluKappa * v2 * v));
+      const float d = 0.5f * (1.f + t) + 0.5f * v * (1.f - t * t) * kGeluBeta * (1.f + 3.f * kGeluKappa * v2);
+      o.h[e] = from_f<T16>(g[e] * d);
+    }
+    ov[i] = o.u;
+  }
+}
+
+int sm_count_model() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <typename F2, typename F4, typename F8, typename F12, typename F16>
+int pick_row_kernel(int cols, F2 f2, F4 f4, F8 f8, F12 f12, F16 f16) {
+  const int per_lane = (cols / 8 + 31) / 32;
+  if (per_lane <= 2) return f2(), 0;
+  if (per_lane <= 4) return f4(), 0;
+  if (per_lane <= 8) return f8(), 0;
+  if (per_lane <= 12) return f12(), 0;
+  return f16(), 0;
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 }  // namespace
@@ -321,6 +539,117 @@ int elx_ln_param_grad(void* dgamma, void* dbeta, const void* x, const void* dy, 
         static_cast<const __half*>(x), static_cast<const __half*>(dy), mean, rstd, rows, cols,
         static_cast<__half*>(dgamma), static_cast<__half*>(dbeta));
   return check("elx_ln_param_grad");
+}
+
+#define ELX_ROWS_GRID(rows) (unsigned)(((rows) + kRowWarps - 1) / kRowWarps)
+
+int elx_layer_norm_fwd(void* y, float* mean, float* rstd, const void* x, const void* w, const void* b, int32_t dtype,
+                       int64_t rows, int64_t cols, float eps, void* stream) {
+  elx::clear_error();
+  if (!y || !mean || !rstd || !x || !w || !b) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "layer norm must be bf16/f16");
+  if (rows < 0 || cols < 8 || (cols % 8) != 0 || cols > 4096)
+    return elx::fail(ELX_ERR_VALIDATION, "layer norm needs 8 <= cols <= 4096, cols %% 8 == 0");
+  if (!aligned16(x) || !aligned16(y) || !aligned16(w) || !aligned16(b))
+    return elx::fail(ELX_ERR_VALIDATION, "layer norm tensors must be 16-byte aligned");
+  if (rows == 0) return ELX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int c = (int)cols;
+  if (dtype == ELX_BF16) {
+    using T = __nv_bfloat16;
+    auto k = [&](auto kern) {
+      kern<<<ELX_ROWS_GRID(rows), kRowWarps * 32, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(w),
+                                                           static_cast<const T*>(b), static_cast<T*>(y), mean, rstd,
+                                                           rows, c, eps);
+    };
+    pick_row_kernel(c, [&] { k(ln_fwd_kernel<T, 2>); }, [&] { k(ln_fwd_kernel<T, 4>); },
+                    [&] { k(ln_fwd_kernel<T, 8>); }, [&] { k(ln_fwd_kernel<T, 12>); },
+                    [&] { k(ln_fwd_kernel<T, 16>); });
+  } else {
+    using T = __half;
+    auto k = [&](auto kern) {
+      kern<<<ELX_ROWS_GRID(rows), kRowWarps * 32, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(w),
+                                                           static_cast<const T*>(b), static_cast<T*>(y), mean, rstd,
+                                                           rows, c, eps);
+    };
+    pick_row_kernel(c, [&] { k(ln_fwd_kernel<T, 2>); }, [&] { k(ln_fwd_kernel<T, 4>); },
+                    [&] { k(ln_fwd_kernel<T, 8>); }, [&] { k(ln_fwd_kernel<T, 12>); },
+                    [&] { k(ln_fwd_kernel<T, 16>); });
+  }
+  return check("elx_layer_norm_fwd");
+}
+
+int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w, const float* mean, const float* rstd,
+                          int32_t dtype, int64_t rows, int64_t cols, void* stream) {
+  elx::clear_error();
+  if (!dx || !x || !dy || !w || !mean || !rstd) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "layer norm must be bf16/f16");
+  if (rows < 0 || cols < 8 || (cols % 8) != 0 || cols > 4096)
+    return elx::fail(ELX_ERR_VALIDATION, "layer norm needs 8 <= cols <= 4096, cols %% 8 == 0");
+  if (!aligned16(x) || !aligned16(dy) || !aligned16(dx) || !aligned16(w))
+    return elx::fail(ELX_ERR_VALIDATION, "layer norm tensors must be 16-byte aligned");
+  if (rows == 0) return ELX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int c = (int)cols;
+  if (dtype == ELX_BF16) {
+    using T = __nv_bfloat16;
+    auto k = [&](auto kern) {
+      kern<<<ELX_ROWS_GRID(rows), kRowWarps * 32, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(dy),
+                                                           static_cast<const T*>(w), mean, rstd, static_cast<T*>(dx),
+                                                           rows, c);
+    };
+    pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2>); }, [&] { k(ln_bwd_dx_kernel<T, 4>); },
+                    [&] { k(ln_bwd_dx_kernel<T, 8>); }, [&] { k(ln_bwd_dx_kernel<T, 12>); },
+                    [&] { k(ln_bwd_dx_kernel<T, 16>); });
+  } else {
+    using T = __half;
+    auto k = [&](auto kern) {
+      kern<<<ELX_ROWS_GRID(rows), kRowWarps * 32, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(dy),
+                                                           static_cast<const T*>(w), mean, rstd, static_cast<T*>(dx),
+                                                           rows, c);
+    };
+    pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2>); }, [&] { k(ln_bwd_dx_kernel<T, 4>); },
+                    [&] { k(ln_bwd_dx_kernel<T, 8>); }, [&] { k(ln_bwd_dx_kernel<T, 12>); },
+                    [&] { k(ln_bwd_dx_kernel<T, 16>); });
+  }
+  return check("elx_layer_norm_bwd_dx");
+}
+
+int elx_gelu_fwd(void* y, const void* x, int32_t dtype, int64_t n, void* stream) {
+  elx::clear_error();
+  if (!y || !x) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "gelu must be bf16/f16");
+  if (n < 0 || (n % 8) != 0) return elx::fail(ELX_ERR_VALIDATION, "gelu needs n %% 8 == 0");
+  if (!aligned16(x) || !aligned16(y)) return elx::fail(ELX_ERR_VALIDATION, "gelu tensors must be 16-byte aligned");
+  if (n == 0) return ELX_OK;
+  const int64_t nvec = n / 8;
+  const int grid = (int)std::min<int64_t>((nvec + 255) / 256, (int64_t)sm_count_model() * 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == ELX_BF16)
+    gelu_fwd_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), static_cast<__nv_bfloat16*>(y), nvec);
+  else
+    gelu_fwd_kernel<<<grid, 256, 0, st>>>(static_cast<const __half*>(x), static_cast<__half*>(y), nvec);
+  return check("elx_gelu_fwd");
+}
+
+int elx_gelu_bwd(void* dx, const void* x, const void* dy, int32_t dtype, int64_t n, void* stream) {
+  elx::clear_error();
+  if (!dx || !x || !dy) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "gelu must be bf16/f16");
+  if (n < 0 || (n % 8) != 0) return elx::fail(ELX_ERR_VALIDATION, "gelu needs n %% 8 == 0");
+  if (!aligned16(x) || !aligned16(dy) || !aligned16(dx))
+    return elx::fail(ELX_ERR_VALIDATION, "gelu tensors must be 16-byte aligned");
+  if (n == 0) return ELX_OK;
+  const int64_t nvec = n / 8;
+  const int grid = (int)std::min<int64_t>((nvec + 255) / 256, (int64_t)sm_count_model() * 8);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == ELX_BF16)
+    gelu_bwd_kernel<<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy),
+                                          static_cast<__nv_bfloat16*>(dx), nvec);
+  else
+    gelu_bwd_kernel<<<grid, 256, 0, st>>>(static_cast<const __half*>(x), static_cast<const __half*>(dy),
+                                          static_cast<__half*>(dx), nvec);
+  return check("elx_gelu_bwd");
 }
 
 }  // extern "C"

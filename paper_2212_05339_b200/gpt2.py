@@ -138,27 +138,61 @@ class _OverwriteLinear(torch.autograd.Function):
         return gx, None, None, None, None
 
 
-class _OverwriteLayerNorm(torch.autograd.Function):
-    """LayerNorm over the last dimension (eps 1e-5) whose backward computes
-    dX with torch's LayerNorm backward (input gradient only) and writes dW/db
-    straight into `targets` (the chunk slots) with the deterministic K9
-    reduction: no GammaBeta kernel, no gradient tensors, no K1 write-back."""
+class _LayerNorm(torch.autograd.Function):
+    """LayerNorm over the last dimension (eps 1e-5) on our kernels: forward
+    K10 (y plus the fp32 mean/rstd), backward K11 for dX and K9 for dW/db.
+    With `targets` (chunk slots) the weight/bias gradients are written
+    straight over the parameter data and no gradient
+    tensor is returned for them: no GammaBeta kernel, no K1 write-back."""
 
     @staticmethod
     def forward(ctx, x, w, b, w_target, b_target):
-        y, mean, rstd = torch.native_layer_norm(x, (x.shape[-1],), w, b, 1e-5)
-        ctx.save_for_backward(x, w, b, mean, rstd)
+        x = x.contiguous()
+        y, mean, rstd = kernels.layer_norm_fwd(x, w, b)
+        ctx.save_for_backward(x, w, mean, rstd)
         ctx.targets = (w_target, b_target)
         return y
 
     @staticmethod
     def backward(ctx, gy):
-        x, w, b, mean, rstd = ctx.saved_tensors
+        x, w, mean, rstd = ctx.saved_tensors
         H = x.shape[-1]
         gy = gy.contiguous()
-        gx = torch.ops.aten.native_layer_norm_backward(gy, x, (H,), mean, rstd, w, b, [True, False, False])[0]
-        kernels.ln_param_grad(x.reshape(-1, H), gy.reshape(-1, H), mean.reshape(-1), rstd.reshape(-1), *ctx.targets)
-        return gx, None, None, None, None
+        gx = kernels.layer_norm_bwd_dx(x, gy, w, mean, rstd)
+        w_t, b_t = ctx.targets
+        own = w_t is None
+        if own:
+            w_t, b_t = torch.empty_like(w), torch.empty_like(w)
+        kernels.ln_param_grad(x.reshape(-1, H), gy.reshape(-1, H), mean.reshape(-1), rstd.reshape(-1), w_t, b_t)
+        return gx, (w_t if own else None), (b_t if own else None), None, None
+
+
+def layer_norm(x, w, b, w_target=None, b_target=None):
+    """GPT-2 LayerNorm on K10/K11/K9 (autograd only when a gradient is needed)."""
+    if torch.is_grad_enabled() and (x.requires_grad or w.requires_grad or b.requires_grad):
+        return _LayerNorm.apply(x, w, b, w_target, b_target)
+    return kernels.layer_norm_fwd(x.contiguous(), w, b)[0]
+
+
+class _Gelu(torch.autograd.Function):
+    """tanh-GELU on K12 (forward and backward kernels)."""
+
+    @staticmethod
+    def forward(ctx, x):
+        x = x.contiguous()
+        ctx.save_for_backward(x)
+        return kernels.gelu_fwd(x)
+
+    @staticmethod
+    def backward(ctx, gy):
+        (x,) = ctx.saved_tensors
+        return kernels.gelu_bwd(x, gy.contiguous())
+
+
+def gelu(x):
+    if torch.is_grad_enabled() and x.requires_grad:
+        return _Gelu.apply(x)
+    return kernels.gelu_fwd(x.contiguous())
 
 
 def _alias(t: torch.Tensor) -> torch.Tensor:
@@ -190,15 +224,15 @@ def _block(x, p, heads, targets=None):
 
     def ln(inp, wi, bi):
         if targets is None:
-            return F.layer_norm(inp, (H,), p[wi], p[bi], 1e-5)
-        return _OverwriteLayerNorm.apply(inp, p[wi], p[bi], targets[wi], targets[bi])
+            return layer_norm(inp, p[wi], p[bi])
+        return layer_norm(inp, p[wi], p[bi], targets[wi], targets[bi])
 
     h = ln(x, 0, 1)
     q, k, v = (lin(h, wi, bi).view(B, T, heads, hd).transpose(1, 2) for wi, bi in _LINEARS[:3])
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
     x = x + lin(a.transpose(1, 2).reshape(B, T, H), *_LINEARS[3])
     h = ln(x, 10, 11)
-    return x + lin(F.gelu(lin(h, *_LINEARS[4]), approximate="tanh"), *_LINEARS[5])
+    return x + lin(gelu(lin(h, *_LINEARS[4])), *_LINEARS[5])
 
 
 class ElixirGPT2:
@@ -273,7 +307,7 @@ class ElixirGPT2:
             return kernels.lm_head_cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1), cfg.vocab)
         if i == self.K - 2:  # ln_f
             w, b = params
-            return F.layer_norm(x, (cfg.hidden,), w, b, 1e-5)
+            return layer_norm(x, w, b)
         return _block(x, params, cfg.heads, grad_targets)
 
     def pieces(self, i: int, lookup) -> list:

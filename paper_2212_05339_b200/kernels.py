@@ -309,6 +309,62 @@ def ln_param_grad(x2d: torch.Tensor, dy2d: torch.Tensor, mean: torch.Tensor, rst
     _lib.check(rc, "elx_ln_param_grad")
 
 
+def layer_norm_fwd(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor, eps: float = 1e-5, stream=None):
+    """K10: LayerNorm over the last dimension; returns (y, mean, rstd) with
+    fp32 mean/rstd of shape x.shape[:-1] (what K9 and K11 read back)."""
+    lib = _lib.load()
+    for t, n in ((x, "x"), (w, "w"), (b, "b")):
+        _cuda(t, n)
+    H = x.shape[-1]
+    if w.numel() != H or b.numel() != H or w.dtype != x.dtype or b.dtype != x.dtype:
+        raise ValidationError("layer_norm_fwd: w/b must hold x.shape[-1] elements of x's dtype")
+    rows = x.numel() // H
+    y = torch.empty_like(x)
+    mean = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
+    rstd = torch.empty(x.shape[:-1], dtype=torch.float32, device=x.device)
+    rc = lib.elx_layer_norm_fwd(y.data_ptr(), mean.data_ptr(), rstd.data_ptr(), x.data_ptr(), w.data_ptr(),
+                                b.data_ptr(), elx_dtype(x.dtype), rows, H, float(eps), _stream(stream))
+    _lib.check(rc, "elx_layer_norm_fwd")
+    return y, mean, rstd
+
+
+def layer_norm_bwd_dx(x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, mean: torch.Tensor, rstd: torch.Tensor,
+                      stream=None) -> torch.Tensor:
+    """K11: the LayerNorm input gradient (the weight/bias gradients are K9's)."""
+    lib = _lib.load()
+    for t, n in ((x, "x"), (dy, "dy"), (w, "w"), (mean, "mean"), (rstd, "rstd")):
+        _cuda(t, n)
+    H = x.shape[-1]
+    if dy.shape != x.shape or dy.dtype != x.dtype or mean.numel() * H != x.numel():
+        raise ValidationError("layer_norm_bwd_dx: dy must match x; mean/rstd one per row")
+    dx = torch.empty_like(x)
+    rc = lib.elx_layer_norm_bwd_dx(dx.data_ptr(), x.data_ptr(), dy.data_ptr(), w.data_ptr(), mean.data_ptr(),
+                                   rstd.data_ptr(), elx_dtype(x.dtype), x.numel() // H, H, _stream(stream))
+    _lib.check(rc, "elx_layer_norm_bwd_dx")
+    return dx
+
+
+def gelu_fwd(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """K12: tanh-approximated GELU (the GPT-2 MLP activation)."""
+    _cuda(x, "x")
+    y = torch.empty_like(x)
+    rc = _lib.load().elx_gelu_fwd(y.data_ptr(), x.data_ptr(), elx_dtype(x.dtype), x.numel(), _stream(stream))
+    _lib.check(rc, "elx_gelu_fwd")
+    return y
+
+
+def gelu_bwd(x: torch.Tensor, dy: torch.Tensor, stream=None) -> torch.Tensor:
+    _cuda(x, "x")
+    _cuda(dy, "dy")
+    if dy.shape != x.shape or dy.dtype != x.dtype:
+        raise ValidationError("gelu_bwd: dy must match x")
+    dx = torch.empty_like(x)
+    rc = _lib.load().elx_gelu_bwd(dx.data_ptr(), x.data_ptr(), dy.data_ptr(), elx_dtype(x.dtype), x.numel(),
+                                  _stream(stream))
+    _lib.check(rc, "elx_gelu_bwd")
+    return dx
+
+
 class LMHeadCrossEntropy(torch.autograd.Function):
     """K8: mean softmax cross-entropy over the padded bf16/f16 lm_head logits
     [rows, ld] (columns >= vocab excluded), with no fp32 copy of the logits.

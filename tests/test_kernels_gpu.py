@@ -581,3 +581,77 @@ def test_ln_param_grad_matches_float64(cuda, dtype, rows, cols):
     dg2, db2 = torch.empty_like(dg), torch.empty_like(db)
     kernels.ln_param_grad(x, dy, mean.reshape(-1), rstd.reshape(-1), dg2, db2)
     assert torch.equal(dg, dg2) and torch.equal(db, db2)
+
+
+# ------------------------------------------------------------------ K10-K12 LayerNorm / GELU
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+@pytest.mark.parametrize("rows,cols", [(1, 8), (5, 64), (300, 768), (8192, 2048), (64, 3072), (33, 4096)])
+def test_layer_norm_matches_torch(cuda, dtype, rows, cols):
+    """K10/K11 vs torch's LayerNorm (fp32 math on the same inputs): y and dx
+    within the output dtype's rounding, mean/rstd within 1e-5."""
+    g = torch.Generator(device=cuda).manual_seed(rows + cols)
+    x = (torch.randn(rows, cols, device=cuda, generator=g) * 1.5 + 0.3).to(dtype)
+    w = (torch.randn(cols, device=cuda, generator=g) * 0.5 + 1).to(dtype)
+    b = (torch.randn(cols, device=cuda, generator=g) * 0.1).to(dtype)
+    dy = torch.randn(rows, cols, device=cuda, generator=g).to(dtype)
+    y, mean, rstd = kernels.layer_norm_fwd(x, w, b)
+    xf = x.float().requires_grad_(True)
+    ref = torch.nn.functional.layer_norm(xf, (cols,), w.float(), b.float(), 1e-5)
+    (gref,) = torch.autograd.grad(ref, [xf], dy.float())
+    eps = 2 ** -7 if dtype == torch.bfloat16 else 2 ** -10
+    assert torch.allclose(y.float(), ref, rtol=eps, atol=eps)
+    m_ref = x.float().mean(-1)
+    r_ref = torch.rsqrt(x.float().var(-1, unbiased=False) + 1e-5)
+    assert torch.allclose(mean, m_ref, rtol=1e-5, atol=1e-5) and torch.allclose(rstd, r_ref, rtol=1e-5)
+    dx = kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd)
+    scale = float(gref.abs().max())
+    assert torch.allclose(dx.float(), gref, rtol=2 * eps, atol=2 * eps * scale)
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_gelu_matches_torch(cuda, dtype):
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = (torch.randn(8192 * 8 + 8, device=cuda, generator=g) * 3).to(dtype)
+    dy = torch.randn(x.shape, device=cuda, generator=g).to(dtype)
+    y = kernels.gelu_fwd(x)
+    xf = x.float().requires_grad_(True)
+    ref = torch.nn.functional.gelu(xf, approximate="tanh")
+    (gref,) = torch.autograd.grad(ref, [xf], dy.float())
+    eps = 2 ** -7 if dtype == torch.bfloat16 else 2 ** -9
+    assert torch.allclose(y.float(), ref, rtol=eps, atol=1e-3)
+    dx = kernels.gelu_bwd(x, dy)
+    assert torch.allclose(dx.float(), gref, rtol=2 * eps, atol=2e-3)
+
+
+def test_gpt2_layer_on_our_kernels_matches_stock_torch(cuda):
+    """The product's GPT-2 layer (K10/K11/K9 LayerNorm, K12 GELU, K7 bias sums,
+    overwrite-linear) vs the stock-torch layer of the CPU baseline
+    (oracle/gpt2_ref.py) on the same bf16 inputs: output and input gradient
+    agree to bf16 accuracy."""
+    from oracle.gpt2_ref import block as ref_block
+    from paper_2212_05339_b200 import gpt2
+    H, heads, B, T = 256, 4, 2, 64
+    g = torch.Generator(device=cuda).manual_seed(0)
+    pieces = [(pid, off, shape) for pid, off, shape in gpt2.layer_pieces(0, H)]
+    ps = []
+    for pid, _, shape in pieces:
+        if pid.endswith(".b"):
+            ps.append((torch.randn(shape, device=cuda, generator=g) * 0.02).to(torch.bfloat16))
+        elif "ln_" in pid:
+            ps.append((1 + torch.randn(shape, device=cuda, generator=g) * 0.1).to(torch.bfloat16))
+        else:
+            ps.append((torch.randn(shape, device=cuda, generator=g) * 0.05).to(torch.bfloat16))
+    x = torch.randn(B, T, H, device=cuda, generator=g).to(torch.bfloat16)
+    dy = torch.randn(B, T, H, device=cuda, generator=g).to(torch.bfloat16)
+    outs = []
+    for fn, tgt in ((ref_block, None), (gpt2._block, True)):
+        xi = x.clone().requires_grad_(True)
+        q = [p.clone().requires_grad_(True) for p in ps]
+        targets = [torch.empty_like(p) for p in ps] if tgt else None
+        out = fn(xi, q, heads) if targets is None else fn(xi, q, heads, targets)
+        (gx,) = torch.autograd.grad(out, [xi], dy, allow_unused=True)
+        outs.append((out.float(), gx.float()))
+    (o_ref, g_ref), (o, gxx) = outs
+    assert (o - o_ref).abs().max() <= 0.05 * o_ref.abs().max()
+    assert (gxx - g_ref).abs().max() <= 0.05 * g_ref.abs().max()
