@@ -158,16 +158,16 @@ __global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(T16* __restrict_
 // LayerNorm weight/bias gradients of one wrapped LayerNorm, written straight
 // over the weight/bias slots of the chunk (like K7 for the
 // linear biases): dgamma[j] = sum_r dy[r,j] * (x[r,j] - mean[r]) * rstd[r],
-// dbeta[j] = sum_r dy[r,j]. Same deterministic cluster shape as K7: a cluster
-// of kLnCluster CTAs per 128-column strip, contiguous row ranges per warp,
+// dbeta[j] = sum_r dy[r,j]. Same deterministic cluster shape as K7 (with a
+// 16-CTA cluster per 128-column strip), contiguous row ranges per warp,
 // warps combined in order through shared memory, CTAs in cluster-rank order
 // through distributed shared memory. Replaces torch's GammaBetaBackward
 // (73 us per LayerNorm at 8192 x 2048, profiles/r01h_launches.md) and the K1
 // write-back of the LayerNorm gradients.
-constexpr int kLnWarps = 16;
+constexpr int kLnWarps = 8;
 constexpr int kLnThreads = kLnWarps * 32;
 constexpr int kLnStrip = 128;
-constexpr int kLnCluster = 8;
+constexpr int kLnCluster = 16;  // non-portable cluster size: 256 CTAs at 2048 columns
 constexpr int kLnU = 8;
 
 __device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
@@ -177,7 +177,7 @@ __device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
 }
 
 template <typename T16>
-__global__ void __cluster_dims__(1, kLnCluster, 1) __launch_bounds__(kLnThreads, 1)
+__global__ void __cluster_dims__(1, kLnCluster, 1) __launch_bounds__(kLnThreads, 2)
     ln_param_grad_kernel(const T16* __restrict__ x, const T16* __restrict__ dy, const float* __restrict__ mean,
                          const float* __restrict__ rstd, int64_t rows, int64_t cols, T16* __restrict__ dgamma,
                          T16* __restrict__ dbeta) {
@@ -199,33 +199,40 @@ __global__ void __cluster_dims__(1, kLnCluster, 1) __launch_bounds__(kLnThreads,
     const char* pd = reinterpret_cast<const char*>(dy + r0 * cols + cc);
     const int64_t sb = cols * (int64_t)sizeof(T16);
     int64_t r = r0;
-    for (; r < r1; r += kLnU) {
-      const int nu = (int)min((int64_t)kLnU, r1 - r);
+    for (; r + kLnU <= r1; r += kLnU) {  // full groups: every load issued before the first use
       uint2 qx[kLnU], qd[kLnU];
       float mu[kLnU], rs[kLnU];
 #pragma unroll
       for (int u = 0; u < kLnU; ++u) {
-        if (u < nu) {
-          qx[u] = ld_nc_u2(px + u * sb);
-          qd[u] = ld_nc_u2(pd + u * sb);
-          mu[u] = mean[r + u];
-          rs[u] = rstd[r + u];
-        }
+        qx[u] = ld_nc_u2(px + u * sb);
+        qd[u] = ld_nc_u2(pd + u * sb);
+        mu[u] = mean[r + u];
+        rs[u] = rstd[r + u];
       }
       px += kLnU * sb;
       pd += kLnU * sb;
 #pragma unroll
       for (int u = 0; u < kLnU; ++u) {
-        if (u < nu) {
-          const T16* hx = reinterpret_cast<const T16*>(&qx[u]);
-          const T16* hd = reinterpret_cast<const T16*>(&qd[u]);
+        const T16* hx = reinterpret_cast<const T16*>(&qx[u]);
+        const T16* hd = reinterpret_cast<const T16*>(&qd[u]);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float g = to_f(hd[e]);
-            ag[e] += g * ((to_f(hx[e]) - mu[u]) * rs[u]);
-            ab[e] += g;
-          }
+        for (int e = 0; e < 4; ++e) {
+          const float g = to_f(hd[e]);
+          ag[e] += g * ((to_f(hx[e]) - mu[u]) * rs[u]);
+          ab[e] += g;
         }
+      }
+    }
+    for (; r < r1; ++r, px += sb, pd += sb) {
+      const uint2 qx = ld_nc_u2(px), qd = ld_nc_u2(pd);
+      const float mu = mean[r], rs = rstd[r];
+      const T16* hx = reinterpret_cast<const T16*>(&qx);
+      const T16* hd = reinterpret_cast<const T16*>(&qd);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float g = to_f(hd[e]);
+        ag[e] += g * ((to_f(hx[e]) - mu) * rs);
+        ab[e] += g;
       }
     }
   }
@@ -264,7 +271,7 @@ __global__ void __cluster_dims__(1, kLnCluster, 1) __launch_bounds__(kLnThreads,
 // held in registers as 16-byte vectors: mean, then the variance about it
 // (two passes over registers, no Welford drift), rstd = rsqrt(var + eps).
 // Forward writes y and the fp32 mean/rstd the backward (K9 and K11) reads.
-constexpr int kRowWarps = 8;
+constexpr int kRowWarps = 4;
 
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
@@ -530,6 +537,12 @@ int elx_ln_param_grad(void* dgamma, void* dbeta, const void* x, const void* dy, 
     return elx::fail(ELX_ERR_VALIDATION, "x/dy not 8-byte aligned");
   const dim3 grid((unsigned)((cols + kLnStrip - 1) / kLnStrip), kLnCluster);
   cudaStream_t st = (cudaStream_t)stream;
+  static bool configured = false;
+  if (!configured) {  // cluster of 16 > the portable 8
+    cudaFuncSetAttribute(ln_param_grad_kernel<__nv_bfloat16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(ln_param_grad_kernel<__half>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    configured = true;
+  }
   if (dtype == ELX_BF16)
     ln_param_grad_kernel<__nv_bfloat16><<<grid, kLnThreads, 0, st>>>(
         static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), mean, rstd, rows, cols,

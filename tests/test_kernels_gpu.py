@@ -444,7 +444,7 @@ def test_adam_device_step_equals_host_step(cuda):
     assert sc.tolist()[:3] == [0.0, 0.0, 6.0]
 
 
-@pytest.mark.parametrize("rows,cols", [(1, 8), (7, 24), (8192, 2048), (1000, 8200), (4096, 6144)])
+@pytest.mark.parametrize("rows,cols", [(1, 8), (7, 24), (8192, 2048), (1000, 8200), (4096, 6144), (300, 768)])
 def test_colsum_deterministic_and_exact(cuda, rows, cols):
     """K7 bias-gradient column sum: fp32 accumulation in the library's fixed
     order (rows within a sub-slice, sub-slices within a slice, slices) —
@@ -558,7 +558,7 @@ def test_lm_head_cross_entropy_deterministic(cuda):
 # ------------------------------------------------------------------ K9 LayerNorm parameter gradients
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("rows,cols", [(1, 4), (7, 132), (8192, 2048), (1000, 3072)])
+@pytest.mark.parametrize("rows,cols", [(1, 4), (7, 132), (8192, 2048), (1000, 3072), (4096, 4096)])
 def test_ln_param_grad_matches_float64(cuda, dtype, rows, cols):
     """K9 vs a float64 reduction of the same inputs (dgamma = sum dy*(x-mean)*rstd,
     dbeta = sum dy) within the output dtype's rounding; deterministic."""
