@@ -64,7 +64,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200", "-i", str(self.index)], stdout=subprocess.PIPE,
+                                          "-lms", "50", "-i", str(self.index)], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self._t = threading.Thread(target=self._read, daemon=True)
             self._t.start()
@@ -285,26 +285,52 @@ def run_ours(args):
         model.train_step(tok, tgt)
     _barrier(world)
 
-    # ---- device-resident timed region
     opt = model.optimizer
-    opt.time_adam = True
-    opt.adam_events.clear()
-    model.fetcher.time_release = True
-    model.fetcher.release_events.clear()
-    model.fetcher.copy_events.clear()
-    opt.cpu_wait_s = opt.cpu_update_s = 0.0
     cur = torch.cuda.current_stream(dev)
+
+    def timing(on: bool) -> None:
+        opt.time_adam = on
+        model.fetcher.time_release = on
+        if on:
+            opt.adam_events.clear()
+            model.fetcher.release_events.clear()
+            model.fetcher.copy_events.clear()
+            opt.cpu_wait_s = opt.cpu_update_s = 0.0
+
+    # CUDA graph: the whole step as one graph launch (world 1, every chunk GPU-home). The per-kernel
+    # event timings then come from `warmup` eager steps of the same launches, run just before capture.
+    use_graph = args.graph and world == 1 and not model.manager.cpu_ids
+    step_fn = model.train_step
+    probe_steps = args.steps
+    if use_graph:
+        timing(True)
+        l0 = _lib.launch_count()
+        for _ in range(args.warmup):
+            model.train_step(tok, tgt)
+        model.synchronize()
+        torch.cuda.synchronize(dev)
+        per_step_launches = (_lib.launch_count() - l0) / args.warmup
+        probe_steps = args.warmup
+        timing(False)
+        model.capture(tok, tgt, warmup=1)
+        step_fn = model.graph_step
+    else:
+        timing(True)
+
+    # ---- device-resident timed region
     l0 = _lib.launch_count()
     with ClockSampler(local) as clk:
         _barrier(world)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(cur)
         for _ in range(args.steps):
-            model.train_step(tok, tgt)
+            step_fn(tok, tgt)
         model.synchronize()  # the last step's overlapped update is inside the timed region
         e1.record(cur)
         torch.cuda.synchronize(dev)
     launches = _lib.launch_count() - l0
+    if use_graph:  # our kernels run inside the graph replays: the captured step's launches, per replay
+        launches = int(round(per_step_launches * args.steps))
     ms = e0.elapsed_time(e1)
     ms = _max_over_ranks(ms, world)
     adam_ms = [a.elapsed_time(b) for a, b in opt.adam_events]
@@ -313,10 +339,9 @@ def run_ours(args):
     for kind, a, b, nb in model.fetcher.copy_events:
         ms_, nb0 = copies.get(kind, (0.0, 0))
         copies[kind] = (ms_ + a.elapsed_time(b), nb0 + nb)
-    cpu_wait_ms = opt.cpu_wait_s * 1e3 / args.steps
-    cpu_update_ms = opt.cpu_update_s * 1e3 / args.steps
-    opt.time_adam = False
-    model.fetcher.time_release = False
+    cpu_wait_ms = opt.cpu_wait_s * 1e3 / probe_steps
+    cpu_update_ms = opt.cpu_update_s * 1e3 / probe_steps
+    timing(False)
     loss = float(model.last_loss)
 
     # ---- end to end through the public API with host buffers
@@ -328,7 +353,7 @@ def run_ours(args):
     f0.record(cur)
     for _ in range(args.steps):
         dev_ids.copy_(host_ids, non_blocking=True)
-        lo = model.train_step(dev_ids[:, :-1], dev_ids[:, 1:])
+        lo = step_fn(dev_ids[:, :-1], dev_ids[:, 1:])
         loss_host.copy_(lo.reshape(1), non_blocking=True)
         cur.synchronize()
     model.synchronize()
@@ -368,8 +393,8 @@ def run_ours(args):
     bpe = opt.bytes_per_element
     adam_avg = statistics.mean(adam_ms) if adam_ms else float("nan")
     adam_gbs = bpe * adam_elems / (adam_avg * 1e-3) / 1e9
-    rel_ms = sum(r for r, _ in rel) / max(1, args.steps)
-    rel_elems = sum(n for _, n in rel) / max(1, args.steps)
+    rel_ms = sum(r for r, _ in rel) / max(1, probe_steps)
+    rel_elems = sum(n for _, n in rel) / max(1, probe_steps)
     es = 2  # bf16
     rel_local_bytes = rel_elems * (es * world + (0 if world == 1 else 4))  # world 1: norm/overflow pass only
     traffic = None
@@ -388,7 +413,7 @@ def run_ours(args):
     offload = {"cpu_home_chunks": len(model.manager.cpu_ids), "gpu_home_chunks": len(model.manager.gpu_ids),
                "bytes_moved_per_step": {k: v for k, v in model.fetcher.bytes_moved.items()},
                "sim_counters": model.fetcher.counters(),
-               "offload_copies_per_step": {k: {"ms": v[0] / args.steps, "bytes": v[1] / args.steps,
+               "offload_copies_per_step": {k: {"ms": v[0] / probe_steps, "bytes": v[1] / probe_steps,
                                                "gbs": v[1] / (v[0] * 1e-3) / 1e9 if v[0] else None}
                                            for k, v in copies.items()},
                "cpu_update_ms_per_step": cpu_update_ms, "host_wait_on_cpu_update_ms_per_step": cpu_wait_ms,
@@ -414,6 +439,7 @@ def run_ours(args):
             "parallelism": f"elixir-chunk-dp{world}", "transport": args.transport if world > 1 else "local", "chunk_length": model.layout.chunk_length,
             "n_chunks": model.layout.n_chunks, "n_block": model.manager.plan.n_block,
             "l2": "working set (>20 GB of chunk/optimizer state per step) far exceeds the 126 MB L2; no flush needed",
+            "cuda_graph": use_graph,
             **({"oversubscribed": oversub} if oversub else {}),
         },
         "tflops_per_gpu": flops / (ms / args.steps * 1e-3) / 1e12,
@@ -423,7 +449,9 @@ def run_ours(args):
                            "launches_timed": len(adam_ms),
                            "overlapped_with_next_forward": args.overlap,
                            "note": "per step: all K4 launches (one per chunk group) on the optimizer stream, "
-                                   "timed first-to-last with CUDA events on that stream"},
+                                   "timed first-to-last with CUDA events on that stream"
+                                   + (" (in the eager steps of the same launches run just before the graph "
+                                      "capture)" if use_graph else "")},
             "release": {"ms_per_step": rel_ms, "elements_per_step": rel_elems,
                         "local_hbm_gbs": rel_local_bytes / (rel_ms * 1e-3) / 1e9 if rel_ms else None,
                         "bus_gbs": (None if world == 1 else
@@ -522,6 +550,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-update", choices=["split", "host", "stream"], default="split",
                     help="CPU-home chunk update: host threads, GPU-streamed, or split by measured rate")
+    ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
+                    help="world 1 with every chunk GPU-home: capture the whole step as one CUDA graph")
     ap.add_argument("--overlap", action="store_true",
                     help="issue the GPU update per chunk on an optimizer stream under the next forward")
     ap.add_argument("--transport", choices=["nccl", "p2p", "ipc"], default=os.environ.get("ELX_TRANSPORT", "nccl"),

@@ -414,6 +414,58 @@ class ElixirGPT2:
         a timed region / before reading parameters)."""
         self.optimizer.synchronize()
 
+    # -------------------------------------------------------------- CUDA graph
+    def capture(self, tokens: torch.Tensor, targets: torch.Tensor, warmup: int = 3) -> None:
+        """Capture one whole training step — forward, backward with the
+        gradient write-backs, the K3 releases on the comm stream, the K4
+        update and the device step counter — as ONE CUDA graph, so a step is a
+        single graph launch instead of ~1400 host-issued kernels (the small
+        GPT-2 step is launch-bound in eager mode). `warmup` eager steps run
+        first (they train, like any step) on a side stream. The captured step
+        depends on nothing outside the graph: every side stream rejoins the
+        capture stream, and consecutive replays on one stream are ordered.
+        Needs every chunk GPU-home (no host-thread update), a static loss
+        scale and world 1; the inputs of each later step are copied into the
+        captured input buffers by graph_step()."""
+        mgr = self.manager
+        if mgr.cpu_ids or self.scaler.dynamic or self.optimizer.overlap or mgr.world != 1:
+            raise ValidationError("graph capture needs world 1, every chunk GPU-home, a static loss scale "
+                                  "and the single-launch optimizer")
+        self._g_tok = tokens.detach().clone()
+        self._g_tgt = targets.detach().clone()
+        if self.optimizer.tables is not None:
+            self.optimizer.tables.ensure(1 << 20)  # the captured table pointers must stay valid
+        cur = torch.cuda.current_stream(self.device)
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(cur)
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self.train_step(self._g_tok, self._g_tgt)
+            self.synchronize()
+        cur.wait_stream(side)
+        torch.cuda.synchronize(self.device)
+        # nothing recorded before the capture may be waited on inside it
+        self.optimizer.done_event = None
+        self.optimizer.pending = {}
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            loss = self.train_step(self._g_tok, self._g_tgt)
+            self.synchronize()
+        self.optimizer.done_event = None  # events recorded during capture are graph-internal
+        self._graph, self._g_loss = graph, loss
+
+    def graph_step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        """One training step by replaying the captured graph on new inputs
+        (same shapes); returns the loss (a device scalar, overwritten by the
+        next replay)."""
+        if getattr(self, "_graph", None) is None:
+            raise ValidationError("call capture() first")
+        self._g_tok.copy_(tokens, non_blocking=True)
+        self._g_tgt.copy_(targets, non_blocking=True)
+        self._graph.replay()
+        self.last_loss = self._g_loss
+        return self._g_loss
+
     # -------------------------------------------------------------- misc
     @property
     def n_params(self) -> int:

@@ -178,3 +178,37 @@ def test_offloaded_update_modes_bit_exact(cuda, cpu_update):
         got = _masters(model)
         for pid, want in ref.master.items():
             assert np.array_equal(got[pid], want), (s, pid)
+
+
+@pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min"])
+def test_cuda_graph_step_equals_eager(cuda, plan_name):
+    """The whole step captured as ONE CUDA graph (capture() + graph_step())
+    trains exactly like the eager step: same losses, bit-identical fp32
+    masters and compute copies after warm-up + replayed steps on new batches."""
+    plan = dict(_plans(CFG))[plan_name]
+    init = gpt2.init_params(CFG, cuda, seed=5)
+    batches = [_batch(CFG, cuda, 100 + s) for s in range(6)]
+    eager = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
+    graph = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
+    want = [eager.train_step(*batches[0]).item() for _ in range(3)]
+    want += [eager.train_step(*b).item() for b in batches[1:]]
+    graph.capture(*batches[0], warmup=3)  # the warm-up steps train on batches[0]
+    got = [graph.graph_step(*b).item() for b in batches[1:]]
+    assert got == want[3:]
+    a, b = _masters(eager), _masters(graph)
+    assert set(a) == set(b)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    # the compute copy (bf16 chunk) follows the masters too
+    for c in eager.manager.gpu_ids:
+        r = eager.manager.row[c]
+        assert torch.equal(eager.manager.p16[r], graph.manager.p16[r])
+    assert eager.optimizer.step_count == graph.optimizer.step_count == 8
+
+
+def test_cuda_graph_refuses_offloaded_plans(cuda):
+    from paper_2212_05339_b200.errors import ValidationError
+    plan = dict(_plans(CFG))["offload-half"]
+    model = ElixirGPT2(CFG, plan, device=cuda, **HP)
+    with pytest.raises(ValidationError):
+        model.capture(*_batch(CFG, cuda, 1))
