@@ -168,7 +168,7 @@ constexpr int kLnWarps = 8;
 constexpr int kLnThreads = kLnWarps * 32;
 constexpr int kLnStrip = 128;
 constexpr int kLnCluster = 16;  // non-portable cluster size: 256 CTAs at 2048 columns
-constexpr int kLnU = 8;
+constexpr int kLnU = 16;
 
 __device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
   uint2 r;
@@ -289,17 +289,15 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_fwd_kernel(const T16* __res
   if (row >= rows) return;
   const int nvec = cols >> 3;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
-  uint4 q[kV];
+  float f[kV][8];  // the row, unpacked once
   float s = 0.f;
 #pragma unroll
   for (int j = 0; j < kV; ++j) {
     const int v = lane + 32 * j;
     if (v < nvec) {
-      q[j] = __ldcs(xr + v);
-      float f[8];
-      unpack8<T16>(q[j], f);
+      unpack8<T16>(__ldcs(xr + v), f[j]);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) s += f[e];
+      for (int e = 0; e < 8; ++e) s += f[j][e];
     }
   }
   const float mu = warp_sum(s) / (float)cols;
@@ -307,11 +305,9 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_fwd_kernel(const T16* __res
 #pragma unroll
   for (int j = 0; j < kV; ++j) {
     if (lane + 32 * j < nvec) {
-      float f[8];
-      unpack8<T16>(q[j], f);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float d = f[e] - mu;
+        const float d = f[j][e] - mu;
         s2 += d * d;
       }
     }
@@ -324,8 +320,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_fwd_kernel(const T16* __res
   for (int j = 0; j < kV; ++j) {
     const int v = lane + 32 * j;
     if (v < nvec) {
-      float f[8], fw[8], fb[8];
-      unpack8<T16>(q[j], f);
+      float fw[8], fb[8];
       unpack8<T16>(__ldg(wv + v), fw);
       unpack8<T16>(__ldg(bv + v), fb);
       union {
@@ -333,7 +328,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_fwd_kernel(const T16* __res
         uint4 u;
       } o;
 #pragma unroll
-      for (int e = 0; e < 8; ++e) o.h[e] = from_f<T16>((f[e] - mu) * rs * fw[e] + fb[e]);
+      for (int e = 0; e < 8; ++e) o.h[e] = from_f<T16>((f[j][e] - mu) * rs * fw[e] + fb[e]);
       yr[v] = o.u;
     }
   }
