@@ -323,6 +323,33 @@ int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w
 int elx_gelu_fwd(void* y, const void* x, int32_t dtype, int64_t n, void* stream);
 int elx_gelu_bwd(void* dx, const void* x, const void* dy, int32_t dtype, int64_t n, void* stream);
 
+/* ------------------------------ cuBLASLt GEMMs with fused epilogues
+ * Library GEMMs for the caller's wrapped operators, used for their epilogues:
+ * the bias gradient lands straight in the chunk's bias slot
+ * and the MLP's GELU is folded into the GEMM producing / consuming it.
+ * cuBLAS column-major convention: D[m,n] = op(A) op(B), op = transpose when
+ * trans != 0, lda/ldb/ldd leading dimensions; dtype BF16/F16, fp32 accumulate.
+ *   ELX_EPI_NONE           plain GEMM
+ *   ELX_EPI_BIAS           D += bias[m] (broadcast over columns)
+ *   ELX_EPI_GELU_BIAS      D = gelu(D + bias)                 (tanh-GELU)
+ *   ELX_EPI_GELU_AUX_BIAS  D = gelu(D + bias), aux = D + bias (aux: m x n, ldaux)
+ *   ELX_EPI_DGELU_BGRAD    D = D * gelu'(aux), bias = sum over columns of D
+ *   ELX_EPI_BGRADB         bias[n] = sum over k of op(B)      (weight gradient + bias gradient)
+ * Reducing epilogues are planned without split-K (deterministic bias
+ * gradients). `workspace` is caller-owned device memory. Fails with
+ * ELX_ERR_CUDA if cuBLASLt has no algorithm for the combination. */
+enum {
+  ELX_EPI_NONE = 0,
+  ELX_EPI_BIAS = 1,
+  ELX_EPI_GELU_BIAS = 2,
+  ELX_EPI_GELU_AUX_BIAS = 3,
+  ELX_EPI_DGELU_BGRAD = 4,
+  ELX_EPI_BGRADB = 5
+};
+int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
+                  const void* a, int64_t lda, const void* b, int64_t ldb, void* d, int64_t ldd, void* bias,
+                  void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream);
+
 /* Host Adam for CPU-home optimizer shards (update rate v_c,
  * rcache_sim.py:176-184): same arithmetic as elx_adam, OpenMP over
  * `threads` host threads. All pointers are host pointers; step_scalars is a

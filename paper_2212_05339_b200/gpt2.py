@@ -174,25 +174,41 @@ def layer_norm(x, w, b, w_target=None, b_target=None):
     return kernels.layer_norm_fwd(x.contiguous(), w, b)[0]
 
 
-class _Gelu(torch.autograd.Function):
-    """tanh-GELU on K12 (forward and backward kernels)."""
+class _OverwriteFcGelu(torch.autograd.Function):
+    """a = gelu(x W^T + b), the MLP's first wrapped operator, as ONE cuBLASLt
+    GEMM with the bias + tanh-GELU epilogue (keeping the pre-activation for the
+    backward): the separate GELU pass over the [T, 4H] activation disappears.
+    Backward: K12's GELU derivative, dW by cuBLAS into the weight slot, db by
+    K7 into the bias slot, dX by cuBLAS. (cuBLASLt's fused
+    DGELU_BGRAD and BGRADB epilogues measured slower on B200 than this
+    sequence: 0.62 vs 0.26 ms and 62 vs 60 us, profiles/r01m_model_kernels.jsonl.)"""
 
     @staticmethod
-    def forward(ctx, x):
-        x = x.contiguous()
-        ctx.save_for_backward(x)
-        return kernels.gelu_fwd(x)
+    def forward(ctx, x, w, b, w_target, b_target):
+        x2 = x.reshape(-1, x.shape[-1])
+        y, pre = kernels.linear_gelu(x2, w, b, keep_aux=True)
+        ctx.save_for_backward(x2, w, pre)
+        ctx.targets = (w_target, b_target)
+        ctx.xshape = x.shape
+        return y.view(*x.shape[:-1], w.shape[0])
 
     @staticmethod
     def backward(ctx, gy):
-        (x,) = ctx.saved_tensors
-        return kernels.gelu_bwd(x, gy.contiguous())
+        x2, w, pre = ctx.saved_tensors
+        w_t, b_t = ctx.targets
+        d = kernels.gelu_bwd(pre, gy.reshape(-1, gy.shape[-1]).contiguous())
+        gx = torch.mm(d, w).view(ctx.xshape) if ctx.needs_input_grad[0] else None
+        torch.mm(d.t(), x2, out=w_t)
+        kernels.colsum(d, b_t)
+        return gx, None, None, None, None
 
 
-def gelu(x):
-    if torch.is_grad_enabled() and x.requires_grad:
-        return _Gelu.apply(x)
-    return kernels.gelu_fwd(x.contiguous())
+def fc_gelu(x, w, b, w_target=None, b_target=None):
+    """gelu(x W^T + b) as one GEMM with a fused epilogue (K12 derivative in the backward)."""
+    if w_target is not None:
+        return _OverwriteFcGelu.apply(x, w, b, w_target, b_target)
+    y, _ = kernels.linear_gelu(x.reshape(-1, x.shape[-1]), w, b, keep_aux=False)
+    return y.view(*x.shape[:-1], w.shape[0])
 
 
 def _alias(t: torch.Tensor) -> torch.Tensor:
@@ -232,7 +248,9 @@ def _block(x, p, heads, targets=None):
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
     x = x + lin(a.transpose(1, 2).reshape(B, T, H), *_LINEARS[3])
     h = ln(x, 10, 11)
-    return x + lin(gelu(lin(h, *_LINEARS[4])), *_LINEARS[5])
+    fi, bi = _LINEARS[4]
+    a = fc_gelu(h, p[fi], p[bi]) if targets is None else fc_gelu(h, p[fi], p[bi], targets[fi], targets[bi])
+    return x + lin(a, *_LINEARS[5])
 
 
 class ElixirGPT2:

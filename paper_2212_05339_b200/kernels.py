@@ -408,3 +408,68 @@ class LMHeadCrossEntropy(torch.autograd.Function):
 
 def lm_head_cross_entropy(logits: torch.Tensor, targets: torch.Tensor, vocab: int, ignore_index: int = -100):
     return LMHeadCrossEntropy.apply(logits, targets, vocab, ignore_index)
+
+
+# ------------------------------------------------------------------ cuBLASLt GEMMs with fused epilogues
+EPI_NONE, EPI_BIAS, EPI_GELU_BIAS, EPI_GELU_AUX_BIAS, EPI_DGELU_BGRAD, EPI_BGRADB = range(6)
+_LT_WS: dict = {}
+_LT_WS_BYTES = 32 * 2 ** 20
+
+
+def _lt_workspace(device: torch.device, stream) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(device)
+    key = (device.index, s.cuda_stream)
+    ws = _LT_WS.get(key)
+    if ws is None:
+        ws = torch.empty(_LT_WS_BYTES, dtype=torch.uint8, device=device)
+        _LT_WS[key] = ws
+    return ws.data_ptr()
+
+
+def _lt(epi, ta, tb, m, n, k, a, lda, b, ldb, d, ldd, bias=None, aux=None, ldaux=0, stream=None):
+    lib = _lib.load()
+    rc = lib.elx_lt_matmul(epi, elx_dtype(d.dtype), ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
+                           d.data_ptr(), ldd, None if bias is None else bias.data_ptr(),
+                           None if aux is None else aux.data_ptr(), ldaux, _lt_workspace(d.device, stream),
+                           _LT_WS_BYTES, _stream(stream))
+    _lib.check(rc, "elx_lt_matmul")
+
+
+def linear_gelu(x2d: torch.Tensor, w: torch.Tensor, b: torch.Tensor, keep_aux: bool, stream=None):
+    """gelu(x W^T + b) in one GEMM (tanh-GELU epilogue); with keep_aux also the
+    pre-activation x W^T + b the backward needs. x2d [T, I], w [O, I], b [O]."""
+    T, I = x2d.shape
+    O = w.shape[0]
+    for t, n in ((x2d, "x"), (w, "w"), (b, "b")):
+        _cuda(t, n)
+    y = torch.empty(T, O, dtype=x2d.dtype, device=x2d.device)
+    aux = torch.empty(T, O, dtype=x2d.dtype, device=x2d.device) if keep_aux else None
+    # column-major: y^T [O, T] = W [O, I] . x^T [I, T]
+    _lt(EPI_GELU_AUX_BIAS if keep_aux else EPI_GELU_BIAS, 1, 0, O, T, I, w, I, x2d, I, y, O, bias=b, aux=aux,
+        ldaux=O if keep_aux else 0, stream=stream)
+    return y, aux
+
+
+def linear_dgelu_bgrad(dy2d: torch.Tensor, w: torch.Tensor, pre: torch.Tensor, dbias: torch.Tensor, stream=None):
+    """For y = gelu(pre) W^T + c: d_pre = (dy W) * gelu'(pre) in one GEMM, and
+    the bias gradient of `pre` (= colsum of d_pre) written into `dbias`.
+    dy2d [T, O], w [O, I], pre [T, I], dbias [I]."""
+    T, O = dy2d.shape
+    I = w.shape[1]
+    for t, n in ((dy2d, "dy"), (w, "w"), (pre, "pre"), (dbias, "dbias")):
+        _cuda(t, n)
+    d = torch.empty(T, I, dtype=dy2d.dtype, device=dy2d.device)
+    # column-major: d^T [I, T] = W^T [I, O] . dy^T [O, T]
+    _lt(EPI_DGELU_BGRAD, 0, 0, I, T, O, w, I, dy2d, O, d, I, bias=dbias, aux=pre, ldaux=I, stream=stream)
+    return d
+
+
+def wgrad_bgrad(x2d: torch.Tensor, dy2d: torch.Tensor, dw: torch.Tensor, db: torch.Tensor | None, stream=None):
+    """dW = dy^T x written into `dw` [O, I] and (db given) db = colsum(dy) from
+    the same GEMM's epilogue. x2d [T, I], dy2d [T, O]."""
+    T, I = x2d.shape
+    O = dy2d.shape[1]
+    for t, n in ((x2d, "x"), (dy2d, "dy"), (dw, "dw")):
+        _cuda(t, n)
+    # column-major: dW^T [I, O] = x^T [I, T] . dy [T, O]
+    _lt(EPI_BGRADB if db is not None else EPI_NONE, 0, 1, I, O, T, x2d, I, dy2d, O, dw, I, bias=db, stream=stream)

@@ -80,3 +80,27 @@ scale = torch.ones(1, device=dev)
 report("K8 xent_bwd 8192x50304", timed(lambda: lib.elx_xent_bwd(logits.data_ptr(), _lib.BF16, R, V, 50257,
                                                                   tgt.data_ptr(), -100, lse.data_ptr(), scale.data_ptr(),
                                                                   torch.cuda.current_stream().cuda_stream)), 2 * R * V * 2)
+
+# cuBLASLt fused-epilogue GEMMs vs the unfused sequence they replace (GPT-2 1.3B MLP / attention shapes)
+H4 = 4 * H
+wfc = torch.randn(H4, H, device=dev, generator=g).to(bf)
+bfc = torch.zeros(H4, device=dev, dtype=bf)
+wmp = torch.randn(H, H4, device=dev, generator=g).to(bf)
+pre = torch.randn(R, H4, device=dev, generator=g).to(bf)
+dbf = torch.empty(H4, device=dev, dtype=bf)
+gemm_fc = 2 * R * H * H4 / 1e12
+
+
+def report_tf(name, ms, tflop):
+    print(json.dumps({"kernel": name, "ms": round(ms, 4), "tflops": round(tflop / (ms * 1e-3), 1)}), flush=True)
+
+
+report_tf("lt fc fwd GELU_AUX_BIAS", timed(lambda: kernels.linear_gelu(x, wfc, bfc, True)), gemm_fc)
+report_tf("lt fc fwd GELU_BIAS", timed(lambda: kernels.linear_gelu(x, wfc, bfc, False)), gemm_fc)
+report_tf("torch linear + K12 gelu", timed(lambda: kernels.gelu_fwd(torch.nn.functional.linear(x, wfc, bfc))), gemm_fc)
+report_tf("lt mproj dX DGELU_BGRAD", timed(lambda: kernels.linear_dgelu_bgrad(dy, wmp, pre, dbf)), gemm_fc)
+report_tf("torch mm + K12 gelu_bwd + K7", timed(lambda: kernels.colsum(kernels.gelu_bwd(pre, dy @ wmp), dbf)), gemm_fc)
+dw = torch.empty(H, H, device=dev, dtype=bf)
+report_tf("lt wgrad BGRADB 2048x2048", timed(lambda: kernels.wgrad_bgrad(x, dy, dw, db)), 2 * R * H * H / 1e12)
+report_tf("torch mm(out) + K7 2048x2048", timed(lambda: (torch.mm(dy.t(), x, out=dw), kernels.colsum(dy, db))),
+          2 * R * H * H / 1e12)

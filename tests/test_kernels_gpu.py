@@ -655,3 +655,58 @@ def test_gpt2_layer_on_our_kernels_matches_stock_torch(cuda):
     (o_ref, g_ref), (o, gxx) = outs
     assert (o - o_ref).abs().max() <= 0.05 * o_ref.abs().max()
     assert (gxx - g_ref).abs().max() <= 0.05 * g_ref.abs().max()
+
+
+# ------------------------------------------------------------------ cuBLASLt fused-epilogue GEMMs
+
+def _gelu_ref(x):
+    return torch.nn.functional.gelu(x, approximate="tanh")
+
+
+@pytest.mark.parametrize("T,I,O", [(256, 64, 256), (8192, 2048, 8192), (512, 768, 3072)])
+def test_lt_linear_gelu_and_dgelu_bgrad(cuda, T, I, O):
+    """GELU_AUX_BIAS forward and DGELU_BGRAD backward vs fp32 torch: outputs
+    within bf16 rounding, the bias gradient too; repeated calls bit-identical."""
+    g = torch.Generator(device=cuda).manual_seed(T + O)
+    x = (torch.randn(T, I, device=cuda, generator=g)).to(torch.bfloat16)
+    w = (torch.randn(O, I, device=cuda, generator=g) * I ** -0.5).to(torch.bfloat16)
+    b = (torch.randn(O, device=cuda, generator=g) * 0.1).to(torch.bfloat16)
+    y, pre = kernels.linear_gelu(x, w, b, keep_aux=True)
+    y2, none = kernels.linear_gelu(x, w, b, keep_aux=False)
+    pre_ref = x.float() @ w.float().t() + b.float()
+    assert none is None and torch.equal(y, y2)
+    assert torch.allclose(pre.float(), pre_ref, rtol=2 ** -7, atol=2e-2)
+    assert torch.allclose(y.float(), _gelu_ref(pre_ref), rtol=2 ** -7, atol=2e-2)
+    # backward of out = gelu(pre) Wp^T + c through DGELU_BGRAD
+    wp = (torch.randn(I, O, device=cuda, generator=g) * O ** -0.5).to(torch.bfloat16)
+    dy = torch.randn(T, I, device=cuda, generator=g).to(torch.bfloat16)
+    db = torch.empty(O, dtype=torch.bfloat16, device=cuda)
+    d = kernels.linear_dgelu_bgrad(dy, wp, pre, db)
+    pf = pre.float().requires_grad_(True)
+    (want,) = torch.autograd.grad(_gelu_ref(pf) @ wp.float().t(), [pf], dy.float())
+    scale = float(want.abs().max())
+    assert torch.allclose(d.float(), want, rtol=2 ** -6, atol=2 ** -6 * scale)
+    db_want = d.float().sum(0)
+    assert torch.allclose(db.float(), db_want, rtol=2 ** -6, atol=2 ** -6 * float(db_want.abs().max()))
+    db2 = torch.empty_like(db)
+    d2 = kernels.linear_dgelu_bgrad(dy, wp, pre, db2)
+    assert torch.equal(d, d2) and torch.equal(db, db2)
+
+
+@pytest.mark.parametrize("T,I,O", [(256, 64, 128), (8192, 2048, 2048), (8192, 8192, 2048), (8192, 2048, 8192)])
+def test_lt_wgrad_bgrad(cuda, T, I, O):
+    """Weight gradient with the bias gradient from the same GEMM's epilogue
+    (BGRADB) vs fp32 torch; deterministic."""
+    g = torch.Generator(device=cuda).manual_seed(T * 3 + I)
+    x = torch.randn(T, I, device=cuda, generator=g).to(torch.bfloat16)
+    dy = torch.randn(T, O, device=cuda, generator=g).to(torch.bfloat16)
+    dw = torch.empty(O, I, dtype=torch.bfloat16, device=cuda)
+    db = torch.empty(O, dtype=torch.bfloat16, device=cuda)
+    kernels.wgrad_bgrad(x, dy, dw, db)
+    want_w = dy.float().t() @ x.float()
+    want_b = dy.float().sum(0)
+    assert torch.allclose(dw.float(), want_w, rtol=2 ** -7, atol=2 ** -7 * float(want_w.abs().max()))
+    assert torch.allclose(db.float(), want_b, rtol=2 ** -7, atol=2 ** -7 * float(want_b.abs().max()))
+    dw2, db2 = torch.empty_like(dw), torch.empty_like(db)
+    kernels.wgrad_bgrad(x, dy, dw2, db2)
+    assert torch.equal(dw, dw2) and torch.equal(db, db2)
