@@ -329,6 +329,8 @@ int elx_gelu_bwd(void* dx, const void* x, const void* dy, int32_t dtype, int64_t
  * and the MLP's GELU is folded into the GEMM producing / consuming it.
  * cuBLAS column-major convention: D[m,n] = op(A) op(B), op = transpose when
  * trans != 0, lda/ldb/ldd leading dimensions; dtype BF16/F16, fp32 accumulate.
+ * c != NULL adds a C operand laid out like D (D = A B + C, then the epilogue):
+ * the residual add of an output projection folded into its GEMM.
  *   ELX_EPI_NONE           plain GEMM
  *   ELX_EPI_BIAS           D += bias[m] (broadcast over columns)
  *   ELX_EPI_GELU_BIAS      D = gelu(D + bias)                 (tanh-GELU)
@@ -347,8 +349,8 @@ enum {
   ELX_EPI_BGRADB = 5
 };
 int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
-                  const void* a, int64_t lda, const void* b, int64_t ldb, void* d, int64_t ldd, void* bias,
-                  void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream);
+                  const void* a, int64_t lda, const void* b, int64_t ldb, const void* c, void* d, int64_t ldd,
+                  void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Host Adam for CPU-home optimizer shards (update rate v_c,
  * rcache_sim.py:176-184): same arithmetic as elx_adam, OpenMP over

@@ -103,7 +103,7 @@ _SIGNATURES = {
     "elx_gelu_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i64, c_vp]),
     "elx_gelu_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp]),
     "elx_lt_matmul": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
-                                     c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
+                                     c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "elx_copy_h2d": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_copy_d2h": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_cpu_adam": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i32]),

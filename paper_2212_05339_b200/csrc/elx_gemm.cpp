@@ -7,6 +7,8 @@
 //   GELU_BIAS      fc forward without autograd (no aux)
 //   DGELU_BGRAD    mlp.proj input gradient: d = (dy W) * gelu'(aux), bias = colsum(d)
 //   BGRADB         weight gradient: dW = dy^T x, bias = colsum(dy)
+// and, with a C operand, D = A B + C + bias: the residual add folded into the
+// attention / MLP output projections.
 // Column-major (cuBLAS) argument convention; paper_2212_05339_b200/kernels.py
 // maps PyTorch's row-major tensors onto it. Plans (descriptors, layouts and the
 // heuristic's algorithm) are cached per shape; epilogues that reduce (BGRAD)
@@ -58,8 +60,8 @@ bool has_bias(int e) { return e != ELX_EPI_NONE; }
 extern "C" {
 
 int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
-                  const void* a, int64_t lda, const void* b, int64_t ldb, void* d, int64_t ldd, void* bias,
-                  void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream) {
+                  const void* a, int64_t lda, const void* b, int64_t ldb, const void* c, void* d, int64_t ldd,
+                  void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream) {
   elx::clear_error();
   if (epilogue < ELX_EPI_NONE || epilogue > ELX_EPI_BGRADB) return elx::fail(ELX_ERR_VALIDATION, "bad epilogue");
   if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "lt matmul dtype must be bf16/f16");
@@ -73,8 +75,8 @@ int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t trans
   std::lock_guard<std::mutex> lock(g_mu);
   cublasStatus_t st;
   if (!g_handle && (st = cublasLtCreate(&g_handle)) != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtCreate", st);
-  const LtKey key{epilogue, transa, transb, m, n, k, lda, ldb, ldd, has_aux(epilogue) ? ldaux : 0, dtype,
-                  workspace_bytes};
+  const LtKey key{epilogue, transa, transb, m, n, k, lda, ldb, ldd, has_aux(epilogue) ? ldaux : 0,
+                  dtype * 2 + (c ? 1 : 0), workspace_bytes};
   auto it = g_plans.find(key);
   if (it == g_plans.end()) {
     LtPlan p;
@@ -126,8 +128,8 @@ int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t trans
   if (has_bias(epilogue)) cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
   if (has_aux(epilogue))
     cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_POINTER, &aux, sizeof(aux));
-  const float alpha = 1.f, beta = 0.f;
-  st = cublasLtMatmul(g_handle, p.op, &alpha, a, p.a, b, p.b, &beta, d, p.d, d, p.d, &p.algo, workspace,
+  const float alpha = 1.f, beta = c ? 1.f : 0.f;  // c: D = A B + C (+ epilogue), C laid out like D
+  st = cublasLtMatmul(g_handle, p.op, &alpha, a, p.a, b, p.b, &beta, c ? c : d, p.d, d, p.d, &p.algo, workspace,
                       (size_t)workspace_bytes, (cudaStream_t)stream);
   if (st != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtMatmul", st);
   return ELX_OK;

@@ -138,6 +138,32 @@ class _OverwriteLinear(torch.autograd.Function):
         return gx, None, None, None, None
 
 
+class _OverwriteLinearResidual(torch.autograd.Function):
+    """y = res + x W^T + b as ONE cuBLASLt GEMM (C operand + bias epilogue):
+    an output projection (attn.proj, mlp.proj) with the residual add folded in.
+    Backward as _OverwriteLinear (dW, db into the chunk slots); the residual's
+    gradient is dy itself."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, res, w_target, b_target):
+        x2 = x.reshape(-1, x.shape[-1])
+        y = kernels.linear_residual(x2, w, b, res.reshape(-1, w.shape[0]))
+        ctx.save_for_backward(x2, w)
+        ctx.targets = (w_target, b_target)
+        ctx.xshape = x.shape
+        return y.view(res.shape)
+
+    @staticmethod
+    def backward(ctx, gy):
+        x2, w = ctx.saved_tensors
+        w_t, b_t = ctx.targets
+        gy2 = gy.reshape(-1, gy.shape[-1])
+        gx = torch.mm(gy2, w).view(ctx.xshape) if ctx.needs_input_grad[0] else None
+        torch.mm(gy2.t(), x2, out=w_t)
+        kernels.colsum(gy2, b_t)
+        return gx, None, None, gy, None, None
+
+
 class _LayerNorm(torch.autograd.Function):
     """LayerNorm over the last dimension (eps 1e-5) on our kernels: forward
     K10 (y plus the fp32 mean/rstd), backward K11 for dX and K9 for dW/db.
@@ -243,14 +269,20 @@ def _block(x, p, heads, targets=None):
             return layer_norm(inp, p[wi], p[bi])
         return layer_norm(inp, p[wi], p[bi], targets[wi], targets[bi])
 
+    def lin_res(inp, res, wi, bi):  # res + inp W^T + b, the residual add folded into the GEMM
+        if targets is None:
+            return kernels.linear_residual(inp.reshape(-1, inp.shape[-1]), p[wi], p[bi],
+                                           res.reshape(-1, res.shape[-1])).view(res.shape)
+        return _OverwriteLinearResidual.apply(inp, p[wi], p[bi], res, targets[wi], targets[bi])
+
     h = ln(x, 0, 1)
     q, k, v = (lin(h, wi, bi).view(B, T, heads, hd).transpose(1, 2) for wi, bi in _LINEARS[:3])
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
-    x = x + lin(a.transpose(1, 2).reshape(B, T, H), *_LINEARS[3])
+    x = lin_res(a.transpose(1, 2).reshape(B, T, H), x, *_LINEARS[3])
     h = ln(x, 10, 11)
     fi, bi = _LINEARS[4]
     a = fc_gelu(h, p[fi], p[bi]) if targets is None else fc_gelu(h, p[fi], p[bi], targets[fi], targets[bi])
-    return x + lin(a, *_LINEARS[5])
+    return lin_res(a, x, *_LINEARS[5])
 
 
 class ElixirGPT2:

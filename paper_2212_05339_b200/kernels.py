@@ -426,10 +426,11 @@ def _lt_workspace(device: torch.device, stream) -> int:
     return ws.data_ptr()
 
 
-def _lt(epi, ta, tb, m, n, k, a, lda, b, ldb, d, ldd, bias=None, aux=None, ldaux=0, stream=None):
+def _lt(epi, ta, tb, m, n, k, a, lda, b, ldb, d, ldd, bias=None, aux=None, ldaux=0, stream=None, c=None):
     lib = _lib.load()
     rc = lib.elx_lt_matmul(epi, elx_dtype(d.dtype), ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
-                           d.data_ptr(), ldd, None if bias is None else bias.data_ptr(),
+                           None if c is None else c.data_ptr(), d.data_ptr(), ldd,
+                           None if bias is None else bias.data_ptr(),
                            None if aux is None else aux.data_ptr(), ldaux, _lt_workspace(d.device, stream),
                            _LT_WS_BYTES, _stream(stream))
     _lib.check(rc, "elx_lt_matmul")
@@ -473,3 +474,19 @@ def wgrad_bgrad(x2d: torch.Tensor, dy2d: torch.Tensor, dw: torch.Tensor, db: tor
         _cuda(t, n)
     # column-major: dW^T [I, O] = x^T [I, T] . dy [T, O]
     _lt(EPI_BGRADB if db is not None else EPI_NONE, 0, 1, I, O, T, x2d, I, dy2d, O, dw, I, bias=db, stream=stream)
+
+
+def linear_residual(x2d: torch.Tensor, w: torch.Tensor, b: torch.Tensor, res2d: torch.Tensor, stream=None):
+    """res + x W^T + b in one GEMM (C operand + bias epilogue): the residual add
+    of an output projection without a separate elementwise pass.
+    x2d [T, I], w [O, I], b [O], res2d [T, O]."""
+    T, I = x2d.shape
+    O = w.shape[0]
+    for t, n in ((x2d, "x"), (w, "w"), (b, "b"), (res2d, "res")):
+        _cuda(t, n)
+    if res2d.shape != (T, O) or res2d.dtype != x2d.dtype:
+        raise ValidationError("linear_residual: res must be [T, O] of x's dtype")
+    y = torch.empty(T, O, dtype=x2d.dtype, device=x2d.device)
+    # column-major: y^T [O, T] = W [O, I] . x^T [I, T] + res^T
+    _lt(EPI_BIAS, 1, 0, O, T, I, w, I, x2d, I, y, O, bias=b, c=res2d, stream=stream)
+    return y

@@ -710,3 +710,15 @@ def test_lt_wgrad_bgrad(cuda, T, I, O):
     dw2, db2 = torch.empty_like(dw), torch.empty_like(db)
     kernels.wgrad_bgrad(x, dy, dw2, db2)
     assert torch.equal(dw, dw2) and torch.equal(db, db2)
+
+
+def test_lt_linear_residual(cuda):
+    """res + x W^T + b from one GEMM (C operand + bias epilogue) vs fp32 torch."""
+    g = torch.Generator(device=cuda).manual_seed(1)
+    x = torch.randn(4096, 2048, device=cuda, generator=g).to(torch.bfloat16)
+    w = (torch.randn(1024, 2048, device=cuda, generator=g) * 0.02).to(torch.bfloat16)
+    b = torch.randn(1024, device=cuda, generator=g).to(torch.bfloat16)
+    r = torch.randn(4096, 1024, device=cuda, generator=g).to(torch.bfloat16)
+    y = kernels.linear_residual(x, w, b, r)
+    want = r.float() + x.float() @ w.float().t() + b.float()
+    assert torch.allclose(y.float(), want, rtol=2 ** -7, atol=2 ** -6 * float(want.abs().max()))
