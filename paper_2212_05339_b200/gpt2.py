@@ -10,7 +10,11 @@ writes the parameter gradients over the parameter data in the chunk
 (K1) and releases chunks at their reduce positions
 (rcache_sim.py:160-167, K3). After the walk HybridAdam updates the shards.
 
-GEMMs/attention are PyTorch (cuBLAS / SDPA); the chunk path is ours.
+GEMMs are cuBLAS (through torch, or cuBLASLt with fused epilogues: the MLP's
+bias + GELU, the output projections' residual add), attention is torch SDPA;
+LayerNorm, the lm_head cross-entropy and every gradient reduction written into
+the chunk are our kernels (csrc/elx_model_kernels.cu), and the chunk path
+itself is ours (csrc/elx_kernels.cu).
 """
 
 from __future__ import annotations
@@ -89,10 +93,6 @@ def init_params(cfg: GPT2Config, device, seed: int = 1234, dtype=torch.bfloat16)
         else:
             out[pid] = (torch.randn(shp, generator=g, device=device, dtype=torch.float32) * 0.02).to(dtype)
     return out
-
-
-_LAYER_KEYS = ("ln_1.w", "ln_1.b", "attn.qkv.w", "attn.qkv.b", "attn.proj.w", "attn.proj.b",
-               "ln_2.w", "ln_2.b", "mlp.fc.w", "mlp.fc.b", "mlp.proj.w", "mlp.proj.b")
 
 
 def layer_pieces(i: int, h: int) -> list[tuple[str, int, tuple[int, ...]]]:
@@ -256,7 +256,6 @@ def _block(x, p, heads, targets=None):
     `targets` (per-piece gradient destinations) the linear operators write
     their parameter gradients there during backward."""
     B, T, H = x.shape
-    ln1w, ln1b, qw, kw, vw, qb, kb, vb, projw, projb, ln2w, ln2b, fcw, fcb, mpw, mpb = p
     hd = H // heads
 
     def lin(inp, wi, bi):
@@ -275,6 +274,8 @@ def _block(x, p, heads, targets=None):
                                            res.reshape(-1, res.shape[-1])).view(res.shape)
         return _OverwriteLinearResidual.apply(inp, p[wi], p[bi], res, targets[wi], targets[bi])
 
+    # pieces: 0/1 ln_1, 2-4 q/k/v weight blocks, 5-7 their biases, 8/9 attn.proj, 10/11 ln_2,
+    # 12/13 mlp.fc, 14/15 mlp.proj (layer_pieces order)
     h = ln(x, 0, 1)
     q, k, v = (lin(h, wi, bi).view(B, T, heads, hd).transpose(1, 2) for wi, bi in _LINEARS[:3])
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
