@@ -268,3 +268,32 @@ def test_native_vs_live_reference(offplan):
                 continue
             got = schedule.simulate(tr_r, nb, C, {c: d.value for c, d in homes.items()}, gpu_count=3)
             assert got.__dict__ == want.__dict__
+
+
+from hypothesis import given, settings, strategies as st  # noqa: E402
+
+
+@settings(max_examples=200, derandomize=True, deadline=None)
+@given(st.lists(st.integers(1, 5000), min_size=1, max_size=40), st.integers(0, 3000))
+def test_native_pack_property(numels, slack):
+    """The reference's packing property (tests/test_chunking.py:97-116 of the
+    reference, same hypothesis settings) on the native packer: in-order, no
+    straddling, offsets contiguous from 0 inside each chunk, no chunk over C,
+    a parameter opens a new chunk only when it would not fit — and equal to
+    the oracle's packing."""
+    C = max(numels) + slack
+    seq = [(f"p{i}", n) for i, n in enumerate(numels)]
+    lay = layout.pack_chunks(_specs(seq), C)
+    flat = [m for c in lay.chunks for m in c.members]
+    assert [m.param_id for m in flat] == [p for p, _ in seq]
+    for ci, c in enumerate(lay.chunks):
+        off = 0
+        for m in c.members:
+            assert m.offset == off
+            off += m.numel
+        assert off <= C
+        if ci + 1 < len(lay.chunks):  # greedy: the next chunk's first member did not fit here
+            assert off + lay.chunks[ci + 1].members[0].numel > C
+    chunks, _ = L.pack(seq, C)
+    assert [[(m.param_id, m.offset, m.numel) for m in c.members] for c in lay.chunks] == \
+        [[(p, o, n) for p, o, n in ch] for ch in chunks]
