@@ -228,7 +228,7 @@ typedef struct {
   double max_norm;  /* <= 0 disables clipping */
   double grad_scale; /* multiplies compute-dtype gradients (1 / loss scale) */
   int32_t p16_dtype; /* ELX_BF16 or ELX_F16 */
-  int32_t pad_;
+  int32_t max_ctas;  /* > 0: cap the grid at this many CTAs (an update sharing the GPU); 0: full grid */
   /* Device step (used when elx_adam's `step` is 0): the step number is
    * t = step_scalars[2] + 1 (completed, non-skipped steps + 1), read on the
    * device, and the bias corrections come from caller-owned DEVICE tables

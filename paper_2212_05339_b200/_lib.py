@@ -64,7 +64,7 @@ class AdamSeg(ctypes.Structure):
 class AdamHP(ctypes.Structure):
     _fields_ = [("lr", c_f64), ("beta1", c_f64), ("beta2", c_f64), ("eps", c_f64),
                 ("weight_decay", c_f64), ("max_norm", c_f64), ("grad_scale", c_f64),
-                ("p16_dtype", c_i32), ("pad_", c_i32), ("bc1_table", c_vp), ("bc2s_table", c_vp),
+                ("p16_dtype", c_i32), ("max_ctas", c_i32), ("bc1_table", c_vp), ("bc2s_table", c_vp),
                 ("table_len", c_i64)]
 
 

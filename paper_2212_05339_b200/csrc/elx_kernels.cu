@@ -1010,6 +1010,10 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1)
   }
 }
 
+thread_local int t_max_ctas = 0;  // elx_adam_hp.max_ctas of the call being launched (0: full grid)
+
+int cap_grid(int grid) { return t_max_ctas > 0 ? std::min(grid, t_max_ctas) : grid; }
+
 template <typename T16, int kStages, int kTile, int kCW>
 int launch_adam_tma_st(const elx_adam_seg* segs, int nseg, int64_t ntiles, const AdamK& k, const double* sc,
                        cudaStream_t st) {
@@ -1024,7 +1028,7 @@ int launch_adam_tma_st(const elx_adam_seg* segs, int nseg, int64_t ntiles, const
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  const int grid = (int)std::min<int64_t>(ntiles * (ELX_ADAM_TILE / kTile), (int64_t)sm_count() * per_sm);
+  const int grid = cap_grid((int)std::min<int64_t>(ntiles * (ELX_ADAM_TILE / kTile), (int64_t)sm_count() * per_sm));
   kern<<<grid, kThreads, smem, st>>>(segs, nseg, ntiles, k, sc);
   return check_launch("elx_adam (tma in/out)");
 }
@@ -1043,7 +1047,7 @@ int launch_adam_tma(const elx_adam_seg* segs, int nseg, int64_t ntiles, const Ad
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kThreads, smem);
   if (per_sm < 1) per_sm = 1;
-  const int grid = (int)std::min<int64_t>(ntiles * (ELX_ADAM_TILE / kTile), (int64_t)sm_count() * per_sm);
+  const int grid = cap_grid((int)std::min<int64_t>(ntiles * (ELX_ADAM_TILE / kTile), (int64_t)sm_count() * per_sm));
   kern<<<grid, kThreads, smem, st>>>(segs, nseg, ntiles, k, sc);
   return check_launch("elx_adam (tma)");
 }
@@ -1060,7 +1064,7 @@ int launch_adam(int variant, const elx_adam_seg* segs, int nseg, int64_t ntiles,
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kAdamThreads, 0);
     if (per_sm < 1) per_sm = 1;
-    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)sm_count() * per_sm);
+    const int grid = cap_grid((int)std::min<int64_t>(ntiles, (int64_t)sm_count() * per_sm));
     kern<<<grid, kAdamThreads, 0, st>>>(segs, nseg, ntiles, k, sc);
     return check_launch("elx_adam");
   };
@@ -1412,6 +1416,8 @@ int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const e
     return e ? atoi(e) : 0;
   }();
   cudaStream_t st = (cudaStream_t)stream;
+  if (hp->max_ctas < 0) return elx::fail(ELX_ERR_VALIDATION, "max_ctas must be >= 0");
+  t_max_ctas = hp->max_ctas;
   if (hp->p16_dtype == ELX_BF16) return launch_adam<__nv_bfloat16>(variant, segs_dev, nseg, ntiles, k, step_scalars, st);
   if (hp->p16_dtype == ELX_F16) return launch_adam<__half>(variant, segs_dev, nseg, ntiles, k, step_scalars, st);
   return elx::fail(ELX_ERR_VALIDATION, "p16_dtype must be bf16/f16");

@@ -197,13 +197,14 @@ class BiasTables:
 
 
 def adam(table: AdamTable, hp: dict, step: int, step_scalars: torch.Tensor, p16_dtype: torch.dtype,
-         stream=None, grad_scale: float = 1.0, bias_tables: BiasTables | None = None) -> None:
+         stream=None, grad_scale: float = 1.0, bias_tables: BiasTables | None = None, max_ctas: int = 0) -> None:
     """K4 over every segment of `table` in one launch. Segments whose
     gradient is in the compute dtype are unscaled by `grad_scale` in-register.
     step >= 1: host step; step == 0: device step (step_scalars[2] + 1) with
-    `bias_tables`."""
+    `bias_tables`. max_ctas > 0 caps the grid (an update sharing the GPU)."""
     lib = _lib.load()
     h = _hp(hp, p16_dtype, grad_scale, None if bias_tables is None else bias_tables.pair())
+    h.max_ctas = int(max_ctas)
     rc = lib.elx_adam(table.dev.data_ptr(), table.nseg, table.ntiles, ctypes.byref(h), int(step),
                       step_scalars.data_ptr(), _stream(stream))
     _lib.check(rc, "elx_adam")
