@@ -41,6 +41,25 @@ from .errors import InfeasibleCacheError, ValidationError
 from .schedule import Device, Plan, Schedule, as_plan, compile_schedule, report_from_counters
 from .transport import LocalTransport
 
+# NVTX ranges around every fetch, release and optimizer step when ELX_NVTX=1
+# (for nsys / ncu --nvtx timelines); a no-op otherwise.
+_NVTX = os.environ.get("ELX_NVTX") == "1"
+
+
+class _nvtx:
+    __slots__ = ("name",)
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        if _NVTX:
+            torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *exc):
+        if _NVTX:
+            torch.cuda.nvtx.range_pop()
+
 SHARD_ALIGN = 8  # elements; keeps every shard and rCache segment 16-byte aligned
 ELX_TILE = _lib.ADAM_TILE
 # (host update, GPU-streamed update) in elements/s, measured on the B200 box
@@ -414,6 +433,10 @@ class ChunkFetcher:
 
     # ------------------------------------------------------------ events
     def _gather(self, rec) -> None:
+        with _nvtx(f"elx.fetch c{rec[0]} b{rec[1]}"):
+            self._gather_impl(rec)
+
+    def _gather_impl(self, rec) -> None:
         c, b, victim, pos = rec
         mgr = self.mgr
         if victim >= 0:
@@ -471,6 +494,10 @@ class ChunkFetcher:
 
     def _release(self, c: int, grads_written: torch.cuda.Event) -> None:
         """Reduce-scatter chunk c's gradients into this rank's fp32 shard (K3)."""
+        with _nvtx(f"elx.release c{c}"):
+            self._release_impl(c, grads_written)
+
+    def _release_impl(self, c: int, grads_written: torch.cuda.Event) -> None:
         mgr = self.mgr
         n = mgr.valid(c)
         comm = self.comm
@@ -848,6 +875,10 @@ class HybridAdam:
         only when read. `releases_done` is the event ChunkFetcher.finish()
         returns (None: synchronise the device); `grad_scale` = 1/loss_scale,
         applied in-register to compute-dtype gradients (world 1)."""
+        with _nvtx("elx.adam"):
+            return self._step_impl(releases_done, grad_scale)
+
+    def _step_impl(self, releases_done: torch.cuda.Event | None, grad_scale: float) -> "StepStats":
         self.grad_scale = float(grad_scale)
         m = self.mgr
         dev = m.device
