@@ -273,6 +273,10 @@ int64_t elx_colsum_workspace(int64_t rows, int64_t cols);
 int elx_colsum_geometry(int64_t rows, int64_t cols, int32_t* ctas, int32_t* groups);
 int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, int64_t rows, int64_t cols,
                float* workspace, void* stream);
+/* The same column sum over n (1..4) same-shape inputs in ONE launch (outs[i] =
+ * colsum(ins[i]), same order), e.g. the q/k/v bias gradients of a layer. */
+int elx_colsum_batched(int32_t n, void* const* outs, int32_t out_dtype, const void* const* ins, int32_t in_dtype,
+                       int64_t rows, int64_t cols, void* stream);
 
 /* ------------------------------------------------------- K6 offload
  * Pinned-host <-> HBM moves for CPU-home chunks on a side stream, with an

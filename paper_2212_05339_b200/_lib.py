@@ -95,6 +95,7 @@ _SIGNATURES = {
     "elx_colsum_workspace": (c_i64, [c_i64, c_i64]),
     "elx_colsum_geometry": (ctypes.c_int, [c_i64, c_i64, c_vp, c_vp]),
     "elx_colsum": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_i64, c_i64, c_vp, c_vp]),
+    "elx_colsum_batched": (ctypes.c_int, [c_i32, c_vp, c_i32, c_vp, c_i32, c_i64, c_i64, c_vp]),
     "elx_xent_fwd": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "elx_xent_bwd": (ctypes.c_int, [c_vp, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "elx_ln_param_grad": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i64, c_vp]),

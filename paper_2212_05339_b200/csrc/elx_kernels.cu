@@ -1194,9 +1194,19 @@ constexpr int kCcStrip = 128;
 constexpr int kCcCluster = 8;
 constexpr int kCcU = 16;
 
+// Up to kCcMaxBatch same-shape column sums in one launch (blockIdx.z picks the
+// tensor): the q/k/v bias gradients of a layer come out of one launch.
+constexpr int kCcMaxBatch = 4;
+struct ColsumBatch {
+  const void* in[kCcMaxBatch];
+  void* out[kCcMaxBatch];
+};
+
 template <typename T16>
 __global__ void __cluster_dims__(1, kCcCluster, 1) __launch_bounds__(kCcThreads, 1)
-    colsum_cluster_kernel(const T16* __restrict__ in, int64_t rows, int64_t cols, void* out, int out_dt) {
+    colsum_cluster_kernel(const ColsumBatch batch, int64_t rows, int64_t cols, int out_dt) {
+  const T16* __restrict__ in = static_cast<const T16*>(batch.in[blockIdx.z]);
+  void* out = batch.out[blockIdx.z];
   __shared__ float part[kCcWarps][kCcStrip];
   __shared__ float cta_sum[kCcStrip];
   cg::cluster_group cluster = cg::this_cluster();
@@ -1480,16 +1490,7 @@ int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, i
   if (elx::dtype_size(out_dtype) == 0) return elx::fail(ELX_ERR_VALIDATION, "bad out dtype");
   if (in_dtype != ELX_BF16 && in_dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "colsum input must be bf16/f16");
   cudaStream_t st = (cudaStream_t)stream;
-  if (colsum_variant() == 0) {
-    const dim3 grid((unsigned)((cols + kCcStrip - 1) / kCcStrip), kCcCluster);
-    if (in_dtype == ELX_BF16)
-      colsum_cluster_kernel<__nv_bfloat16><<<grid, kCcThreads, 0, st>>>(static_cast<const __nv_bfloat16*>(in), rows,
-                                                                        cols, out, out_dtype);
-    else
-      colsum_cluster_kernel<__half><<<grid, kCcThreads, 0, st>>>(static_cast<const __half*>(in), rows, cols, out,
-                                                                 out_dtype);
-    return check_launch("elx_colsum (cluster)");
-  }
+  if (colsum_variant() == 0) return elx_colsum_batched(1, &out, out_dtype, &in, in_dtype, rows, cols, stream);
   if (!workspace || !aligned16(workspace)) return elx::fail(ELX_ERR_VALIDATION, "workspace null or not 16-byte aligned");
   const int slices = colsum_slices(rows, cols);
   const dim3 grid((unsigned)((cols + kCsCols - 1) / kCsCols), (unsigned)slices);
@@ -1506,6 +1507,29 @@ int elx_colsum(void* out, int32_t out_dtype, const void* in, int32_t in_dtype, i
   const int g2 = (int)std::min<int64_t>((cols + 127) / 128, (int64_t)sm_count() * 4);
   colsum_final_kernel<<<g2, 128, 0, st>>>(workspace, slices, cols, out, out_dtype);
   return check_launch("elx_colsum final");
+}
+
+int elx_colsum_batched(int32_t n, void* const* outs, int32_t out_dtype, const void* const* ins, int32_t in_dtype,
+                       int64_t rows, int64_t cols, void* stream) {
+  elx::clear_error();
+  if (n < 1 || n > kCcMaxBatch || !outs || !ins) return elx::fail(ELX_ERR_VALIDATION, "batch of 1..4 tensors");
+  if (rows < 1 || cols < 1 || cols % 8) return elx::fail(ELX_ERR_VALIDATION, "need rows >= 1, cols a multiple of 8");
+  if (elx::dtype_size(out_dtype) == 0) return elx::fail(ELX_ERR_VALIDATION, "bad out dtype");
+  if (in_dtype != ELX_BF16 && in_dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "colsum input must be bf16/f16");
+  ColsumBatch b{};
+  for (int i = 0; i < n; ++i) {
+    if (!outs[i] || !ins[i]) return elx::fail(ELX_ERR_VALIDATION, "null pointer in batch entry %d", i);
+    if (!aligned16(ins[i])) return elx::fail(ELX_ERR_VALIDATION, "input %d not 16-byte aligned", i);
+    b.in[i] = ins[i];
+    b.out[i] = outs[i];
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  const dim3 grid((unsigned)((cols + kCcStrip - 1) / kCcStrip), kCcCluster, (unsigned)n);
+  if (in_dtype == ELX_BF16)
+    colsum_cluster_kernel<__nv_bfloat16><<<grid, kCcThreads, 0, st>>>(b, rows, cols, out_dtype);
+  else
+    colsum_cluster_kernel<__half><<<grid, kCcThreads, 0, st>>>(b, rows, cols, out_dtype);
+  return check_launch("elx_colsum (cluster)");
 }
 
 int elx_copy_h2d(void* dst_dev, const void* src_host, int64_t bytes, void* stream, void* event) {

@@ -138,6 +138,39 @@ class _OverwriteLinear(torch.autograd.Function):
         return gx, None, None, None, None
 
 
+class _OverwriteQKV(torch.autograd.Function):
+    """The three attention input projections q/k/v = h W^T + b as ONE wrapped
+    operator (three row blocks of attn.qkv, each output dense for SDPA). Its
+    backward accumulates dH = dq Wq + dk Wk + dv Wv in the GEMMs (beta = 1, no
+    separate add kernels), writes the three weight gradients into their row
+    blocks of the chunk slot, and the three bias gradients with ONE batched K7
+    launch (PAPER.md:233-236)."""
+
+    @staticmethod
+    def forward(ctx, h, wq, wk, wv, bq, bk, bv, tq, tk, tv, sq, sk, sv):
+        ctx.save_for_backward(h, wq, wk, wv)
+        ctx.targets = (tq, tk, tv, sq, sk, sv)
+        return F.linear(h, wq, bq), F.linear(h, wk, bk), F.linear(h, wv, bv)
+
+    @staticmethod
+    def backward(ctx, gq, gk, gv):
+        h, wq, wk, wv = ctx.saved_tensors
+        tq, tk, tv, sq, sk, sv = ctx.targets
+        H = h.shape[-1]
+        gs = [g.reshape(-1, g.shape[-1]) for g in (gq, gk, gv)]
+        h2 = h.reshape(-1, H)
+        gh = None
+        if ctx.needs_input_grad[0]:
+            gh = torch.mm(gs[0], wq)
+            gh.addmm_(gs[1], wk)
+            gh.addmm_(gs[2], wv)
+            gh = gh.view(h.shape)
+        for g, t in zip(gs, (tq, tk, tv)):
+            torch.mm(g.t(), h2, out=t)
+        kernels.colsum_batched(gs, (sq, sk, sv))
+        return (gh,) + (None,) * 12
+
+
 class _OverwriteLinearResidual(torch.autograd.Function):
     """y = res + x W^T + b as ONE cuBLASLt GEMM (C operand + bias epilogue):
     an output projection (attn.proj, mlp.proj) with the residual add folded in.
@@ -277,7 +310,12 @@ def _block(x, p, heads, targets=None):
     # pieces: 0/1 ln_1, 2-4 q/k/v weight blocks, 5-7 their biases, 8/9 attn.proj, 10/11 ln_2,
     # 12/13 mlp.fc, 14/15 mlp.proj (layer_pieces order)
     h = ln(x, 0, 1)
-    q, k, v = (lin(h, wi, bi).view(B, T, heads, hd).transpose(1, 2) for wi, bi in _LINEARS[:3])
+    if targets is None:
+        qkv = [F.linear(h, p[wi], p[bi]) for wi, bi in _LINEARS[:3]]
+    else:
+        qkv = _OverwriteQKV.apply(h, p[2], p[3], p[4], p[5], p[6], p[7],
+                                  targets[2], targets[3], targets[4], targets[5], targets[6], targets[7])
+    q, k, v = (t.view(B, T, heads, hd).transpose(1, 2) for t in qkv)
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
     x = lin_res(a.transpose(1, 2).reshape(B, T, H), x, *_LINEARS[3])
     h = ln(x, 10, 11)

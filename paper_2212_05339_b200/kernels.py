@@ -282,6 +282,23 @@ def colsum(x2d: torch.Tensor, out: torch.Tensor, stream=None) -> None:
     _lib.check(rc, "elx_colsum")
 
 
+def colsum_batched(xs: Sequence[torch.Tensor], outs: Sequence[torch.Tensor], stream=None) -> None:
+    """K7 over up to 4 same-shape 2-D inputs in one launch: outs[i] = colsum(xs[i])."""
+    lib = _lib.load()
+    if not 1 <= len(xs) <= 4 or len(xs) != len(outs):
+        raise ValidationError("colsum_batched takes 1..4 inputs and as many outputs")
+    rows, cols = xs[0].shape
+    for x, o in zip(xs, outs):
+        _cuda(x, "x")
+        if x.shape != (rows, cols) or x.dtype != xs[0].dtype or o.numel() != cols or o.dtype != outs[0].dtype:
+            raise ValidationError("colsum_batched inputs/outputs must share shape and dtype")
+    ins = _ptr_array([x.data_ptr() for x in xs])
+    ots = _ptr_array([o.data_ptr() for o in outs])
+    rc = lib.elx_colsum_batched(len(xs), ctypes.addressof(ots), elx_dtype(outs[0].dtype), ctypes.addressof(ins),
+                                elx_dtype(xs[0].dtype), rows, cols, _stream(stream))
+    _lib.check(rc, "elx_colsum_batched")
+
+
 def colsum_geometry(rows: int, cols: int) -> tuple[int, int]:
     """(slices, sub-slices per slice) of K7's fixed summation order."""
     lib = _lib.load()

@@ -722,3 +722,15 @@ def test_lt_linear_residual(cuda):
     y = kernels.linear_residual(x, w, b, r)
     want = r.float() + x.float() @ w.float().t() + b.float()
     assert torch.allclose(y.float(), want, rtol=2 ** -7, atol=2 ** -6 * float(want.abs().max()))
+
+
+def test_colsum_batched_equals_single(cuda):
+    """K7 over 3 same-shape inputs in one launch == three single launches, bit for bit."""
+    g = torch.Generator(device=cuda).manual_seed(8)
+    xs = [torch.randn(8192, 2048, device=cuda, generator=g).to(torch.bfloat16) for _ in range(3)]
+    outs = [torch.empty(2048, dtype=torch.bfloat16, device=cuda) for _ in range(3)]
+    kernels.colsum_batched(xs, outs)
+    for x, o in zip(xs, outs):
+        single = torch.empty_like(o)
+        kernels.colsum(x, single)
+        assert torch.equal(o, single)
