@@ -434,13 +434,16 @@ _LT_WS: dict = {}
 _LT_WS_BYTES = 32 * 2 ** 20
 
 
-def _lt_workspace(device: torch.device, stream) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream(device)
-    key = (device.index, s.cuda_stream)
-    ws = _LT_WS.get(key)
+def _lt_workspace(device: torch.device) -> int:
+    """One cuBLASLt workspace per device. The model issues its GEMMs on one
+    stream at a time (eager steps and graph replays are ordered on the current
+    stream), so calls never overlap; allocated on first use, which capture()
+    guarantees happens before a graph capture (its warm-up steps run eagerly),
+    so the captured pointer is ordinary device memory, not the graph's pool."""
+    ws = _LT_WS.get(device.index)
     if ws is None:
         ws = torch.empty(_LT_WS_BYTES, dtype=torch.uint8, device=device)
-        _LT_WS[key] = ws
+        _LT_WS[device.index] = ws
     return ws.data_ptr()
 
 
@@ -449,7 +452,7 @@ def _lt(epi, ta, tb, m, n, k, a, lda, b, ldb, d, ldd, bias=None, aux=None, ldaux
     rc = lib.elx_lt_matmul(epi, elx_dtype(d.dtype), ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
                            None if c is None else c.data_ptr(), d.data_ptr(), ldd,
                            None if bias is None else bias.data_ptr(),
-                           None if aux is None else aux.data_ptr(), ldaux, _lt_workspace(d.device, stream),
+                           None if aux is None else aux.data_ptr(), ldaux, _lt_workspace(d.device),
                            _LT_WS_BYTES, _stream(stream))
     _lib.check(rc, "elx_lt_matmul")
 
