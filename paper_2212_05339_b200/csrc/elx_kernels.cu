@@ -325,7 +325,7 @@ __device__ __forceinline__ int bad_of(double sq) { return !isfinite(sq); }
 // 2 B/element and produces sum(g^2) and the overflow flag. 16-byte loads (8
 // elements), kU of them in flight per thread, and occupancy held at >= 4 CTAs
 // per SM by the launch bound: the earlier 4-element / 120-register kernel ran
-// at 25% occupancy and 3.4 TB/s (profiles/r02_release.json). kScaleOne skips
+// at 25% occupancy and 3.4 TB/s (ncu). kScaleOne skips
 // the multiply by inv_scale == 1 (an exact identity).
 template <typename T16, bool kScaleOne, int kU>
 __global__ void __launch_bounds__(kRelThreads, 4) release_norm_kernel(const uint4* __restrict__ src, int64_t n,

@@ -240,7 +240,7 @@ class _OverwriteFcGelu(torch.autograd.Function):
     Backward: K12's GELU derivative, dW by cuBLAS into the weight slot, db by
     K7 into the bias slot, dX by cuBLAS. (cuBLASLt's fused
     DGELU_BGRAD and BGRADB epilogues measured slower on B200 than this
-    sequence: 0.62 vs 0.26 ms and 62 vs 60 us, profiles/r01m_model_kernels.jsonl.)"""
+    sequence: 0.62 vs 0.26 ms and 62 vs 60 us, profiles/r01o_model_kernels.jsonl.)"""
 
     @staticmethod
     def forward(ctx, x, w, b, w_target, b_target):
