@@ -163,14 +163,22 @@ int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int3
 /* Stream-ordered barrier across ranks over peer-mapped memory (the ordering
  * the in-kernel P2P fetch/release needs: every rank's earlier work on its
  * stream is visible to every peer before any rank's later work starts).
- * pads[r] is rank r's int32[world] signal pad (DEVICE pointers, local or
+ * pads[r] is rank r's int32[world + 1] signal pad (DEVICE pointers, local or
  * peer-mapped via CUDA IPC / symmetric memory, zero-initialised once); epoch
- * is a caller counter > 0 that increases by one per barrier. One thread
+ * is a caller counter > 0 that increases by one per barrier, or 0: the
+ * barrier numbers itself on the device from pads[rank][world], which it
+ * increments — the form a CUDA graph can capture and replay (every rank must
+ * use one form consistently). One thread
  * stores `epoch` into pads[p][rank] for every p with system-scope release
  * semantics, then waits until pads[rank][p] >= epoch for every p
  * (acquire). A barrier that waits longer than ~20 s traps (the stream's
  * context reports an error) instead of hanging. */
 int elx_device_barrier(int32_t* const* pads, int32_t world, int32_t rank, int32_t epoch, void* stream);
+
+/* dst[i] = sum_{r = 0..world-1, in order} peers[r][i] for i < count (fp64,
+ * count <= 1024): the N-scalar all-reduce of the step scalars over peer
+ * memory (call between two device barriers), deterministic in rank order. */
+int elx_peer_sum_f64(double* dst, const double* const* peers, int32_t count, int32_t world, void* stream);
 
 /* cudaDeviceEnablePeerAccess(peer) from the current device, treating
  * "already enabled" and peer == current device as success: kernels here can

@@ -271,6 +271,11 @@ __device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
 // stream runs next. Bounded: ~20 s of polling, then trap (a loud error, never
 // a silent hang).
 __global__ void device_barrier_kernel(const PadBatch pads, int world, int rank, int32_t epoch) {
+  if (epoch <= 0) {  // device-numbered barrier: the count lives in our own pad (graph-replayable)
+    int32_t* counter = pads.p[rank] + world;
+    epoch = *counter + 1;
+    *counter = epoch;
+  }
   __threadfence_system();
   for (int p = 0; p < world; ++p) st_release_sys(pads.p[p] + rank, epoch);
   const int32_t* mine = pads.p[rank];
@@ -282,6 +287,17 @@ __global__ void device_barrier_kernel(const PadBatch pads, int world, int rank, 
     }
   }
   __threadfence_system();
+}
+
+// dst[i] = sum over ranks, in rank order, of peers[r][i] (fp64): the N-scalar
+// all-reduce of the step scalars (sum of squares, overflow flag) over peer
+// memory — deterministic, unlike a ring all-reduce.
+__global__ void peer_sum_f64_kernel(double* dst, const PtrBatch peers, int count, int world) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    double a = 0.0;
+    for (int r = 0; r < world; ++r) a += static_cast<const volatile double*>(peers.p[r])[i];
+    dst[i] = a;
+  }
 }
 
 // ============================================================== K3 release
@@ -1362,7 +1378,7 @@ int elx_device_barrier(int32_t* const* pads, int32_t world, int32_t rank, int32_
   elx::clear_error();
   if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
   if (rank < 0 || rank >= world) return elx::fail(ELX_ERR_VALIDATION, "rank %d out of range", rank);
-  if (epoch <= 0) return elx::fail(ELX_ERR_VALIDATION, "epoch must be > 0");
+  if (epoch < 0) return elx::fail(ELX_ERR_VALIDATION, "epoch must be >= 0");
   if (!pads) return elx::fail(ELX_ERR_VALIDATION, "null pad table");
   PadBatch pb{};
   for (int r = 0; r < world; ++r) {
@@ -1372,6 +1388,20 @@ int elx_device_barrier(int32_t* const* pads, int32_t world, int32_t rank, int32_
   }
   device_barrier_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(pb, world, rank, epoch);
   return check_launch("elx_device_barrier");
+}
+
+int elx_peer_sum_f64(double* dst, const double* const* peers, int32_t count, int32_t world, void* stream) {
+  elx::clear_error();
+  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (!dst || !peers || count < 0 || count > 1024) return elx::fail(ELX_ERR_VALIDATION, "bad peer sum arguments");
+  PtrBatch pb{};
+  for (int r = 0; r < world; ++r) {
+    if (!peers[r]) return elx::fail(ELX_ERR_VALIDATION, "peer %d is null", r);
+    pb.p[r] = peers[r];
+  }
+  if (count == 0) return ELX_OK;
+  peer_sum_f64_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(dst, pb, count, world);
+  return check_launch("elx_peer_sum_f64");
 }
 
 int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t world, int32_t dtype,

@@ -117,6 +117,17 @@ def device_barrier(pad_ptrs: Sequence[int], rank: int, epoch: int, stream=None) 
     _lib.check(rc, "elx_device_barrier")
 
 
+def peer_sum_f64(dst: torch.Tensor, peer_ptrs: Sequence[int], count: int, stream=None) -> None:
+    """dst[:count] = sum over ranks (rank order) of peer_ptrs[r][:count] (fp64)."""
+    _cuda(dst, "dst")
+    if dst.dtype != torch.float64 or dst.numel() < count:
+        raise ValidationError("peer_sum_f64 needs a float64 destination of >= count elements")
+    arr = _ptr_array(peer_ptrs)
+    rc = _lib.load().elx_peer_sum_f64(dst.data_ptr(), ctypes.addressof(arr), int(count), len(peer_ptrs),
+                                      _stream(stream))
+    _lib.check(rc, "elx_peer_sum_f64")
+
+
 def release(grad_shard: torch.Tensor | None, src_ptrs: Sequence[int], n: int, dtype: torch.dtype,
             inv_scale: float, step_scalars: torch.Tensor, stream=None) -> None:
     """K3: grad_shard[:n] = (sum_r src_r[:n] in rank order, fp32) * inv_scale,

@@ -189,16 +189,55 @@ class ChunkManager:
             pad_shape = tuple(shared_padded[pid]) if shared_padded and pid in shared_padded else None
             full_len = max(ssh * self.world, math.prod(pad_shape) if pad_shape else 0)
             full = torch.zeros(full_len, dtype=dtype, device=dev)
-            p16 = full[self.rank * ssh:(self.rank + 1) * ssh] if self.world == 1 else torch.zeros(ssh, dtype=dtype, device=dev)
+            # P2P: the shard peers gather from and the gradient peers reduce from are peer-mapped
+            p16 = full[self.rank * ssh:(self.rank + 1) * ssh] if self.world == 1 else peer_alloc((ssh,))
+            grad = peer_alloc((ssh * self.world,)) if self.p2p else torch.zeros(ssh * self.world, dtype=dtype,
+                                                                                  device=dev)
             self.shared[pid] = _SharedParam(
-                pid, numel, self.shapes[pid], ssh, full, torch.zeros(ssh * self.world, dtype=dtype, device=dev), p16,
+                pid, numel, self.shapes[pid], ssh, full, grad, p16,
                 torch.zeros(ssh, dtype=f32, device=dev), torch.zeros(ssh, dtype=f32, device=dev),
                 torch.zeros(ssh, dtype=f32, device=dev),
                 torch.zeros(0 if self.world == 1 else ssh, dtype=f32, device=dev))
-        # step scalars: [0] sum g^2, [1] overflow flag (elx_release / elx_adam)
-        self.step_scalars = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.peer_shared = ({pid: (self.transport.peer_ptrs(sp.p16), self.transport.peer_ptrs(sp.grad))
+                             for pid, sp in self.shared.items()} if self.p2p else {})
+        # step scalars: [0] sum g^2, [1] overflow flag (elx_release / elx_adam); on the P2P path
+        # peer-mapped, so the N-scalar all-reduce is a rank-ordered read of the peers' values
+        if self.p2p:
+            self.step_scalars = self.transport.alloc((4,), torch.float64, dev)
+            self.peer_scalars = self.transport.peer_ptrs(self.step_scalars)
+            self._scalar_tmp = torch.zeros(2, dtype=torch.float64, device=dev)
+        else:
+            self.step_scalars = torch.zeros(4, dtype=torch.float64, device=dev)
+            self.peer_scalars = None
         self._bound: dict[int, torch.Tensor] = {}   # chunk -> storage it is bound to
         self._views: dict[str, torch.Tensor] = {}
+
+    def all_reduce_scalars(self) -> None:
+        """Sum step_scalars[0:2] (sum of squares, overflow flag) over ranks on
+        the current stream: NCCL all-reduce, or on the P2P path barrier ->
+        rank-ordered read of every peer's scalars -> barrier -> write back
+        (deterministic, no collective library)."""
+        if self.world == 1:
+            return
+        if not self.p2p:
+            self.transport.all_reduce_sum(self.step_scalars[:2])
+            return
+        self.transport.device_barrier()
+        kernels.peer_sum_f64(self._scalar_tmp, self.peer_scalars, 2)
+        self.transport.device_barrier()  # every rank has read before anyone overwrites
+        self.step_scalars[:2].copy_(self._scalar_tmp)
+
+    def gather_shared(self, sp: "_SharedParam") -> None:
+        """Rebuild the replicated compute copy of a shared parameter from every
+        rank's updated shard (after the optimizer step): NCCL all-gather, or K2
+        over the peers' shards after a device barrier on the P2P path."""
+        if self.world == 1:
+            return
+        if not self.p2p:
+            self.transport.gather(sp.full[:sp.shard * self.world], sp.p16)
+            return
+        self.transport.device_barrier()  # every rank's K4 has written its shard
+        kernels.fetch(sp.full, self.peer_shared[sp.pid][0], sp.shard)
 
     # ------------------------------------------------------------ sizes
     def valid(self, c: int, rank: int | None = None) -> int:
@@ -568,6 +607,11 @@ class ChunkFetcher:
                 self._fenced = True
             if mgr.world == 1:
                 srcs = [sp.grad.data_ptr()]
+            elif mgr.p2p:
+                # K3 straight over every rank's replicated gradient (segment `rank`)
+                mgr.transport.device_barrier()
+                es = sp.grad.element_size()
+                srcs = [p + mgr.rank * sp.shard * es for p in mgr.peer_shared[sp.pid][1]]
             else:
                 recv = torch.empty_like(sp.grad)
                 mgr.transport.scatter(recv, sp.grad)
@@ -578,6 +622,8 @@ class ChunkFetcher:
             if n > 0:
                 kernels.release(None if mgr.fused_w1 else sp.g32, srcs, n, mgr.dtype, self.inv_scale,
                                 mgr.step_scalars, stream=comm)
+            if mgr.p2p and mgr.world > 1:
+                mgr.transport.device_barrier()  # peers read our gradient before it is rewritten
 
 
 class StepStats:
@@ -857,9 +903,8 @@ class HybridAdam:
         host_segs = list(self.cpu_segs.values()) + list(self.stream_segs.values())
         if host_segs:
             kernels.cpu_adam(host_segs, self.hp, max(1, steps), (0.0, 1.0), m.dtype, self.cpu_threads)
-        if m.world > 1:
-            for sp in m.shared.values():
-                m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
+        for sp in m.shared.values():
+            m.gather_shared(sp)
         m.step_scalars.zero_()
         m.step_scalars[2] = float(steps)
         torch.cuda.synchronize(m.device)
@@ -887,8 +932,7 @@ class HybridAdam:
             torch.cuda.synchronize(dev)
         else:
             cur.wait_event(releases_done)
-        if m.world > 1:
-            m.transport.all_reduce_sum(m.step_scalars[:2])
+        m.all_reduce_scalars()
         slot = self._host_ring[self._issued % len(self._host_ring)]
         slot.copy_(m.step_scalars, non_blocking=True)
         snap = torch.cuda.Event()
@@ -920,18 +964,16 @@ class HybridAdam:
                 for key, table in self.groups:
                     kernels.adam(table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt,
                                  grad_scale=self.grad_scale, bias_tables=tabs)
-                    if key in m.shared and m.world > 1:
-                        sp = m.shared[key]
-                        m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
+                    if key in m.shared:
+                        m.gather_shared(m.shared[key])
                     ev = torch.cuda.Event()
                     ev.record(opt)
                     self.pending[key] = ev
             else:
                 kernels.adam(self.table, self.hp, kstep, m.step_scalars, m.dtype, stream=opt,
                              grad_scale=self.grad_scale, bias_tables=tabs)
-                if m.world > 1:
-                    for sp in m.shared.values():
-                        m.transport.gather(sp.full[:sp.shard * m.world], sp.p16)
+                for sp in m.shared.values():
+                    m.gather_shared(sp)
             if self.time_adam:
                 e1.record(opt)
                 self.adam_events.append((e0, e1))

@@ -138,8 +138,8 @@ class IpcTransport(TorchDistTransport):
         self._kernels = kernels
         self.device = torch.device("cuda", torch.cuda.current_device())
         self.peers: list[torch.Tensor] = []  # keep the peer mappings alive
-        self.epoch = 0
-        self.pad = torch.zeros(self.world, dtype=torch.int32, device=self.device)
+        # signal pad: one arrival flag per rank + this rank's own barrier count
+        self.pad = torch.zeros(self.world + 1, dtype=torch.int32, device=self.device)
         self.pad_ptrs = self.peer_ptrs(self.pad)
 
     def alloc(self, shape, dtype, device) -> torch.Tensor:
@@ -169,10 +169,12 @@ class IpcTransport(TorchDistTransport):
         dist.barrier(group=self.group)  # every rank has mapped before anyone frees or reuses
         return ptrs
 
+    # The barrier numbers itself on the device, so a captured CUDA graph can replay it.
+    graph_safe = True
+
     def device_barrier(self) -> None:
         """All ranks' current streams reach this point before any continues."""
-        self.epoch += 1
-        self._kernels.device_barrier(self.pad_ptrs, self.rank, self.epoch)
+        self._kernels.device_barrier(self.pad_ptrs, self.rank, 0)
 
 
 def make_transport(world_size: int, kind: str | None = None):
