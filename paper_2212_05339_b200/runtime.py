@@ -420,9 +420,12 @@ class ChunkFetcher:
         opt = self.optimizer
         for rec in self.early[pos]:  # prefetch, up to the schedule's horizon
             c = rec[0]
-            if (opt is not None and self.mgr.homes[c] is Device.CPU and c in opt.cpu_ready
-                    and not opt.cpu_ready[c].is_set()):
-                # its host update is still running: issue at the due position instead of blocking here
+            if (opt is not None and self.mgr.world == 1 and self.mgr.homes[c] is Device.CPU
+                    and c in opt.cpu_ready and not opt.cpu_ready[c].is_set()):
+                # its host update is still running: issue at the due position instead of blocking here.
+                # Only at world 1: with several ranks the choice depends on host timing, so ranks could
+                # issue their gathers (collectives, or barrier-ordered peer reads) in different orders;
+                # there _gather blocks on the update instead and the issue order stays the schedule's.
                 self.deferred.setdefault(rec[3], []).append(rec)
                 continue
             self._gather(rec)
@@ -520,7 +523,15 @@ class ChunkFetcher:
                     c1.record(comm)
                     self.copy_events.append(("h2d", c0, c1, seg.numel() * seg.element_size()))
                 self.bytes_moved["h2d"] += seg.numel() * seg.element_size()
-                if mgr.world > 1:
+                if mgr.world > 1 and mgr.p2p:
+                    # every rank has landed its segment of block b; read the others' over peer memory
+                    es = block.element_size()
+                    off = b * mgr.P * es
+                    mgr.transport.device_barrier()
+                    kernels.fetch(block, [p + off + r * mgr.S * es for r, p in enumerate(mgr.peer_blocks)], mgr.S,
+                                  stream=comm, engine=getattr(mgr.transport, "fetch_engine", "sm"))
+                    mgr.transport.device_barrier()  # peers may reuse block b only after every rank read it
+                elif mgr.world > 1:
                     mgr.transport.gather(block, seg)
             else:
                 mgr.transport.gather(block, mgr.p16[mgr.row[c]])
