@@ -297,9 +297,11 @@ def run_ours(args):
             model.fetcher.copy_events.clear()
             opt.cpu_wait_s = opt.cpu_update_s = 0.0
 
-    # CUDA graph: the whole step as one graph launch (world 1, every chunk GPU-home). The per-kernel
+    # CUDA graph: the whole step as one graph launch (every chunk GPU-home; world 1, or N ranks on the
+    # IPC P2P transport, whose exchanges are our kernels between device-numbered barriers). The per-kernel
     # event timings then come from `warmup` eager steps of the same launches, run just before capture.
-    use_graph = args.graph and world == 1 and not model.manager.cpu_ids
+    use_graph = (args.graph and not model.manager.cpu_ids and
+                 (world == 1 or (model.manager.p2p and getattr(model.manager.transport, "graph_safe", False))))
     step_fn = model.train_step
     probe_steps = args.steps
     if use_graph:
@@ -551,7 +553,7 @@ def main():
     ap.add_argument("--cpu-update", choices=["split", "host", "stream"], default="split",
                     help="CPU-home chunk update: host threads, GPU-streamed, or split by measured rate")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
-                    help="world 1 with every chunk GPU-home: capture the whole step as one CUDA graph")
+                    help="every chunk GPU-home, world 1 or --transport ipc: capture the whole step as one CUDA graph")
     ap.add_argument("--overlap", action="store_true",
                     help="issue the GPU update per chunk on an optimizer stream under the next forward")
     ap.add_argument("--transport", choices=["nccl", "p2p", "ipc"], default=os.environ.get("ELX_TRANSPORT", "nccl"),

@@ -514,12 +514,16 @@ class ElixirGPT2:
         depends on nothing outside the graph: every side stream rejoins the
         capture stream, and consecutive replays on one stream are ordered.
         Needs every chunk GPU-home (no host-thread update), a static loss
-        scale and world 1; the inputs of each later step are copied into the
-        captured input buffers by graph_step()."""
+        scale, and world 1 or a graph-safe P2P transport (IpcTransport: every
+        exchange is our kernels over peer memory, ordered by device-numbered
+        barriers, so N ranks replay N graphs in lockstep without a collective
+        library); the inputs of each later step are copied into the captured
+        input buffers by graph_step()."""
         mgr = self.manager
-        if mgr.cpu_ids or self.scaler.dynamic or self.optimizer.overlap or mgr.world != 1:
-            raise ValidationError("graph capture needs world 1, every chunk GPU-home, a static loss scale "
-                                  "and the single-launch optimizer")
+        multi_ok = mgr.world == 1 or (mgr.p2p and getattr(mgr.transport, "graph_safe", False))
+        if mgr.cpu_ids or self.scaler.dynamic or self.optimizer.overlap or not multi_ok:
+            raise ValidationError("graph capture needs every chunk GPU-home, a static loss scale, the "
+                                  "single-launch optimizer, and world 1 or a graph-safe P2P transport")
         self._g_tok = tokens.detach().clone()
         self._g_tgt = targets.detach().clone()
         if self.optimizer.tables is not None:

@@ -405,6 +405,9 @@ class ChunkFetcher:
         before anyone fetches: one device barrier on the comm stream."""
         self._reset()
         if self.mgr.p2p:
+            # fork the comm stream from the compute stream: orders it after this rank's previous
+            # step and, during a CUDA graph capture, brings it into the capture
+            self.comm.wait_stream(torch.cuda.current_stream(self.mgr.device))
             with torch.cuda.stream(self.comm):
                 if after is not None:
                     self.comm.wait_event(after)

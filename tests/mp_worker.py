@@ -14,7 +14,9 @@ rank's losses, fp32 master shards and live counters to <out>/rank<r>.npz.
 "ipc" runs the in-kernel P2P path instead: K2 reads the peers' shards and K3
 the peers' rCache blocks through CUDA-IPC mappings of the other processes'
 allocations, ordered by elx_device_barrier over IPC-mapped signal pads;
-"ipc-ce" does the same with K2 on the copy engines (elx_fetch_ce).
+"ipc-ce" does the same with K2 on the copy engines (elx_fetch_ce); "ipc-graph"
+captures the second step as one CUDA graph per rank (the ranks' graphs meet
+at device-numbered barriers) and replays it.
 """
 
 import json
@@ -45,7 +47,7 @@ def main():
     dist.init_process_group("gloo")
     plan, _, _ = _plan(kind)
     init = gpt2.init_params(CFG, dev, seed=11)
-    if path.startswith("ipc"):  # "ipc": K2 kernel, "ipc-ce": K2 on the copy engines
+    if path.startswith("ipc"):  # "ipc": K2 kernel, "ipc-ce": K2 on the copy engines, "ipc-graph": captured step
         transport = IpcTransport(fetch_engine="ce" if path == "ipc-ce" else "sm")
     else:
         transport = TorchDistTransport()
@@ -54,7 +56,11 @@ def main():
     losses = []
     for s in range(2):
         tok, tgt = _batches(world, s, dev)[rank]
-        losses.append(model.train_step(tok, tgt).item())
+        if path == "ipc-graph" and s == 1:  # step 1 replays a CUDA graph captured on every rank
+            model.capture(tok, tgt, warmup=0)
+            losses.append(model.graph_step(tok, tgt).item())
+        else:
+            losses.append(model.train_step(tok, tgt).item())
     model.synchronize()
     torch.cuda.synchronize()
     rec = {"losses": np.array(losses, np.float64), "counters": np.array(json.dumps(model.fetcher.counters()))}

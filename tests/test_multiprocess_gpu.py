@@ -52,13 +52,17 @@ def _torchrun(world: int, args: list[str], timeout: int = 600) -> subprocess.Com
     return p
 
 
-@pytest.mark.parametrize("path", ["exchange", "ipc", "ipc-ce"])
+@pytest.mark.parametrize("path", ["exchange", "ipc", "ipc-ce", "ipc-graph"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kind", ["rcache-min", "offload"])
 def test_multiprocess_gloo_equals_loopback(cuda, tmp_path, world, kind, path):
     """path "exchange": gloo all-gather / all-to-all + K3. path "ipc": the
     in-kernel P2P path across processes (CUDA-IPC peer mappings, our device
-    barrier kernel), which symmetric memory cannot run on a shared GPU."""
+    barrier kernel), which symmetric memory cannot run on a shared GPU;
+    "ipc-ce" with the fetch on the copy engines; "ipc-graph" with the second
+    step captured and replayed as one CUDA graph per rank."""
+    if path == "ipc-graph" and kind == "offload":
+        pytest.skip("graph capture needs every chunk GPU-home")
     _torchrun(world, ["tests/mp_worker.py", kind, str(tmp_path), path])
     got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
 
@@ -100,7 +104,7 @@ def test_multiprocess_gloo_equals_loopback(cuda, tmp_path, world, kind, path):
 
 
 @pytest.mark.parametrize("plan,transport", [("gpt2-small_n2.json", "nccl"), ("gpt2-small_rcache_n2.json", "nccl"),
-                                            ("gpt2-small_rcache_n2.json", "ipc")])
+                                            ("gpt2-small_rcache_n2.json", "ipc"), ("gpt2-small_n2.json", "ipc")])
 def test_bench_two_ranks_one_gpu(cuda, plan, transport):
     """transport "nccl" falls back to gloo on a shared GPU (same TorchDistTransport code)."""
     p = _torchrun(2, ["bench.py", "--gpus", "2", "--model", "gpt2-small", "--plan", plan, "--steps", "2",
@@ -123,3 +127,5 @@ def test_bench_two_ranks_one_gpu(cuda, plan, transport):
         assert live[k] == sim[k], (k, live, sim)
     if plan == "gpt2-small_rcache_n2.json":
         assert sim["replaced_ops"] > 0 and sim["c2g_units"] > 0
+    # the IPC transport with every chunk GPU-home runs the step as CUDA graphs on both ranks
+    assert line["config"]["cuda_graph"] == (transport == "ipc" and plan == "gpt2-small_n2.json")
