@@ -212,3 +212,40 @@ def test_cuda_graph_refuses_offloaded_plans(cuda):
     model = ElixirGPT2(CFG, plan, device=cuda, **HP)
     with pytest.raises(ValidationError):
         model.capture(*_batch(CFG, cuda, 1))
+
+
+@pytest.mark.parametrize("world", [1, 2])
+def test_memory_contract_chunk_footprint(cuda, world):
+    """The runtime's per-rank allocation against the reference's memory
+    contract: every GPU-home chunk holds exactly its shard of p16 + fp32
+    p32/m/v (chunk_footprint, cost_model.py:147-153, up to the 8-element shard
+    round-up); at N > 1 plus the documented 4 B/element fp32 gradient shard;
+    at N = 1 no gradient shard and no rCache for GPU-home chunks (used in place).
+    The shared wte holds shared_state_bytes (search.py:116-126) plus its
+    vocab padding and, at N > 1, a replicated (not partitioned) gradient."""
+    from _refstep import run_ranks
+    from paper_2212_05339_b200.runtime import shard_length
+    plan = dict(_plans(CFG))["all-gpu-max"]
+    C = plan.chunk_length
+
+    def rank_fn(r, transport):
+        m = ElixirGPT2(CFG, plan, device=cuda, transport=transport, **HP).manager
+        return m.memory_report(), len(m.gpu_ids), m.shared["wte"]
+
+    res = [rank_fn(0, None)] if world == 1 else run_ranks(world, rank_fn)
+    S = shard_length(C, world)
+    for rep, n_gpu, sp in res:
+        per_chunk = rep["gpu_chunk_state_bytes"] // n_gpu
+        assert per_chunk == 14 * S
+        assert 0 <= per_chunk - L.chunk_footprint(C, world) < 14 * 8
+        assert rep["gpu_grad_shard_bytes"] == (0 if world == 1 else 4 * S * n_gpu)
+        if world == 1:
+            assert rep["rcache_bytes"] == 0
+        # contract: replicated compute copy 2*S + partitioned ceil(14*S/N) (p16/gradient + 12 B state)
+        contract = L.shared_state_bytes(sp.numel, world)
+        vocab_pad = 2 * (sp.full.numel() - sp.numel)      # the lm_head's padded rows (compute view only)
+        if world == 1:  # the shard IS the full copy; the gradient buffer is the contract's 2 B term
+            ledger = vocab_pad + 2 * (sp.grad.numel() - sp.numel) + 12 * (sp.shard - sp.numel)
+        else:           # replicated bf16 gradient buffer + fp32 gradient shard on top of the contract
+            ledger = vocab_pad + 2 * sp.grad.numel() + (14 * sp.shard - -(-14 * sp.numel // world)) + 4 * sp.shard
+        assert rep["shared_bytes"] - contract == ledger, (rep["shared_bytes"], contract, ledger)
