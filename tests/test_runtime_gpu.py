@@ -249,3 +249,30 @@ def test_memory_contract_chunk_footprint(cuda, world):
         else:           # replicated bf16 gradient buffer + fp32 gradient shard on top of the contract
             ledger = vocab_pad + 2 * sp.grad.numel() + (14 * sp.shard - -(-14 * sp.numel // world)) + 4 * sp.shard
         assert rep["shared_bytes"] - contract == ledger, (rep["shared_bytes"], contract, ledger)
+
+
+def test_cuda_graph_checkpoint_round_trip(cuda):
+    """A trainer stepping by graph replays checkpoints like an eager one: its
+    state_dict (step count from the device counter) restores into a fresh
+    eager trainer, and loading a checkpoint INTO the captured trainer (in
+    place, same buffers) is picked up by the next replay."""
+    plan = dict(_plans(CFG))["all-gpu-max"]
+    init = gpt2.init_params(CFG, cuda, seed=12)
+    tok, tgt = _batch(CFG, cuda, 6)
+    g = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
+    g.capture(tok, tgt, warmup=2)
+    g.graph_step(tok, tgt)
+    g.graph_step(tok, tgt)
+    st = g.optimizer.state_dict()
+    assert st["step"] == 4
+    e = ElixirGPT2(CFG, plan, device=cuda, init=gpt2.init_params(CFG, cuda, seed=99), **HP)
+    e.optimizer.load_state_dict(st)
+    le = e.train_step(tok, tgt).item()
+    lg = g.graph_step(tok, tgt).item()
+    assert le == lg
+    me, mg = _masters(e), _masters(g)
+    for k in me:
+        assert np.array_equal(me[k], mg[k]), k
+    # restore the step-4 state into the captured trainer and replay: equals the eager continuation
+    g.optimizer.load_state_dict(st)
+    assert g.graph_step(tok, tgt).item() == le
