@@ -484,7 +484,7 @@ int run_release(float* g, const PtrBatch& pb, int64_t n, int world, float inv_sc
     const char* e = getenv("ELX_REL_VARIANT");
     return e ? atoi(e) : 0;
   }();
-  if (world == 1 && g == nullptr && aligned16(pb.p[0]) && variant == 0) {  // norm/overflow only
+  if (world == 1 && g == nullptr && aligned16(pb.p[0]) && (variant == 0 || variant >= 10)) {  // norm/overflow only
     auto go_norm = [&](auto kern, int u) {
       int per_sm = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelThreads, 0);
@@ -494,7 +494,9 @@ int run_release(float* g, const PtrBatch& pb, int64_t n, int world, float inv_sc
           1, std::min<int64_t>((work + kRelThreads - 1) / kRelThreads, (int64_t)sm_count() * per_sm));
       kern<<<grid, kRelThreads, 0, st>>>(static_cast<const uint4*>(pb.p[0]), n, inv_scale, sc);
     };
-    if (inv_scale == 1.0f) go_norm(release_norm_kernel<T16, true, 4>, 4);
+    if (variant == 10) go_norm(release_norm_kernel<T16, true, 8>, 8);        // sweep variants (ELX_REL_VARIANT)
+    else if (variant == 11) go_norm(release_norm_kernel<T16, true, 2>, 2);
+    else if (inv_scale == 1.0f) go_norm(release_norm_kernel<T16, true, 4>, 4);
     else go_norm(release_norm_kernel<T16, false, 4>, 4);
     return check_launch("elx_release (norm)");
   }
