@@ -322,7 +322,8 @@ int elx_ln_param_grad(void* dgamma, void* dbeta, const void* x, const void* dy, 
 
 /* ------------------------- K10-K12 the GPT-2 layer's row/elementwise ops
  * LayerNorm over the last dimension of [rows, cols] (BF16/F16, cols % 8 == 0,
- * cols <= 4096, 16-byte aligned; one warp per row held in registers):
+ * cols <= 2^20, 16-byte aligned; one warp per row held in registers up to
+ * 4096 columns, one CTA per row beyond):
  *   fwd:    y = (x - mean) * rstd * w + b, mean/rstd float32 [rows] out;
  *   bwd_dx: dx = rstd * (g - mean(g) - xhat * mean(g * xhat)), g = dy * w
  *           (the weight/bias gradients are elx_ln_param_grad's).

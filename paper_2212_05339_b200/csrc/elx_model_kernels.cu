@@ -398,6 +398,111 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __
   }
 }
 
+// Rows wider than a warp can hold in registers (cols > 4096): one CTA per row,
+// the row re-read from L2 on each pass, block reductions through shared memory.
+constexpr int kWideThreads = 256;
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();  // red may still be read by a previous call
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+  for (int w = 0; w < kWideThreads / 32; ++w) t += red[w];
+  return t;
+}
+
+template <typename T16>
+__global__ void __launch_bounds__(kWideThreads) ln_fwd_wide_kernel(const T16* __restrict__ x, const T16* __restrict__ w,
+                                                                   const T16* __restrict__ b, T16* __restrict__ y,
+                                                                   float* __restrict__ mean, float* __restrict__ rstd,
+                                                                   int cols, float eps) {
+  __shared__ float red[kWideThreads / 32];
+  const int64_t row = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  const int nvec = cols >> 3;
+  float s = 0.f;
+  for (int v = threadIdx.x; v < nvec; v += kWideThreads) {
+    float f[8];
+    unpack8<T16>(xr[v], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s += f[e];
+  }
+  const float mu = block_sum(s, red) / (float)cols;
+  float s2 = 0.f;
+  for (int v = threadIdx.x; v < nvec; v += kWideThreads) {
+    float f[8];
+    unpack8<T16>(xr[v], f);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) s2 += (f[e] - mu) * (f[e] - mu);
+  }
+  const float rs = rsqrtf(block_sum(s2, red) / (float)cols + eps);
+  uint4* yr = reinterpret_cast<uint4*>(y + row * cols);
+  for (int v = threadIdx.x; v < nvec; v += kWideThreads) {
+    float f[8], fw[8], fb[8];
+    unpack8<T16>(xr[v], f);
+    unpack8<T16>(__ldg(reinterpret_cast<const uint4*>(w) + v), fw);
+    unpack8<T16>(__ldg(reinterpret_cast<const uint4*>(b) + v), fb);
+    union {
+      T16 h[8];
+      uint4 u;
+    } o;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o.h[e] = from_f<T16>((f[e] - mu) * rs * fw[e] + fb[e]);
+    yr[v] = o.u;
+  }
+  if (threadIdx.x == 0) {
+    mean[row] = mu;
+    rstd[row] = rs;
+  }
+}
+
+template <typename T16>
+__global__ void __launch_bounds__(kWideThreads) ln_bwd_dx_wide_kernel(const T16* __restrict__ x,
+                                                                      const T16* __restrict__ dy,
+                                                                      const T16* __restrict__ w,
+                                                                      const float* __restrict__ mean,
+                                                                      const float* __restrict__ rstd,
+                                                                      T16* __restrict__ dx, int cols) {
+  __shared__ float red[kWideThreads / 32];
+  const int64_t row = blockIdx.x;
+  const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
+  const uint4* dr = reinterpret_cast<const uint4*>(dy + row * cols);
+  const uint4* wv = reinterpret_cast<const uint4*>(w);
+  const int nvec = cols >> 3;
+  const float mu = mean[row], rs = rstd[row];
+  float c1 = 0.f, c2 = 0.f;
+  for (int v = threadIdx.x; v < nvec; v += kWideThreads) {
+    float fx[8], fd[8], fw[8];
+    unpack8<T16>(xr[v], fx);
+    unpack8<T16>(dr[v], fd);
+    unpack8<T16>(__ldg(wv + v), fw);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const float g = fd[e] * fw[e];
+      c1 += g * ((fx[e] - mu) * rs);
+      c2 += g;
+    }
+  }
+  c1 = block_sum(c1, red) / (float)cols;
+  c2 = block_sum(c2, red) / (float)cols;
+  uint4* o = reinterpret_cast<uint4*>(dx + row * cols);
+  for (int v = threadIdx.x; v < nvec; v += kWideThreads) {
+    float fx[8], fd[8], fw[8];
+    unpack8<T16>(xr[v], fx);
+    unpack8<T16>(dr[v], fd);
+    unpack8<T16>(__ldg(wv + v), fw);
+    union {
+      T16 h[8];
+      uint4 u;
+    } r;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) r.h[e] = from_f<T16>(rs * (fd[e] * fw[e] - c2 - ((fx[e] - mu) * rs) * c1));
+    o[v] = r.u;
+  }
+}
+
 // ---------------------------------------------------------- K12 tanh-GELU
 // y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))) and its derivative,
 // 16-byte vectors, grid-stride; tanh via the SFU (tanh.approx.f32, ~2^-11
@@ -556,13 +661,25 @@ int elx_layer_norm_fwd(void* y, float* mean, float* rstd, const void* x, const v
   elx::clear_error();
   if (!y || !mean || !rstd || !x || !w || !b) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "layer norm must be bf16/f16");
-  if (rows < 0 || cols < 8 || (cols % 8) != 0 || cols > 4096)
-    return elx::fail(ELX_ERR_VALIDATION, "layer norm needs 8 <= cols <= 4096, cols %% 8 == 0");
+  if (rows < 0 || cols < 8 || (cols % 8) != 0 || cols > (1 << 20))
+    return elx::fail(ELX_ERR_VALIDATION, "layer norm needs 8 <= cols <= 2^20, cols %% 8 == 0");
   if (!aligned16(x) || !aligned16(y) || !aligned16(w) || !aligned16(b))
     return elx::fail(ELX_ERR_VALIDATION, "layer norm tensors must be 16-byte aligned");
   if (rows == 0) return ELX_OK;
+  if (rows > 0x7fffffff) return elx::fail(ELX_ERR_VALIDATION, "too many rows");
   cudaStream_t st = (cudaStream_t)stream;
   const int c = (int)cols;
+  if (cols > 4096) {  // wider than a warp's registers: CTA per row
+    if (dtype == ELX_BF16)
+      ln_fwd_wide_kernel<__nv_bfloat16><<<(unsigned)rows, kWideThreads, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(w),
+          static_cast<const __nv_bfloat16*>(b), static_cast<__nv_bfloat16*>(y), mean, rstd, c, eps);
+    else
+      ln_fwd_wide_kernel<__half><<<(unsigned)rows, kWideThreads, 0, st>>>(
+          static_cast<const __half*>(x), static_cast<const __half*>(w), static_cast<const __half*>(b),
+          static_cast<__half*>(y), mean, rstd, c, eps);
+    return check("elx_layer_norm_fwd (wide)");
+  }
   if (dtype == ELX_BF16) {
     using T = __nv_bfloat16;
     auto k = [&](auto kern) {
@@ -592,13 +709,25 @@ int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w
   elx::clear_error();
   if (!dx || !x || !dy || !w || !mean || !rstd) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "layer norm must be bf16/f16");
-  if (rows < 0 || cols < 8 || (cols % 8) != 0 || cols > 4096)
-    return elx::fail(ELX_ERR_VALIDATION, "layer norm needs 8 <= cols <= 4096, cols %% 8 == 0");
+  if (rows < 0 || cols < 8 || (cols % 8) != 0 || cols > (1 << 20))
+    return elx::fail(ELX_ERR_VALIDATION, "layer norm needs 8 <= cols <= 2^20, cols %% 8 == 0");
   if (!aligned16(x) || !aligned16(dy) || !aligned16(dx) || !aligned16(w))
     return elx::fail(ELX_ERR_VALIDATION, "layer norm tensors must be 16-byte aligned");
   if (rows == 0) return ELX_OK;
+  if (rows > 0x7fffffff) return elx::fail(ELX_ERR_VALIDATION, "too many rows");
   cudaStream_t st = (cudaStream_t)stream;
   const int c = (int)cols;
+  if (cols > 4096) {
+    if (dtype == ELX_BF16)
+      ln_bwd_dx_wide_kernel<__nv_bfloat16><<<(unsigned)rows, kWideThreads, 0, st>>>(
+          static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy),
+          static_cast<const __nv_bfloat16*>(w), mean, rstd, static_cast<__nv_bfloat16*>(dx), c);
+    else
+      ln_bwd_dx_wide_kernel<__half><<<(unsigned)rows, kWideThreads, 0, st>>>(
+          static_cast<const __half*>(x), static_cast<const __half*>(dy), static_cast<const __half*>(w), mean, rstd,
+          static_cast<__half*>(dx), c);
+    return check("elx_layer_norm_bwd_dx (wide)");
+  }
   if (dtype == ELX_BF16) {
     using T = __nv_bfloat16;
     auto k = [&](auto kern) {

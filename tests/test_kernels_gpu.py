@@ -586,7 +586,8 @@ def test_ln_param_grad_matches_float64(cuda, dtype, rows, cols):
 # ------------------------------------------------------------------ K10-K12 LayerNorm / GELU
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
-@pytest.mark.parametrize("rows,cols", [(1, 8), (5, 64), (300, 768), (8192, 2048), (64, 3072), (33, 4096)])
+@pytest.mark.parametrize("rows,cols", [(1, 8), (5, 64), (300, 768), (8192, 2048), (64, 3072), (33, 4096),
+                                       (17, 6144), (3, 20480)])
 def test_layer_norm_matches_torch(cuda, dtype, rows, cols):
     """K10/K11 vs torch's LayerNorm (fp32 math on the same inputs): y and dx
     within the output dtype's rounding, mean/rstd within 1e-5."""
