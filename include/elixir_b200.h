@@ -335,6 +335,11 @@ int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w
                           int32_t dtype, int64_t rows, int64_t cols, void* stream);
 int elx_gelu_fwd(void* y, const void* x, int32_t dtype, int64_t n, void* stream);
 int elx_gelu_bwd(void* dx, const void* x, const void* dy, int32_t dtype, int64_t n, void* stream);
+/* elx_gelu_bwd over [rows, cols] fused with K7 on its output: dx as above and
+ * dbias[j] = colsum of dx (the bf16/f16-rounded values) in elx_colsum's exact
+ * fp32 order — bit-identical to elx_gelu_bwd then elx_colsum, one pass. */
+int elx_gelu_bwd_colsum(void* dx, void* dbias, int32_t dbias_dtype, const void* x, const void* dy, int32_t dtype,
+                        int64_t rows, int64_t cols, void* stream);
 
 /* ------------------------------ cuBLASLt GEMMs with fused epilogues
  * Library GEMMs for the caller's wrapped operators, used for their epilogues:

@@ -104,6 +104,7 @@ _SIGNATURES = {
     "elx_layer_norm_bwd_dx": (ctypes.c_int, [c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i64, c_i64, c_vp]),
     "elx_gelu_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i64, c_vp]),
     "elx_gelu_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp]),
+    "elx_gelu_bwd_colsum": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_i64, c_vp]),
     "elx_lt_matmul": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                                      c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "elx_copy_h2d": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),

@@ -237,8 +237,9 @@ class _OverwriteFcGelu(torch.autograd.Function):
     """a = gelu(x W^T + b), the MLP's first wrapped operator, as ONE cuBLASLt
     GEMM with the bias + tanh-GELU epilogue (keeping the pre-activation for the
     backward): the separate GELU pass over the [T, 4H] activation disappears.
-    Backward: K12's GELU derivative, dW by cuBLAS into the weight slot, db by
-    K7 into the bias slot, dX by cuBLAS. (cuBLASLt's fused
+    Backward: K12's GELU derivative fused with K7's column sum (db straight
+    into the bias slot) in one pass, dW by cuBLAS into the
+    weight slot, dX by cuBLAS. (cuBLASLt's fused
     DGELU_BGRAD and BGRADB epilogues measured slower on B200 than this
     sequence: 0.62 vs 0.26 ms and 62 vs 60 us, profiles/r01o_model_kernels.jsonl.)"""
 
@@ -255,10 +256,9 @@ class _OverwriteFcGelu(torch.autograd.Function):
     def backward(ctx, gy):
         x2, w, pre = ctx.saved_tensors
         w_t, b_t = ctx.targets
-        d = kernels.gelu_bwd(pre, gy.reshape(-1, gy.shape[-1]).contiguous())
+        d = kernels.gelu_bwd_colsum(pre, gy.reshape(-1, gy.shape[-1]).contiguous(), b_t)  # db in the same pass
         gx = torch.mm(d, w).view(ctx.xshape) if ctx.needs_input_grad[0] else None
         torch.mm(d.t(), x2, out=w_t)
-        kernels.colsum(d, b_t)
         return gx, None, None, None, None
 
 

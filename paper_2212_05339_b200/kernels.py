@@ -394,6 +394,21 @@ def gelu_bwd(x: torch.Tensor, dy: torch.Tensor, stream=None) -> torch.Tensor:
     return dx
 
 
+def gelu_bwd_colsum(x2d: torch.Tensor, dy2d: torch.Tensor, dbias: torch.Tensor, stream=None) -> torch.Tensor:
+    """K12 backward fused with K7: returns dx = dy * gelu'(x) and writes
+    colsum(dx) into `dbias` (bit-identical to gelu_bwd + colsum)."""
+    _cuda(x2d, "x")
+    _cuda(dy2d, "dy")
+    if x2d.dim() != 2 or dy2d.shape != x2d.shape or dy2d.dtype != x2d.dtype or dbias.numel() != x2d.shape[1]:
+        raise ValidationError("gelu_bwd_colsum: x, dy [rows, cols] of one dtype; dbias of cols elements")
+    dx = torch.empty_like(x2d)
+    rows, cols = x2d.shape
+    rc = _lib.load().elx_gelu_bwd_colsum(dx.data_ptr(), dbias.data_ptr(), elx_dtype(dbias.dtype), x2d.data_ptr(),
+                                         dy2d.data_ptr(), elx_dtype(x2d.dtype), rows, cols, _stream(stream))
+    _lib.check(rc, "elx_gelu_bwd_colsum")
+    return dx
+
+
 class LMHeadCrossEntropy(torch.autograd.Function):
     """K8: mean softmax cross-entropy over the padded bf16/f16 lm_head logits
     [rows, ld] (columns >= vocab excluded), with no fp32 copy of the logits.

@@ -62,6 +62,10 @@ Ef = R * 4 * H * 2
 report("K7 colsum 8192x8192", timed(lambda: kernels.colsum(dyf, torch.empty(4 * H, device=dev, dtype=bf))), Ef)
 report("K12 gelu_fwd 8192x8192", timed(lambda: kernels.gelu_fwd(xf)), 2 * Ef)
 report("K12 gelu_bwd 8192x8192", timed(lambda: kernels.gelu_bwd(xf, dyf)), 3 * Ef)
+dbf4 = torch.empty(4 * H, device=dev, dtype=bf)
+report("K12 gelu_bwd + K7 colsum 8192x8192 (unfused)",
+       timed(lambda: kernels.colsum(kernels.gelu_bwd(xf, dyf), dbf4)), 3 * Ef)
+report("K12+K7 gelu_bwd_colsum 8192x8192 (fused)", timed(lambda: kernels.gelu_bwd_colsum(xf, dyf, dbf4)), 3 * Ef)
 report("torch gelu fwd (tanh) 8192x8192",
        timed(lambda: torch.nn.functional.gelu(xf, approximate="tanh")), 2 * Ef)
 report("torch layer_norm fwd 8192x2048",

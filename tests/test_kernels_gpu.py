@@ -735,3 +735,18 @@ def test_colsum_batched_equals_single(cuda):
         single = torch.empty_like(o)
         kernels.colsum(x, single)
         assert torch.equal(o, single)
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 8192), (1000, 3072), (7, 264)])
+def test_gelu_bwd_colsum_equals_unfused(cuda, rows, cols):
+    """The fused GELU-backward + bias column sum is bit-identical to K12's
+    backward followed by K7 (same rounding, same fp32 summation order)."""
+    g = torch.Generator(device=cuda).manual_seed(rows + cols)
+    x = (torch.randn(rows, cols, device=cuda, generator=g) * 2).to(torch.bfloat16)
+    dy = torch.randn(rows, cols, device=cuda, generator=g).to(torch.bfloat16)
+    db = torch.empty(cols, dtype=torch.bfloat16, device=cuda)
+    dx = kernels.gelu_bwd_colsum(x, dy, db)
+    dx2 = kernels.gelu_bwd(x, dy)
+    db2 = torch.empty_like(db)
+    kernels.colsum(dx2, db2)
+    assert torch.equal(dx, dx2) and torch.equal(db, db2)
