@@ -333,6 +333,12 @@ int elx_layer_norm_fwd(void* y, float* mean, float* rstd, const void* x, const v
                        int64_t rows, int64_t cols, float eps, void* stream);
 int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w, const float* mean, const float* rstd,
                           int32_t dtype, int64_t rows, int64_t cols, void* stream);
+/* elx_layer_norm_bwd_dx plus the residual branch's gradient: dx = K11 + dres
+ * (both rounded to the element type, the sum rounded once — the same bits as
+ * a separate add); dres may be NULL. */
+int elx_layer_norm_bwd_dx_res(void* dx, const void* x, const void* dy, const void* w, const float* mean,
+                              const float* rstd, const void* dres, int32_t dtype, int64_t rows, int64_t cols,
+                              void* stream);
 int elx_gelu_fwd(void* y, const void* x, int32_t dtype, int64_t n, void* stream);
 int elx_gelu_bwd(void* dx, const void* x, const void* dy, int32_t dtype, int64_t n, void* stream);
 /* elx_gelu_bwd over [rows, cols] fused with K7 on its output: dx as above and

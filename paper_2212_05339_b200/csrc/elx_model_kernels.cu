@@ -338,13 +338,25 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_fwd_kernel(const T16* __res
   }
 }
 
+// h[e] = h[e] + res[e], each operand already rounded to T16, the sum rounded
+// once: the same bits as a separate elementwise add of the two tensors (the
+// residual branch's gradient joining the LayerNorm's, folded into K11).
+template <typename T16>
+__device__ __forceinline__ void add_res8(T16* h, uint4 q) {
+  float fr[8];
+  unpack8<T16>(q, fr);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) h[e] = from_f<T16>(to_f(h[e]) + fr[e]);
+}
+
 // dx = rstd * (g - mean(g) - xhat * mean(g * xhat)), g = dy * w, xhat = (x - mean) * rstd
+// (+ dres, the gradient reaching x through the residual branch, when given)
 template <typename T16, int kV>
 __global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __restrict__ x, const T16* __restrict__ dy,
                                                                    const T16* __restrict__ w,
                                                                    const float* __restrict__ mean,
                                                                    const float* __restrict__ rstd, T16* __restrict__ dx,
-                                                                   int64_t rows, int cols) {
+                                                                   const T16* __restrict__ dres, int64_t rows, int cols) {
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -393,6 +405,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __
         const float xh = (fx[e] - mu) * rs;
         r.h[e] = from_f<T16>(rs * (fd[e] * fw[e] - c2 - xh * c1));
       }
+      if (dres) add_res8<T16>(r.h, __ldcs(reinterpret_cast<const uint4*>(dres + row * cols) + v));
       o[v] = r.u;
     }
   }
@@ -464,7 +477,8 @@ __global__ void __launch_bounds__(kWideThreads) ln_bwd_dx_wide_kernel(const T16*
                                                                       const T16* __restrict__ w,
                                                                       const float* __restrict__ mean,
                                                                       const float* __restrict__ rstd,
-                                                                      T16* __restrict__ dx, int cols) {
+                                                                      T16* __restrict__ dx,
+                                                                      const T16* __restrict__ dres, int cols) {
   __shared__ float red[kWideThreads / 32];
   const int64_t row = blockIdx.x;
   const uint4* xr = reinterpret_cast<const uint4*>(x + row * cols);
@@ -499,6 +513,7 @@ __global__ void __launch_bounds__(kWideThreads) ln_bwd_dx_wide_kernel(const T16*
     } r;
 #pragma unroll
     for (int e = 0; e < 8; ++e) r.h[e] = from_f<T16>(rs * (fd[e] * fw[e] - c2 - ((fx[e] - mu) * rs) * c1));
+    if (dres) add_res8<T16>(r.h, reinterpret_cast<const uint4*>(dres + row * cols)[v]);
     o[v] = r.u;
   }
 }
@@ -804,8 +819,15 @@ int elx_layer_norm_fwd(void* y, float* mean, float* rstd, const void* x, const v
 
 int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w, const float* mean, const float* rstd,
                           int32_t dtype, int64_t rows, int64_t cols, void* stream) {
+  return elx_layer_norm_bwd_dx_res(dx, x, dy, w, mean, rstd, nullptr, dtype, rows, cols, stream);
+}
+
+int elx_layer_norm_bwd_dx_res(void* dx, const void* x, const void* dy, const void* w, const float* mean,
+                              const float* rstd, const void* dres, int32_t dtype, int64_t rows, int64_t cols,
+                              void* stream) {
   elx::clear_error();
   if (!dx || !x || !dy || !w || !mean || !rstd) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dres && !aligned16(dres)) return elx::fail(ELX_ERR_VALIDATION, "dres must be 16-byte aligned");
   if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "layer norm must be bf16/f16");
   if (rows < 0 || cols < 8 || (cols % 8) != 0 || cols > (1 << 20))
     return elx::fail(ELX_ERR_VALIDATION, "layer norm needs 8 <= cols <= 2^20, cols %% 8 == 0");
@@ -819,11 +841,12 @@ int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w
     if (dtype == ELX_BF16)
       ln_bwd_dx_wide_kernel<__nv_bfloat16><<<(unsigned)rows, kWideThreads, 0, st>>>(
           static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy),
-          static_cast<const __nv_bfloat16*>(w), mean, rstd, static_cast<__nv_bfloat16*>(dx), c);
+          static_cast<const __nv_bfloat16*>(w), mean, rstd, static_cast<__nv_bfloat16*>(dx),
+          static_cast<const __nv_bfloat16*>(dres), c);
     else
       ln_bwd_dx_wide_kernel<__half><<<(unsigned)rows, kWideThreads, 0, st>>>(
           static_cast<const __half*>(x), static_cast<const __half*>(dy), static_cast<const __half*>(w), mean, rstd,
-          static_cast<__half*>(dx), c);
+          static_cast<__half*>(dx), static_cast<const __half*>(dres), c);
     return check("elx_layer_norm_bwd_dx (wide)");
   }
   if (dtype == ELX_BF16) {
@@ -831,7 +854,7 @@ int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w
     auto k = [&](auto kern) {
       kern<<<ELX_ROWS_GRID(rows), kRowWarps * 32, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(dy),
                                                            static_cast<const T*>(w), mean, rstd, static_cast<T*>(dx),
-                                                           rows, c);
+                                                           static_cast<const T*>(dres), rows, c);
     };
     pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2>); }, [&] { k(ln_bwd_dx_kernel<T, 4>); },
                     [&] { k(ln_bwd_dx_kernel<T, 8>); }, [&] { k(ln_bwd_dx_kernel<T, 12>); },
@@ -841,7 +864,7 @@ int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w
     auto k = [&](auto kern) {
       kern<<<ELX_ROWS_GRID(rows), kRowWarps * 32, 0, st>>>(static_cast<const T*>(x), static_cast<const T*>(dy),
                                                            static_cast<const T*>(w), mean, rstd, static_cast<T*>(dx),
-                                                           rows, c);
+                                                           static_cast<const T*>(dres), rows, c);
     };
     pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2>); }, [&] { k(ln_bwd_dx_kernel<T, 4>); },
                     [&] { k(ln_bwd_dx_kernel<T, 8>); }, [&] { k(ln_bwd_dx_kernel<T, 12>); },

@@ -138,6 +138,27 @@ class _OverwriteLinear(torch.autograd.Function):
         return gx, None, None, None, None
 
 
+def _qkv_proj(h, wq, wk, wv, bq, bk, bv):
+    """q, k, v = h W^T + b for the three row blocks of attn.qkv as ONE GEMM
+    with N = 3H (the blocks are consecutive in the chunk, so W and b are one
+    strided view each). The outputs are [B, T, H] column blocks of one
+    [B, T, 3H] result; SDPA takes them strided at the same speed (0.136 vs
+    0.146 ms for three N = H GEMMs at the 1.3B shape, scripts/qkv_probe.py)."""
+    H = wq.shape[1]
+    es = wq.element_size()
+    same = (wq.untyped_storage().data_ptr() == wk.untyped_storage().data_ptr() == wv.untyped_storage().data_ptr()
+            and bq.untyped_storage().data_ptr() == bk.untyped_storage().data_ptr() == bv.untyped_storage().data_ptr())
+    packed = same and (wk.data_ptr() == wq.data_ptr() + wq.numel() * es and wv.data_ptr() == wk.data_ptr() + wk.numel() * es
+              and bk.data_ptr() == bq.data_ptr() + bq.numel() * es and bv.data_ptr() == bk.data_ptr() + bk.numel() * es
+              and wq.is_contiguous() and wk.is_contiguous() and wv.is_contiguous())
+    if not packed:
+        return F.linear(h, wq, bq), F.linear(h, wk, bk), F.linear(h, wv, bv)
+    n = wq.shape[0] + wk.shape[0] + wv.shape[0]
+    y = F.linear(h, wq.as_strided((n, H), (H, 1)), bq.as_strided((n,), (1,)))
+    a, b = wq.shape[0], wq.shape[0] + wk.shape[0]
+    return y[..., :a], y[..., a:b], y[..., b:]
+
+
 class _OverwriteQKV(torch.autograd.Function):
     """The three attention input projections q/k/v = h W^T + b as ONE wrapped
     operator (three row blocks of attn.qkv, each output dense for SDPA). Its
@@ -150,7 +171,7 @@ class _OverwriteQKV(torch.autograd.Function):
     def forward(ctx, h, wq, wk, wv, bq, bk, bv, tq, tk, tv, sq, sk, sv):
         ctx.save_for_backward(h, wq, wk, wv)
         ctx.targets = (tq, tk, tv, sq, sk, sv)
-        return F.linear(h, wq, bq), F.linear(h, wk, bk), F.linear(h, wv, bv)
+        return _qkv_proj(h, wq, wk, wv, bq, bk, bv)
 
     @staticmethod
     def backward(ctx, gq, gk, gv):
@@ -226,6 +247,42 @@ class _LayerNorm(torch.autograd.Function):
         return gx, (w_t if own else None), (b_t if own else None), None, None
 
 
+class _LayerNormResidual(torch.autograd.Function):
+    """_LayerNorm for an x that also feeds a residual branch: returns (y, x')
+    with x' an alias of x for the residual. The two gradients reaching x (the
+    LayerNorm's and the residual's) are summed inside K11's store instead of
+    by autograd's separate add kernel over [T, H] (bit-identical)."""
+
+    @staticmethod
+    def forward(ctx, x, w, b, w_target, b_target):
+        x = x.contiguous()
+        y, mean, rstd = kernels.layer_norm_fwd(x, w, b)
+        ctx.save_for_backward(x, w, mean, rstd)
+        ctx.targets = (w_target, b_target)
+        return y, x.view_as(x)
+
+    @staticmethod
+    def backward(ctx, gy, gres):
+        x, w, mean, rstd = ctx.saved_tensors
+        H = x.shape[-1]
+        gy = gy.contiguous()
+        gx = kernels.layer_norm_bwd_dx(x, gy, w, mean, rstd, dres=None if gres is None else gres.contiguous())
+        w_t, b_t = ctx.targets
+        own = w_t is None
+        if own:
+            w_t, b_t = torch.empty_like(w), torch.empty_like(w)
+        kernels.ln_param_grad(x.reshape(-1, H), gy.reshape(-1, H), mean.reshape(-1), rstd.reshape(-1), w_t, b_t)
+        return gx, (w_t if own else None), (b_t if own else None), None, None
+
+
+def layer_norm_residual(x, w, b, w_target=None, b_target=None):
+    """(layer_norm(x), x) where the returned x feeds a residual branch; under
+    autograd the two gradients of x are joined inside K11."""
+    if torch.is_grad_enabled() and (x.requires_grad or w.requires_grad or b.requires_grad):
+        return _LayerNormResidual.apply(x, w, b, w_target, b_target)
+    return kernels.layer_norm_fwd(x.contiguous(), w, b)[0], x
+
+
 def layer_norm(x, w, b, w_target=None, b_target=None):
     """GPT-2 LayerNorm on K10/K11/K9 (autograd only when a gradient is needed)."""
     if torch.is_grad_enabled() and (x.requires_grad or w.requires_grad or b.requires_grad):
@@ -296,10 +353,10 @@ def _block(x, p, heads, targets=None):
             return F.linear(inp, p[wi], p[bi])
         return _OverwriteLinear.apply(inp, p[wi], p[bi], targets[wi], targets[bi])
 
-    def ln(inp, wi, bi):
+    def ln(inp, wi, bi):  # (LayerNorm(inp), inp for the residual branch)
         if targets is None:
-            return layer_norm(inp, p[wi], p[bi])
-        return layer_norm(inp, p[wi], p[bi], targets[wi], targets[bi])
+            return layer_norm_residual(inp, p[wi], p[bi])
+        return layer_norm_residual(inp, p[wi], p[bi], targets[wi], targets[bi])
 
     def lin_res(inp, res, wi, bi):  # res + inp W^T + b, the residual add folded into the GEMM
         if targets is None:
@@ -309,16 +366,16 @@ def _block(x, p, heads, targets=None):
 
     # pieces: 0/1 ln_1, 2-4 q/k/v weight blocks, 5-7 their biases, 8/9 attn.proj, 10/11 ln_2,
     # 12/13 mlp.fc, 14/15 mlp.proj (layer_pieces order)
-    h = ln(x, 0, 1)
+    h, x = ln(x, 0, 1)
     if targets is None:
-        qkv = [F.linear(h, p[wi], p[bi]) for wi, bi in _LINEARS[:3]]
+        qkv = _qkv_proj(h, p[2], p[3], p[4], p[5], p[6], p[7])
     else:
         qkv = _OverwriteQKV.apply(h, p[2], p[3], p[4], p[5], p[6], p[7],
                                   targets[2], targets[3], targets[4], targets[5], targets[6], targets[7])
     q, k, v = (t.view(B, T, heads, hd).transpose(1, 2) for t in qkv)
     a = F.scaled_dot_product_attention(q, k, v, is_causal=True)
     x = lin_res(a.transpose(1, 2).reshape(B, T, H), x, *_LINEARS[3])
-    h = ln(x, 10, 11)
+    h, x = ln(x, 10, 11)
     fi, bi = _LINEARS[4]
     a = fc_gelu(h, p[fi], p[bi]) if targets is None else fc_gelu(h, p[fi], p[bi], targets[fi], targets[bi])
     return lin_res(a, x, *_LINEARS[5])

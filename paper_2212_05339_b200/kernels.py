@@ -358,17 +358,24 @@ def layer_norm_fwd(x: torch.Tensor, w: torch.Tensor, b: torch.Tensor, eps: float
 
 
 def layer_norm_bwd_dx(x: torch.Tensor, dy: torch.Tensor, w: torch.Tensor, mean: torch.Tensor, rstd: torch.Tensor,
-                      stream=None) -> torch.Tensor:
-    """K11: the LayerNorm input gradient (the weight/bias gradients are K9's)."""
+                      dres: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """K11: the LayerNorm input gradient (the weight/bias gradients are K9's);
+    with `dres` (the gradient reaching x through a residual branch) it is
+    added in the same pass, bit-identical to a separate add."""
     lib = _lib.load()
     for t, n in ((x, "x"), (dy, "dy"), (w, "w"), (mean, "mean"), (rstd, "rstd")):
         _cuda(t, n)
     H = x.shape[-1]
     if dy.shape != x.shape or dy.dtype != x.dtype or mean.numel() * H != x.numel():
         raise ValidationError("layer_norm_bwd_dx: dy must match x; mean/rstd one per row")
+    if dres is not None:
+        _cuda(dres, "dres")
+        if dres.shape != x.shape or dres.dtype != x.dtype or not dres.is_contiguous():
+            raise ValidationError("layer_norm_bwd_dx: dres must be a contiguous tensor like x")
     dx = torch.empty_like(x)
-    rc = lib.elx_layer_norm_bwd_dx(dx.data_ptr(), x.data_ptr(), dy.data_ptr(), w.data_ptr(), mean.data_ptr(),
-                                   rstd.data_ptr(), elx_dtype(x.dtype), x.numel() // H, H, _stream(stream))
+    rc = lib.elx_layer_norm_bwd_dx_res(dx.data_ptr(), x.data_ptr(), dy.data_ptr(), w.data_ptr(), mean.data_ptr(),
+                                       rstd.data_ptr(), None if dres is None else dres.data_ptr(),
+                                       elx_dtype(x.dtype), x.numel() // H, H, _stream(stream))
     _lib.check(rc, "elx_layer_norm_bwd_dx")
     return dx
 

@@ -750,3 +750,18 @@ def test_gelu_bwd_colsum_equals_unfused(cuda, rows, cols):
     db2 = torch.empty_like(db)
     kernels.colsum(dx2, db2)
     assert torch.equal(dx, dx2) and torch.equal(db, db2)
+
+
+@pytest.mark.parametrize("rows,cols", [(8192, 2048), (33, 264), (5, 6144)])
+def test_layer_norm_bwd_dx_residual_equals_separate_add(cuda, rows, cols):
+    """K11 with the residual gradient folded in == K11 then a bf16 add."""
+    g = torch.Generator(device=cuda).manual_seed(rows)
+    x = torch.randn(rows, cols, device=cuda, generator=g).to(torch.bfloat16)
+    dy = torch.randn(rows, cols, device=cuda, generator=g).to(torch.bfloat16)
+    dres = torch.randn(rows, cols, device=cuda, generator=g).to(torch.bfloat16)
+    w = (1 + 0.1 * torch.randn(cols, device=cuda, generator=g)).to(torch.bfloat16)
+    b = torch.zeros(cols, device=cuda, dtype=torch.bfloat16)
+    _, mean, rstd = kernels.layer_norm_fwd(x, w, b)
+    fused = kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd, dres=dres)
+    sep = kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd) + dres
+    assert torch.equal(fused, sep)
