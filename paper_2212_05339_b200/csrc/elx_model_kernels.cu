@@ -351,7 +351,7 @@ __device__ __forceinline__ void add_res8(T16* h, uint4 q) {
 
 // dx = rstd * (g - mean(g) - xhat * mean(g * xhat)), g = dy * w, xhat = (x - mean) * rstd
 // (+ dres, the gradient reaching x through the residual branch, when given)
-template <typename T16, int kV>
+template <typename T16, int kV, bool kRes>
 __global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __restrict__ x, const T16* __restrict__ dy,
                                                                    const T16* __restrict__ w,
                                                                    const float* __restrict__ mean,
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __
   const uint4* dr = reinterpret_cast<const uint4*>(dy + row * cols);
   const uint4* wv = reinterpret_cast<const uint4*>(w);
   const float mu = mean[row], rs = rstd[row];
-  uint4 qx[kV], qd[kV];
+  uint4 qx[kV], qd[kV], qr[kRes ? kV : 1];
   float c1 = 0.f, c2 = 0.f;
 #pragma unroll
   for (int j = 0; j < kV; ++j) {
@@ -373,6 +373,8 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __
     if (v < nvec) {
       qx[j] = __ldcs(xr + v);
       qd[j] = __ldcs(dr + v);
+      // the residual gradient is loaded with x and dy: in flight during the row reductions
+      if constexpr (kRes) qr[j] = __ldcs(reinterpret_cast<const uint4*>(dres + row * cols) + v);
       float fx[8], fd[8], fw[8];
       unpack8<T16>(qx[j], fx);
       unpack8<T16>(qd[j], fd);
@@ -405,7 +407,7 @@ __global__ void __launch_bounds__(kRowWarps * 32) ln_bwd_dx_kernel(const T16* __
         const float xh = (fx[e] - mu) * rs;
         r.h[e] = from_f<T16>(rs * (fd[e] * fw[e] - c2 - xh * c1));
       }
-      if (dres) add_res8<T16>(r.h, __ldcs(reinterpret_cast<const uint4*>(dres + row * cols) + v));
+      if constexpr (kRes) add_res8<T16>(r.h, qr[j]);
       o[v] = r.u;
     }
   }
@@ -856,9 +858,14 @@ int elx_layer_norm_bwd_dx_res(void* dx, const void* x, const void* dy, const voi
                                                            static_cast<const T*>(w), mean, rstd, static_cast<T*>(dx),
                                                            static_cast<const T*>(dres), rows, c);
     };
-    pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2>); }, [&] { k(ln_bwd_dx_kernel<T, 4>); },
-                    [&] { k(ln_bwd_dx_kernel<T, 8>); }, [&] { k(ln_bwd_dx_kernel<T, 12>); },
-                    [&] { k(ln_bwd_dx_kernel<T, 16>); });
+    if (dres)
+      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, true>); }, [&] { k(ln_bwd_dx_kernel<T, 4, true>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 8, true>); }, [&] { k(ln_bwd_dx_kernel<T, 12, true>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 16, true>); });
+    else
+      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, false>); }, [&] { k(ln_bwd_dx_kernel<T, 4, false>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 8, false>); }, [&] { k(ln_bwd_dx_kernel<T, 12, false>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 16, false>); });
   } else {
     using T = __half;
     auto k = [&](auto kern) {
@@ -866,9 +873,14 @@ int elx_layer_norm_bwd_dx_res(void* dx, const void* x, const void* dy, const voi
                                                            static_cast<const T*>(w), mean, rstd, static_cast<T*>(dx),
                                                            static_cast<const T*>(dres), rows, c);
     };
-    pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2>); }, [&] { k(ln_bwd_dx_kernel<T, 4>); },
-                    [&] { k(ln_bwd_dx_kernel<T, 8>); }, [&] { k(ln_bwd_dx_kernel<T, 12>); },
-                    [&] { k(ln_bwd_dx_kernel<T, 16>); });
+    if (dres)
+      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, true>); }, [&] { k(ln_bwd_dx_kernel<T, 4, true>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 8, true>); }, [&] { k(ln_bwd_dx_kernel<T, 12, true>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 16, true>); });
+    else
+      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, false>); }, [&] { k(ln_bwd_dx_kernel<T, 4, false>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 8, false>); }, [&] { k(ln_bwd_dx_kernel<T, 12, false>); },
+                      [&] { k(ln_bwd_dx_kernel<T, 16, false>); });
   }
   return check("elx_layer_norm_bwd_dx");
 }

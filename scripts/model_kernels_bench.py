@@ -52,6 +52,11 @@ y, mean, rstd = kernels.layer_norm_fwd(x, w, b)
 E = R * H * 2
 report("K10 layer_norm_fwd 8192x2048", timed(lambda: kernels.layer_norm_fwd(x, w, b)), 2 * E + 8 * R)
 report("K11 layer_norm_bwd_dx 8192x2048", timed(lambda: kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd)), 3 * E + 8 * R)
+dres = torch.randn(R, H, device=dev, generator=g).to(bf)
+report("K11 layer_norm_bwd_dx + dres 8192x2048 (fused)",
+       timed(lambda: kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd, dres=dres)), 4 * E + 8 * R)
+report("K11 layer_norm_bwd_dx then torch add 8192x2048",
+       timed(lambda: kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd) + dres), 4 * E + 8 * R)
 dg, db = torch.empty(H, device=dev, dtype=bf), torch.empty(H, device=dev, dtype=bf)
 report("K9 ln_param_grad 8192x2048", timed(lambda: kernels.ln_param_grad(x, dy, mean.view(-1), rstd.view(-1), dg, db)),
        2 * E + 8 * R)
