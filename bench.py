@@ -275,7 +275,8 @@ def run_ours(args):
     plan_text = plan_path.read_text()
     from paper_2212_05339_b200.transport import make_transport
     model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234, transport=make_transport(world, args.transport),
-                       overlap_update=args.overlap, cpu_update=args.cpu_update)
+                       overlap_update=args.overlap, cpu_update=args.cpu_update,
+                       recompute={"auto": "auto", "on": True, "off": False}[args.recompute])
     B, T = cfg.batch, cfg.seq_len
     gen = torch.Generator(device=dev).manual_seed(1234 + rank)
     ids = torch.randint(0, cfg.vocab, (B, T + 1), generator=gen, device=dev)
@@ -442,9 +443,18 @@ def run_ours(args):
             "n_chunks": model.layout.n_chunks, "n_block": model.manager.plan.n_block,
             "l2": "working set (>20 GB of chunk/optimizer state per step) far exceeds the 126 MB L2; no flush needed",
             "cuda_graph": use_graph,
+            "activation_checkpointing": not model.keep_graph,
+            "recompute_note": ("off: every chunk stays resident forward->backward and the activations fit, so "
+                               "each node's forward graph is kept instead of recomputed — results bit-identical "
+                               "to checkpointing (tests/test_runtime_gpu.py::test_keep_graph_step_equals_"
+                               "recompute); --recompute on for the reference's per-layer checkpointing"
+                               if model.keep_graph else
+                               "on: per-layer activation checkpointing (PAPER.md:145-150)"),
             **({"oversubscribed": oversub} if oversub else {}),
         },
         "tflops_per_gpu": flops / (ms / args.steps * 1e-3) / 1e12,
+        "tflops_note": "executed model FLOPs: 6·M·D, plus 2·M·D for the recompute when checkpointing "
+                       "(PAPER.md:356 counts 8·M·D)",
         "final_loss": loss,
         "kernels": {
             "chunk_adam": {"ms_per_launch": adam_avg, "valid_elements": adam_elems, "hbm_gbs": adam_gbs,
@@ -552,6 +562,10 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-update", choices=["split", "host", "stream"], default="split",
                     help="CPU-home chunk update: host threads, GPU-streamed, or split by measured rate")
+    ap.add_argument("--recompute", choices=["auto", "on", "off"], default="auto",
+                    help="activation checkpointing: on = recompute each node in the backward (the reference's "
+                         "design), off = keep the forward graphs, auto = off when every chunk stays resident "
+                         "and the activations fit in HBM")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
                     help="every chunk GPU-home, world 1 or --transport ipc: capture the whole step as one CUDA graph")
     ap.add_argument("--overlap", action="store_true",

@@ -393,7 +393,7 @@ class ElixirGPT2:
                  lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, weight_decay: float = 0.01,
                  max_norm: float | None = 1.0, loss_scale: float | None = None, transport=None,
                  prefetch: bool = True, cpu_threads: int | None = None, init: dict | None = None,
-                 overlap_update: bool = False, cpu_update: str = "split"):
+                 overlap_update: bool = False, cpu_update: str = "split", recompute=True):
         import torch.distributed as dist
 
         self.cfg = cfg
@@ -437,6 +437,32 @@ class ElixirGPT2:
                 self.node_pieces.append([(pid, 0, self.shapes[pid]) for pid in pids])
         self.wte = self.manager.shared["wte"]
         self.last_loss = None
+        self.keep_graph = self._resolve_recompute(recompute)
+
+    def _resolve_recompute(self, recompute) -> bool:
+        """Whether the forward keeps each node's autograd graph (no recompute
+        in the backward) instead of activation checkpointing (PAPER.md:145-150,
+        the reference's design and the default). Keeping it is valid only when
+        no chunk can leave its block between a node's forward and backward —
+        every rCache block stays put (n_block >= n_chunks: the schedule never
+        evicts; at world 1 with every chunk GPU-home the chunks are used in
+        place) — because the saved tensors are views of the chunk storage;
+        "auto" also requires the activations (~17 B*T*H elements per layer)
+        to fit in half the HBM left after the chunk store."""
+        if recompute is True:
+            return False
+        m = self.manager
+        resident = (m.world == 1 and not m.cpu_ids) or m.plan.n_block >= m.n_chunks  # world 1 GPU-home: in place
+        if recompute is False:
+            if not resident:
+                raise ValidationError("recompute=False needs every chunk resident (n_block >= n_chunks)")
+            return True
+        if recompute != "auto":
+            raise ValidationError("recompute must be True, False or 'auto'")
+        cfg = self.cfg
+        act = cfg.layers * 17 * cfg.batch * cfg.seq_len * cfg.hidden * self.manager.p16.element_size()
+        free, _ = torch.cuda.mem_get_info(self.device)
+        return resident and act < 0.5 * free
 
     # -------------------------------------------------------------- nodes
     def _run_node(self, i: int, x, tokens, targets, params, grad_targets=None):
@@ -490,14 +516,25 @@ class ElixirGPT2:
         fx.begin_step(after=self.optimizer.done_event)
         self.optimizer.wait_gpu("wte", torch.cuda.current_stream(self.device))
         acts = []
+        saved = [None] * K
         x = None
-        with torch.no_grad():
-            for i in range(K):
-                fx.enter(i)
-                acts.append(x)
-                if i < K - 1:  # the head's loss comes from its backward recompute
+        for i in range(K):
+            fx.enter(i)
+            acts.append(x)
+            if i < K - 1 and self.keep_graph:  # keep the node's graph for the backward (no recompute)
+                raw = self._params_of(i)
+                params = [p.detach().requires_grad_(True) for p in raw]
+                layer = 0 < i < K - 2
+                xin = None if i == 0 else x.detach().requires_grad_(True)
+                with torch.enable_grad():
+                    out = self._run_node(i, xin, tokens, targets, params,
+                                         grad_targets=[_alias(t) for t in raw] if layer else None)
+                saved[i] = (out, xin, params)
+                x = out.detach()
+            elif i < K - 1:  # the head's loss comes from its backward recompute
+                with torch.no_grad():
                     x = self._run_node(i, x, tokens, targets, self._params_of(i))
-                fx.after_compute(i)
+            fx.after_compute(i)
         loss = None
         grad = torch.full((), self.scaler.scale, dtype=torch.float32, device=self.device)
         wte_grad_set = False
@@ -505,14 +542,19 @@ class ElixirGPT2:
             i = K - 1 - j
             pos = K + j
             fx.enter(pos)
-            raw = self._params_of(i)
-            params = [p.detach().requires_grad_(True) for p in raw]
             layer = 0 < i < K - 2
+            if saved[i] is not None:
+                out, xin, params = saved[i]
+                saved[i] = None
+            else:
+                raw = self._params_of(i)
+                params = [p.detach().requires_grad_(True) for p in raw]
+                with torch.enable_grad():
+                    xin = None if i == 0 else acts[i].detach().requires_grad_(True)
+                    # layers: linear gradients land in their chunk slots (raw views) directly
+                    out = self._run_node(i, xin, tokens, targets, params,
+                                         grad_targets=[_alias(t) for t in raw] if layer else None)
             with torch.enable_grad():
-                xin = None if i == 0 else acts[i].detach().requires_grad_(True)
-                # layers: linear gradients land in their chunk slots (raw views) directly
-                out = self._run_node(i, xin, tokens, targets, params,
-                                     grad_targets=[_alias(t) for t in raw] if layer else None)
                 inputs = ([xin] if i > 0 else []) + params
                 grads = torch.autograd.grad(out, inputs, grad_outputs=grad, allow_unused=layer)
             if i == K - 1:
@@ -622,5 +664,7 @@ class ElixirGPT2:
         return self.profile.total_elements
 
     def flops_per_step(self) -> float:
-        """8·M·D (cost_model.py:170-174) for this rank's batch."""
-        return 8.0 * self.n_params * self.cfg.batch * self.cfg.seq_len
+        """Executed model FLOPs for this rank's batch: 8·M·D with per-layer
+        recompute (cost_model.py:170-174), 6·M·D when the
+        forward graphs are kept."""
+        return (6.0 if self.keep_graph else 8.0) * self.n_params * self.cfg.batch * self.cfg.seq_len

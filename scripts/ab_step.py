@@ -4,7 +4,7 @@ alternately (ABAB...) and timed with CUDA events, so clock / power-cap drift
 hits every variant alike (bench.py-to-bench.py differences on this
 power-capped box are +-3%, larger than the effects measured here).
 
-    python scripts/ab_step.py [model] [rounds]
+    python scripts/ab_step.py [model] [rounds] [--recompute]
 
 Variants (monkeypatched, the product keeps the first):
   new         — as shipped
@@ -24,8 +24,9 @@ ROOT = Path(__file__).resolve().parents[1]
 sys.path.insert(0, str(ROOT))
 from paper_2212_05339_b200 import gpt2, kernels  # noqa: E402
 
-model_name = sys.argv[1] if len(sys.argv) > 1 else "gpt2-1.3b"
-rounds = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+model_name = args[0] if args else "gpt2-1.3b"
+rounds = int(args[1]) if len(args) > 1 else 8
 dev = torch.device("cuda:0")
 cfg = gpt2.PRESETS[model_name]
 plan = (ROOT / "plans" / f"{model_name}_n1.json").read_text()
@@ -52,6 +53,8 @@ def _unfused_gc(x, dy, db):
 VARIANTS = {"new": {}, "sep_qkv": {(gpt2, "_qkv_proj"): _sep_qkv},
             "unfused_res": {(gpt2, "layer_norm_residual"): _unfused_res},
             "unfused_gc": {(gpt2.kernels, "gelu_bwd_colsum"): _unfused_gc}}
+if "--recompute" in sys.argv:  # A/B activation checkpointing vs keeping the forward graphs
+    VARIANTS = {"new": {}, "no_recompute": {(model, "keep_graph"): True}}
 graphs = {}
 for name, patches in VARIANTS.items():
     saved = {k: getattr(*k) for k in patches}

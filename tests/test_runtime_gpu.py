@@ -206,6 +206,34 @@ def test_cuda_graph_step_equals_eager(cuda, plan_name):
     assert eager.optimizer.step_count == graph.optimizer.step_count == 8
 
 
+@pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min"])
+def test_keep_graph_step_equals_recompute(cuda, plan_name):
+    """recompute=False (the forward keeps each node's autograd graph) trains
+    bit-identically to activation checkpointing: same losses, same fp32
+    masters — the recompute reproduces the forward exactly, so dropping it
+    changes no result, only the work."""
+    plan = dict(_plans(CFG))[plan_name]
+    init = gpt2.init_params(CFG, cuda, seed=6)
+    batches = [_batch(CFG, cuda, 200 + s) for s in range(3)]
+    ac = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
+    kg = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, recompute=False, **HP)
+    assert kg.keep_graph and not ac.keep_graph
+    assert [ac.train_step(*b).item() for b in batches] == [kg.train_step(*b).item() for b in batches]
+    a, b = _masters(ac), _masters(kg)
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    kg.capture(*batches[0], warmup=1)  # and under graph capture
+    kg.graph_step(*batches[1])
+
+
+def test_keep_graph_refused_when_chunks_can_be_evicted(cuda):
+    from paper_2212_05339_b200.errors import ValidationError
+    plan = dict(_plans(CFG))["offload-all"]
+    with pytest.raises(ValidationError):
+        ElixirGPT2(CFG, plan, device=cuda, recompute=False, **HP)
+    assert not ElixirGPT2(CFG, plan, device=cuda, recompute="auto", **HP).keep_graph
+
+
 def test_cuda_graph_refuses_offloaded_plans(cuda):
     from paper_2212_05339_b200.errors import ValidationError
     plan = dict(_plans(CFG))["offload-half"]
