@@ -9,6 +9,7 @@ validates sizes and alignment and returns typed errors (_lib.check).
 from __future__ import annotations
 
 import ctypes
+import threading
 from typing import Sequence
 
 import torch
@@ -468,15 +469,19 @@ _LT_WS_BYTES = 32 * 2 ** 20
 
 
 def _lt_workspace(device: torch.device) -> int:
-    """One cuBLASLt workspace per device. The model issues its GEMMs on one
-    stream at a time (eager steps and graph replays are ordered on the current
-    stream), so calls never overlap; allocated on first use, which capture()
-    guarantees happens before a graph capture (its warm-up steps run eagerly),
-    so the captured pointer is ordinary device memory, not the graph's pool."""
-    ws = _LT_WS.get(device.index)
+    """One cuBLASLt workspace per (device, host thread). A thread issues its
+    GEMMs on one stream at a time (eager steps and graph replays are ordered
+    on the current stream), so its calls never overlap; ranks run as threads
+    on one GPU (tests/_refstep.py, scripts/emulate_ranks.py) get their own,
+    since split-K scratch shared between concurrent streams would race.
+    Allocated on first use, which capture() guarantees happens before a graph
+    capture (its warm-up steps run eagerly on the same thread), so the
+    captured pointer is ordinary device memory, not the graph's pool."""
+    key = (device.index, threading.get_ident())
+    ws = _LT_WS.get(key)
     if ws is None:
         ws = torch.empty(_LT_WS_BYTES, dtype=torch.uint8, device=device)
-        _LT_WS[device.index] = ws
+        _LT_WS[key] = ws
     return ws.data_ptr()
 
 

@@ -1,6 +1,6 @@
 """The N > 1 runtime on a full-size plan, with N rank-threads sharing ONE GPU.
 
-    python scripts/emulate_ranks.py [model] [world] [plan file] [--p2p] > gpurun_out/emulate.json
+    python scripts/emulate_ranks.py [model] [world] [plan file] [--p2p] [--no-recompute] > gpurun_out/emulate.json
 
 Each rank builds its chunk store from the reference planner's plan for N
 GPUs (plans/<model>_n<N>.json, e.g. BASELINE config 2: GPT-2 1.3B at 8
@@ -30,6 +30,7 @@ model_name = args[0] if args else "gpt2-1.3b"
 world = int(args[1]) if len(args) > 1 else 8
 plan_file = args[2] if len(args) > 2 else f"{model_name}_n{world}.json"
 p2p = "--p2p" in sys.argv
+keep = "--no-recompute" in sys.argv  # the bench's mode when every chunk stays resident
 base = PRESETS[model_name]
 cfg = GPT2Config(base.hidden, base.layers, base.heads, base.vocab, base.seq_len, batch=1)
 plan_text = (ROOT / "plans" / plan_file).read_text()
@@ -38,7 +39,8 @@ steps = 2
 
 
 def rank_fn(r, transport):
-    model = ElixirGPT2(cfg, plan_text, device=dev, transport=transport, seed=1234)
+    model = ElixirGPT2(cfg, plan_text, device=dev, transport=transport, seed=1234,
+                       recompute=False if keep else True)
     g = torch.Generator(device=dev).manual_seed(1234 + r)
     ids = torch.randint(0, cfg.vocab, (cfg.batch, cfg.seq_len + 1), generator=g, device=dev)
     losses, t0 = [], time.perf_counter()
@@ -64,6 +66,7 @@ keys = ("gather_ops", "replaced_ops", "reduce_ops", "c2g_units", "g2c_units")
 ok = all(rr["counters"][k] == sim[k] for rr in res for k in keys)
 finite = all(all(x == x and abs(x) < 1e6 for x in rr["losses"]) for rr in res)
 print(json.dumps({"model": model_name, "world": world, "plan": plan_file, "transport": "p2p" if p2p else "exchange",
+                  "recompute": not keep,
                   "per_rank_batch": cfg.batch, "steps": steps, "wall_s": round(wall, 2),
                   "counters_equal_simulate": ok, "losses_finite": finite, "simulate": {k: sim[k] for k in keys},
                   "ranks": res}, indent=1, default=str))
