@@ -35,6 +35,8 @@ base = PRESETS[model_name]
 cfg = GPT2Config(base.hidden, base.layers, base.heads, base.vocab, base.seq_len, batch=1)
 plan_text = (ROOT / "plans" / plan_file).read_text()
 dev = torch.device("cuda:0")
+if "--flash" in sys.argv:  # SDPA's flash backend instead of cuDNN (multi-thread determinism probe)
+    torch.backends.cuda.enable_cudnn_sdp(False)
 steps = 2
 
 
