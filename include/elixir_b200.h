@@ -375,6 +375,14 @@ enum {
 int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
                   const void* a, int64_t lda, const void* b, int64_t ldb, const void* c, void* d, int64_t ldd,
                   void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream);
+/* elx_lt_matmul with the algorithm chosen by index into cuBLASLt's heuristic
+ * candidate list (0..15; -1 = the first, or autotuned with ELX_LT_AUTOTUNE=1):
+ * a per-shape table of indices tuned once on the B200 gives every process the
+ * same algorithm. An index past the list fails with ELX_ERR_VALIDATION. */
+int elx_lt_matmul_ex(int32_t epilogue, int32_t dtype, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
+                     const void* a, int64_t lda, const void* b, int64_t ldb, const void* c, void* d, int64_t ldd,
+                     void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes,
+                     int32_t algo_index, void* stream);
 
 /* Host Adam for CPU-home optimizer shards (update rate v_c,
  * rcache_sim.py:176-184): same arithmetic as elx_adam, OpenMP over

@@ -108,6 +108,8 @@ _SIGNATURES = {
     "elx_gelu_bwd_colsum": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_i64, c_vp]),
     "elx_lt_matmul": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                                      c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
+    "elx_lt_matmul_ex": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
+                                        c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_i32, c_vp]),
     "elx_copy_h2d": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_copy_d2h": (ctypes.c_int, [c_vp, c_vp, c_i64, c_vp, c_vp]),
     "elx_cpu_adam": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i64, c_vp, c_i32]),

@@ -16,6 +16,7 @@
 #include <cublasLt.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -30,6 +31,8 @@ struct LtPlan {
   cublasLtMatmulAlgo_t algo{};
   size_t ws = 0;
 };
+
+constexpr int kMaxAlgos = 16;
 
 using LtKey = std::tuple<int, int, int, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, int, int64_t>;
 
@@ -55,6 +58,66 @@ cublasLtEpilogue_t to_epilogue(int e) {
 bool has_aux(int e) { return e == ELX_EPI_GELU_AUX_BIAS || e == ELX_EPI_DGELU_BGRAD; }
 bool has_bias(int e) { return e != ELX_EPI_NONE; }
 
+// Algorithm choice. algo_index >= 0 takes the heuristic's algo_index-th
+// candidate (a deterministic list for a given cuBLASLt, GPU and shape): the
+// caller's per-shape table (plans/lt_algos_b200.json, made by
+// scripts/tune_lt.py on the B200) picks it, reproducibly in every process.
+// algo_index = -1: the first candidate, or with ELX_LT_AUTOTUNE=1 the fastest
+// of the top 16 timed on the caller's operands when the shape is first planned.
+// Autotuning (ELX_LT_AUTOTUNE=1): when a shape is first planned, time the
+// heuristic's top candidates on the caller's operands and keep the fastest.
+// Off by default: the choice depends on timing noise, so two processes could
+// pick different algorithms (different fp32 accumulation orders) for one
+// shape; the default (the heuristic's first choice) is reproducible. Skipped
+// while the stream is being captured and when C aliases D (a candidate run
+// would then accumulate into the result).
+bool autotune_allowed(const void* c, const void* d, void* stream) {
+  const char* e = getenv("ELX_LT_AUTOTUNE");
+  if (!e || e[0] != '1') return false;
+  if (c && c == d) return false;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing((cudaStream_t)stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+  return true;
+}
+
+int pick_fastest(LtPlan& p, const cublasLtMatmulHeuristicResult_t* cand, int found, const void* a, const void* b,
+                 const void* c, void* d, void* bias, void* aux, int epilogue, void* workspace, int64_t wsb,
+                 cudaStream_t st) {
+  if (has_bias(epilogue)) cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_BIAS_POINTER, &bias, sizeof(bias));
+  if (has_aux(epilogue)) cublasLtMatmulDescSetAttribute(p.op, CUBLASLT_MATMUL_DESC_EPILOGUE_AUX_POINTER, &aux, sizeof(aux));
+  const float alpha = 1.f, beta = c ? 1.f : 0.f;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  int best = -1;
+  float best_ms = 0.f;
+  for (int i = 0; i < found; ++i) {
+    if (cand[i].state != CUBLAS_STATUS_SUCCESS || cand[i].workspaceSize > (size_t)wsb) continue;
+    bool ok = true;
+    for (int w = 0; w < 2 && ok; ++w)
+      ok = cublasLtMatmul(g_handle, p.op, &alpha, a, p.a, b, p.b, &beta, c ? c : d, p.d, d, p.d, &cand[i].algo,
+                          workspace, (size_t)wsb, st) == CUBLAS_STATUS_SUCCESS;
+    if (!ok) continue;
+    cudaEventRecord(e0, st);
+    constexpr int kReps = 5;
+    for (int r = 0; r < kReps; ++r)
+      cublasLtMatmul(g_handle, p.op, &alpha, a, p.a, b, p.b, &beta, c ? c : d, p.d, d, p.d, &cand[i].algo, workspace,
+                     (size_t)wsb, st);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (best < 0 || ms < best_ms) {
+      best = i;
+      best_ms = ms;
+    }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaGetLastError();
+  return best;
+}
+
 }  // namespace
 
 extern "C" {
@@ -62,7 +125,16 @@ extern "C" {
 int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
                   const void* a, int64_t lda, const void* b, int64_t ldb, const void* c, void* d, int64_t ldd,
                   void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes, void* stream) {
+  return elx_lt_matmul_ex(epilogue, dtype, transa, transb, m, n, k, a, lda, b, ldb, c, d, ldd, bias, aux, ldaux,
+                          workspace, workspace_bytes, -1, stream);
+}
+
+int elx_lt_matmul_ex(int32_t epilogue, int32_t dtype, int32_t transa, int32_t transb, int64_t m, int64_t n, int64_t k,
+                     const void* a, int64_t lda, const void* b, int64_t ldb, const void* c, void* d, int64_t ldd,
+                     void* bias, void* aux, int64_t ldaux, void* workspace, int64_t workspace_bytes,
+                     int32_t algo_index, void* stream) {
   elx::clear_error();
+  if (algo_index < -1 || algo_index >= kMaxAlgos) return elx::fail(ELX_ERR_VALIDATION, "algo_index out of range");
   if (epilogue < ELX_EPI_NONE || epilogue > ELX_EPI_BGRADB) return elx::fail(ELX_ERR_VALIDATION, "bad epilogue");
   if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "lt matmul dtype must be bf16/f16");
   if (m < 1 || n < 1 || k < 1) return elx::fail(ELX_ERR_VALIDATION, "need m, n, k >= 1");
@@ -76,7 +148,7 @@ int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t trans
   cublasStatus_t st;
   if (!g_handle && (st = cublasLtCreate(&g_handle)) != CUBLAS_STATUS_SUCCESS) return lt_fail("cublasLtCreate", st);
   const LtKey key{epilogue, transa, transb, m, n, k, lda, ldb, ldd, has_aux(epilogue) ? ldaux : 0,
-                  dtype * 2 + (c ? 1 : 0), workspace_bytes};
+                  (dtype * 2 + (c ? 1 : 0)) * 64 + (algo_index + 1), workspace_bytes};
   auto it = g_plans.find(key);
   if (it == g_plans.end()) {
     LtPlan p;
@@ -108,10 +180,25 @@ int elx_lt_matmul(int32_t epilogue, int32_t dtype, int32_t transa, int32_t trans
       const uint32_t none = CUBLASLT_REDUCTION_SCHEME_NONE;  // deterministic bias gradient
       cublasLtMatmulPreferenceSetAttribute(pref, CUBLASLT_MATMUL_PREF_REDUCTION_SCHEME_MASK, &none, sizeof(none));
     }
-    cublasLtMatmulHeuristicResult_t res{};
+    cublasLtMatmulHeuristicResult_t cand[kMaxAlgos]{};
     int found = 0;
-    st = cublasLtMatmulAlgoGetHeuristic(g_handle, p.op, p.a, p.b, p.d, p.d, pref, 1, &res, &found);
+    const bool tune = algo_index < 0 && autotune_allowed(c, d, stream);
+    const int want = algo_index >= 0 ? algo_index + 1 : (tune ? kMaxAlgos : 1);
+    st = cublasLtMatmulAlgoGetHeuristic(g_handle, p.op, p.a, p.b, p.d, p.d, pref, want, cand, &found);
     cublasLtMatmulPreferenceDestroy(pref);
+    if (st == CUBLAS_STATUS_SUCCESS && algo_index >= found) {
+      cublasLtMatrixLayoutDestroy(p.a);
+      cublasLtMatrixLayoutDestroy(p.b);
+      cublasLtMatrixLayoutDestroy(p.d);
+      cublasLtMatmulDescDestroy(p.op);
+      return elx::fail(ELX_ERR_VALIDATION, "algo_index %d: the heuristic offers %d candidates", algo_index, found);
+    }
+    cublasLtMatmulHeuristicResult_t res = cand[algo_index >= 0 ? algo_index : 0];
+    if (tune && st == CUBLAS_STATUS_SUCCESS && found > 1) {
+      const int best = pick_fastest(p, cand, found, a, b, c, d, bias, aux, epilogue, workspace, workspace_bytes,
+                                    (cudaStream_t)stream);
+      if (best >= 0) res = cand[best];
+    }
     if (st != CUBLAS_STATUS_SUCCESS || found < 1) {
       cublasLtMatrixLayoutDestroy(p.a);
       cublasLtMatrixLayoutDestroy(p.b);

@@ -132,8 +132,9 @@ class _OverwriteLinear(torch.autograd.Function):
         x, w = ctx.saved_tensors
         w_t, b_t = ctx.targets
         gy2 = gy.reshape(-1, gy.shape[-1])
-        gx = torch.mm(gy2, w).view(*gy.shape[:-1], w.shape[1]) if ctx.needs_input_grad[0] else None
-        torch.mm(gy2.t(), x.reshape(-1, x.shape[-1]), out=w_t)
+        gy2 = gy2.contiguous()
+        gx = kernels.gemm(gy2, w).view(*gy.shape[:-1], w.shape[1]) if ctx.needs_input_grad[0] else None
+        kernels.gemm(gy2, x.reshape(-1, x.shape[-1]).contiguous(), ta=True, out=w_t)
         kernels.colsum(gy2, b_t)
         return gx, None, None, None, None
 
@@ -154,7 +155,8 @@ def _qkv_proj(h, wq, wk, wv, bq, bk, bv):
     if not packed:
         return F.linear(h, wq, bq), F.linear(h, wk, bk), F.linear(h, wv, bv)
     n = wq.shape[0] + wk.shape[0] + wv.shape[0]
-    y = F.linear(h, wq.as_strided((n, H), (H, 1)), bq.as_strided((n,), (1,)))
+    y = kernels.gemm(h.reshape(-1, H).contiguous(), wq.as_strided((n, H), (H, 1)), tb=True,
+                     bias=bq.as_strided((n,), (1,))).view(*h.shape[:-1], n)
     a, b = wq.shape[0], wq.shape[0] + wk.shape[0]
     return y[..., :a], y[..., a:b], y[..., b:]
 
@@ -178,16 +180,16 @@ class _OverwriteQKV(torch.autograd.Function):
         h, wq, wk, wv = ctx.saved_tensors
         tq, tk, tv, sq, sk, sv = ctx.targets
         H = h.shape[-1]
-        gs = [g.reshape(-1, g.shape[-1]) for g in (gq, gk, gv)]
-        h2 = h.reshape(-1, H)
+        gs = [g.reshape(-1, g.shape[-1]).contiguous() for g in (gq, gk, gv)]
+        h2 = h.reshape(-1, H).contiguous()
         gh = None
         if ctx.needs_input_grad[0]:
-            gh = torch.mm(gs[0], wq)
-            gh.addmm_(gs[1], wk)
-            gh.addmm_(gs[2], wv)
+            gh = kernels.gemm(gs[0], wq)
+            kernels.gemm(gs[1], wk, out=gh, c=gh)  # accumulated in the GEMM (beta = 1)
+            kernels.gemm(gs[2], wv, out=gh, c=gh)
             gh = gh.view(h.shape)
         for g, t in zip(gs, (tq, tk, tv)):
-            torch.mm(g.t(), h2, out=t)
+            kernels.gemm(g, h2, ta=True, out=t)
         kernels.colsum_batched(gs, (sq, sk, sv))
         return (gh,) + (None,) * 12
 
@@ -212,8 +214,9 @@ class _OverwriteLinearResidual(torch.autograd.Function):
         x2, w = ctx.saved_tensors
         w_t, b_t = ctx.targets
         gy2 = gy.reshape(-1, gy.shape[-1])
-        gx = torch.mm(gy2, w).view(ctx.xshape) if ctx.needs_input_grad[0] else None
-        torch.mm(gy2.t(), x2, out=w_t)
+        gy2 = gy2.contiguous()
+        gx = kernels.gemm(gy2, w).view(ctx.xshape) if ctx.needs_input_grad[0] else None
+        kernels.gemm(gy2, x2, ta=True, out=w_t)
         kernels.colsum(gy2, b_t)
         return gx, None, None, gy, None, None
 
@@ -314,8 +317,8 @@ class _OverwriteFcGelu(torch.autograd.Function):
         x2, w, pre = ctx.saved_tensors
         w_t, b_t = ctx.targets
         d = kernels.gelu_bwd_colsum(pre, gy.reshape(-1, gy.shape[-1]).contiguous(), b_t)  # db in the same pass
-        gx = torch.mm(d, w).view(ctx.xshape) if ctx.needs_input_grad[0] else None
-        torch.mm(d.t(), x2, out=w_t)
+        gx = kernels.gemm(d, w).view(ctx.xshape) if ctx.needs_input_grad[0] else None
+        kernels.gemm(d, x2, ta=True, out=w_t)
         return gx, None, None, None, None
 
 

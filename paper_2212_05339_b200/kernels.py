@@ -9,7 +9,10 @@ validates sizes and alignment and returns typed errors (_lib.check).
 from __future__ import annotations
 
 import ctypes
+import json
+import os
 import threading
+from pathlib import Path
 from typing import Sequence
 
 import torch
@@ -485,14 +488,67 @@ def _lt_workspace(device: torch.device) -> int:
     return ws.data_ptr()
 
 
-def _lt(epi, ta, tb, m, n, k, a, lda, b, ldb, d, ldd, bias=None, aux=None, ldaux=0, stream=None, c=None):
+# Per-shape cuBLASLt algorithm choice: index into the heuristic's candidate
+# list, tuned once on the B200 by scripts/tune_lt.py (fastest with L2 flushed,
+# median of repeats) and committed, so every process picks the same algorithm.
+# Shapes not in the table take the heuristic's first candidate.
+_LT_TABLE_PATH = Path(__file__).resolve().parents[1] / "plans" / "lt_algos_b200.json"
+_LT_TABLE: dict | None = None
+LT_RECORD: set | None = None  # scripts/tune_lt.py collects the step's GEMM keys here
+
+
+def lt_key(epi, dt, ta, tb, m, n, k, lda, ldb, ldd, ldaux, has_c) -> tuple:
+    return (int(epi), int(dt), int(ta), int(tb), int(m), int(n), int(k), int(lda), int(ldb), int(ldd), int(ldaux),
+            int(bool(has_c)))
+
+
+def _lt_table() -> dict:
+    global _LT_TABLE
+    if _LT_TABLE is None:
+        table = {}
+        if os.environ.get("ELX_LT_TABLE", "1") != "0" and _LT_TABLE_PATH.exists():
+            for rec in json.loads(_LT_TABLE_PATH.read_text())["choices"]:
+                table[tuple(rec["key"])] = int(rec["index"])
+        _LT_TABLE = table
+    return _LT_TABLE
+
+
+def _lt(epi, ta, tb, m, n, k, a, lda, b, ldb, d, ldd, bias=None, aux=None, ldaux=0, stream=None, c=None,
+        algo=None):
     lib = _lib.load()
-    rc = lib.elx_lt_matmul(epi, elx_dtype(d.dtype), ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
-                           None if c is None else c.data_ptr(), d.data_ptr(), ldd,
-                           None if bias is None else bias.data_ptr(),
-                           None if aux is None else aux.data_ptr(), ldaux, _lt_workspace(d.device),
-                           _LT_WS_BYTES, _stream(stream))
+    dt = elx_dtype(d.dtype)
+    key = lt_key(epi, dt, ta, tb, m, n, k, lda, ldb, ldd, ldaux, c is not None)
+    if LT_RECORD is not None:
+        LT_RECORD.add(key)
+    idx = _lt_table().get(key, -1) if algo is None else algo
+    rc = lib.elx_lt_matmul_ex(epi, dt, ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
+                              None if c is None else c.data_ptr(), d.data_ptr(), ldd,
+                              None if bias is None else bias.data_ptr(),
+                              None if aux is None else aux.data_ptr(), ldaux, _lt_workspace(d.device),
+                              _LT_WS_BYTES, idx, _stream(stream))
     _lib.check(rc, "elx_lt_matmul")
+
+
+def gemm(a: torch.Tensor, b: torch.Tensor, out: torch.Tensor | None = None, *, ta: bool = False, tb: bool = False,
+         bias: torch.Tensor | None = None, c: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Row-major out[M, N] = op(a) @ op(b) (+ c) (+ bias[N]) through
+    elx_lt_matmul (op = transpose when ta / tb); 2-D contiguous operands."""
+    for t, n in ((a, "a"), (b, "b")):
+        _cuda(t, n)
+        if t.dim() != 2 or not t.is_contiguous():
+            raise ValidationError(f"gemm: {n} must be a contiguous 2-D tensor")
+    M, K = (a.shape[1], a.shape[0]) if ta else a.shape
+    K2, N = (b.shape[1], b.shape[0]) if tb else b.shape
+    if K != K2:
+        raise ValidationError(f"gemm: inner dimensions {K} and {K2} differ")
+    if out is None:
+        out = torch.empty(M, N, dtype=a.dtype, device=a.device)
+    if out.shape != (M, N) or not out.is_contiguous():
+        raise ValidationError("gemm: out must be a contiguous [M, N] tensor")
+    # column-major: out^T [N, M] = op(b)^T [N, K] . op(a)^T [K, M]
+    _lt(EPI_BIAS if bias is not None else EPI_NONE, 1 if tb else 0, 1 if ta else 0, N, M, K, b, b.shape[1], a,
+        a.shape[1], out, N, bias=bias, c=c, stream=stream)
+    return out
 
 
 def linear_gelu(x2d: torch.Tensor, w: torch.Tensor, b: torch.Tensor, keep_aux: bool, stream=None):

@@ -4,7 +4,7 @@ alternately (ABAB...) and timed with CUDA events, so clock / power-cap drift
 hits every variant alike (bench.py-to-bench.py differences on this
 power-capped box are +-3%, larger than the effects measured here).
 
-    python scripts/ab_step.py [model] [rounds] [--recompute]
+    python scripts/ab_step.py [model] [rounds] [--recompute | --lt]
 
 Variants (monkeypatched, the product keeps the first):
   new         — as shipped
@@ -30,7 +30,7 @@ rounds = int(args[1]) if len(args) > 1 else 8
 dev = torch.device("cuda:0")
 cfg = gpt2.PRESETS[model_name]
 plan = (ROOT / "plans" / f"{model_name}_n1.json").read_text()
-model = gpt2.ElixirGPT2(cfg, plan, device=dev, seed=1234)
+model = gpt2.ElixirGPT2(cfg, plan, device=dev, seed=1234, recompute=True if "--recompute" in sys.argv else "auto")
 g = torch.Generator(device=dev).manual_seed(1234)
 ids = torch.randint(0, cfg.vocab, (cfg.batch, cfg.seq_len + 1), generator=g, device=dev)
 tok, tgt = ids[:, :-1].contiguous(), ids[:, 1:].contiguous()
@@ -53,6 +53,8 @@ def _unfused_gc(x, dy, db):
 VARIANTS = {"new": {}, "sep_qkv": {(gpt2, "_qkv_proj"): _sep_qkv},
             "unfused_res": {(gpt2, "layer_norm_residual"): _unfused_res},
             "unfused_gc": {(gpt2.kernels, "gelu_bwd_colsum"): _unfused_gc}}
+if "--lt" in sys.argv:  # the tuned cuBLASLt algorithm table vs the heuristic's first choice
+    VARIANTS = {"new": {}, "lt_first": {(kernels, "_lt_table"): lambda: {}}}
 if "--recompute" in sys.argv:  # A/B activation checkpointing vs keeping the forward graphs
     VARIANTS = {"new": {}, "no_recompute": {(model, "keep_graph"): True}}
 graphs = {}
