@@ -153,3 +153,19 @@ def test_device_step_bias_tables_equal_oracle_constants():
             assert bc2s[t] == k["bc2_sqrt"], t
         tab.ensure(50_000)
         assert tab.bc1.numel() >= 50_002
+
+
+def test_lt_algorithm_table_well_formed():
+    """plans/lt_algos_b200.json (scripts/tune_lt.py): one entry per GEMM key
+    of the step, heuristic-candidate indices in range, loaded by kernels."""
+    import json
+    from pathlib import Path
+    from paper_2212_05339_b200 import kernels
+    d = json.loads((Path(__file__).resolve().parents[1] / "plans" / "lt_algos_b200.json").read_text())
+    keys = [tuple(c["key"]) for c in d["choices"]]
+    assert len(keys) == len(set(keys)) > 0
+    for c in d["choices"]:
+        assert len(c["key"]) == 12 and all(isinstance(v, int) for v in c["key"])
+        assert 0 <= c["index"] < 16 and str(c["index"]) in c["ms"]
+    table = kernels._lt_table()
+    assert all(table[k] == c["index"] for k, c in zip(keys, d["choices"]))

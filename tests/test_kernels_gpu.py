@@ -765,3 +765,55 @@ def test_layer_norm_bwd_dx_residual_equals_separate_add(cuda, rows, cols):
     fused = kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd, dres=dres)
     sep = kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd) + dres
     assert torch.equal(fused, sep)
+
+
+@pytest.mark.parametrize("ta,tb,M,N,K", [(False, False, 256, 384, 128), (True, False, 128, 256, 512),
+                                         (False, True, 512, 768, 256), (False, False, 8192, 2048, 2048)])
+def test_gemm_matches_torch(cuda, ta, tb, M, N, K):
+    """kernels.gemm (elx_lt_matmul_ex, row-major op(a) @ op(b) [+ c] [+ bias])
+    vs torch.mm in fp32 on the same bf16 operands."""
+    g = torch.Generator(device=cuda).manual_seed(M + N + K)
+    a = (torch.randn((K, M) if ta else (M, K), device=cuda, generator=g) * 0.1).to(torch.bfloat16)
+    b = (torch.randn((N, K) if tb else (K, N), device=cuda, generator=g) * 0.1).to(torch.bfloat16)
+    bias = torch.randn(N, device=cuda, generator=g).to(torch.bfloat16)
+    c = torch.randn(M, N, device=cuda, generator=g).to(torch.bfloat16)
+    A = a.float().t() if ta else a.float()
+    B = b.float().t() if tb else b.float()
+    for kw, want in (({}, A @ B), ({"bias": bias}, A @ B + bias.float()), ({"c": c}, A @ B + c.float())):
+        got = kernels.gemm(a, b, ta=ta, tb=tb, **kw).float()
+        assert (got - want).abs().max() <= 1e-2 * want.abs().max() + 1e-2, kw
+    out = c.clone()
+    kernels.gemm(a, b, ta=ta, tb=tb, out=out, c=out)  # in place: out += op(a) op(b)
+    assert (out.float() - (A @ B + c.float())).abs().max() <= 1e-2 * (A @ B).abs().max() + 2e-2
+
+
+def test_lt_table_choices_compute_the_same_gemm(cuda):
+    """Every tuned entry of plans/lt_algos_b200.json, run through
+    elx_lt_matmul_ex with its index, equals the heuristic's first candidate to
+    bf16 accumulation-order accuracy (the table only changes the algorithm)."""
+    from paper_2212_05339_b200 import _lib
+    lib = _lib.load()
+    ws = kernels._lt_workspace(cuda)
+    g = torch.Generator(device=cuda).manual_seed(7)
+    for key, idx in kernels._lt_table().items():
+        epi, dt, ta, tb, m, n, k, lda, ldb, ldd, ldaux, has_c = key
+        if m * n * k > 2 ** 34 or idx == 0:
+            continue
+        tdt = torch.bfloat16 if dt == _lib.BF16 else torch.float16
+        A = (torch.randn(lda * (m if ta else k), device=cuda, generator=g) * 0.1).to(tdt)
+        B = (torch.randn(ldb * (k if tb else n), device=cuda, generator=g) * 0.1).to(tdt)
+        C = torch.randn(ldd * n, device=cuda, generator=g).to(tdt) if has_c else None
+        bias = torch.randn(max(m, n), device=cuda, generator=g).to(tdt) if epi else None
+        aux = torch.randn(max(ldaux, 1) * n, device=cuda, generator=g).to(tdt) if ldaux else None
+        outs = []
+        for i in (0, idx):
+            D = torch.zeros(ldd * n, dtype=tdt, device=cuda)
+            bb = None if bias is None else bias.clone()
+            rc = lib.elx_lt_matmul_ex(epi, dt, ta, tb, m, n, k, A.data_ptr(), lda, B.data_ptr(), ldb,
+                                      None if C is None else C.data_ptr(), D.data_ptr(), ldd,
+                                      None if bb is None else bb.data_ptr(), None if aux is None else aux.data_ptr(),
+                                      ldaux, ws, kernels._LT_WS_BYTES, i, torch.cuda.current_stream().cuda_stream)
+            _lib.check(rc, "elx_lt_matmul_ex")
+            outs.append(D.float())
+        ref = outs[0]
+        assert (outs[1] - ref).abs().max() <= 2e-2 * ref.abs().max() + 1e-2, key
