@@ -139,6 +139,36 @@ class _OverwriteLinear(torch.autograd.Function):
         return gx, None, None, None, None
 
 
+class _TiedHead(torch.autograd.Function):
+    """logits = x wte^T over the padded vocab rows (the tied lm_head), GEMMs
+    through elx_lt_matmul_ex. Backward: dX = dlogits wte; dW = dlogits^T x
+    over the `vocab` real rows only — written straight into `w_target` (the
+    shared wte gradient buffer, [vocab, H]) when given, so no padded gradient
+    tensor and no K1 copy exist; without a target it is returned (padded)."""
+
+    @staticmethod
+    def forward(ctx, x2, wte, vocab, w_target):
+        ctx.save_for_backward(x2, wte)
+        ctx.vocab, ctx.target = int(vocab), w_target
+        return kernels.gemm(x2.contiguous(), wte, tb=True)
+
+    @staticmethod
+    def backward(ctx, gl):
+        x2, wte = ctx.saved_tensors
+        gl = gl.contiguous()
+        T, Vp = gl.shape
+        H = x2.shape[1]
+        gx = kernels.gemm(gl, wte) if ctx.needs_input_grad[0] else None
+        tgt = ctx.target
+        if tgt is None:
+            dw = torch.zeros_like(wte)
+            kernels.gemm(gl[:, :ctx.vocab].contiguous(), x2, ta=True, out=dw[:ctx.vocab])
+            return gx, dw, None, None
+        # column-major: dW^T [H, vocab] = x^T [H, T] . dlogits[:, :vocab] [T, vocab] (ld = Vp)
+        kernels._lt(kernels.EPI_NONE, 0, 1, H, ctx.vocab, T, x2, H, gl, Vp, tgt, H)
+        return gx, None, None, None
+
+
 def _qkv_proj(h, wq, wk, wv, bq, bk, bv):
     """q, k, v = h W^T + b for the three row blocks of attn.qkv as ONE GEMM
     with N = 3H (the blocks are consecutive in the chunk, so W and b are one
@@ -476,7 +506,9 @@ class ElixirGPT2:
             return F.embedding(tokens, wte) + wpe[:T]
         if i == self.K - 1:  # tied lm_head + loss (wte viewed with padded vocab rows)
             (wte,) = params
-            logits = F.linear(x, wte)  # [B, T, vocab_padded] bf16, straight from the GEMM
+            # [B*T, vocab_padded] bf16 straight from the GEMM; with a target the wte gradient is written there
+            logits = _TiedHead.apply(x.reshape(-1, x.shape[-1]), wte, cfg.vocab,
+                                     grad_targets[0] if grad_targets else None)
             # K8: cross-entropy on the padded bf16 logits (pad columns excluded), gradient written
             # in place: no sliced fp32 copy of the 0.8 GB logits and no separate softmax kernels
             return kernels.lm_head_cross_entropy(logits.view(-1, logits.shape[-1]), targets.reshape(-1), cfg.vocab)
@@ -555,11 +587,16 @@ class ElixirGPT2:
                 with torch.enable_grad():
                     xin = None if i == 0 else acts[i].detach().requires_grad_(True)
                     # layers: linear gradients land in their chunk slots (raw views) directly
-                    out = self._run_node(i, xin, tokens, targets, params,
-                                         grad_targets=[_alias(t) for t in raw] if layer else None)
+                    if layer:
+                        tg = [_alias(t) for t in raw]
+                    elif i == K - 1:  # the tied head writes its wte gradient straight into the shared grad buffer
+                        tg = [self.wte.grad[:self.wte.numel].view(self.cfg.vocab, self.cfg.hidden)]
+                    else:
+                        tg = None
+                    out = self._run_node(i, xin, tokens, targets, params, grad_targets=tg)
             with torch.enable_grad():
                 inputs = ([xin] if i > 0 else []) + params
-                grads = torch.autograd.grad(out, inputs, grad_outputs=grad, allow_unused=layer)
+                grads = torch.autograd.grad(out, inputs, grad_outputs=grad, allow_unused=layer or i == K - 1)
             if i == K - 1:
                 loss = out.detach()
             acts[i] = None
@@ -569,7 +606,9 @@ class ElixirGPT2:
                 pgrads = grads
             chunk_grads = pgrads[:len(self.node_pieces[i])]
             self._write_grads(i, chunk_grads)
-            if i == 0 or i == K - 1:
+            if i == K - 1 and pgrads[-1] is None:  # written in place by _TiedHead
+                wte_grad_set = True
+            elif i == 0 or i == K - 1:
                 wg = pgrads[-1].reshape(-1)[:self.wte.numel]
                 buf = self.wte.grad[:self.wte.numel]
                 if wte_grad_set:
