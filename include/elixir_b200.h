@@ -339,6 +339,13 @@ int elx_layer_norm_bwd_dx(void* dx, const void* x, const void* dy, const void* w
 int elx_layer_norm_bwd_dx_res(void* dx, const void* x, const void* dy, const void* w, const float* mean,
                               const float* rstd, const void* dres, int32_t dtype, int64_t rows, int64_t cols,
                               void* stream);
+/* K13: token-embedding gradient accumulated into grad_w ([rows, ldw], e.g.
+ * the shared wte gradient buffer): for each distinct token t of sorted_tok
+ * (positions sorted by token, stable; perm[i] = original position of the
+ * i-th), grad_w[t] = round(grad_w[t] + round(S_t)), S_t the fp32 sum of dy
+ * rows over t's positions in position order. Deterministic, no atomics. */
+int elx_embedding_bwd(void* grad_w, int64_t ldw, const void* dy, const int64_t* sorted_tok, const int64_t* perm,
+                      int64_t n, int64_t cols, int32_t dtype, void* stream);
 int elx_gelu_fwd(void* y, const void* x, int32_t dtype, int64_t n, void* stream);
 int elx_gelu_bwd(void* dx, const void* x, const void* dy, int32_t dtype, int64_t n, void* stream);
 /* elx_gelu_bwd over [rows, cols] fused with K7 on its output: dx as above and

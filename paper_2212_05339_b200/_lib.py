@@ -106,6 +106,7 @@ _SIGNATURES = {
     "elx_gelu_fwd": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i64, c_vp]),
     "elx_gelu_bwd": (ctypes.c_int, [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp]),
     "elx_gelu_bwd_colsum": (ctypes.c_int, [c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i64, c_i64, c_vp]),
+    "elx_embedding_bwd": (ctypes.c_int, [c_vp, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64, c_i32, c_vp]),
     "elx_lt_matmul": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,
                                      c_vp, c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp]),
     "elx_lt_matmul_ex": (ctypes.c_int, [c_i32, c_i32, c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64,

@@ -520,6 +520,51 @@ __global__ void __launch_bounds__(kWideThreads) ln_bwd_dx_wide_kernel(const T16*
   }
 }
 
+// ------------------------------------------------- K13 embedding backward
+// The token embedding's gradient accumulated straight into the (shared wte)
+// gradient buffer: for every distinct token t, S = the fp32 sum of dy over
+// the positions holding t, in position order; grad_w[t] = round(grad_w[t] +
+// round(S)) — the same bits as adding a separately materialised embedding
+// gradient. Positions arrive sorted by token (stable, so position order
+// within a token); the CTA at the first position of each run owns that
+// token's row: no atomics, deterministic. Replaces the dense [vocab, H]
+// gradient (206 MB zero fill + sort-based scatter) and its add into the buffer.
+constexpr int kEmbThreads = 256;
+
+template <typename T16>
+__global__ void __launch_bounds__(kEmbThreads) embedding_bwd_kernel(T16* __restrict__ grad_w, int64_t ldw,
+                                                                     const T16* __restrict__ dy,
+                                                                     const int64_t* __restrict__ sorted_tok,
+                                                                     const int64_t* __restrict__ perm, int64_t n,
+                                                                     int cols) {
+  const int64_t j = blockIdx.x;
+  const int64_t tok = sorted_tok[j];
+  if (j > 0 && sorted_tok[j - 1] == tok) return;  // not the first position of its run
+  int64_t end = j + 1;
+  while (end < n && sorted_tok[end] == tok) ++end;
+  const int nvec = cols >> 3;
+  uint4* wr = reinterpret_cast<uint4*>(grad_w + tok * ldw);
+  for (int v = threadIdx.x; v < nvec; v += kEmbThreads) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 4
+    for (int64_t r = j; r < end; ++r) {
+      float f[8];
+      unpack8<T16>(reinterpret_cast<const uint4*>(dy + perm[r] * cols)[v], f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], f[e]);
+    }
+    float g[8];
+    unpack8<T16>(wr[v], g);
+    union {
+      T16 h[8];
+      uint4 u;
+    } o;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o.h[e] = from_f<T16>(__fadd_rn(g[e], to_f(from_f<T16>(acc[e]))));
+    wr[v] = o.u;
+  }
+}
+
 // ---------------------------------------------------------- K12 tanh-GELU
 // y = 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))) and its derivative,
 // 16-byte vectors, grid-stride; tanh via the SFU (tanh.approx.f32, ~2^-11
@@ -943,6 +988,28 @@ int elx_gelu_bwd_colsum(void* dx, void* dbias, int32_t dbias_dtype, const void* 
                                                                 static_cast<__half*>(dx), dbias, dbias_dtype, rows,
                                                                 cols);
   return check("elx_gelu_bwd_colsum");
+}
+
+int elx_embedding_bwd(void* grad_w, int64_t ldw, const void* dy, const int64_t* sorted_tok, const int64_t* perm,
+                      int64_t n, int64_t cols, int32_t dtype, void* stream) {
+  elx::clear_error();
+  if (!grad_w || !dy || !sorted_tok || !perm) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "embedding grads must be bf16/f16");
+  if (n < 0 || cols < 8 || (cols % 8) != 0 || ldw < cols || (ldw % 8) != 0)
+    return elx::fail(ELX_ERR_VALIDATION, "need cols %% 8 == 0, ldw >= cols, ldw %% 8 == 0");
+  if (!aligned16(grad_w) || !aligned16(dy)) return elx::fail(ELX_ERR_VALIDATION, "grad_w/dy not 16-byte aligned");
+  if (n == 0) return ELX_OK;
+  if (n > 0x7fffffff) return elx::fail(ELX_ERR_VALIDATION, "too many positions");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == ELX_BF16)
+    embedding_bwd_kernel<<<(unsigned)n, kEmbThreads, 0, st>>>(static_cast<__nv_bfloat16*>(grad_w), ldw,
+                                                               static_cast<const __nv_bfloat16*>(dy), sorted_tok, perm,
+                                                               n, (int)cols);
+  else
+    embedding_bwd_kernel<<<(unsigned)n, kEmbThreads, 0, st>>>(static_cast<__half*>(grad_w), ldw,
+                                                               static_cast<const __half*>(dy), sorted_tok, perm, n,
+                                                               (int)cols);
+  return check("elx_embedding_bwd");
 }
 
 }  // extern "C"

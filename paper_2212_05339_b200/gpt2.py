@@ -139,6 +139,31 @@ class _OverwriteLinear(torch.autograd.Function):
         return gx, None, None, None, None
 
 
+class _Embedding(torch.autograd.Function):
+    """The token embedding lookup wte[tokens]. Backward: K13 accumulates the
+    gradient into `w_target` (the shared wte gradient buffer, [vocab, H],
+    already holding the tied head's part) in place; without a target it
+    returns a dense gradient made by the same kernel over zeros — so both
+    paths give the same bits."""
+
+    @staticmethod
+    def forward(ctx, tokens, wte, w_target):
+        ctx.save_for_backward(tokens)
+        ctx.wshape, ctx.target = wte.shape, w_target
+        return F.embedding(tokens, wte)
+
+    @staticmethod
+    def backward(ctx, gy):
+        (tokens,) = ctx.saved_tensors
+        gy2 = gy.reshape(-1, gy.shape[-1]).contiguous()
+        if ctx.target is None:
+            dw = torch.zeros(ctx.wshape, dtype=gy.dtype, device=gy.device)
+            kernels.embedding_bwd(dw, tokens, gy2)
+            return None, dw, None
+        kernels.embedding_bwd(ctx.target, tokens, gy2)
+        return None, None, None
+
+
 class _TiedHead(torch.autograd.Function):
     """logits = x wte^T over the padded vocab rows (the tied lm_head), GEMMs
     through elx_lt_matmul_ex. Backward: dX = dlogits wte; dW = dlogits^T x
@@ -159,14 +184,12 @@ class _TiedHead(torch.autograd.Function):
         T, Vp = gl.shape
         H = x2.shape[1]
         gx = kernels.gemm(gl, wte) if ctx.needs_input_grad[0] else None
-        tgt = ctx.target
-        if tgt is None:
-            dw = torch.zeros_like(wte)
-            kernels.gemm(gl[:, :ctx.vocab].contiguous(), x2, ta=True, out=dw[:ctx.vocab])
-            return gx, dw, None, None
-        # column-major: dW^T [H, vocab] = x^T [H, T] . dlogits[:, :vocab] [T, vocab] (ld = Vp)
+        dw = torch.zeros_like(wte) if ctx.target is None else None
+        tgt = ctx.target if dw is None else dw[:ctx.vocab]
+        # column-major: dW^T [H, vocab] = x^T [H, T] . dlogits[:, :vocab] [T, vocab] (ld = Vp); the same
+        # call (same algorithm) with or without a target, so both give the same bits
         kernels._lt(kernels.EPI_NONE, 0, 1, H, ctx.vocab, T, x2, H, gl, Vp, tgt, H)
-        return gx, None, None, None
+        return gx, dw, None, None
 
 
 def _qkv_proj(h, wq, wk, wv, bq, bk, bv):
@@ -500,10 +523,10 @@ class ElixirGPT2:
     # -------------------------------------------------------------- nodes
     def _run_node(self, i: int, x, tokens, targets, params, grad_targets=None):
         cfg = self.cfg
-        if i == 0:  # embed: wte (shared) + wpe
+        if i == 0:  # embed: wte (shared) + wpe; with a target the wte gradient accumulates there (K13)
             wpe, wte = params
             T = tokens.shape[1]
-            return F.embedding(tokens, wte) + wpe[:T]
+            return _Embedding.apply(tokens, wte, grad_targets[0] if grad_targets else None) + wpe[:T]
         if i == self.K - 1:  # tied lm_head + loss (wte viewed with padded vocab rows)
             (wte,) = params
             # [B*T, vocab_padded] bf16 straight from the GEMM; with a target the wte gradient is written there
@@ -562,8 +585,7 @@ class ElixirGPT2:
                 layer = 0 < i < K - 2
                 xin = None if i == 0 else x.detach().requires_grad_(True)
                 with torch.enable_grad():
-                    out = self._run_node(i, xin, tokens, targets, params,
-                                         grad_targets=[_alias(t) for t in raw] if layer else None)
+                    out = self._run_node(i, xin, tokens, targets, params, grad_targets=self._targets(i, raw))
                 saved[i] = (out, xin, params)
                 x = out.detach()
             elif i < K - 1:  # the head's loss comes from its backward recompute
@@ -587,16 +609,10 @@ class ElixirGPT2:
                 with torch.enable_grad():
                     xin = None if i == 0 else acts[i].detach().requires_grad_(True)
                     # layers: linear gradients land in their chunk slots (raw views) directly
-                    if layer:
-                        tg = [_alias(t) for t in raw]
-                    elif i == K - 1:  # the tied head writes its wte gradient straight into the shared grad buffer
-                        tg = [self.wte.grad[:self.wte.numel].view(self.cfg.vocab, self.cfg.hidden)]
-                    else:
-                        tg = None
-                    out = self._run_node(i, xin, tokens, targets, params, grad_targets=tg)
+                    out = self._run_node(i, xin, tokens, targets, params, grad_targets=self._targets(i, raw))
             with torch.enable_grad():
                 inputs = ([xin] if i > 0 else []) + params
-                grads = torch.autograd.grad(out, inputs, grad_outputs=grad, allow_unused=layer or i == K - 1)
+                grads = torch.autograd.grad(out, inputs, grad_outputs=grad, allow_unused=i != K - 2)
             if i == K - 1:
                 loss = out.detach()
             acts[i] = None
@@ -606,7 +622,7 @@ class ElixirGPT2:
                 pgrads = grads
             chunk_grads = pgrads[:len(self.node_pieces[i])]
             self._write_grads(i, chunk_grads)
-            if i == K - 1 and pgrads[-1] is None:  # written in place by _TiedHead
+            if (i == 0 or i == K - 1) and pgrads[-1] is None:  # written in place (_TiedHead, then K13)
                 wte_grad_set = True
             elif i == 0 or i == K - 1:
                 wg = pgrads[-1].reshape(-1)[:self.wte.numel]
@@ -625,6 +641,16 @@ class ElixirGPT2:
             self.scaler.update(stats.found_inf)
         self.last_loss = loss
         return loss
+
+    def _targets(self, i: int, raw):
+        """Where node i's wrapped operators write their parameter gradients:
+        a layer's chunk slots (aliases); for the tied head (first in the
+        backward) and then the embedding, the shared wte gradient buffer."""
+        if 0 < i < self.K - 2:
+            return [_alias(t) for t in raw]
+        if i == 0 or i == self.K - 1:
+            return [self.wte.grad[:self.wte.numel].view(self.cfg.vocab, self.cfg.hidden)]
+        return None
 
     def _write_grads(self, i: int, grads) -> None:
         """Overwrite the node's parameter slots in the chunk with their

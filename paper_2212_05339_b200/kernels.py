@@ -420,6 +420,23 @@ def gelu_bwd_colsum(x2d: torch.Tensor, dy2d: torch.Tensor, dbias: torch.Tensor, 
     return dx
 
 
+def embedding_bwd(grad_w: torch.Tensor, tokens: torch.Tensor, dy2d: torch.Tensor, stream=None) -> None:
+    """K13: grad_w[t] += sum of dy rows at the positions of token t (fp32 sum
+    in position order, rounded once, then added) — deterministic, in place.
+    grad_w [rows, H] (row stride may exceed H), tokens int64 [n], dy2d [n, H]."""
+    if not grad_w.is_cuda:
+        raise ValidationError("grad_w must be a CUDA tensor")
+    _cuda(dy2d, "dy")
+    n, H = dy2d.shape
+    if grad_w.dim() != 2 or grad_w.shape[1] != H or grad_w.stride(1) != 1 or grad_w.dtype != dy2d.dtype \
+            or not dy2d.is_contiguous() or tokens.numel() != n:
+        raise ValidationError("embedding_bwd: grad_w [rows, H] (unit column stride), dy [n, H] contiguous, n tokens")
+    sorted_tok, perm = torch.sort(tokens.reshape(-1), stable=True)
+    rc = _lib.load().elx_embedding_bwd(grad_w.data_ptr(), grad_w.stride(0), dy2d.data_ptr(), sorted_tok.data_ptr(),
+                                       perm.data_ptr(), n, H, elx_dtype(dy2d.dtype), _stream(stream))
+    _lib.check(rc, "elx_embedding_bwd")
+
+
 class LMHeadCrossEntropy(torch.autograd.Function):
     """K8: mean softmax cross-entropy over the padded bf16/f16 lm_head logits
     [rows, ld] (columns >= vocab excluded), with no fp32 copy of the logits.

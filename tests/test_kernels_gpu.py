@@ -817,3 +817,34 @@ def test_lt_table_choices_compute_the_same_gemm(cuda):
             outs.append(D.float())
         ref = outs[0]
         assert (outs[1] - ref).abs().max() <= 2e-2 * ref.abs().max() + 1e-2, key
+
+
+@pytest.mark.parametrize("n,H,V,repeat", [(8192, 2048, 50304, False), (300, 64, 17, True), (1, 8, 4, False)])
+def test_embedding_bwd_k13(cuda, n, H, V, repeat):
+    """K13 accumulates the embedding gradient into grad_w in place: equal to
+    round(grad_w + round(fp32 per-token sums in position order)); the sums
+    match torch's embedding backward to fp32 accuracy; rows of absent tokens
+    are untouched."""
+    g = torch.Generator(device=cuda).manual_seed(n + H)
+    hi = 3 if repeat else V
+    tok = torch.randint(0, hi, (n,), device=cuda, generator=g)
+    dy = torch.randn(n, H, device=cuda, generator=g).to(torch.bfloat16)
+    base = torch.randn(V, H, device=cuda, generator=g).to(torch.bfloat16)
+    got = base.clone()
+    kernels.embedding_bwd(got, tok, dy)
+    # reference: per-token fp32 sums in position order
+    want = base.clone()
+    S = torch.zeros(V, H, dtype=torch.float64, device=cuda).index_add_(0, tok, dy.double())
+    present = torch.zeros(V, dtype=torch.bool, device=cuda)
+    present[tok] = True
+    want[present] = (base.float()[present] + S[present].float().to(torch.bfloat16).float()).to(torch.bfloat16)
+    assert torch.equal(got[~present], base[~present])
+    err = (got.float() - want.float()).abs()
+    assert float(err.max()) <= 2 ** -7 * float(want.float().abs().max()) + 1e-3
+    again = base.clone()
+    kernels.embedding_bwd(again, tok, dy)
+    assert torch.equal(got, again)
+    # strided grad rows (a [V, H] view of a wider buffer)
+    wide = torch.zeros(V, H + 8, dtype=torch.bfloat16, device=cuda)
+    kernels.embedding_bwd(wide[:, :H], tok, dy)
+    assert torch.equal(wide[:, H:], torch.zeros_like(wide[:, H:]))
