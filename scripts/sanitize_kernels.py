@@ -83,6 +83,20 @@ dg, db = torch.empty_like(w), torch.empty_like(b)
 kernels.ln_param_grad(x, dy, mean.view(-1), rstd.view(-1), dg, db)
 gy = kernels.gelu_fwd(x)
 gx = kernels.gelu_bwd(x, dy)
+dres = torch.randn(1000, 3072, device=dev, generator=g).to(bf)
+dxr = kernels.layer_norm_bwd_dx(x, dy, w, mean, rstd, dres=dres)  # K11 + residual gradient
+x2, dy2, dres2 = x[:, :2048].contiguous(), dy[:, :2048].contiguous(), dres[:, :2048].contiguous()
+y2, mean2, rstd2 = kernels.layer_norm_fwd(x2, w[:2048], b[:2048])
+dxr2 = kernels.layer_norm_bwd_dx(x2, dy2, w[:2048], mean2, rstd2, dres=dres2)  # warp-per-row variant
+dbg = torch.empty(3072, dtype=bf, device=dev)
+gxc = kernels.gelu_bwd_colsum(x, dy, dbg)  # K12 backward + K7
+wg = torch.randn(500, 3072, device=dev, generator=g).to(bf)
+tok = torch.randint(0, 500, (1000,), device=dev, generator=g)
+kernels.embedding_bwd(wg, tok, dy)  # K13
+a_ = torch.randn(256, 384, device=dev, generator=g).to(bf)
+b_ = torch.randn(384, 512, device=dev, generator=g).to(bf)
+cg = kernels.gemm(a_, b_)  # elx_lt_matmul_ex
+kernels.gemm(a_, b_, out=cg, c=cg)
 logits = torch.randn(64, 1032, device=dev, generator=g).to(bf).requires_grad_(True)
 tgt = torch.randint(0, 1000, (64,), device=dev, generator=g)
 loss = kernels.lm_head_cross_entropy(logits, tgt, 1000)

@@ -2,7 +2,7 @@
 through elx_lt_matmul, on the B200, and write plans/lt_algos_b200.json (the
 table kernels._lt reads: heuristic-candidate index per shape).
 
-    python scripts/tune_lt.py [model ...]      # default: gpt2-1.3b gpt2-small
+    python scripts/tune_lt.py [model ...]      # default: gpt2-1.3b gpt2-small gpt2-4b gpt2-10b
 
 For each model one eager training step runs with kernels.LT_RECORD set, which
 collects the (epilogue, dtype, transposes, m, n, k, leading dimensions, C?)
@@ -28,11 +28,13 @@ from paper_2212_05339_b200 import _lib, kernels  # noqa: E402
 from paper_2212_05339_b200.gpt2 import PRESETS, ElixirGPT2  # noqa: E402
 
 dev = torch.device("cuda:0")
-models = sys.argv[1:] or ["gpt2-1.3b", "gpt2-small"]
+PLANS = {"gpt2-4b": "gpt2-4b_offload_n1.json", "gpt2-10b": "gpt2-10b_offload_n1.json"}
+models = sys.argv[1:] or ["gpt2-1.3b", "gpt2-small", "gpt2-4b", "gpt2-10b"]
 keys = set()
 for name in models:
     cfg = PRESETS[name]
-    model = ElixirGPT2(cfg, (ROOT / "plans" / f"{name}_n1.json").read_text(), device=dev, recompute="auto")
+    plan = PLANS.get(name, f"{name}_n1.json")
+    model = ElixirGPT2(cfg, (ROOT / "plans" / plan).read_text(), device=dev, recompute="auto")
     ids = torch.randint(0, cfg.vocab, (cfg.batch, cfg.seq_len + 1), device=dev)
     model.train_step(ids[:, :-1].contiguous(), ids[:, 1:].contiguous())
     kernels.LT_RECORD = set()
@@ -40,7 +42,11 @@ for name in models:
     torch.cuda.synchronize()
     keys |= kernels.LT_RECORD
     kernels.LT_RECORD = None
+    model.synchronize()
+    torch.cuda.synchronize()
     del model
+    import gc
+    gc.collect()
     torch.cuda.empty_cache()
 
 flush = torch.ones(64 * 2 ** 20, device=dev)
