@@ -113,32 +113,6 @@ def layer_pieces(i: int, h: int) -> list[tuple[str, int, tuple[int, ...]]]:
     return out
 
 
-class _OverwriteLinear(torch.autograd.Function):
-    """y = x W^T + b (a wrapped operator) whose backward
-    writes dW and db straight into `targets` — at run time the chunk slots of
-    W and b themselves: the gradient overwrites the parameter data
-    (Fig. 3). dX is computed first, while W is intact; dW
-    is a cuBLAS GEMM into the slot, db the deterministic K7 column sum. No
-    separate weight-gradient tensor and no K1 write-back copy exist."""
-
-    @staticmethod
-    def forward(ctx, x, w, b, w_target, b_target):
-        ctx.save_for_backward(x, w)
-        ctx.targets = (w_target, b_target)
-        return F.linear(x, w, b)
-
-    @staticmethod
-    def backward(ctx, gy):
-        x, w = ctx.saved_tensors
-        w_t, b_t = ctx.targets
-        gy2 = gy.reshape(-1, gy.shape[-1])
-        gy2 = gy2.contiguous()
-        gx = kernels.gemm(gy2, w).view(*gy.shape[:-1], w.shape[1]) if ctx.needs_input_grad[0] else None
-        kernels.gemm(gy2, x.reshape(-1, x.shape[-1]).contiguous(), ta=True, out=w_t)
-        kernels.colsum(gy2, b_t)
-        return gx, None, None, None, None
-
-
 class _Embedding(torch.autograd.Function):
     """The token embedding lookup wte[tokens]. Backward: K13 accumulates the
     gradient into `w_target` (the shared wte gradient buffer, [vocab, H],
@@ -250,8 +224,10 @@ class _OverwriteQKV(torch.autograd.Function):
 class _OverwriteLinearResidual(torch.autograd.Function):
     """y = res + x W^T + b as ONE cuBLASLt GEMM (C operand + bias epilogue):
     an output projection (attn.proj, mlp.proj) with the residual add folded in.
-    Backward as _OverwriteLinear (dW, db into the chunk slots); the residual's
-    gradient is dy itself."""
+    Backward: dX first (W intact), then dW by a GEMM straight into the
+    weight's chunk slot and db by K7 into the bias slot — the gradient
+    overwrites the parameter data (Fig. 3) with no gradient
+    tensor and no K1 copy; the residual's gradient is dy itself."""
 
     @staticmethod
     def forward(ctx, x, w, b, res, w_target, b_target):
@@ -403,11 +379,6 @@ def _block(x, p, heads, targets=None):
     their parameter gradients there during backward."""
     B, T, H = x.shape
     hd = H // heads
-
-    def lin(inp, wi, bi):
-        if targets is None:
-            return F.linear(inp, p[wi], p[bi])
-        return _OverwriteLinear.apply(inp, p[wi], p[bi], targets[wi], targets[bi])
 
     def ln(inp, wi, bi):  # (LayerNorm(inp), inp for the residual branch)
         if targets is None:
@@ -657,7 +628,7 @@ class ElixirGPT2:
         gradients (Fig. 3): one K1 launch per chunk."""
         by_chunk: dict[int, list] = {}
         for (pid, sub, _), g in zip(self.node_pieces[i], grads):
-            if g is None:  # written in place by the wrapped linear (_OverwriteLinear)
+            if g is None:  # written in place by a wrapped operator (linear, LayerNorm)
                 continue
             c, off, _ = self.manager.members[pid]
             by_chunk.setdefault(c, []).append((g.reshape(-1), off + sub))
