@@ -481,7 +481,8 @@ def run_ours(args):
         "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s",
                 "h2d_bytes_per_step": host_ids.numel() * host_ids.element_size(),
                 "d2h_bytes_per_step": loss_host.numel() * loss_host.element_size(),
-                "api": "ElixirGPT2.train_step on tokens copied from pinned host memory, loss read back"},
+                "api": ("ElixirGPT2.graph_step (the captured train_step)" if use_graph else "ElixirGPT2.train_step")
+                       + " on tokens copied from pinned host memory, loss read back"},
         "chunk_runtime": offload,
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
