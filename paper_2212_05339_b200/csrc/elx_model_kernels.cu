@@ -164,11 +164,7 @@ __global__ void __launch_bounds__(kXentThreads) xent_bwd_kernel(T16* __restrict_
 // through distributed shared memory. Replaces torch's GammaBetaBackward
 // (73 us per LayerNorm at 8192 x 2048, profiles/r01h_launches.md) and the K1
 // write-back of the LayerNorm gradients.
-constexpr int kLnWarps = 8;
-constexpr int kLnThreads = kLnWarps * 32;
 constexpr int kLnStrip = 128;
-constexpr int kLnCluster = 16;  // non-portable cluster size: 256 CTAs at 2048 columns
-constexpr int kLnU = 16;
 
 __device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
   uint2 r;
@@ -176,8 +172,8 @@ __device__ __forceinline__ uint2 ld_nc_u2(const void* p) {
   return r;
 }
 
-template <typename T16>
-__global__ void __cluster_dims__(1, kLnCluster, 1) __launch_bounds__(kLnThreads, 2)
+template <typename T16, int kLnCluster, int kLnWarps, int kLnU, int kMinB>
+__global__ void __launch_bounds__(kLnWarps * 32, kMinB)
     ln_param_grad_kernel(const T16* __restrict__ x, const T16* __restrict__ dy, const float* __restrict__ mean,
                          const float* __restrict__ rstd, int64_t rows, int64_t cols, T16* __restrict__ dgamma,
                          T16* __restrict__ dbeta) {
@@ -795,22 +791,36 @@ int elx_ln_param_grad(void* dgamma, void* dbeta, const void* x, const void* dy, 
   if (rows < 1 || cols < 1 || (cols % 4) != 0) return elx::fail(ELX_ERR_VALIDATION, "need rows >= 1, cols % 4 == 0");
   if ((reinterpret_cast<uintptr_t>(x) & 7u) || (reinterpret_cast<uintptr_t>(dy) & 7u))
     return elx::fail(ELX_ERR_VALIDATION, "x/dy not 8-byte aligned");
-  const dim3 grid((unsigned)((cols + kLnStrip - 1) / kLnStrip), kLnCluster);
   cudaStream_t st = (cudaStream_t)stream;
-  static bool configured = false;
-  if (!configured) {  // cluster of 16 > the portable 8
-    cudaFuncSetAttribute(ln_param_grad_kernel<__nv_bfloat16>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(ln_param_grad_kernel<__half>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    configured = true;
-  }
+  // 16-CTA clusters (non-portable) of 8 warps, 8 rows of loads in flight per warp: 78 registers, 3 CTAs
+  // per SM, so the 256 CTAs at 2048 columns are resident at once (with 16 rows in flight, 123 registers,
+  // 2 CTAs/SM, only 14 clusters fit and the grid ran in two waves: 28.7 vs 22.5 us at 8192 x 2048)
+  constexpr int kCl = 16, kW = 8;
+  auto launch = [&](auto kern, auto tag) {
+    using T = decltype(tag);
+    static bool configured = false;
+    if (!configured) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      configured = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((cols + kLnStrip - 1) / kLnStrip), kCl);
+    cfg.blockDim = dim3(kW * 32);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = kCl;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<const T*>(x), static_cast<const T*>(dy), mean, rstd, rows, cols,
+                       static_cast<T*>(dgamma), static_cast<T*>(dbeta));
+  };
   if (dtype == ELX_BF16)
-    ln_param_grad_kernel<__nv_bfloat16><<<grid, kLnThreads, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), mean, rstd, rows, cols,
-        static_cast<__nv_bfloat16*>(dgamma), static_cast<__nv_bfloat16*>(dbeta));
+    launch(ln_param_grad_kernel<__nv_bfloat16, kCl, kW, 8, 3>, __nv_bfloat16{});
   else
-    ln_param_grad_kernel<__half><<<grid, kLnThreads, 0, st>>>(
-        static_cast<const __half*>(x), static_cast<const __half*>(dy), mean, rstd, rows, cols,
-        static_cast<__half*>(dgamma), static_cast<__half*>(dbeta));
+    launch(ln_param_grad_kernel<__half, kCl, kW, 8, 3>, __half{});
   return check("elx_ln_param_grad");
 }
 
