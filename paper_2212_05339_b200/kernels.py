@@ -520,12 +520,17 @@ def lt_key(epi, dt, ta, tb, m, n, k, lda, ldb, ldd, ldaux, has_c) -> tuple:
 
 
 def _lt_table() -> dict:
+    """The tuned table, used only on the GPU model it was tuned on (on other
+    hardware every shape takes the heuristic's first candidate)."""
     global _LT_TABLE
     if _LT_TABLE is None:
         table = {}
         if os.environ.get("ELX_LT_TABLE", "1") != "0" and _LT_TABLE_PATH.exists():
-            for rec in json.loads(_LT_TABLE_PATH.read_text())["choices"]:
-                table[tuple(rec["key"])] = int(rec["index"])
+            doc = json.loads(_LT_TABLE_PATH.read_text())
+            gpu = torch.cuda.get_device_name() if torch.cuda.is_available() else doc.get("gpu")
+            if doc.get("gpu") == gpu:
+                for rec in doc["choices"]:
+                    table[tuple(rec["key"])] = int(rec["index"])
         _LT_TABLE = table
     return _LT_TABLE
 
@@ -538,11 +543,14 @@ def _lt(epi, ta, tb, m, n, k, a, lda, b, ldb, d, ldd, bias=None, aux=None, ldaux
     if LT_RECORD is not None:
         LT_RECORD.add(key)
     idx = _lt_table().get(key, -1) if algo is None else algo
-    rc = lib.elx_lt_matmul_ex(epi, dt, ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb,
-                              None if c is None else c.data_ptr(), d.data_ptr(), ldd,
-                              None if bias is None else bias.data_ptr(),
-                              None if aux is None else aux.data_ptr(), ldaux, _lt_workspace(d.device),
-                              _LT_WS_BYTES, idx, _stream(stream))
+    args = (epi, dt, ta, tb, m, n, k, a.data_ptr(), lda, b.data_ptr(), ldb, None if c is None else c.data_ptr(),
+            d.data_ptr(), ldd, None if bias is None else bias.data_ptr(), None if aux is None else aux.data_ptr(),
+            ldaux, _lt_workspace(d.device), _LT_WS_BYTES)
+    rc = lib.elx_lt_matmul_ex(*args, idx, _stream(stream))
+    if rc == _lib.ERR_VALIDATION and algo is None and idx > 0:
+        # the table's index is past this library's candidate list (another cuBLASLt): drop the entry
+        _lt_table().pop(key, None)
+        rc = lib.elx_lt_matmul_ex(*args, -1, _stream(stream))
     _lib.check(rc, "elx_lt_matmul")
 
 
