@@ -3,18 +3,21 @@
 Every coarse node of the access trace (profiles.py:490-521: wpe embed, one
 node per AC-grouped layer, ln_f, the tied lm_head) is a "wrapped operator"
 (PAPER.md:203-206): before it runs, the ChunkFetcher makes its chunks
-resident; the forward runs without saving activations except each node's
-input (activation checkpointing); the backward walks the
-nodes in reverse (chunking.py:165), recomputes each node with autograd,
-writes the parameter gradients over the parameter data in the chunk
-(K1) and releases chunks at their reduce positions
+resident. With activation checkpointing (recompute=True)
+the forward saves only each node's input and the backward recomputes each
+node with autograd; when no chunk can leave its block between a node's
+forward and backward, recompute="auto"/False keeps the forward's autograd
+graph instead (same results). The backward walks the nodes in reverse
+(chunking.py:165), writes the parameter gradients over the parameter data in
+the chunk and releases chunks at their reduce positions
 (rcache_sim.py:160-167, K3). After the walk HybridAdam updates the shards.
 
-GEMMs are cuBLAS (through torch, or cuBLASLt with fused epilogues: the MLP's
-bias + GELU, the output projections' residual add), attention is torch SDPA;
-LayerNorm, the lm_head cross-entropy and every gradient reduction written into
-the chunk are our kernels (csrc/elx_model_kernels.cu), and the chunk path
-itself is ours (csrc/elx_kernels.cu).
+GEMMs are cuBLASLt through elx_lt_matmul_ex (fused epilogues: the MLP's bias
++ GELU, the output projections' residual add; a per-shape algorithm table
+tuned on the B200), attention is torch SDPA (cuDNN); LayerNorm, GELU, the
+lm_head cross-entropy, the embedding gradient and every gradient reduction
+written into the chunk are our kernels (csrc/elx_model_kernels.cu), and the
+chunk path itself is ours (csrc/elx_kernels.cu).
 """
 
 from __future__ import annotations
