@@ -583,6 +583,12 @@ def main():
         run_sweep(args)
     else:
         run_ours(args)
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            # no rank exits (releasing the CUDA-IPC memory it exported) while a peer still maps it
+            torch.cuda.synchronize()
+            dist.barrier()
+            dist.destroy_process_group()
 
 
 if __name__ == "__main__":
