@@ -279,7 +279,8 @@ __device__ __forceinline__ float warp_sum(float v) {
 // of the row (vectors interleaved in 512-byte runs, v = lane + 32 (kS j + h)),
 // so a thread keeps 1/4 of the registers and four times as many rows are in
 // flight per SM; the warps' partial sums meet in shared memory in warp order.
-// At 8192 x 2048: K10 20.5 -> 18.4 us, K11 with the residual 37.9 -> 28.7 us.
+// K11 with the residual at 8192 rows: 38.9 -> 28.7 us (2048 columns), 61 -> 39 (3072), 98 -> 49 (4096);
+// rows of <= 1024 columns stay one warp per row (as fast or faster there).
 template <int kS>
 __device__ __forceinline__ float row_sum(float v, float* red) {
   v = warp_sum(v);
@@ -891,7 +892,7 @@ int elx_layer_norm_fwd(void* y, float* mean, float* rstd, const void* x, const v
                                                            static_cast<const T*>(b), static_cast<T*>(y), mean, rstd,
                                                            rows, c, eps);
     };
-    pick_row_kernel(c, [&] { k(ln_fwd_kernel<T, 2, 1>, 1); }, [&] { k(ln_fwd_kernel<T, 1, 4>, 4); },
+    pick_row_kernel(c, [&] { k(ln_fwd_kernel<T, 2, 1>, 1); }, [&] { k(ln_fwd_kernel<T, 4, 1>, 1); },
                     [&] { k(ln_fwd_kernel<T, 2, 4>, 4); }, [&] { k(ln_fwd_kernel<T, 3, 4>, 4); },
                     [&] { k(ln_fwd_kernel<T, 4, 4>, 4); });
   } else {
@@ -901,7 +902,7 @@ int elx_layer_norm_fwd(void* y, float* mean, float* rstd, const void* x, const v
                                                            static_cast<const T*>(b), static_cast<T*>(y), mean, rstd,
                                                            rows, c, eps);
     };
-    pick_row_kernel(c, [&] { k(ln_fwd_kernel<T, 2, 1>, 1); }, [&] { k(ln_fwd_kernel<T, 1, 4>, 4); },
+    pick_row_kernel(c, [&] { k(ln_fwd_kernel<T, 2, 1>, 1); }, [&] { k(ln_fwd_kernel<T, 4, 1>, 1); },
                     [&] { k(ln_fwd_kernel<T, 2, 4>, 4); }, [&] { k(ln_fwd_kernel<T, 3, 4>, 4); },
                     [&] { k(ln_fwd_kernel<T, 4, 4>, 4); });
   }
@@ -948,12 +949,12 @@ int elx_layer_norm_bwd_dx_res(void* dx, const void* x, const void* dy, const voi
                                                            static_cast<const T*>(dres), rows, c);
     };
     if (dres)
-      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, true, 1>, 1); }, [&] { k(ln_bwd_dx_kernel<T, 1, true, 4>, 4); },
+      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, true, 1>, 1); }, [&] { k(ln_bwd_dx_kernel<T, 4, true, 1>, 1); },
                       [&] { k(ln_bwd_dx_kernel<T, 2, true, 4>, 4); }, [&] { k(ln_bwd_dx_kernel<T, 3, true, 4>, 4); },
                       [&] { k(ln_bwd_dx_kernel<T, 4, true, 4>, 4); });
     else
       pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, false, 1>, 1); },
-                      [&] { k(ln_bwd_dx_kernel<T, 1, false, 4>, 4); }, [&] { k(ln_bwd_dx_kernel<T, 2, false, 4>, 4); },
+                      [&] { k(ln_bwd_dx_kernel<T, 4, false, 1>, 1); }, [&] { k(ln_bwd_dx_kernel<T, 2, false, 4>, 4); },
                       [&] { k(ln_bwd_dx_kernel<T, 3, false, 4>, 4); }, [&] { k(ln_bwd_dx_kernel<T, 4, false, 4>, 4); });
   } else {
     using T = __half;
@@ -963,12 +964,12 @@ int elx_layer_norm_bwd_dx_res(void* dx, const void* x, const void* dy, const voi
                                                            static_cast<const T*>(dres), rows, c);
     };
     if (dres)
-      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, true, 1>, 1); }, [&] { k(ln_bwd_dx_kernel<T, 1, true, 4>, 4); },
+      pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, true, 1>, 1); }, [&] { k(ln_bwd_dx_kernel<T, 4, true, 1>, 1); },
                       [&] { k(ln_bwd_dx_kernel<T, 2, true, 4>, 4); }, [&] { k(ln_bwd_dx_kernel<T, 3, true, 4>, 4); },
                       [&] { k(ln_bwd_dx_kernel<T, 4, true, 4>, 4); });
     else
       pick_row_kernel(c, [&] { k(ln_bwd_dx_kernel<T, 2, false, 1>, 1); },
-                      [&] { k(ln_bwd_dx_kernel<T, 1, false, 4>, 4); }, [&] { k(ln_bwd_dx_kernel<T, 2, false, 4>, 4); },
+                      [&] { k(ln_bwd_dx_kernel<T, 4, false, 1>, 1); }, [&] { k(ln_bwd_dx_kernel<T, 2, false, 4>, 4); },
                       [&] { k(ln_bwd_dx_kernel<T, 3, false, 4>, 4); }, [&] { k(ln_bwd_dx_kernel<T, 4, false, 4>, 4); });
   }
   return check("elx_layer_norm_bwd_dx");
