@@ -678,20 +678,23 @@ __device__ __forceinline__ uint2 ld_nc_u2b(const void* p) {
   return r;
 }
 
-template <typename T16>
-__global__ void __cluster_dims__(1, kGcCluster, 1) __launch_bounds__(kGcThreads, 2)
+// kPW physical warps per CTA run K7's kGcWarps row groups (group g on warp
+// g % kPW, in turn): the groups, and so the fp32 order, are K7's whatever kPW.
+template <typename T16, int kPW>
+__global__ void __cluster_dims__(1, kGcCluster, 1) __launch_bounds__(kPW * 32, kGcWarps / kPW * 2)
     gelu_bwd_colsum_kernel(const T16* __restrict__ x, const T16* __restrict__ dy, T16* __restrict__ dx,
                            void* dbias, int db_dt, int64_t rows, int64_t cols) {
   __shared__ float part[kGcWarps][kGcStrip];
   __shared__ float cta_sum[kGcStrip];
   cg::cluster_group cluster = cg::this_cluster();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31;
   const int c = (int)cluster.block_rank();
   const int64_t col0 = (int64_t)blockIdx.x * kGcStrip;
   const int64_t cc = col0 + lane * 4;
   const int64_t per_cta = (rows + kGcCluster - 1) / kGcCluster;
   const int64_t per_warp = (per_cta + kGcWarps - 1) / kGcWarps;
   const int64_t cta_end = min(rows, (int64_t)(c + 1) * per_cta);
+  for (int warp = threadIdx.x >> 5; warp < kGcWarps; warp += kPW) {
   const int64_t r0 = (int64_t)c * per_cta + (int64_t)warp * per_warp;
   const int64_t r1 = min(cta_end, r0 + per_warp);
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
@@ -732,6 +735,7 @@ __global__ void __cluster_dims__(1, kGcCluster, 1) __launch_bounds__(kGcThreads,
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) part[warp][lane * 4 + e] = acc[e];
+  }
   __syncthreads();
   if (threadIdx.x < kGcStrip) {
     float a = 0.f;
@@ -1023,15 +1027,16 @@ int elx_gelu_bwd_colsum(void* dx, void* dbias, int32_t dbias_dtype, const void* 
     return elx::fail(ELX_ERR_VALIDATION, "gelu tensors must be 16-byte aligned");
   const dim3 grid((unsigned)((cols + kGcStrip - 1) / kGcStrip), kGcCluster);
   cudaStream_t st = (cudaStream_t)stream;
+  // 8 warps per CTA, each running two of K7's 16 row groups in turn: 4 CTAs/SM hold all 512 CTAs of an
+  // 8192 x 8192 gradient at once (0.076 vs 0.078 ms with 16 warps; 4 warps: 0.092)
   if (dtype == ELX_BF16)
-    gelu_bwd_colsum_kernel<__nv_bfloat16><<<grid, kGcThreads, 0, st>>>(
+    gelu_bwd_colsum_kernel<__nv_bfloat16, 8><<<grid, 8 * 32, 0, st>>>(
         static_cast<const __nv_bfloat16*>(x), static_cast<const __nv_bfloat16*>(dy), static_cast<__nv_bfloat16*>(dx),
         dbias, dbias_dtype, rows, cols);
   else
-    gelu_bwd_colsum_kernel<__half><<<grid, kGcThreads, 0, st>>>(static_cast<const __half*>(x),
-                                                                static_cast<const __half*>(dy),
-                                                                static_cast<__half*>(dx), dbias, dbias_dtype, rows,
-                                                                cols);
+    gelu_bwd_colsum_kernel<__half, 8><<<grid, 8 * 32, 0, st>>>(static_cast<const __half*>(x),
+                                                               static_cast<const __half*>(dy), static_cast<__half*>(dx),
+                                                               dbias, dbias_dtype, rows, cols);
   return check("elx_gelu_bwd_colsum");
 }
 
