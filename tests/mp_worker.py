@@ -16,7 +16,8 @@ the peers' rCache blocks through CUDA-IPC mappings of the other processes'
 allocations, ordered by elx_device_barrier over IPC-mapped signal pads;
 "ipc-ce" does the same with K2 on the copy engines (elx_fetch_ce); "ipc-graph"
 captures the second step as one CUDA graph per rank (the ranks' graphs meet
-at device-numbered barriers) and replays it.
+at device-numbered barriers) and replays it. A "-keep" suffix runs the step
+with the forward graphs kept instead of recomputed (recompute=False).
 """
 
 import json
@@ -51,7 +52,10 @@ def main():
         transport = IpcTransport(fetch_engine="ce" if path == "ipc-ce" else "sm")
     else:
         transport = TorchDistTransport()
-    model = ElixirGPT2(CFG, plan, device=dev, transport=transport, init=init, **HP)
+    keep = path.endswith("-keep")  # the bench's mode: forward graphs kept instead of recomputed
+    path = path.removesuffix("-keep")
+    model = ElixirGPT2(CFG, plan, device=dev, transport=transport, init=init, recompute=not keep, **HP)
+    assert model.keep_graph == keep
     assert model.manager.p2p == path.startswith("ipc")
     losses = []
     for s in range(2):

@@ -52,6 +52,45 @@ def _torchrun(world: int, args: list[str], timeout: int = 600) -> subprocess.Com
     return p
 
 
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("path", ["exchange-keep", "ipc-graph-keep"])
+def test_multiprocess_keep_graph_equals_checkpointed_loopback(cuda, tmp_path, world, path):
+    """The bench's N > 1 mode — every chunk resident (n_block = n_chunks), the
+    forward graphs kept instead of recomputed, over the gloo exchange or the
+    IPC P2P path with the second step replayed as a CUDA graph — in separate
+    processes equals the checkpointed rank-thread run bit for bit (losses,
+    masters) and its counters equal simulate."""
+    _torchrun(world, ["tests/mp_worker.py", "rcache-max", str(tmp_path), path])
+    got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    plan, fwd, red = _plan("rcache-max")
+    init = gpt2.init_params(CFG, cuda, seed=11)
+
+    def rank_fn(r, transport):
+        model = ElixirGPT2(CFG, plan, device=cuda, transport=transport,
+                           init={k: v.clone() for k, v in init.items()}, **HP)
+        losses = []
+        for s in range(2):
+            tok, tgt = _batches(world, s, cuda)[r]
+            losses.append(model.train_step(tok, tgt).item())
+        model.synchronize()
+        torch.cuda.synchronize()
+        return losses, _rank_masters(model)
+
+    want = run_ranks(world, rank_fn)
+    sim, _ = L.simulate(fwd, plan.n_block, set(), red)
+    for r in range(world):
+        assert list(got[r]["losses"]) == want[r][0], r
+        live = json.loads(str(got[r]["counters"]))
+        for k in ("gather_ops", "replaced_ops", "reduce_ops"):
+            assert live[k] == sim[k], (r, k)
+        for pid, (off, ref_vals) in want[r][1].items():
+            vals = got[r][f"val::{pid}"]
+            if world == 2:
+                assert np.array_equal(vals, ref_vals), (r, pid)
+            else:  # gloo's fp64 all-reduce of the N sum-of-squares partials (see above)
+                np.testing.assert_allclose(vals, ref_vals, rtol=1e-6, atol=0)
+
+
 @pytest.mark.parametrize("path", ["exchange", "ipc", "ipc-ce", "ipc-graph"])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("kind", ["rcache-min", "offload"])
