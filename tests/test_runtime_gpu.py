@@ -218,6 +218,7 @@ def test_keep_graph_step_equals_recompute(cuda, plan_name):
     ac = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, **HP)
     kg = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, recompute=False, **HP)
     assert kg.keep_graph and not ac.keep_graph
+    assert ElixirGPT2(CFG, plan, device=cuda, recompute="auto", **HP).keep_graph  # resident, small activations
     assert [ac.train_step(*b).item() for b in batches] == [kg.train_step(*b).item() for b in batches]
     a, b = _masters(ac), _masters(kg)
     for k in a:
