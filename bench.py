@@ -464,6 +464,7 @@ def run_ours(args):
             "n_chunks": model.layout.n_chunks, "n_block": model.manager.plan.n_block,
             "l2": "working set (>20 GB of chunk/optimizer state per step) far exceeds the 126 MB L2; no flush needed",
             "cuda_graph": use_graph,
+            "deterministic": bool(args.deterministic),
             "activation_checkpointing": not model.keep_graph,
             "recompute_note": ("off: every chunk stays resident forward->backward and the activations fit, so "
                                "each node's forward graph is kept instead of recomputed — results bit-identical "
@@ -589,6 +590,9 @@ def main():
                     help="activation checkpointing: on = recompute each node in the backward (the reference's "
                          "design), off = keep the forward graphs, auto = off when every chunk stays resident "
                          "and the activations fit in HBM")
+    ap.add_argument("--deterministic", action="store_true",
+                    help="deterministic library algorithms (cuDNN attention's deterministic backward): the whole "
+                         "step becomes run-to-run bit-reproducible (our kernels always are)")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
                     help="every chunk GPU-home, world 1 or --transport ipc: capture the whole step as one CUDA graph")
     ap.add_argument("--overlap", action="store_true",
@@ -597,6 +601,10 @@ def main():
                     help="N>1 fetch/release path: NCCL collectives + K3, or in-kernel P2P with peer pointers from "
                          "symmetric memory (p2p) or CUDA IPC + our device barrier (ipc)")
     args = ap.parse_args()
+    if args.deterministic:
+        os.environ.setdefault("CUBLAS_WORKSPACE_CONFIG", ":4096:8")
+        torch.backends.cudnn.deterministic = True
+        torch.use_deterministic_algorithms(True)
     if args.warmup < 3 and not args.sweep and args.impl == "ours":
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
     if args.impl == "reference":
