@@ -1,6 +1,6 @@
 """The N > 1 runtime on a full-size plan, with N rank-threads sharing ONE GPU.
 
-    python scripts/emulate_ranks.py [model] [world] [plan file] [--p2p] [--no-recompute] > gpurun_out/emulate.json
+    python scripts/emulate_ranks.py [model] [world] [plan file] [--p2p] [--no-recompute] [--det] > gpurun_out/emulate.json
 
 Each rank builds its chunk store from the reference planner's plan for N
 GPUs (plans/<model>_n<N>.json, e.g. BASELINE config 2: GPT-2 1.3B at 8
@@ -35,6 +35,9 @@ base = PRESETS[model_name]
 cfg = GPT2Config(base.hidden, base.layers, base.heads, base.vocab, base.seq_len, batch=1)
 plan_text = (ROOT / "plans" / plan_file).read_text()
 dev = torch.device("cuda:0")
+if "--det" in sys.argv:  # deterministic library algorithms (cuDNN attention's deterministic backward)
+    torch.backends.cudnn.deterministic = True
+    torch.use_deterministic_algorithms(True)
 if "--flash" in sys.argv:  # SDPA's flash backend instead of cuDNN (multi-thread determinism probe)
     torch.backends.cuda.enable_cudnn_sdp(False)
 steps = 2
