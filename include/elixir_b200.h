@@ -186,22 +186,60 @@ int elx_peer_sum_f64(double* dst, const double* const* peers, int32_t count, int
 int elx_enable_peer_access(int32_t peer_device);
 
 /* ----------------------------------------------------- K3 grad release
- * Reduce-scatter of one chunk's gradients into this rank's fp32 grad shard,
- * fused with loss-scale unscale, fp32 cast, the sum-of-squares partial and
- * the overflow flag (rcache_sim.py:160-167 fires it at
- * reduce_after[c]):
+ * Reduce-scatter of chunk gradients into this rank's fp32 grad shards, fused
+ * with loss-scale unscale, fp32 cast, the sum of squares and the overflow
+ * flag (rcache_sim.py:160-167 fires it at reduce_after[c]):
  *   g[i] = (sum_{r=0..world-1, in order} float(src[r][i])) * inv_scale
- *   step_scalars[0] += sum_i g[i]^2   (fp64)
+ *   step_scalars[0] += sum_i g[i]^2   (fp64, fixed order, see below)
  *   step_scalars[1]  = 1.0 if any g[i] is not finite
  * src[r] points at rank r's copy of THIS rank's segment (peer block + rank*S,
  * or a local all-to-all staging buffer). n = valid elements (padding
- * excluded). dtype is BF16 or F16. step_scalars is a DEVICE double[2].
- * grad_shard may be NULL: only the sum of squares and the overflow flag are
- * produced. At world 1 the reduction is the identity, so the runtime keeps
- * the gradient in the compute-dtype chunk and the update (elx_adam with a
- * compute-dtype `g`) applies the same float(g) * inv_scale in-register. */
+ * excluded). dtype is BF16 or F16. g may be NULL: only the sum of squares and
+ * the overflow flag are produced. At world 1 the reduction is the identity, so
+ * the runtime keeps the gradient in the compute-dtype chunk and the update
+ * (elx_adam with a compute-dtype `g`) applies the same float(g) * inv_scale
+ * in-register.
+ *
+ * Step-scalar block: step_scalars is a DEVICE double[ELX_STEP_SCALARS],
+ * zero-initialised once:
+ *   [0] sum of squares  [1] overflow flag  [2] completed optimizer steps
+ *   [ELX_SC_TICKET]     arrival ticket of the release in flight (uint32)
+ *   [ELX_SC_PARTIALS + b] the partial sum of CTA b of that release.
+ * The sum of squares is deterministic (no floating-point atomics): every CTA
+ * reduces its elements in a fixed order into its partial slot, and the last
+ * CTA to arrive adds the partials in slot order (elx_release_geometry gives
+ * the grid; oracle/c/elx_oracle.c restates the order). Releases that share a
+ * step-scalar block must be issued on ONE stream (they are serialised).
+ * Peer sources are read with coherent 16-byte loads (call after a device
+ * barrier that orders the peers' gradient writes). */
+#define ELX_STEP_SCALARS 2048
+#define ELX_SC_TICKET 4
+#define ELX_SC_PARTIALS 8
+#define ELX_RELEASE_MAX_CTAS (ELX_STEP_SCALARS - ELX_SC_PARTIALS)
+#define ELX_RELEASE_MAX_SEGS 16
+
+typedef struct {
+  float* g;                        /* fp32 destination (16-byte aligned for the vector path) or NULL */
+  const void* src[ELX_MAX_WORLD];  /* rank r's copy of the segment, r < world (16-byte aligned) */
+  int64_t n;                       /* valid elements */
+} elx_release_seg;
+
+/* One chunk (the replaced ColossalAI chunk-reduce call of PAPER.md:221-238). */
 int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t world,
                 int32_t dtype, float inv_scale, double* step_scalars, void* stream);
+/* Every chunk due at one reduce position in ONE launch (per
+ * ELX_RELEASE_MAX_SEGS segments); `segs` is a HOST array (batched into kernel
+ * parameters). Segments are reduced in table order into one sum of squares. */
+int elx_release_batch(const elx_release_seg* segs, int32_t nseg, int32_t world, int32_t dtype, float inv_scale,
+                      double* step_scalars, void* stream);
+/* Summation geometry of elx_release_batch on the current device for segment
+ * lengths n[0..nseg) (nseg <= ELX_RELEASE_MAX_SEGS): *ctas = grid size G (0
+ * if empty), *tile_vecs = 8-element vectors per tile (threads * unroll). Tile
+ * k of the batch (segments' tiles concatenated) goes to CTA k % G; thread t
+ * of a tile takes vectors t, t + 256, ...; a thread sums its squares in that
+ * order, then CTA and grid reductions as described above. */
+int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t dtype, int32_t* ctas,
+                         int32_t* tile_vecs);
 
 /* ------------------------------------------------------ K4 chunk Adam
  * Fused mixed-precision AdamW over fp32 master/m/v shards with the fp32

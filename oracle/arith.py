@@ -107,6 +107,59 @@ def release(srcs, inv_scale: float, dtype: str = "bf16"):
     return g, sq, bool(not np.isfinite(g).all())
 
 
+def _block_sum_fixed(x: np.ndarray) -> np.ndarray:
+    """The release kernel's fixed CTA reduction over the last axis (256 fp64
+    values): a butterfly (xor 16, 8, 4, 2, 1) inside each warp of 32, then the
+    same butterfly over the 8 warp sums padded with zeros; lane 0's value."""
+    lanes = np.arange(32)
+    w = x.reshape(x.shape[:-1] + (8, 32))
+    for o in (16, 8, 4, 2, 1):
+        w = w + w[..., lanes ^ o]
+    y = np.zeros(x.shape[:-1] + (32,), np.float64)
+    y[..., :8] = w[..., 0]
+    for o in (16, 8, 4, 2, 1):
+        y = y + y[..., lanes ^ o]
+    return y[..., 0]
+
+
+def release_norm_ordered(gs, ctas: int, tile_vecs: int) -> float:
+    """Sum of squares of one K3 launch (elx_release_batch) in the kernel's
+    exact fp64 order (include/elixir_b200.h, K3; elx_release_geometry gives
+    ctas/tile_vecs): the segments' tiles of `tile_vecs` 8-element vectors
+    concatenated, tile k to CTA k % ctas, thread t of 256 taking vectors t,
+    t+256, ... of a tile; per thread a sequential sum of squares (d*d is exact
+    in fp64, so numpy's multiply then add equals the kernel's DFMA; np.cumsum
+    is sequential), elements past a segment's end +0.0; per CTA the fixed block
+    reduction; the partials summed per thread in slot order, then reduced the
+    same way. Vectorised over CTAs and threads."""
+    T = 256
+    U = tile_vecs // T
+    tiles = []
+    for g in gs:
+        g = np.asarray(g, np.float32).reshape(-1)
+        te = tile_vecs * 8
+        nt = -(-g.size // te)
+        pad = np.zeros(nt * te, np.float64)
+        pad[:g.size] = g
+        tiles.append(pad.reshape(nt, U, T, 8))
+    if not tiles or sum(t.shape[0] for t in tiles) == 0 or ctas <= 0:
+        return 0.0
+    allt = np.concatenate(tiles)                    # [tiles, U, T, 8]
+    nt = allt.shape[0]
+    k = -(-nt // ctas)
+    full = np.zeros((k * ctas, U, T, 8), np.float64)
+    full[:nt] = allt
+    # [k, ctas, U, T, 8] -> per (cta, thread): sequence over (k, U, 8)
+    seq = full.reshape(k, ctas, U, T, 8).transpose(1, 3, 0, 2, 4).reshape(ctas, T, -1)
+    sq = np.cumsum(seq * seq, axis=-1)[..., -1]      # [ctas, T]
+    part = _block_sum_fixed(sq)                       # [ctas]
+    rows = -(-ctas // T)
+    slots = np.zeros(rows * T, np.float64)
+    slots[:ctas] = part
+    per_thread = np.cumsum(slots.reshape(rows, T), axis=0)[-1]   # thread t: slots t, t+256, ... in order
+    return float(_block_sum_fixed(per_thread))
+
+
 def colsum_ordered(x: np.ndarray, slices: int, groups: int) -> np.ndarray:
     """Bias-gradient column sum (K7) in its fixed fp32 order: rows cut into
     `slices` contiguous slices of ceil(rows/slices) rows, each slice into

@@ -10,6 +10,7 @@
  */
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 static inline float bf16_to_f32(uint16_t b) {
@@ -79,4 +80,100 @@ void oracle_pack_bf16(uint16_t* chunk, int64_t phys, int64_t used, const uint16_
   }
 #pragma omp parallel for num_threads(threads) schedule(static)
   for (int64_t i = used; i < phys; ++i) chunk[i] = 0;
+}
+
+/* Fixed-shape reduction of 256 per-thread fp64 values exactly as the release
+ * kernel's block_sum_fixed: a butterfly (xor 16, 8, 4, 2, 1) inside each warp
+ * of 32, then the same butterfly over the 8 warp sums padded with zeros;
+ * returns lane 0's value. */
+static double block_sum_fixed(const double* x) {
+  double w[32];
+  double lane[32];
+  for (int wp = 0; wp < 8; ++wp) {
+    for (int i = 0; i < 32; ++i) lane[i] = x[wp * 32 + i];
+    for (int o = 16; o > 0; o >>= 1) {
+      double y[32];
+      for (int i = 0; i < 32; ++i) y[i] = lane[i] + lane[i ^ o];
+      memcpy(lane, y, sizeof(y));
+    }
+    w[wp] = lane[0];
+  }
+  for (int i = 8; i < 32; ++i) w[i] = 0.0;
+  for (int o = 16; o > 0; o >>= 1) {
+    double y[32];
+    for (int i = 0; i < 32; ++i) y[i] = w[i] + w[i ^ o];
+    memcpy(w, y, sizeof(y));
+  }
+  return w[0];
+}
+
+/* Sum of squares of the released fp32 values of one elx_release_batch launch,
+ * in the kernel's order (include/elixir_b200.h, K3): the segments' tiles of
+ * tile_vecs 8-element vectors are concatenated; tile k goes to CTA k % ctas;
+ * thread t (of 256) takes vectors t, t+256, ... of its tiles; each thread
+ * accumulates a*a in fp64 (d*d is exact, so a multiply then one rounded add
+ * equals the kernel's DFMA), elements past a segment's end count as +0.0;
+ * per-CTA block_sum_fixed into a partial; the partials summed per thread in
+ * slot order (thread t: slots t, t+256, ...) and reduced by block_sum_fixed.
+ * Returns that total (the kernel adds it to step_scalars[0]). */
+double oracle_release_norm_ordered(const float* const* g, const int64_t* n, int nseg, int ctas, int tile_vecs,
+                                   int threads) {
+  const int T = 256;
+  const int U = tile_vecs / T;
+  const int64_t tile_elems = (int64_t)tile_vecs * 8;
+  int64_t tile0[65];
+  tile0[0] = 0;
+  for (int s = 0; s < nseg; ++s) tile0[s + 1] = tile0[s] + (n[s] + tile_elems - 1) / tile_elems;
+  const int64_t ntiles = tile0[nseg];
+  if (ctas <= 0 || ntiles == 0) return 0.0;
+  double* part = (double*)calloc((size_t)ctas, sizeof(double));
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 1)
+  for (int b = 0; b < ctas; ++b) {
+    double sq[256];
+    for (int t = 0; t < T; ++t) sq[t] = 0.0;
+    int s = 0;
+    for (int64_t k = b; k < ntiles; k += ctas) {
+      while (s + 1 < nseg && tile0[s + 1] <= k) ++s;
+      const int64_t v0 = (k - tile0[s]) * tile_vecs;
+      for (int t = 0; t < T; ++t) {
+        double acc = sq[t];
+        for (int u = 0; u < U; ++u) {
+          const int64_t v = v0 + (int64_t)u * T + t;
+          for (int e = 0; e < 8; ++e) {
+            const int64_t i = v * 8 + e;
+            const double d = i < n[s] ? (double)g[s][i] : 0.0;
+            acc = acc + d * d;
+          }
+        }
+        sq[t] = acc;
+      }
+    }
+    part[b] = block_sum_fixed(sq);
+  }
+  double x[256];
+  for (int t = 0; t < T; ++t) {
+    double a = 0.0;
+    for (int i = t; i < ctas; i += T) a = a + part[i];
+    x[t] = a;
+  }
+  free(part);
+  return block_sum_fixed(x);
+}
+
+/* World-1 norm pass of elx_release_batch over bf16 chunks (g = NULL): the
+ * released values are float(bf16) * inv_scale. Same order as above. */
+double oracle_release_norm_bf16_ordered(const uint16_t* const* src, const int64_t* n, int nseg, float inv_scale,
+                                        int ctas, int tile_vecs, int threads) {
+  float** g = (float**)calloc((size_t)(nseg > 0 ? nseg : 1), sizeof(float*));
+  for (int s = 0; s < nseg; ++s) {
+    g[s] = (float*)malloc(sizeof(float) * (size_t)(n[s] > 0 ? n[s] : 1));
+    const uint16_t* p = src[s];
+    float* q = g[s];
+#pragma omp parallel for num_threads(threads) schedule(static)
+    for (int64_t i = 0; i < n[s]; ++i) q[i] = bf16_to_f32(p[i]) * inv_scale;
+  }
+  const double r = oracle_release_norm_ordered((const float* const*)g, n, nseg, ctas, tile_vecs, threads);
+  for (int s = 0; s < nseg; ++s) free(g[s]);
+  free(g);
+  return r;
 }

@@ -34,6 +34,11 @@ ERR_CUDA = 300
 F32, BF16, F16 = 0, 1, 2
 ADAM_TILE = 4096
 MAX_WORLD = 16
+# step-scalar block (include/elixir_b200.h, K3)
+STEP_SCALARS = 2048
+SC_TICKET = 4
+SC_PARTIALS = 8
+RELEASE_MAX_SEGS = 16
 EV_GATHER, EV_REDUCE = 0, 1
 
 c_i32, c_i64, c_f32, c_f64, c_vp = (
@@ -73,6 +78,10 @@ class CpuSeg(ctypes.Structure):
                 ("n", c_i64), ("g_dtype", c_i32), ("pad_", c_i32)]
 
 
+class ReleaseSeg(ctypes.Structure):
+    _fields_ = [("g", c_vp), ("src", c_vp * MAX_WORLD), ("n", c_i64)]
+
+
 # name -> (restype, argtypes)
 _SIGNATURES = {
     "elx_abi_version": (c_i32, []),
@@ -89,6 +98,8 @@ _SIGNATURES = {
     "elx_peer_sum_f64": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
     "elx_enable_peer_access": (ctypes.c_int, [c_i32]),
     "elx_release": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_f32, c_vp, c_vp]),
+    "elx_release_batch": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_f32, c_vp, c_vp]),
+    "elx_release_geometry": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),
     "elx_adam": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_i64, c_vp, c_vp]),
     "elx_norm_finalize": (ctypes.c_int, [c_vp, c_f64, c_vp, c_vp]),
     "elx_step_reset": (ctypes.c_int, [c_vp, c_vp]),
@@ -138,7 +149,7 @@ def load() -> ctypes.CDLL:
         fn.argtypes = args
     if lib.elx_abi_version() != 1:
         raise ExtensionMissingError("libelixir_b200 ABI version mismatch")
-    for i, st in enumerate((Event, SimCounters, Member, AdamSeg, AdamHP, CpuSeg)):
+    for i, st in enumerate((Event, SimCounters, Member, AdamSeg, AdamHP, CpuSeg, ReleaseSeg)):
         if lib.elx_sizeof(i) != ctypes.sizeof(st):
             raise ExtensionMissingError(f"libelixir_b200 struct {st.__name__} layout mismatch "
                                         f"({lib.elx_sizeof(i)} != {ctypes.sizeof(st)}): rebuild the library")

@@ -35,6 +35,7 @@ int64_t elx_sizeof(int32_t which) {
     case 3: return (int64_t)sizeof(elx_adam_seg);
     case 4: return (int64_t)sizeof(elx_adam_hp);
     case 5: return (int64_t)sizeof(elx_cpu_seg);
+    case 6: return (int64_t)sizeof(elx_release_seg);
     default: return -1;
   }
 }

@@ -103,9 +103,16 @@ __device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
   asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
   return r;
 }
-// Plain (coherent) 128-bit load, used where the source may be a peer
-// mapping written by another GPU during this kernel's lifetime window.
-__device__ __forceinline__ uint4 ld_plain(const uint4* p) { return *p; }
+// Coherent 16-byte load that does not allocate in L1: the source may be a
+// peer's HBM (NVLink / CUDA IPC mapping) written before the preceding device
+// barrier, so no non-coherent (.nc) path.
+__device__ __forceinline__ uint4 ld_rel(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
 
 // ================================================================ K1 pack
 constexpr int kPackBatch = 48;
@@ -228,11 +235,15 @@ constexpr int kCopyThreads = 256;
 constexpr int kCopyUnroll = 4;
 
 // blockIdx.y = source rank; grid-stride over that rank's 16-byte vectors.
-__global__ void __launch_bounds__(kCopyThreads) fetch_kernel(uint4* block, const PtrBatch src,
+// The pointer table is a __grid_constant__ parameter: indexing it with
+// blockIdx.y reads the constant bank directly (no local-memory copy of the
+// struct, which the by-value form spilled to: 16 x STL.64 per CTA).
+__global__ void __launch_bounds__(kCopyThreads) fetch_kernel(uint4* __restrict__ block,
+                                                             const __grid_constant__ PtrBatch src,
                                                              int64_t shard_vecs) {
   const int r = blockIdx.y;
-  const uint4* s = static_cast<const uint4*>(src.p[r]);
-  uint4* d = block + (int64_t)r * shard_vecs;
+  const uint4* __restrict__ s = static_cast<const uint4*>(src.p[r]);
+  uint4* __restrict__ d = block + (int64_t)r * shard_vecs;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x * kCopyUnroll;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kCopyUnroll + threadIdx.x; i0 < shard_vecs;
        i0 += stride) {
@@ -240,7 +251,7 @@ __global__ void __launch_bounds__(kCopyThreads) fetch_kernel(uint4* block, const
 #pragma unroll
     for (int u = 0; u < kCopyUnroll; ++u) {
       const int64_t i = i0 + (int64_t)u * blockDim.x;
-      if (i < shard_vecs) v[u] = ld_plain(s + i);
+      if (i < shard_vecs) v[u] = ld_rel(s + i);
     }
 #pragma unroll
     for (int u = 0; u < kCopyUnroll; ++u) {
@@ -301,30 +312,78 @@ __global__ void peer_sum_f64_kernel(double* dst, const PtrBatch peers, int count
 }
 
 // ============================================================== K3 release
+// One launch reduces a batch of segments (every chunk due at one reduce
+// position, plus the shared parameter at the last one):
+//   g[i] = (sum_{r in rank order} float(src_r[i])) * inv_scale   (fp32)
+//   sq  += g[i]^2  (fp64)        flag |= !isfinite(g[i])
+// The elements of the batch are cut into tiles of kRelThreads * kU vectors of
+// 8 (16-byte loads per rank); CTA b of a G-CTA grid takes tiles b, b+G, ...,
+// and thread t of a tile handles vectors t, t+256, ... (kU of them, all loads
+// of a tile issued before any is reduced: kU * world 16-byte loads in flight
+// per thread). Each thread accumulates its elements' squares in fp64 in that
+// order (one DFMA each: d*d is exact in fp64, so it rounds like the oracle's
+// multiply-then-add); the CTA reduces its 256 values with a fixed butterfly
+// (warps, then warp 0 over the 8 warp sums) into partial slot b of the step
+// scalar block; the LAST CTA to finish (arrival ticket) adds the G partials in
+// slot order with the same butterfly and adds the total to step_scalars[0].
+// No floating-point atomics: the sum is a fixed function of the inputs and the
+// grid (elx_release_geometry), restated by the oracle
+// (oracle/c/elx_oracle.c: oracle_release_norm_ordered) and bit-exact to it.
 constexpr int kRelThreads = 256;
+constexpr int kRelMaxSeg = ELX_RELEASE_MAX_SEGS;
 
-__device__ __forceinline__ void block_reduce_and_publish(double sq, int bad, double* sc) {
-  __shared__ double s_sq[kRelThreads / 32];
+struct RelBatch {
+  const void* src[kRelMaxSeg][ELX_MAX_WORLD];
+  float* g[kRelMaxSeg];
+  int64_t n[kRelMaxSeg];
+  int64_t tile0[kRelMaxSeg + 1];
+  int32_t nseg;
+};
+
+// Fixed-shape fp64 reduction of one value per thread; thread 0 gets the total.
+// Warp butterfly (xor 16, 8, 4, 2, 1), then warp 0 over the warp sums (zeros
+// for lanes >= warps) with the same butterfly.
+__device__ __forceinline__ double block_sum_fixed(double x, double* s_w) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) s_sq[warp] = sq;
-  const int any_bad = __syncthreads_or(bad);
+  if (lane == 0) s_w[warp] = x;
+  __syncthreads();
+  double y = 0.0;
   if (warp == 0) {
-    double x = lane < (int)(blockDim.x >> 5) ? s_sq[lane] : 0.0;
+    y = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0.0;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
-    if (lane == 0) {
-      if (x != 0.0) atomicAdd(sc, x);
-      if (any_bad) sc[1] = 1.0;
-    }
+    for (int o = 16; o > 0; o >>= 1) y += __shfl_xor_sync(0xffffffffu, y, o);
+  }
+  __syncthreads();  // s_w may be reused
+  return y;
+}
+
+// Per-CTA partial -> slot; the last CTA folds the slots in order into sc[0].
+__device__ __forceinline__ void publish_partial(double sq, int bad, double* sc) {
+  __shared__ double s_w[kRelThreads / 32];
+  __shared__ int s_last;
+  const int any_bad = __syncthreads_or(bad);
+  const double part = block_sum_fixed(sq, s_w);
+  if (threadIdx.x == 0) {
+    sc[ELX_SC_PARTIALS + blockIdx.x] = part;
+    if (any_bad) sc[1] = 1.0;
+    __threadfence();
+    unsigned int* ticket = reinterpret_cast<unsigned int*>(sc + ELX_SC_TICKET);
+    s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  double x = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) x += __ldcg(sc + ELX_SC_PARTIALS + i);
+  const double tot = block_sum_fixed(x, s_w);
+  if (threadIdx.x == 0) {
+    sc[0] = sc[0] + tot;
+    *reinterpret_cast<unsigned int*>(sc + ELX_SC_TICKET) = 0u;
   }
 }
 
-// Sum of squares of one fp32 value into an fp64 accumulator. d*d is exact in
-// fp64 (a 24-bit significand squared fits in 53 bits, and the exponent range
-// of a float squared fits fp64's), so one DFMA rounds exactly like the
-// separate multiply + add the oracle performs.
 __device__ __forceinline__ double sq_acc(double sq, float a) {
   const double d = (double)a;
   return __fma_rn(d, d, sq);
@@ -332,189 +391,212 @@ __device__ __forceinline__ double sq_acc(double sq, float a) {
 
 // Overflow flag from the accumulated sum of squares: a finite float squares
 // to a finite double (<= 1.2e77) and no sum of < 2^60 of them overflows fp64,
-// so sq is non-finite exactly when some element was inf/nan. This replaces a
-// per-element isfinite test (two instructions per element) by one per thread.
+// so sq is non-finite exactly when some element was inf/nan.
 __device__ __forceinline__ int bad_of(double sq) { return !isfinite(sq); }
 
-// World-1 release (norm + overflow only, no gradient written): the gradient
-// stays in the compute-dtype chunk (K4 reads it in place), so this pass reads
-// 2 B/element and produces sum(g^2) and the overflow flag. 16-byte loads (8
-// elements), kU of them in flight per thread, and occupancy held at >= 4 CTAs
-// per SM by the launch bound: the earlier 4-element / 120-register kernel ran
-// at 25% occupancy and 3.4 TB/s (ncu). kScaleOne skips
-// the multiply by inv_scale == 1 (an exact identity).
-template <typename T16, bool kScaleOne, int kU>
-__global__ void __launch_bounds__(kRelThreads, 4) release_norm_kernel(const uint4* __restrict__ src, int64_t n,
-                                                              float inv_scale, double* sc) {
-  const int64_t nv = n >> 3;
-  double sq = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * kU;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kU + threadIdx.x; i0 < nv; i0 += stride) {
-    uint4 raw[kU];
+template <typename T16>
+__device__ __forceinline__ void unpack8(const uint4& q, float* f) {
+  const T16* h = reinterpret_cast<const T16*>(&q);
 #pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int64_t i = i0 + (int64_t)u * blockDim.x;
-      raw[u] = i < nv ? ld_stream(src + i) : make_uint4(0, 0, 0, 0);  // zero bits: +0.0, adds nothing
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const T16* h = reinterpret_cast<const T16*>(&raw[u]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        float a = to_f32<T16>(h[e]);
-        if (!kScaleOne) a = __fmul_rn(a, inv_scale);
-        sq = sq_acc(sq, a);
-      }
-    }
-  }
-  if (blockIdx.x == 0) {  // scalar tail (n % 8)
-    const T16* s = reinterpret_cast<const T16*>(src);
-    for (int64_t i = (nv << 3) + threadIdx.x; i < n; i += blockDim.x) {
-      float a = to_f32<T16>(s[i]);
-      if (!kScaleOne) a = __fmul_rn(a, inv_scale);
-      sq = sq_acc(sq, a);
-    }
-  }
-  block_reduce_and_publish(sq, bad_of(sq), sc);
+  for (int e = 0; e < 8; ++e) f[e] = to_f32<T16>(h[e]);
 }
 
-// Vector path: a thread-step reduces 4 consecutive elements from every source
-// (one 8-byte load per rank) and writes one 16-byte float4, so a warp's loads
-// AND stores are each fully contiguous (256 B / 512 B). kU steps per thread are
-// loaded before any is reduced: kU * world loads in flight per thread
-// (kWorld = 0: runtime world, one step at a time).
+// Partial vector (the segment's last < 8 elements): scalar loads, zero bits
+// (+0.0, adds nothing to the sum of squares) past the end.
+__device__ __forceinline__ uint4 ld_tail(const void* p, int64_t v, int64_t n) {
+  union {
+    uint16_t h[8];
+    uint4 q;
+  } u;
+  const uint16_t* s = static_cast<const uint16_t*>(p) + v * 8;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) u.h[e] = (v * 8 + e < n) ? s[e] : (uint16_t)0;
+  return u.q;
+}
+
 template <typename T16, int kWorld, int kU>
-__global__ void __launch_bounds__(kRelThreads) release_kernel(float* __restrict__ g, const PtrBatch src,
-                                                              int world_rt, int64_t n, float inv_scale,
-                                                              double* sc) {
+__global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid_constant__ RelBatch b, int world_rt,
+                                                                    float inv_scale, double* __restrict__ sc) {
   constexpr int kR = kWorld > 0 ? kWorld : 1;
   const int world = kWorld > 0 ? kWorld : world_rt;
-  const int64_t nv = n >> 2;
+  constexpr int64_t kTileVecs = (int64_t)kRelThreads * kU;
+  const int64_t ntiles = b.tile0[b.nseg];
   double sq = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x * kU;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x * kU + threadIdx.x; i0 < nv; i0 += stride) {
-    uint2 raw[kU][kR];
+  int s = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
+    const int64_t n = b.n[s];
+    const int64_t nfull = n >> 3;                 // whole 8-element vectors
+    const int64_t nvec = (n + 7) >> 3;            // vectors incl. the partial one
+    const int64_t v0 = (t - b.tile0[s]) * kTileVecs + threadIdx.x;
+    float* __restrict__ g = b.g[s];
     if (kWorld > 0) {
+      uint4 raw[kU][kR];
 #pragma unroll
       for (int u = 0; u < kU; ++u) {
-        const int64_t i = i0 + (int64_t)u * blockDim.x;
-#pragma unroll
-        for (int r = 0; r < kR; ++r)
-          if (i < nv) raw[u][r] = static_cast<const uint2*>(src.p[r])[i];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int64_t i = i0 + (int64_t)u * blockDim.x;
-      if (i >= nv) break;
-      float acc[4];
-      if (kWorld > 0) {
+        const int64_t v = v0 + (int64_t)u * kRelThreads;
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
-          const T16* h = reinterpret_cast<const T16*>(&raw[u][r]);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
+          const void* p = b.src[s][r];
+          raw[u][r] = v < nfull ? ld_rel(static_cast<const uint4*>(p) + v)
+                                : (v < nvec ? ld_tail(p, v, n) : make_uint4(0, 0, 0, 0));
         }
-      } else {
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int64_t v = v0 + (int64_t)u * kRelThreads;
+        float acc[8];
+        unpack8<T16>(raw[u][0], acc);
+#pragma unroll
+        for (int r = 1; r < kR; ++r) {
+          float x[8];
+          unpack8<T16>(raw[u][r], x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          acc[e] = __fmul_rn(acc[e], inv_scale);
+          sq = sq_acc(sq, acc[e]);
+        }
+        if (g != nullptr && v < nvec) {
+          if (v < nfull) {
+            float4* d = reinterpret_cast<float4*>(g + v * 8);
+            d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (v * 8 + e < n) g[v * 8 + e] = acc[e];
+          }
+        }
+      }
+    } else {  // any world: one vector at a time, ranks in order
+#pragma unroll 1
+      for (int u = 0; u < kU; ++u) {
+        const int64_t v = v0 + (int64_t)u * kRelThreads;
+        float acc[8];
         for (int r = 0; r < world; ++r) {
-          const uint2 q = static_cast<const uint2*>(src.p[r])[i];
-          const T16* h = reinterpret_cast<const T16*>(&q);
+          const void* p = b.src[s][r];
+          const uint4 q = v < nfull ? ld_rel(static_cast<const uint4*>(p) + v)
+                                    : (v < nvec ? ld_tail(p, v, n) : make_uint4(0, 0, 0, 0));
+          float x[8];
+          unpack8<T16>(q, x);
 #pragma unroll
-          for (int e = 0; e < 4; ++e) acc[e] = r == 0 ? to_f32<T16>(h[e]) : __fadd_rn(acc[e], to_f32<T16>(h[e]));
+          for (int e = 0; e < 8; ++e) acc[e] = r == 0 ? x[e] : __fadd_rn(acc[e], x[e]);
+        }
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          acc[e] = __fmul_rn(acc[e], inv_scale);
+          sq = sq_acc(sq, acc[e]);
+        }
+        if (g != nullptr && v < nvec) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            if (v * 8 + e < n) g[v * 8 + e] = acc[e];
         }
       }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        acc[e] = __fmul_rn(acc[e], inv_scale);
-        sq = sq_acc(sq, acc[e]);
-      }
-      if (g) reinterpret_cast<float4*>(g)[i] = make_float4(acc[0], acc[1], acc[2], acc[3]);
     }
   }
-  // Scalar tail (n % 4 elements), handled by block 0.
-  if (blockIdx.x == 0) {
-    for (int64_t i = (nv << 2) + threadIdx.x; i < n; i += blockDim.x) {
+  publish_partial(sq, bad_of(sq), sc);
+}
+
+// Unaligned sources or destination (not 16/32-byte aligned): one element per
+// thread-step, same partial/ticket reduction. Element i of segment s belongs
+// to CTA (i / kRelThreads) % G... (the elements of the batch flattened, grid-stride).
+template <typename T16>
+__global__ void __launch_bounds__(kRelThreads) release_batch_scalar_kernel(const __grid_constant__ RelBatch b,
+                                                                           int world, float inv_scale,
+                                                                           double* __restrict__ sc) {
+  double sq = 0.0;
+  for (int s = 0; s < b.nseg; ++s) {
+    const int64_t n = b.n[s];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
       float a = 0.f;
       for (int r = 0; r < world; ++r) {
-        const float x = to_f32<T16>(static_cast<const T16*>(src.p[r])[i]);
+        const float x = to_f32<T16>(static_cast<const T16*>(b.src[s][r])[i]);
         a = r == 0 ? x : __fadd_rn(a, x);
       }
       a = __fmul_rn(a, inv_scale);
       sq = sq_acc(sq, a);
-      if (g) g[i] = a;
+      if (b.g[s]) b.g[s][i] = a;
     }
   }
-  block_reduce_and_publish(sq, bad_of(sq), sc);
+  publish_partial(sq, bad_of(sq), sc);
 }
 
-// Unaligned fallback: scalar loads for every element.
+// Tile shape per world (vectors of 8 per thread in flight: kU * world).
+constexpr int rel_unroll(int world) { return world == 1 ? 4 : (world <= 4 ? 2 : 1); }
+
+struct RelLaunch {
+  const void* kern;
+  int u;
+};
+
 template <typename T16>
-__global__ void __launch_bounds__(kRelThreads) release_kernel_scalar(float* g, const PtrBatch src, int world,
-                                                                     int64_t n, float inv_scale, double* sc) {
-  double sq = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-    float a = 0.f;
-    for (int r = 0; r < world; ++r) {
-      const float x = to_f32<T16>(static_cast<const T16*>(src.p[r])[i]);
-      a = r == 0 ? x : __fadd_rn(a, x);
-    }
-    a = __fmul_rn(a, inv_scale);
-    sq = sq_acc(sq, a);
-    if (g) g[i] = a;
+RelLaunch rel_kernel(int world, bool vec) {
+  if (!vec) return {(const void*)release_batch_scalar_kernel<T16>, 1};
+  switch (world) {
+    case 1: return {(const void*)release_batch_kernel<T16, 1, rel_unroll(1)>, rel_unroll(1)};
+    case 2: return {(const void*)release_batch_kernel<T16, 2, rel_unroll(2)>, rel_unroll(2)};
+    case 4: return {(const void*)release_batch_kernel<T16, 4, rel_unroll(4)>, rel_unroll(4)};
+    case 8: return {(const void*)release_batch_kernel<T16, 8, rel_unroll(8)>, rel_unroll(8)};
+    default: return {(const void*)release_batch_kernel<T16, 0, 2>, 2};
   }
-  block_reduce_and_publish(sq, bad_of(sq), sc);
+}
+
+// Grid of a release launch: one CTA per tile up to (resident CTAs per SM x
+// SMs), capped at the partial slots of the step-scalar block.
+int rel_grid(const void* kern, int64_t work_ctas) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = std::min<int64_t>((int64_t)sm_count() * per_sm, ELX_RELEASE_MAX_CTAS);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(work_ctas, cap));
+}
+
+// Fill tile prefix sums; returns total tiles.
+int64_t rel_tiles(RelBatch& b, int u) {
+  const int64_t tile_elems = (int64_t)kRelThreads * u * 8;
+  b.tile0[0] = 0;
+  for (int i = 0; i < b.nseg; ++i) b.tile0[i + 1] = b.tile0[i] + (b.n[i] + tile_elems - 1) / tile_elems;
+  return b.tile0[b.nseg];
+}
+
+bool rel_vec_ok(const RelBatch& b, int world) {
+  for (int i = 0; i < b.nseg; ++i) {
+    if (b.g[i] && (reinterpret_cast<uintptr_t>(b.g[i]) & 15u)) return false;
+    for (int r = 0; r < world; ++r)
+      if (reinterpret_cast<uintptr_t>(b.src[i][r]) & 15u) return false;
+  }
+  return true;
 }
 
 template <typename T16>
-int run_release(float* g, const PtrBatch& pb, int64_t n, int world, float inv_scale, double* sc,
-                cudaStream_t st) {
-  bool vec = g == nullptr || aligned16(g);
-  for (int r = 0; r < world; ++r) vec = vec && ((reinterpret_cast<uintptr_t>(pb.p[r]) & 7u) == 0);
-  auto go = [&](auto kern, int64_t work) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelThreads, 0);
-    if (per_sm < 1) per_sm = 1;
-    const int grid = (int)std::max<int64_t>(
-        1, std::min<int64_t>((work + kRelThreads - 1) / kRelThreads, (int64_t)sm_count() * per_sm));
-    kern<<<grid, kRelThreads, 0, st>>>(g, pb, world, n, inv_scale, sc);
-  };
-  const int64_t nv = n >> 2;
-  static int variant = [] {
-    const char* e = getenv("ELX_REL_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  if (world == 1 && g == nullptr && aligned16(pb.p[0]) && (variant == 0 || variant >= 10)) {  // norm/overflow only
-    auto go_norm = [&](auto kern, int u) {
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelThreads, 0);
-      if (per_sm < 1) per_sm = 1;
-      const int64_t work = ((n >> 3) + u - 1) / u;
-      const int grid = (int)std::max<int64_t>(
-          1, std::min<int64_t>((work + kRelThreads - 1) / kRelThreads, (int64_t)sm_count() * per_sm));
-      kern<<<grid, kRelThreads, 0, st>>>(static_cast<const uint4*>(pb.p[0]), n, inv_scale, sc);
-    };
-    if (variant == 10) go_norm(release_norm_kernel<T16, true, 8>, 8);        // sweep variants (ELX_REL_VARIANT)
-    else if (variant == 11) go_norm(release_norm_kernel<T16, true, 2>, 2);
-    else if (inv_scale == 1.0f) go_norm(release_norm_kernel<T16, true, 4>, 4);
-    else go_norm(release_norm_kernel<T16, false, 4>, 4);
-    return check_launch("elx_release (norm)");
-  }
-  if (!vec) {
-    go(release_kernel_scalar<T16>, n);
+int run_release_batch(RelBatch& b, int world, float inv_scale, double* sc, cudaStream_t st) {
+  const bool vec = rel_vec_ok(b, world);
+  const RelLaunch L = rel_kernel<T16>(world, vec);
+  int64_t work;
+  if (vec) {
+    work = rel_tiles(b, L.u);
   } else {
+    int64_t mx = 0;
+    for (int i = 0; i < b.nseg; ++i) mx = std::max(mx, b.n[i]);
+    work = (mx + kRelThreads - 1) / kRelThreads;
+    b.tile0[0] = 0;
+  }
+  if (work == 0) return ELX_OK;
+  const int grid = rel_grid(L.kern, work);
+  if (vec) {
     switch (world) {
-      case 1:
-        // U=8 measured best at world 1 (profiles/r01_kernel_variants.md)
-        if (variant == 1) go(release_kernel<T16, 1, 2>, nv / 2);
-        else if (variant == 2) go(release_kernel<T16, 1, 4>, nv / 4);
-        else go(release_kernel<T16, 1, 8>, nv / 8);
-        break;
-      case 2: go(release_kernel<T16, 2, 2>, nv / 2); break;
-      case 4: go(release_kernel<T16, 4, 2>, nv / 2); break;
-      case 8: go(release_kernel<T16, 8, 1>, nv); break;
-      default: go(release_kernel<T16, 0, 1>, nv); break;
+      case 1: release_batch_kernel<T16, 1, rel_unroll(1)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
+      case 2: release_batch_kernel<T16, 2, rel_unroll(2)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
+      case 4: release_batch_kernel<T16, 4, rel_unroll(4)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
+      case 8: release_batch_kernel<T16, 8, rel_unroll(8)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
+      default: release_batch_kernel<T16, 0, 2><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
     }
+  } else {
+    release_batch_scalar_kernel<T16><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc);
   }
   return check_launch("elx_release");
 }
@@ -1406,22 +1488,71 @@ int elx_peer_sum_f64(double* dst, const double* const* peers, int32_t count, int
   return check_launch("elx_peer_sum_f64");
 }
 
+int elx_release_batch(const elx_release_seg* segs, int32_t nseg, int32_t world, int32_t dtype, float inv_scale,
+                      double* step_scalars, void* stream) {
+  elx::clear_error();
+  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (!step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null step_scalars");
+  if (nseg < 0 || (nseg > 0 && !segs)) return elx::fail(ELX_ERR_VALIDATION, "bad segment table");
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "release dtype must be bf16/f16");
+  cudaStream_t st = (cudaStream_t)stream;
+  // batches of ELX_RELEASE_MAX_SEGS non-empty segments, one launch each, in table order
+  RelBatch b{};
+  b.nseg = 0;
+  auto flush = [&]() -> int {
+    if (b.nseg == 0) return ELX_OK;
+    const int rc = dtype == ELX_BF16 ? run_release_batch<__nv_bfloat16>(b, world, inv_scale, step_scalars, st)
+                                     : run_release_batch<__half>(b, world, inv_scale, step_scalars, st);
+    b = RelBatch{};
+    b.nseg = 0;
+    return rc;
+  };
+  for (int32_t i = 0; i < nseg; ++i) {
+    const elx_release_seg& sg = segs[i];
+    if (sg.n < 0) return elx::fail(ELX_ERR_VALIDATION, "segment %d: negative length", i);
+    if (sg.n == 0) continue;
+    for (int r = 0; r < world; ++r)
+      if (!sg.src[r]) return elx::fail(ELX_ERR_VALIDATION, "segment %d: source %d is null", i, r);
+    for (int r = 0; r < world; ++r) b.src[b.nseg][r] = sg.src[r];
+    b.g[b.nseg] = sg.g;
+    b.n[b.nseg] = sg.n;
+    if (++b.nseg == kRelMaxSeg) {
+      const int rc = flush();
+      if (rc) return rc;
+    }
+  }
+  return flush();
+}
+
 int elx_release(float* grad_shard, const void* const* src, int64_t n, int32_t world, int32_t dtype,
                 float inv_scale, double* step_scalars, void* stream) {
   elx::clear_error();
   if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
   if (!src || !step_scalars) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
   if (n < 0) return elx::fail(ELX_ERR_VALIDATION, "negative length");
-  PtrBatch pb{};
-  for (int r = 0; r < world; ++r) {
-    if (!src[r]) return elx::fail(ELX_ERR_VALIDATION, "source %d is null", r);
-    pb.p[r] = src[r];
-  }
-  if (n == 0) return ELX_OK;
-  cudaStream_t st = (cudaStream_t)stream;
-  if (dtype == ELX_BF16) return run_release<__nv_bfloat16>(grad_shard, pb, n, world, inv_scale, step_scalars, st);
-  if (dtype == ELX_F16) return run_release<__half>(grad_shard, pb, n, world, inv_scale, step_scalars, st);
-  return elx::fail(ELX_ERR_VALIDATION, "release dtype must be bf16/f16");
+  elx_release_seg sg{};
+  sg.g = grad_shard;
+  sg.n = n;
+  for (int r = 0; r < world; ++r) sg.src[r] = src[r];
+  return elx_release_batch(&sg, 1, world, dtype, inv_scale, step_scalars, stream);
+}
+
+int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t dtype, int32_t* ctas,
+                         int32_t* tile_vecs) {
+  elx::clear_error();
+  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (nseg < 0 || nseg > kRelMaxSeg || (nseg > 0 && !n) || !ctas || !tile_vecs)
+    return elx::fail(ELX_ERR_VALIDATION, "bad geometry arguments (1..%d segments)", kRelMaxSeg);
+  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "release dtype must be bf16/f16");
+  RelBatch b{};
+  b.nseg = 0;
+  for (int i = 0; i < nseg; ++i)
+    if (n[i] > 0) b.n[b.nseg++] = n[i];
+  const RelLaunch L = dtype == ELX_BF16 ? rel_kernel<__nv_bfloat16>(world, true) : rel_kernel<__half>(world, true);
+  const int64_t work = rel_tiles(b, L.u);
+  *ctas = work == 0 ? 0 : rel_grid(L.kern, work);
+  *tile_vecs = kRelThreads * L.u;
+  return ELX_OK;
 }
 
 int elx_adam(const elx_adam_seg* segs_dev, int32_t nseg, int64_t ntiles, const elx_adam_hp* hp, int64_t step,

@@ -132,23 +132,69 @@ def peer_sum_f64(dst: torch.Tensor, peer_ptrs: Sequence[int], count: int, stream
     _lib.check(rc, "elx_peer_sum_f64")
 
 
+STEP_SCALARS = _lib.STEP_SCALARS
+
+
+def new_step_scalars(device) -> torch.Tensor:
+    """A zeroed step-scalar block (include/elixir_b200.h, K3): [0] sum of
+    squares, [1] overflow flag, [2] completed steps, then the release kernels'
+    arrival ticket and per-CTA partial slots (deterministic norm)."""
+    return torch.zeros(STEP_SCALARS, dtype=torch.float64, device=device)
+
+
+def _check_scalars(step_scalars: torch.Tensor) -> None:
+    if step_scalars.dtype != torch.float64 or not step_scalars.is_cuda or not step_scalars.is_contiguous():
+        raise ValidationError("step_scalars must be a contiguous CUDA float64 tensor")
+    if step_scalars.numel() < STEP_SCALARS:
+        raise ValidationError(f"step_scalars must hold the {STEP_SCALARS}-double step-scalar block "
+                              "(kernels.new_step_scalars)")
+
+
 def release(grad_shard: torch.Tensor | None, src_ptrs: Sequence[int], n: int, dtype: torch.dtype,
             inv_scale: float, step_scalars: torch.Tensor, stream=None) -> None:
     """K3: grad_shard[:n] = (sum_r src_r[:n] in rank order, fp32) * inv_scale,
-    accumulating sum(g^2) into step_scalars[0] and overflow into step_scalars[1].
-    grad_shard=None: norm/overflow only (world-1 in-place chunks)."""
+    accumulating sum(g^2) into step_scalars[0] (fixed order, deterministic) and
+    overflow into step_scalars[1]. grad_shard=None: norm/overflow only (world-1
+    in-place chunks)."""
+    release_batch([(grad_shard, src_ptrs, n)], dtype, inv_scale, step_scalars, stream=stream)
+
+
+def release_batch(segs: Sequence[tuple[torch.Tensor | None, Sequence[int], int]], dtype: torch.dtype,
+                  inv_scale: float, step_scalars: torch.Tensor, stream=None) -> None:
+    """K3 over several segments in ONE launch (per 16 segments): every chunk due
+    at one reduce position. segs: (grad_shard or None, per-rank source device
+    pointers, valid elements n)."""
     lib = _lib.load()
-    if grad_shard is not None:
-        _cuda(grad_shard, "grad_shard")
-        if grad_shard.dtype != torch.float32 or grad_shard.numel() < n:
-            raise ValidationError("grad_shard must be float32 with >= n elements")
-    if step_scalars.dtype != torch.float64 or not step_scalars.is_cuda:
-        raise ValidationError("step_scalars must be a CUDA float64 tensor")
-    arr = _ptr_array(src_ptrs)
-    rc = lib.elx_release(None if grad_shard is None else grad_shard.data_ptr(), ctypes.addressof(arr), int(n),
-                         len(src_ptrs),
-                         elx_dtype(dtype), float(inv_scale), step_scalars.data_ptr(), _stream(stream))
-    _lib.check(rc, "elx_release")
+    _check_scalars(step_scalars)
+    if not segs:
+        return
+    world = len(segs[0][1])
+    arr = (_lib.ReleaseSeg * len(segs))()
+    for i, (g, ptrs, n) in enumerate(segs):
+        if len(ptrs) != world:
+            raise ValidationError("every release segment needs one source per rank")
+        if g is not None:
+            _cuda(g, "grad_shard")
+            if g.dtype != torch.float32 or g.numel() < n:
+                raise ValidationError("grad_shard must be float32 with >= n elements")
+        arr[i].g = None if g is None else g.data_ptr()
+        for r, p in enumerate(ptrs):
+            arr[i].src[r] = p
+        arr[i].n = int(n)
+    rc = lib.elx_release_batch(ctypes.addressof(arr), len(segs), world, elx_dtype(dtype), float(inv_scale),
+                               step_scalars.data_ptr(), _stream(stream))
+    _lib.check(rc, "elx_release_batch")
+
+
+def release_geometry(lengths: Sequence[int], world: int, dtype: torch.dtype = torch.bfloat16) -> tuple[int, int]:
+    """(ctas, tile_vecs) of one K3 launch over segments of these lengths on the
+    current device: the fixed summation order of its sum of squares."""
+    lib = _lib.load()
+    n = (ctypes.c_int64 * max(1, len(lengths)))(*[int(x) for x in lengths])
+    a, b = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(lib.elx_release_geometry(ctypes.addressof(n), len(lengths), int(world), elx_dtype(dtype),
+                                        ctypes.byref(a), ctypes.byref(b)), "elx_release_geometry")
+    return a.value, b.value
 
 
 class AdamTable:
@@ -291,9 +337,14 @@ def colsum(x2d: torch.Tensor, out: torch.Tensor, stream=None) -> None:
         raise ValidationError("colsum needs a 2-D input and out of x2d.shape[1] elements")
     rows, cols = x2d.shape
     nws = lib.elx_colsum_workspace(rows, cols)
-    ws = torch.empty(nws, dtype=torch.float32, device=x2d.device).data_ptr() if nws > 0 else None
+    # the workspace lives until the launch is enqueued, and the allocator may hand its memory out again
+    # only once the launch stream has passed it (record_stream), whatever stream that is
+    ws = torch.empty(nws, dtype=torch.float32, device=x2d.device) if nws > 0 else None
+    st = stream if stream is not None else torch.cuda.current_stream(x2d.device)
     rc = lib.elx_colsum(out.data_ptr(), elx_dtype(out.dtype), x2d.data_ptr(), elx_dtype(x2d.dtype), rows, cols,
-                        ws, _stream(stream))
+                        None if ws is None else ws.data_ptr(), st.cuda_stream)
+    if ws is not None:
+        ws.record_stream(st)
     _lib.check(rc, "elx_colsum")
 
 

@@ -203,11 +203,11 @@ class ChunkManager:
         # step scalars: [0] sum g^2, [1] overflow flag (elx_release / elx_adam); on the P2P path
         # peer-mapped, so the N-scalar all-reduce is a rank-ordered read of the peers' values
         if self.p2p:
-            self.step_scalars = self.transport.alloc((4,), torch.float64, dev)
+            self.step_scalars = self.transport.alloc((kernels.STEP_SCALARS,), torch.float64, dev)
             self.peer_scalars = self.transport.peer_ptrs(self.step_scalars)
             self._scalar_tmp = torch.zeros(2, dtype=torch.float64, device=dev)
         else:
-            self.step_scalars = torch.zeros(4, dtype=torch.float64, device=dev)
+            self.step_scalars = kernels.new_step_scalars(dev)
             self.peer_scalars = None
         self._bound: dict[int, torch.Tensor] = {}   # chunk -> storage it is bound to
         self._views: dict[str, torch.Tensor] = {}
@@ -398,19 +398,22 @@ class ChunkFetcher:
         self.pos = 0
         self._fenced = False
         self.deferred: dict[int, list] = {}
+        self._dirty: set[int] = set()   # P2P: blocks released since the last device barrier
 
     def begin_step(self, after: torch.cuda.Event | None = None) -> None:
-        """Start a walk. On the P2P path every rank must have finished its
-        previous optimizer step (which rewrote the shards peers will read)
-        before anyone fetches: one device barrier on the comm stream."""
+        """Start a walk. The comm stream is forked from the compute stream
+        (and made to wait on `after`, the previous optimizer step's event):
+        every gather of this step reads shards that step's K4 rewrote — on
+        every transport, not only P2P — and during a CUDA graph capture the
+        fork brings the comm stream into the capture. On the P2P path every
+        rank must also have finished its previous optimizer step before anyone
+        reads its shards: one device barrier on the comm stream."""
         self._reset()
+        self.comm.wait_stream(torch.cuda.current_stream(self.mgr.device))
+        if after is not None:
+            self.comm.wait_event(after)
         if self.mgr.p2p:
-            # fork the comm stream from the compute stream: orders it after this rank's previous
-            # step and, during a CUDA graph capture, brings it into the capture
-            self.comm.wait_stream(torch.cuda.current_stream(self.mgr.device))
             with torch.cuda.stream(self.comm):
-                if after is not None:
-                    self.comm.wait_event(after)
                 self.mgr.transport.device_barrier()
 
     # ------------------------------------------------------------ walk
@@ -450,9 +453,8 @@ class ChunkFetcher:
         ev.record(torch.cuda.current_stream(self.mgr.device))
         for c in self.walk[pos]:
             self.last_use[c] = ev
-        if pos >= self.n_fwd:
-            for c in self.reduces[pos]:
-                self._release(c, ev)
+        if pos >= self.n_fwd and self.reduces[pos]:
+            self._release_group(self.reduces[pos], ev)
         self.pos = pos + 1
 
     # names used by SURVEY.md §8b for the reference runtime's chunk-fetcher
@@ -510,6 +512,8 @@ class ChunkFetcher:
                 comm.wait_event(self.last_use[victim])
             if not cpu and opt is not None:
                 opt.wait_gpu(c, comm)
+            if mgr.p2p and b in self._dirty:
+                self._barrier()  # peers may still be reading block b's gradients (released since the last barrier)
             seg = block[mgr.rank * mgr.S:(mgr.rank + 1) * mgr.S]
             if mgr.p2p and not cpu:
                 # K2 over NVLink: read every rank's shard of c straight from its HBM
@@ -530,10 +534,10 @@ class ChunkFetcher:
                     # every rank has landed its segment of block b; read the others' over peer memory
                     es = block.element_size()
                     off = b * mgr.P * es
-                    mgr.transport.device_barrier()
+                    self._barrier()
                     kernels.fetch(block, [p + off + r * mgr.S * es for r, p in enumerate(mgr.peer_blocks)], mgr.S,
                                   stream=comm, engine=getattr(mgr.transport, "fetch_engine", "sm"))
-                    mgr.transport.device_barrier()  # peers may reuse block b only after every rank read it
+                    self._barrier()  # peers may reuse block b (its gradients, later) only after every rank read it
                 elif mgr.world > 1:
                     mgr.transport.gather(block, seg)
             else:
@@ -545,23 +549,47 @@ class ChunkFetcher:
         self.ready[c] = ev
         mgr.bind(c, block)
 
-    def _release(self, c: int, grads_written: torch.cuda.Event) -> None:
-        """Reduce-scatter chunk c's gradients into this rank's fp32 shard (K3)."""
-        with _nvtx(f"elx.release c{c}"):
-            self._release_impl(c, grads_written)
+    def release(self, chunks) -> None:
+        """Release chunk(s) now (SURVEY.md §8b `release(chunk)`): the
+        reduce-scatter of their gradients, written by the current stream, into
+        this rank's fp32 shards with the unscale, the sum of squares and the
+        overflow flag — one K3 launch for all of them. The schedule replay
+        calls this itself at each chunk's reduce position (after_compute)."""
+        cs = [int(chunks)] if isinstance(chunks, int) else [int(c) for c in chunks]
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.mgr.device))
+        self._release_group(cs, ev)
 
-    def _release_impl(self, c: int, grads_written: torch.cuda.Event) -> None:
+    def _barrier(self) -> None:
+        """Device barrier on the comm stream (P2P). Every rank has then finished
+        its earlier comm work, including its K3 reads of our blocks."""
+        self.mgr.transport.device_barrier()
+        self._dirty.clear()
+
+    def _release_group(self, cs, grads_written: torch.cuda.Event) -> None:
+        with _nvtx(f"elx.release {cs}"):
+            self._release_impl(cs, grads_written)
+
+    def _release_impl(self, cs, grads_written: torch.cuda.Event) -> None:
+        """Every chunk due at one reduce position (rcache_sim.py:160-167): one
+        K3 launch over all of them (per-chunk launches only for CPU-home chunks
+        at N > 1, which share the fp32 staging buffer of their D2H). On the P2P
+        path one device barrier precedes it (every rank's gradients are in its
+        blocks); the blocks are then 'dirty' — peers may still be reading them
+        — until the next barrier, which a gather into one of them issues first."""
         mgr = self.mgr
-        n = mgr.valid(c)
         comm = self.comm
-        storage = mgr.storage(c)
-        self.live["reduce_ops"] += 1
-        cpu = mgr.homes[c] is Device.CPU
-        if cpu:
-            self.live["g2c_units"] += 1
         opt = self.optimizer
-        if cpu and opt is not None:
-            opt.wait_offloaded(c, self.comm)  # previous update still reading the host grad shard
+        es = mgr.p16.element_size()
+        batch, staged = [], []
+        for c in cs:
+            self.live["reduce_ops"] += 1
+            cpu = mgr.homes[c] is Device.CPU
+            if cpu:
+                self.live["g2c_units"] += 1
+                if opt is not None:
+                    opt.wait_offloaded(c, self.comm)  # previous update still reading the host grad shard
+            (staged if cpu and not mgr.fused_w1 else batch).append(c)
         with torch.cuda.stream(comm):
             comm.wait_event(grads_written)
             if not self._fenced and opt is not None and opt.done_event is not None:
@@ -570,42 +598,52 @@ class ChunkFetcher:
             if self.time_release:
                 t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 t0.record(comm)
-            if mgr.world == 1:
-                srcs = [storage.data_ptr()]
-            elif mgr.p2p:
-                # K3 over NVLink: once every rank's gradients are in its copy of
-                # block b, read segment `rank` of all of them in rank order.
-                b = self.block_of[c]
-                es = storage.element_size()
-                off = (b * mgr.P + mgr.rank * mgr.S) * es
-                mgr.transport.device_barrier()
-                srcs = [p + off for p in mgr.peer_blocks]
-                self.bytes_moved["scatter"] += (mgr.world - 1) * mgr.S * es
-            else:
-                mgr.transport.scatter(mgr.recv, storage)
-                self.bytes_moved["scatter"] += (mgr.world - 1) * mgr.S * storage.element_size()
-                es = mgr.recv.element_size()
-                srcs = [mgr.recv.data_ptr() + r * mgr.S * es for r in range(mgr.world)]
-            r = mgr.row[c]
-            target = None if mgr.fused_w1 else (mgr.g32[r] if not cpu else mgr.stage32)
-            if n > 0:
-                kernels.release(target, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
             if mgr.p2p:
-                mgr.transport.device_barrier()  # peers may reuse block b only after every rank read it
+                self._barrier()
+            segs = []
+            for c in batch:
+                if mgr.valid(c) > 0:
+                    segs.append((None if mgr.fused_w1 else mgr.g32[mgr.row[c]], self._release_srcs(c), mgr.valid(c)))
+            if segs:
+                kernels.release_batch(segs, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
             if self.time_release:
                 t1.record(comm)
-                self.release_events.append((t0, t1, n))
-            if cpu and n > 0:
-                src = storage if mgr.fused_w1 else mgr.stage32
+                self.release_events.append((t0, t1, sum(n for _, _, n in segs)))
+            for c in cs:
+                if mgr.world > 1:
+                    self.bytes_moved["scatter"] += (mgr.world - 1) * mgr.S * es
+                if mgr.p2p:
+                    self._dirty.add(self.block_of[c])
+                n = mgr.valid(c)
+                if mgr.homes[c] is not Device.CPU or n == 0:
+                    continue
+                if c in staged:  # CPU-home at N > 1: reduce into the fp32 staging shard, then D2H it
+                    kernels.release(mgr.stage32, self._release_srcs(c), n, mgr.dtype, self.inv_scale,
+                                    mgr.step_scalars, stream=comm)
+                src = mgr.storage(c) if mgr.fused_w1 else mgr.stage32
                 nbytes = n * src.element_size()
                 if self.time_release:
                     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                     c0.record(comm)
-                kernels.copy_d2h(mgr.h_g32[r], src, nbytes, stream=comm)
+                kernels.copy_d2h(mgr.h_g32[mgr.row[c]], src, nbytes, stream=comm)
                 if self.time_release:
                     c1.record(comm)
                     self.copy_events.append(("d2h", c0, c1, nbytes))
                 self.bytes_moved["d2h"] += nbytes
+
+    def _release_srcs(self, c: int) -> list[int]:
+        """Per-rank device pointers of this rank's segment of chunk c's gradients."""
+        mgr = self.mgr
+        storage = mgr.storage(c)
+        es = storage.element_size()
+        if mgr.world == 1:
+            return [storage.data_ptr()]
+        if mgr.p2p:
+            # K3 over NVLink: segment `rank` of every rank's copy of block b, in rank order
+            off = (self.block_of[c] * mgr.P + mgr.rank * mgr.S) * es
+            return [p + off for p in mgr.peer_blocks]
+        mgr.transport.scatter(mgr.recv, storage)
+        return [mgr.recv.data_ptr() + r * mgr.S * es for r in range(mgr.world)]
 
     def release_shared(self, sp: _SharedParam) -> None:
         """Release of a shared parameter's gradient (after its last use)."""
@@ -622,8 +660,10 @@ class ChunkFetcher:
             if mgr.world == 1:
                 srcs = [sp.grad.data_ptr()]
             elif mgr.p2p:
-                # K3 straight over every rank's replicated gradient (segment `rank`)
-                mgr.transport.device_barrier()
+                # K3 straight over every rank's replicated gradient (segment `rank`); peers may read our
+                # gradient until the next barrier (the optimizer step's scalar all-reduce), and it is
+                # rewritten only in the next step's backward, after begin_step's barrier
+                self._barrier()
                 es = sp.grad.element_size()
                 srcs = [p + mgr.rank * sp.shard * es for p in mgr.peer_shared[sp.pid][1]]
             else:
@@ -633,11 +673,15 @@ class ChunkFetcher:
                 es = recv.element_size()
                 srcs = [recv.data_ptr() + r * sp.shard * es for r in range(mgr.world)]
             n = sp.valid(mgr.rank)
+            if self.time_release:
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record(comm)
             if n > 0:
                 kernels.release(None if mgr.fused_w1 else sp.g32, srcs, n, mgr.dtype, self.inv_scale,
                                 mgr.step_scalars, stream=comm)
-            if mgr.p2p and mgr.world > 1:
-                mgr.transport.device_barrier()  # peers read our gradient before it is rewritten
+            if self.time_release:
+                t1.record(comm)
+                self.release_events.append((t0, t1, n))
 
 
 class StepStats:
@@ -778,7 +822,7 @@ class HybridAdam:
         self._tile = T
         self.h2d_stream = torch.cuda.Stream(device=dev)
         self.xfer_stream = torch.cuda.Stream(device=dev)
-        self.sc_stream = torch.zeros(4, dtype=torch.float64, device=dev)
+        self.sc_stream = torch.zeros(4, dtype=torch.float64, device=dev)  # K4 reads [0..2] only
 
     def _slot_table(self, s: int, cnt: int) -> kernels.AdamTable:
         key = (s, cnt)
@@ -948,7 +992,7 @@ class HybridAdam:
             cur.wait_event(releases_done)
         m.all_reduce_scalars()
         slot = self._host_ring[self._issued % len(self._host_ring)]
-        slot.copy_(m.step_scalars, non_blocking=True)
+        slot.copy_(m.step_scalars[:4], non_blocking=True)
         snap = torch.cuda.Event()
         snap.record(cur)
         stats = StepStats(slot, snap)
@@ -964,7 +1008,7 @@ class HybridAdam:
             if not found_inf:
                 self._host_steps += 1
         if self.stream_segs:
-            self.sc_stream.copy_(m.step_scalars)  # snapshot before the opt stream's step_advance
+            self.sc_stream.copy_(m.step_scalars[:4])  # snapshot before the opt stream's step_advance
         opt = self.stream if self.overlap else cur
         if opt is not cur:
             opt.wait_stream(cur)

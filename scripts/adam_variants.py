@@ -22,7 +22,7 @@ if fused:
     p16.copy_(g)
 tab = kernels.AdamTable([(p32[i], m[i], v[i], p16[i] if fused else g[i], p16[i], per) for i in range(segs_n)], dev)
 bpe = 28 if fused else 30
-sc = torch.zeros(4, dtype=torch.float64, device=dev)
+sc = kernels.new_step_scalars(dev)
 hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
 
 

@@ -10,7 +10,7 @@ p32 = torch.randn(segs_n, per, device=dev, generator=g) * 0.02
 m = torch.zeros_like(p32); v = torch.zeros_like(p32)
 p16 = p32.to(torch.bfloat16)
 tab = kernels.AdamTable([(p32[i], m[i], v[i], p16[i], p16[i], per) for i in range(segs_n)], dev)
-sc = torch.zeros(4, dtype=torch.float64, device=dev)
+sc = kernels.new_step_scalars(dev)
 hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=0.0)
 x = torch.randn(8192, 2048, device=dev, generator=g).to(torch.bfloat16)
 w = torch.randn(8192, 2048, device=dev, generator=g).to(torch.bfloat16)

@@ -65,7 +65,7 @@ def measure(n_elems: int = 64 * 2 ** 20, cpu_elems: int = 32 * 2 ** 20):
     f = lambda: torch.randn(n_elems, device=dev) * 1e-3
     p32, m, v, g = f(), f(), f().abs(), f()
     tab = kernels.AdamTable([(p32, m, v, g, d, n_elems)], dev)
-    sc = torch.zeros(4, dtype=torch.float64, device=dev)
+    sc = kernels.new_step_scalars(dev)
     hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=0.0)
     for _ in range(20):
         kernels.adam(tab, hp, 2, sc, torch.bfloat16)

@@ -47,7 +47,7 @@ for engine in ("sm", "ce"):
     assert np.array_equal(bits(block), arith.gather([bits(s) for s in shards]))
 
 # K3 release (world 4 with output; world 1 norm-only incl. tail)
-sc = torch.zeros(4, dtype=torch.float64, device=dev)
+sc = kernels.new_step_scalars(dev)
 out = torch.empty(40_000, device=dev)
 kernels.release(out, [s.data_ptr() for s in shards], 39_997, bf, 0.5, sc)
 kernels.release(None, [shards[0].data_ptr()], 39_999, bf, 1.0, sc)

@@ -17,7 +17,11 @@ allocations, ordered by elx_device_barrier over IPC-mapped signal pads;
 "ipc-ce" does the same with K2 on the copy engines (elx_fetch_ce); "ipc-graph"
 captures the second step as one CUDA graph per rank (the ranks' graphs meet
 at device-numbered barriers) and replays it. A "-keep" suffix runs the step
-with the forward graphs kept instead of recomputed (recompute=False).
+with the forward graphs kept instead of recomputed (recompute=False). A
+"-nosync" suffix trains three steps with no host synchronisation between them
+(losses kept on the device, read at the end): the comm stream's gathers of
+step s+1 must be ordered after step s's optimizer update by the runtime's own
+stream/event ordering, not by a host sync.
 """
 
 import json
@@ -52,19 +56,24 @@ def main():
         transport = IpcTransport(fetch_engine="ce" if path == "ipc-ce" else "sm")
     else:
         transport = TorchDistTransport()
+    nosync = path.endswith("-nosync")
+    path = path.removesuffix("-nosync")
     keep = path.endswith("-keep")  # the bench's mode: forward graphs kept instead of recomputed
     path = path.removesuffix("-keep")
     model = ElixirGPT2(CFG, plan, device=dev, transport=transport, init=init, recompute=not keep, **HP)
     assert model.keep_graph == keep
     assert model.manager.p2p == path.startswith("ipc")
     losses = []
-    for s in range(2):
+    for s in range(3 if nosync else 2):
         tok, tgt = _batches(world, s, dev)[rank]
         if path == "ipc-graph" and s == 1:  # step 1 replays a CUDA graph captured on every rank
             model.capture(tok, tgt, warmup=0)
-            losses.append(model.graph_step(tok, tgt).item())
+            losses.append(model.graph_step(tok, tgt).clone())
         else:
-            losses.append(model.train_step(tok, tgt).item())
+            losses.append(model.train_step(tok, tgt).clone())
+        if not nosync:
+            losses[-1] = losses[-1].item()
+    losses = [float(x) for x in losses]
     model.synchronize()
     torch.cuda.synchronize()
     rec = {"losses": np.array(losses, np.float64), "counters": np.array(json.dumps(model.fetcher.counters()))}

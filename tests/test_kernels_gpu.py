@@ -125,12 +125,15 @@ def test_release_bit_exact(cuda, dtype, world, n):
     srcs = [(torch.randn(n, generator=g) * 3.0).to(dtype) for _ in range(world)]
     dsrc = [s.to(cuda) for s in srcs]
     out = torch.full((n,), -1.0, device=cuda)
-    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc = kernels.new_step_scalars(cuda)
     kernels.release(out, [t.data_ptr() for t in dsrc], n, dtype, 1.0 / 128, sc)
     torch.cuda.synchronize()
     wg, wsq, wbad = arith.release([_bits(s) for s in srcs], 1.0 / 128, _name(dtype))
     assert np.array_equal(out.cpu().numpy(), wg)
     assert sc[0].item() == pytest.approx(wsq, rel=1e-12)
+    # the sum of squares in the kernel's fixed order (no atomics) is bit-exact to the oracle's restatement
+    ctas, tv = kernels.release_geometry([n], world, dtype)
+    assert sc[0].item() == arith.release_norm_ordered([wg], ctas, tv)
     assert sc[1].item() == 0.0 and not wbad
 
 
@@ -139,7 +142,7 @@ def test_release_unaligned_sources_use_scalar_path(cuda):
     g = torch.Generator().manual_seed(5)
     base = [torch.randn(n + 1, generator=g).to(torch.bfloat16).to(cuda) for _ in range(world)]
     out = torch.zeros(n, device=cuda)
-    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc = kernels.new_step_scalars(cuda)
     kernels.release(out, [b.data_ptr() + 2 for b in base], n, torch.bfloat16, 1.0, sc)
     wg, wsq, _ = arith.release([_bits(b)[1:] for b in base], 1.0)
     assert np.array_equal(out.cpu().numpy(), wg)
@@ -160,22 +163,61 @@ def test_release_norm_only_world1(cuda, dtype, inv_scale, n, bad):
     if bad is not None:
         src[(n * 7) // 11] = float(bad)
     d = src.to(cuda)
-    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc = kernels.new_step_scalars(cuda)
     kernels.release(None, [d.data_ptr()], n, dtype, inv_scale, sc)
     torch.cuda.synchronize()
-    _, wsq, wbad = arith.release([_bits(src)], inv_scale, _name(dtype))
+    wg, wsq, wbad = arith.release([_bits(src)], inv_scale, _name(dtype))
     assert sc[1].item() == (1.0 if wbad else 0.0)
     assert wbad == (bad is not None)
     if not wbad:
         assert sc[0].item() == pytest.approx(wsq, rel=1e-12)
+        ctas, tv = kernels.release_geometry([n], 1, dtype)
+        assert sc[0].item() == arith.release_norm_ordered([wg], ctas, tv)
     # 8-byte aligned but not 16: same answer through the general path
     if n > 8 and bad is None:
         buf = torch.zeros(n + 4, dtype=dtype, device=cuda)
         buf[4:] = d
-        sc2 = torch.zeros(4, dtype=torch.float64, device=cuda)
+        sc2 = kernels.new_step_scalars(cuda)
         kernels.release(None, [buf.data_ptr() + 8], n, dtype, inv_scale, sc2)
         torch.cuda.synchronize()
         assert sc2[0].item() == pytest.approx(wsq, rel=1e-12) and sc2[1].item() == 0.0
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8, 3])
+def test_release_batch_one_launch_bit_exact(cuda, world):
+    """Every chunk due at one reduce position in ONE K3 launch: ragged segment
+    lengths (tails of 1..7 elements, an empty one), fp32 outputs or none (the
+    world-1 norm pass), 20 segments (two launches of 16 + 4): released values
+    bit-exact, the sum of squares bit-exact to the oracle's fixed-order
+    restatement per launch, and identical on a second run (deterministic)."""
+    rng = np.random.default_rng(world)
+    lens = [int(x) for x in rng.integers(1, 300_000, 20)]
+    lens[3], lens[7], lens[11] = 0, 5, 8 * 4096 + 3
+    srcs, outs, segs, want = [], [], [], []
+    for i, n in enumerate(lens):
+        hs = [arith.f32_to_bf16_bits((rng.standard_normal(n) * 2).astype(np.float32)) for _ in range(world)]
+        ds = [torch.from_numpy(h.view(np.int16).copy()).view(torch.bfloat16).to(cuda) for h in hs]
+        srcs.append(ds)
+        o = None if (world == 1 and i % 2) else torch.full((max(n, 1),), -1.0, device=cuda)
+        outs.append(o)
+        segs.append((o, [d.data_ptr() for d in ds], n))
+        want.append(arith.release(hs, 0.25)[0])
+    sc = kernels.new_step_scalars(cuda)
+    kernels.release_batch(segs, torch.bfloat16, 0.25, sc)
+    torch.cuda.synchronize()
+    nz = [i for i, n in enumerate(lens) if n > 0]
+    total = 0.0
+    for part in (nz[:16], nz[16:]):
+        ctas, tv = kernels.release_geometry([lens[i] for i in part], world)
+        total = total + arith.release_norm_ordered([want[i] for i in part], ctas, tv)
+    assert sc[0].item() == total
+    for o, w, n in zip(outs, want, lens):
+        if o is not None and n > 0:
+            assert np.array_equal(o[:n].cpu().numpy(), w)
+    sc2 = kernels.new_step_scalars(cuda)
+    kernels.release_batch(segs, torch.bfloat16, 0.25, sc2)
+    torch.cuda.synchronize()
+    assert sc2[0].item() == sc[0].item() and sc2[1].item() == 0.0
 
 
 def test_release_accumulates_norm_and_flags_overflow(cuda):
@@ -184,7 +226,7 @@ def test_release_accumulates_norm_and_flags_overflow(cuda):
     a = torch.randn(n, generator=g).to(torch.bfloat16)
     b = torch.randn(n, generator=g).to(torch.bfloat16)
     b[12345] = float("inf")
-    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc = kernels.new_step_scalars(cuda)
     out = torch.zeros(n, device=cuda)
     kernels.release(out, [a.to(cuda).data_ptr()], n, torch.bfloat16, 1.0, sc)
     first = sc[0].item()
@@ -225,7 +267,7 @@ def test_adam_bit_exact_multi_segment_multi_step(cuda, misalign):
     sizes = [1, 3, 4096, 4097, 12_288, 1_000_003]
     host, dev = _segments(cuda, sizes, 11, misalign)
     table = kernels.AdamTable(dev, cuda)
-    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc = kernels.new_step_scalars(cuda)
     for step in range(1, 4):
         sq = float(sum(np.dot(h[3].astype(np.float64), h[3]) for h in host))
         sc[0] = sq
@@ -263,7 +305,7 @@ def test_adam_f16_output(cuda):
     p16 = torch.zeros(9999, dtype=torch.float16, device=cuda)
     dev = [(d[0], d[1], d[2], d[3], p16, d[5]) for d in dev]
     table = kernels.AdamTable(dev, cuda)
-    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc = kernels.new_step_scalars(cuda)
     hp = dict(HP, max_norm=0.0)
     kernels.adam(table, hp, 2, sc, torch.float16)
     h = host[0]
@@ -299,7 +341,7 @@ def test_offload_copies_round_trip(cuda):
 
 def test_launch_counter_counts_kernels(cuda):
     before = _lib.launch_count()
-    sc = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc = kernels.new_step_scalars(cuda)
     kernels.step_reset(sc)
     kernels.step_reset(sc)
     assert _lib.launch_count() - before == 2
@@ -334,7 +376,7 @@ pb16 = torch.from_numpy(gb.view(np.int16).copy()).view(torch.bfloat16).to(dev)
 segs.append((tb[0], tb[1], tb[2], pb16, pb16, nb))
 tab = kernels.AdamTable(segs, dev)
 hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=1.0)
-sc = torch.zeros(4, dtype=torch.float64, device=dev)
+sc = kernels.new_step_scalars(dev)
 for step in (1,):
     sq = float(sum(np.dot(h[3].astype(np.float64), h[3]) for h in host))
     sc[0] = sq
@@ -395,7 +437,7 @@ def test_adam_compute_dtype_grads_equal_released_path(cuda):
             segs.append((P, M, V, torch.from_numpy(g).to(cuda), torch.empty_like(p16), n))
     sc = torch.tensor([sq, 0, 0, 0], dtype=torch.float64, device=cuda)
     # the norm-only release accumulates the same sum of squares
-    sc2 = torch.zeros(4, dtype=torch.float64, device=cuda)
+    sc2 = kernels.new_step_scalars(cuda)
     for j, ((P, M, V, g, p16, n), (p, m, v, gg)) in enumerate(zip(segs, host)):
         if j % 2 == 0:
             kernels.release(None, [g.data_ptr()], n, torch.bfloat16, inv_scale, sc2)
@@ -481,7 +523,7 @@ assert len(ps) == 1 and ps[0] == shard.data_ptr() and pb[0] == block.data_ptr()
 t.device_barrier()
 kernels.fetch(block, ps, 4096)
 t.device_barrier()
-sc = torch.zeros(4, dtype=torch.float64, device="cuda")
+sc = kernels.new_step_scalars("cuda")
 g = torch.empty(4096, device="cuda")
 kernels.release(g, pb, 4096, torch.bfloat16, 1.0, sc)
 torch.cuda.synchronize()

@@ -168,3 +168,33 @@ def test_bench_two_ranks_one_gpu(cuda, plan, transport):
         assert sim["replaced_ops"] > 0 and sim["c2g_units"] > 0
     # the IPC transport with every chunk GPU-home runs the step as CUDA graphs on both ranks
     assert line["config"]["cuda_graph"] == (transport == "ipc" and plan == "gpt2-small_n2.json")
+
+
+@pytest.mark.parametrize("path", ["exchange-nosync", "ipc-nosync"])
+def test_multiprocess_steps_without_host_sync(cuda, tmp_path, path):
+    """Three steps with no host synchronisation between them (the
+    next step's gathers must wait for the previous step's K4 through the
+    runtime's stream ordering on every transport): losses and masters equal
+    the host-synchronised rank-thread run bit for bit."""
+    world = 2
+    _torchrun(world, ["tests/mp_worker.py", "rcache-min", str(tmp_path), path])
+    got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
+    plan, _, _ = _plan("rcache-min")
+    init = gpt2.init_params(CFG, cuda, seed=11)
+
+    def rank_fn(r, transport):
+        model = ElixirGPT2(CFG, plan, device=cuda, transport=transport,
+                           init={k: v.clone() for k, v in init.items()}, **HP)
+        losses = []
+        for s in range(3):
+            tok, tgt = _batches(world, s, cuda)[r]
+            losses.append(model.train_step(tok, tgt).item())
+        model.synchronize()
+        torch.cuda.synchronize()
+        return losses, _rank_masters(model)
+
+    want = run_ranks(world, rank_fn)
+    for r in range(world):
+        assert list(got[r]["losses"]) == want[r][0], r
+        for pid, (off, ref_vals) in want[r][1].items():
+            assert np.array_equal(got[r][f"val::{pid}"], ref_vals), (r, pid)

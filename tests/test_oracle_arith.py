@@ -122,3 +122,36 @@ def test_c_oracle_matches_numpy_oracle():
     rp, rm, rv, r16 = arith.adamw(p, m, v, wg, 3, 1e-3, 0.9, 0.999, 1e-8, 0.01, coef)
     assert np.array_equal(P, rp) and np.array_equal(M, rm) and np.array_equal(V, rv)
     assert np.array_equal(P16, r16)
+
+
+def _c_oracle_norm():
+    import ctypes
+    from pathlib import Path
+    lib_path = Path(__file__).resolve().parents[1] / "oracle" / "_build" / "liboracle.so"
+    if not lib_path.exists():
+        pytest.skip("C oracle not built")
+    lib = ctypes.CDLL(str(lib_path))
+    lib.oracle_release_norm_ordered.restype = ctypes.c_double
+    lib.oracle_release_norm_ordered.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int]
+    return lib
+
+
+@pytest.mark.parametrize("ctas,tile_vecs", [(1, 256), (3, 512), (148 * 6, 1024), (2040, 256), (7, 1024)])
+def test_release_norm_order_c_equals_numpy(ctas, tile_vecs):
+    """The K3 fixed-order sum of squares restated twice (numpy vectorised and
+    plain C) gives the same bits on ragged multi-segment inputs."""
+    import ctypes
+    lib = _c_oracle_norm()
+    rng = np.random.default_rng(ctas + tile_vecs)
+    gs = [(rng.standard_normal(int(n)) * rng.uniform(0.1, 10)).astype(np.float32)
+          for n in rng.integers(1, 200_000, 5)]
+    gs.append(np.zeros(0, np.float32))
+    want = arith.release_norm_ordered(gs, ctas, tile_vecs)
+    ptrs = (ctypes.c_void_p * len(gs))(*[g.ctypes.data for g in gs])
+    ns = (ctypes.c_int64 * len(gs))(*[g.size for g in gs])
+    got = lib.oracle_release_norm_ordered(ptrs, ns, len(gs), ctas, tile_vecs, 4)
+    assert got == want
+    # and it is a sum of squares: within 1e-12 of the float64 dot product
+    tot = sum(float(np.dot(g.astype(np.float64), g)) for g in gs)
+    assert want == pytest.approx(tot, rel=1e-12)
