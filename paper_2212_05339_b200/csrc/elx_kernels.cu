@@ -15,6 +15,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "elx_internal.h"
 
@@ -414,14 +415,48 @@ __device__ __forceinline__ uint4 ld_tail(const void* p, int64_t v, int64_t n) {
   return u.q;
 }
 
-template <typename T16, int kWorld, int kU>
+template <int kWorld>
+__device__ __forceinline__ uint4 ld_src(const void* p) {
+  // world 1: the rank's own chunk (never a peer mapping), read once -> non-coherent streaming load
+  if (kWorld == 1) return ld_stream(static_cast<const uint4*>(p));
+  return ld_rel(p);
+}
+
+// The thread's world-1 sum of squares through the conversion path only, in the
+// kernel's order (subnormal / inf / nan inputs seen by the integer path).
+template <int kU>
+__device__ __noinline__ double thread_sq_exact_bf16(const RelBatch& b) {
+  constexpr int64_t kTileVecs = (int64_t)kRelThreads * kU;
+  const int64_t ntiles = b.tile0[b.nseg];
+  double sq = 0.0;
+  int s = 0;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
+    const int64_t n = b.n[s];
+    const int64_t v0 = (t - b.tile0[s]) * kTileVecs + threadIdx.x;
+    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(b.src[s][0]);
+    for (int u = 0; u < kU; ++u) {
+      const int64_t v = v0 + (int64_t)u * kRelThreads;
+      for (int e = 0; e < 8; ++e) {
+        const int64_t i = v * 8 + e;
+        sq = sq_acc(sq, i < n ? __bfloat162float(p[i]) : 0.f);
+      }
+    }
+  }
+  return sq;
+}
+
+// kScaleOne: inv_scale == 1 (bf16 training), the multiply is an exact identity and is skipped.
+template <typename T16, int kWorld, int kU, bool kScaleOne>
 __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid_constant__ RelBatch b, int world_rt,
                                                                     float inv_scale, double* __restrict__ sc) {
   constexpr int kR = kWorld > 0 ? kWorld : 1;
   const int world = kWorld > 0 ? kWorld : world_rt;
   constexpr int64_t kTileVecs = (int64_t)kRelThreads * kU;
+  constexpr bool kIntCvt = kWorld == 1 && kScaleOne && std::is_same<T16, __nv_bfloat16>::value;
   const int64_t ntiles = b.tile0[b.nseg];
   double sq = 0.0;
+  uint32_t mx = 0u, mn = 0xFFFFFFFFu;
   int s = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
@@ -438,7 +473,7 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
 #pragma unroll
         for (int r = 0; r < kR; ++r) {
           const void* p = b.src[s][r];
-          raw[u][r] = v < nfull ? ld_rel(static_cast<const uint4*>(p) + v)
+          raw[u][r] = v < nfull ? ld_src<kWorld>(static_cast<const uint4*>(p) + v)
                                 : (v < nvec ? ld_tail(p, v, n) : make_uint4(0, 0, 0, 0));
         }
       }
@@ -454,10 +489,30 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
         }
+        if (kIntCvt) {
+          // world-1 bf16 norm pass: the F2F.F64 conversions run on the XU pipe at ~8/clk/SM, below the
+          // HBM rate (11.5 bf16/clk/SM). Half of them are replaced by an exact integer construction of
+          // the same double: the high bf16 of a 32-bit word IS the float's bits, |x| as a double is
+          // hi = (a >> 3) + (1023 - 127) << 20, lo = 0 for a normal x, 0 for zero. Same values, same
+          // DFMA order as the conversion path: bit-identical sums. Subnormal / inf / nan high halves are
+          // tracked (mx, mn) and make the thread recompute its sum through the conversion path.
+          const uint32_t* w = reinterpret_cast<const uint32_t*>(&raw[u][0]);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          acc[e] = __fmul_rn(acc[e], inv_scale);
-          sq = sq_acc(sq, acc[e]);
+          for (int j = 0; j < 4; ++j) {
+            sq = sq_acc(sq, __uint_as_float(w[j] << 16));
+            const uint32_t a = w[j] & 0x7FFF0000u;
+            mx = max(mx, a);
+            mn = min(mn, a - 1u);
+            const uint32_t hi = a ? (a >> 3) + 0x38000000u : 0u;
+            const double d = __hiloint2double((int)hi, 0);
+            sq = __fma_rn(d, d, sq);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            if (!kScaleOne) acc[e] = __fmul_rn(acc[e], inv_scale);
+            sq = sq_acc(sq, acc[e]);
+          }
         }
         if (g != nullptr && v < nvec) {
           if (v < nfull) {
@@ -498,6 +553,7 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
       }
     }
   }
+  if (kIntCvt && (mx >= 0x7F800000u || mn < 0x007FFFFFu)) sq = thread_sq_exact_bf16<kU>(b);
   publish_partial(sq, bad_of(sq), sc);
 }
 
@@ -533,16 +589,21 @@ struct RelLaunch {
   int u;
 };
 
-template <typename T16>
-RelLaunch rel_kernel(int world, bool vec) {
+template <typename T16, bool kOne>
+RelLaunch rel_kernel_s(int world, bool vec) {
   if (!vec) return {(const void*)release_batch_scalar_kernel<T16>, 1};
   switch (world) {
-    case 1: return {(const void*)release_batch_kernel<T16, 1, rel_unroll(1)>, rel_unroll(1)};
-    case 2: return {(const void*)release_batch_kernel<T16, 2, rel_unroll(2)>, rel_unroll(2)};
-    case 4: return {(const void*)release_batch_kernel<T16, 4, rel_unroll(4)>, rel_unroll(4)};
-    case 8: return {(const void*)release_batch_kernel<T16, 8, rel_unroll(8)>, rel_unroll(8)};
-    default: return {(const void*)release_batch_kernel<T16, 0, 2>, 2};
+    case 1: return {(const void*)release_batch_kernel<T16, 1, rel_unroll(1), kOne>, rel_unroll(1)};
+    case 2: return {(const void*)release_batch_kernel<T16, 2, rel_unroll(2), kOne>, rel_unroll(2)};
+    case 4: return {(const void*)release_batch_kernel<T16, 4, rel_unroll(4), kOne>, rel_unroll(4)};
+    case 8: return {(const void*)release_batch_kernel<T16, 8, rel_unroll(8), kOne>, rel_unroll(8)};
+    default: return {(const void*)release_batch_kernel<T16, 0, 2, kOne>, 2};
   }
+}
+
+template <typename T16>
+RelLaunch rel_kernel(int world, bool vec, bool scale_one) {
+  return scale_one ? rel_kernel_s<T16, true>(world, vec) : rel_kernel_s<T16, false>(world, vec);
 }
 
 // Grid of a release launch: one CTA per tile up to (resident CTAs per SM x
@@ -575,7 +636,7 @@ bool rel_vec_ok(const RelBatch& b, int world) {
 template <typename T16>
 int run_release_batch(RelBatch& b, int world, float inv_scale, double* sc, cudaStream_t st) {
   const bool vec = rel_vec_ok(b, world);
-  const RelLaunch L = rel_kernel<T16>(world, vec);
+  const RelLaunch L = rel_kernel<T16>(world, vec, inv_scale == 1.0f);
   int64_t work;
   if (vec) {
     work = rel_tiles(b, L.u);
@@ -586,18 +647,12 @@ int run_release_batch(RelBatch& b, int world, float inv_scale, double* sc, cudaS
     b.tile0[0] = 0;
   }
   if (work == 0) return ELX_OK;
-  const int grid = rel_grid(L.kern, work);
-  if (vec) {
-    switch (world) {
-      case 1: release_batch_kernel<T16, 1, rel_unroll(1)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
-      case 2: release_batch_kernel<T16, 2, rel_unroll(2)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
-      case 4: release_batch_kernel<T16, 4, rel_unroll(4)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
-      case 8: release_batch_kernel<T16, 8, rel_unroll(8)><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
-      default: release_batch_kernel<T16, 0, 2><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc); break;
-    }
-  } else {
-    release_batch_scalar_kernel<T16><<<grid, kRelThreads, 0, st>>>(b, world, inv_scale, sc);
-  }
+  // the grid (and so the summation order) comes from the general-scale variant's occupancy, whatever
+  // variant runs: elx_release_geometry reports the same order for every inv_scale
+  const int grid = rel_grid(rel_kernel<T16>(world, vec, false).kern, work);
+  void* args[] = {(void*)&b, (void*)&world, (void*)&inv_scale, (void*)&sc};
+  cudaError_t e = cudaLaunchKernel(L.kern, dim3(grid), dim3(kRelThreads), args, 0, st);
+  if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_release: %s", cudaGetErrorString(e));
   return check_launch("elx_release");
 }
 
@@ -1548,7 +1603,9 @@ int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t 
   b.nseg = 0;
   for (int i = 0; i < nseg; ++i)
     if (n[i] > 0) b.n[b.nseg++] = n[i];
-  const RelLaunch L = dtype == ELX_BF16 ? rel_kernel<__nv_bfloat16>(world, true) : rel_kernel<__half>(world, true);
+  // the geometry depends on the tile shape only (the same for scale 1 or not) and the grid
+  const RelLaunch L = dtype == ELX_BF16 ? rel_kernel<__nv_bfloat16>(world, true, false)
+                                        : rel_kernel<__half>(world, true, false);
   const int64_t work = rel_tiles(b, L.u);
   *ctas = work == 0 ? 0 : rel_grid(L.kern, work);
   *tile_vecs = kRelThreads * L.u;

@@ -155,7 +155,29 @@ def test_gpt2_1p3b_release_and_adam_full_table_bit_exact(cuda):
     assert not mism, mism
 
 
-def test_gpt2_small_full_step_equals_reference(cuda):
+@pytest.fixture
+def deterministic_library():
+    """cuDNN's attention backward accumulates dQ non-deterministically at full
+    size, so two computations of the same gradient — the
+    runtime's and the reference step's — differ in the last bits unless the
+    library's deterministic algorithms are on. Our kernels are deterministic
+    either way."""
+    import os
+    old_env = os.environ.get("CUBLAS_WORKSPACE_CONFIG")
+    os.environ["CUBLAS_WORKSPACE_CONFIG"] = ":4096:8"
+    old = (torch.backends.cudnn.deterministic, torch.are_deterministic_algorithms_enabled())
+    torch.backends.cudnn.deterministic = True
+    torch.use_deterministic_algorithms(True)
+    yield
+    torch.backends.cudnn.deterministic = old[0]
+    torch.use_deterministic_algorithms(old[1])
+    if old_env is None:
+        os.environ.pop("CUBLAS_WORKSPACE_CONFIG", None)
+    else:
+        os.environ["CUBLAS_WORKSPACE_CONFIG"] = old_env
+
+
+def test_gpt2_small_full_step_equals_reference(cuda, deterministic_library):
     cfg = PRESETS["gpt2-small"]
     plan = (ROOT / "plans" / "gpt2-small_n1.json").read_text()
     init = gpt2.init_params(cfg, cuda, seed=3)

@@ -183,6 +183,33 @@ def test_release_norm_only_world1(cuda, dtype, inv_scale, n, bad):
         assert sc2[0].item() == pytest.approx(wsq, rel=1e-12) and sc2[1].item() == 0.0
 
 
+@pytest.mark.parametrize("where", ["even", "odd", "both", "zeros"])
+def test_release_norm_subnormal_and_zero_elements_exact(cuda, where):
+    """The world-1 bf16 norm pass converts half of the elements to double with
+    integer ops (exact for normal values and zero); subnormal elements make the
+    thread recompute through the conversion path. The sum stays bit-exact to
+    the oracle's fixed order whatever the element classes and positions."""
+    n = 3 * 2 ** 20 + 5
+    rng = np.random.default_rng(11)
+    x = arith.f32_to_bf16_bits((rng.standard_normal(n) * 1e-3).astype(np.float32))
+    idx = rng.integers(0, n, 4000)
+    if where in ("even", "both"):
+        x[idx[idx % 2 == 0]] = rng.integers(1, 0x80, (idx % 2 == 0).sum()).astype(np.uint16)   # subnormals
+    if where in ("odd", "both"):
+        x[idx[idx % 2 == 1]] = (rng.integers(1, 0x80, (idx % 2 == 1).sum()) | 0x8000).astype(np.uint16)
+    if where == "zeros":
+        x[: n // 2] = 0
+        x[idx] = 0x8000  # -0.0
+    d = torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).to(cuda)
+    sc = kernels.new_step_scalars(cuda)
+    kernels.release(None, [d.data_ptr()], n, torch.bfloat16, 1.0, sc)
+    torch.cuda.synchronize()
+    wg, _, wbad = arith.release([x], 1.0)
+    ctas, tv = kernels.release_geometry([n], 1)
+    assert not wbad and sc[1].item() == 0.0
+    assert sc[0].item() == arith.release_norm_ordered([wg], ctas, tv)
+
+
 @pytest.mark.parametrize("world", [1, 2, 4, 8, 3])
 def test_release_batch_one_launch_bit_exact(cuda, world):
     """Every chunk due at one reduce position in ONE K3 launch: ragged segment
