@@ -262,6 +262,24 @@ def run_reference(args):
 
 # ---------------------------------------------------------------- GPU arm
 
+def _fetch_stats(fet, world, steps, kind):
+    """K2 (or the library all-gather) per gather: (ms, block elements) pairs
+    from the eager probe steps; busBW = (N-1)/N * 2 B * P / t (NCCL's busBw
+    convention for an all-gather of P elements)."""
+    engine = {"ipc": "K2 on SMs reading peers' shards through our CUDA-IPC mappings (NVLink)",
+              "ipc-ce": "K2 on the copy engines (cudaMemcpyAsync per peer) over CUDA-IPC mappings",
+              "p2p": "K2 on SMs reading peers' shards through torch symmetric memory",
+              "nccl": "NCCL all_gather_into_tensor on the comm stream"}.get(kind, kind)
+    if not fet:
+        return {"engine": engine, "gathers_timed": 0}
+    ms = sum(t for t, _ in fet)
+    nbytes = sum((world - 1) / world * 2 * n for _, n in fet)
+    return {"engine": engine, "gathers_per_step": len(fet) / max(1, steps), "ms_per_step": ms / max(1, steps),
+            "ms_per_gather": ms / len(fet), "bus_gbs": nbytes / (ms * 1e-3) / 1e9,
+            "bus_frac_of_900": nbytes / (ms * 1e-3) / 1e9 / 900,
+            "note": "CUDA events around each gather on the comm stream (eager probe steps when the step is a graph)"}
+
+
 def _release_alone(model, dev, cur):
     from paper_2212_05339_b200 import kernels
     mgr = model.manager
@@ -318,8 +336,10 @@ def run_ours(args):
     cfg = PRESETS[args.model]
     plan_path = ROOT / "plans" / (args.plan.format(n=world) if args.plan else f"{args.model}_n{world}.json")
     plan_text = plan_path.read_text()
-    from paper_2212_05339_b200.transport import make_transport
-    model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234, transport=make_transport(world, args.transport),
+    from paper_2212_05339_b200.transport import make_transport, primary_contexts, resolve_kind
+    kind = resolve_kind(world, args.transport)
+    transport = make_transport(world, kind)
+    model = ElixirGPT2(cfg, plan_text, device=dev, seed=1234, transport=transport,
                        overlap_update=args.overlap, cpu_update=args.cpu_update,
                        recompute={"auto": "auto", "on": True, "off": False}[args.recompute])
     B, T = cfg.batch, cfg.seq_len
@@ -340,6 +360,7 @@ def run_ours(args):
         if on:
             opt.adam_events.clear()
             model.fetcher.release_events.clear()
+            model.fetcher.fetch_events.clear()
             model.fetcher.copy_events.clear()
             opt.cpu_wait_s = opt.cpu_update_s = 0.0
 
@@ -383,6 +404,7 @@ def run_ours(args):
     ms = _max_over_ranks(ms, world)
     adam_ms = [a.elapsed_time(b) for a, b in opt.adam_events]
     rel = [(a.elapsed_time(b), n) for a, b, n in model.fetcher.release_events]
+    fet = [(a.elapsed_time(b), n) for a, b, n in model.fetcher.fetch_events]
     copies = {}
     for kind, a, b, nb in model.fetcher.copy_events:
         ms_, nb0 = copies.get(kind, (0.0, 0))
@@ -490,7 +512,8 @@ def run_ours(args):
         "config": {
             "workload": f"{args.model} chunked training step, plan {plan_path.name} (offplan.build_plan)",
             "model": args.model, "global_batch": world * B, "per_rank_batch": B, "seq_len": T,
-            "parallelism": f"elixir-chunk-dp{world}", "transport": args.transport if world > 1 else "local", "chunk_length": model.layout.chunk_length,
+            "parallelism": f"elixir-chunk-dp{world}", "transport": kind, "chunk_length": model.layout.chunk_length,
+            "cuda_contexts_on_devices": primary_contexts(),
             "n_chunks": model.layout.n_chunks, "n_block": model.manager.plan.n_block,
             "l2": "working set (>20 GB of chunk/optimizer state per step) far exceeds the 126 MB L2; no flush needed",
             "cuda_graph": use_graph,
@@ -520,12 +543,13 @@ def run_ours(args):
                         "local_hbm_gbs": rel_local_bytes / (rel_ms * 1e-3) / 1e9 if rel_ms else None,
                         "bus_gbs": (None if world == 1 else
                                     (world - 1) / world * 2 * rel_elems * world / (rel_ms * 1e-3) / 1e9),
+                        "bus_frac_of_900": (None if world == 1 else
+                                            (world - 1) / world * 2 * rel_elems * world / (rel_ms * 1e-3) / 1e9 / 900),
+                        "bus_note": "busBW = (N-1)/N * 2 B * N * S / t per K3 launch (timed after its device barrier)",
                         "in_step_note": "comm stream, concurrent with the backward's GEMMs",
                         "alone": rel_alone},
-            "fetch": {"note": "N=1: GPU-home chunk shards are used in place (zero-copy gathers)"
-                      if world == 1 else {"p2p": "K2 reading peers' shards over NVLink (symmetric memory)",
-                                          "ipc": "K2 reading peers' shards through CUDA-IPC mappings",
-                                          }.get(args.transport, "all_gather_into_tensor on the comm stream")},
+            "fetch": ({"note": "N=1: GPU-home chunk shards are used in place (zero-copy gathers)"} if world == 1 else
+                      _fetch_stats(fet, world, probe_steps, kind)),
         },
         "roofline": {"bound": "hbm", "kernel": "elx_adam (K4)", "achieved": adam_gbs, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": adam_gbs / peak, "traffic": traffic,
@@ -548,59 +572,140 @@ def run_ours(args):
 # ---------------------------------------------------------------- kernel sweep
 
 def run_sweep(args):
-    """configs[4]: K2 fetch / K3 release / K4 Adam over chunk sizes 4-256 MB.
-    One GPU: the N 'ranks' of fetch/release are N local buffers (HBM-bound
-    here; on NVLink the same kernels read peer-mapped pointers)."""
+    """configs[4]: the chunk sweep — K2 fetch (SMs and copy engines), K3
+    release and K4 Adam over chunk sizes 4-256 MB, at N = WORLD_SIZE ranks.
+
+    N > 1 (torchrun, one process per GPU): every rank allocates its shard of a
+    chunk and an rCache block, peers map each other's buffers (our CUDA-IPC
+    mappings, or torch symmetric memory with --transport p2p), and each engine
+    runs on REAL peer pointers between device barriers: K2 reads the N shards
+    into the block (all-gather), K3 reduces segment `rank` of every peer's
+    block (reduce-scatter + unscale + norm). NCCL's all_gather_into_tensor and
+    reduce_scatter_tensor (bf16 and fp32) run on the same buffers as the bar.
+    busBW = (N-1)/N * bytes / t (NCCL's convention; bytes = the gathered block
+    or the reduce-scatter input), against 900 GB/s per direction. Time = max
+    over ranks of the median of `reps` launches, each started after a device
+    barrier, L2 flushed by a 256 MB read before each. Ranks sharing one GPU
+    (the one-GPU box) run the same code as a functional check, flagged
+    `oversubscribed` (NCCL refuses two ranks on one device: its lines say so).
+    N = 1: the same kernels with N local buffers standing in for peers
+    (HBM-bound), world sizes 1/2/4/8 emulated. One JSON line per (size, N,
+    engine)."""
+    import torch.distributed as dist
     from paper_2212_05339_b200 import kernels
-    dev = torch.device("cuda", 0)
+    from paper_2212_05339_b200.runtime import shard_length
+
+    world, rank, local, oversub = _dist_setup(args.gpus)
+    dev = torch.device("cuda", local)
     peak, src = _peaks()
-    # L2 flush by READING 256 MB (2x the 126 MB L2): a write-flush (zero_) would leave the L2 full of
-    # dirty lines whose write-back then lands inside the next timed kernel
+    sizes = [int(x) for x in args.sweep_sizes.split(",")]
+    reps = args.steps
     flush = torch.ones(64 * 2 ** 20, dtype=torch.float32, device=dev)
     flush_sink = torch.empty((), dtype=torch.float32, device=dev)
-    out = []
+    sc = kernels.new_step_scalars(dev)
+    hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=0.0)
+    transport = None
+    kind = "local"
+    if world > 1:
+        from paper_2212_05339_b200.transport import IpcTransport, SymmMemTransport, primary_contexts
+        kind = "p2p" if args.transport == "p2p" else "ipc"
+        transport = SymmMemTransport() if kind == "p2p" else IpcTransport()
+    nccl_ok = world > 1 and not oversub and dist.get_backend() == "nccl"
 
-    def timeit(fn, reps=10):
+    def timeit(fn, barrier):
         ts = []
-        for i in range(reps + 3):
+        for i in range(reps + 2):
             torch.sum(flush, dim=0, out=flush_sink)
+            if barrier is not None:
+                barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
             fn()
             b.record()
             torch.cuda.synchronize()
-            if i >= 3:
+            if i >= 2:
                 ts.append(a.elapsed_time(b))
-        return statistics.median(ts)
+        return _max_over_ranks(statistics.median(ts), world)
 
-    for mb in (4, 8, 16, 32, 64, 128, 256):
-        C = mb * 2 ** 20 // 2
-        for world in (1, 2, 4, 8):
-            S = -(-C // world)
-            S = -(-S // 8) * 8
-            shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(world)]
-            block = torch.empty(world * S, dtype=torch.bfloat16, device=dev)
+    def emit(rec):
+        rec.update({"sweep": "chunk", "world": world, "peers": kind if world > 1 else "local buffers",
+                    "hbm_peak_gbs": peak, "reps": reps})
+        if oversub:
+            rec["oversubscribed"] = oversub
+        if rank == 0:
+            print(json.dumps(rec), flush=True)
+
+    for mb in sizes:
+        C = mb * 2 ** 20 // 2                      # bf16 elements of one chunk
+        if world > 1:
+            S = shard_length(C, world)
+            P = world * S
+            g = torch.Generator(device=dev).manual_seed(77 + rank)
+            shard = transport.alloc((S,), torch.bfloat16, dev)
+            shard.copy_(torch.randn(S, generator=g, device=dev).to(torch.bfloat16))
+            block = transport.alloc((P,), torch.bfloat16, dev)
+            block.copy_(torch.randn(P, generator=g, device=dev).to(torch.bfloat16))
             g32 = torch.empty(S, device=dev)
-            sc = kernels.new_step_scalars(dev)
-            t_f = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S))
-            t_fc = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S, engine="ce"))
-            t_r = timeit(lambda: kernels.release(g32, [s.data_ptr() for s in shards], S, torch.bfloat16, 1.0, sc))
+            ps = transport.peer_ptrs(shard)
+            pb = transport.peer_ptrs(block)
+            segs = [p + rank * S * 2 for p in pb]
+            bar = transport.device_barrier
+            bus = (world - 1) / world * 2 * P      # bytes: the gathered block / the bf16 reduce-scatter input
+            for engine, fn in (("k2_fetch_sm", lambda: kernels.fetch(block, ps, S)),
+                               ("k2_fetch_ce", lambda: kernels.fetch(block, ps, S, engine="ce")),
+                               ("k3_release", lambda: kernels.release(g32, segs, S, torch.bfloat16, 1.0, sc))):
+                ms = timeit(fn, bar)
+                emit({"chunk_mb": mb, "engine": engine, "shard_elems": S, "ms": ms,
+                      "bus_gbs": bus / (ms * 1e-3) / 1e9, "frac_of_900": bus / (ms * 1e-3) / 1e9 / 900})
+            if nccl_ok:
+                out16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+                blk32 = block.float()
+                out32 = torch.empty(S, device=dev)
+                for engine, fn, nbytes in (
+                        ("nccl_all_gather", lambda: dist.all_gather_into_tensor(block, shard), bus),
+                        ("nccl_reduce_scatter_bf16", lambda: dist.reduce_scatter_tensor(out16, block), bus),
+                        ("nccl_reduce_scatter_f32", lambda: dist.reduce_scatter_tensor(out32, blk32), 2 * bus)):
+                    ms = timeit(fn, bar)
+                    emit({"chunk_mb": mb, "engine": engine, "shard_elems": S, "ms": ms,
+                          "bus_gbs": nbytes / (ms * 1e-3) / 1e9, "frac_of_900": nbytes / (ms * 1e-3) / 1e9 / 900})
+                del out16, blk32, out32
+            else:
+                for engine in ("nccl_all_gather", "nccl_reduce_scatter_bf16", "nccl_reduce_scatter_f32"):
+                    emit({"chunk_mb": mb, "engine": engine, "unavailable":
+                          "NCCL needs one GPU per rank" if oversub else "process group is not NCCL"})
+            # K4 on this rank's shard (local HBM)
+            p32, m, v = (torch.zeros(S, device=dev) for _ in range(3))
+            p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+            g32.normal_()
+            tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
+            ms = timeit(lambda: kernels.adam(tab, hp, 1, sc, torch.bfloat16), bar)
+            emit({"chunk_mb": mb, "engine": "k4_adam", "shard_elems": S, "ms": ms,
+                  "hbm_gbs": 30 * S / (ms * 1e-3) / 1e9, "frac": 30 * S / (ms * 1e-3) / 1e9 / peak})
+            del shard, block, g32, p32, m, v, p16, tab
+            continue
+        for w in (1, 2, 4, 8):
+            S = shard_length(C, w)
+            shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(w)]
+            block = torch.empty(w * S, dtype=torch.bfloat16, device=dev)
+            g32 = torch.empty(S, device=dev)
+            t_f = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S), None)
+            t_fc = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S, engine="ce"), None)
+            t_r = timeit(lambda: kernels.release(g32, [s.data_ptr() for s in shards], S, torch.bfloat16, 1.0, sc),
+                         None)
             p32, m, v = (torch.zeros(S, device=dev) for _ in range(3))
             p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
             tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
-            sc.zero_()
-            hp = dict(lr=1e-3, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01, max_norm=0.0)
-            t_a = timeit(lambda: kernels.adam(tab, hp, 1, sc, torch.bfloat16))
-            rec = {"chunk_mb": mb, "world": world, "shard_elems": S,
-                   "fetch": {"ms": t_f, "hbm_gbs": 2 * 2 * world * S / (t_f * 1e-3) / 1e9},
-                   "fetch_copy_engine": {"ms": t_fc, "hbm_gbs": 2 * 2 * world * S / (t_fc * 1e-3) / 1e9},
-                   "release": {"ms": t_r, "hbm_gbs": (2 * world * S + 4 * S) / (t_r * 1e-3) / 1e9},
-                   "adam": {"ms": t_a, "hbm_gbs": 30 * S / (t_a * 1e-3) / 1e9,
-                            "frac": 30 * S / (t_a * 1e-3) / 1e9 / peak}}
-            out.append(rec)
-            print(json.dumps(rec), flush=True)
-            del shards, block, g32, p32, m, v, p16
-    return out
+            t_a = timeit(lambda: kernels.adam(tab, hp, 1, sc, torch.bfloat16), None)
+            for engine, ms, nbytes in (("k2_fetch_sm", t_f, 2 * 2 * w * S), ("k2_fetch_ce", t_fc, 2 * 2 * w * S),
+                                       ("k3_release", t_r, 2 * w * S + 4 * S), ("k4_adam", t_a, 30 * S)):
+                emit({"chunk_mb": mb, "emulated_world": w, "engine": engine, "shard_elems": S, "ms": ms,
+                      "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "frac": nbytes / (ms * 1e-3) / 1e9 / peak})
+            del shards, block, g32, p32, m, v, p16, tab
+    if world > 1:
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            print(json.dumps({"sweep": "contexts", "rank": rank, "cuda_contexts_on_devices": primary_contexts()}))
 
 
 def main():
@@ -611,6 +716,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--model", default="gpt2-1.3b")
     ap.add_argument("--sweep", action="store_true")
+    ap.add_argument("--sweep-sizes", default="4,8,16,32,64,128,256", help="chunk sizes in MB for --sweep")
     ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
                     "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
@@ -627,9 +733,11 @@ def main():
                     help="every chunk GPU-home, world 1 or --transport ipc: capture the whole step as one CUDA graph")
     ap.add_argument("--overlap", action="store_true",
                     help="issue the GPU update per chunk on an optimizer stream under the next forward")
-    ap.add_argument("--transport", choices=["nccl", "p2p", "ipc"], default=os.environ.get("ELX_TRANSPORT", "nccl"),
-                    help="N>1 fetch/release path: NCCL collectives + K3, or in-kernel P2P with peer pointers from "
-                         "symmetric memory (p2p) or CUDA IPC + our device barrier (ipc)")
+    ap.add_argument("--transport", choices=["auto", "nccl", "p2p", "ipc", "ipc-ce"],
+                    default=os.environ.get("ELX_TRANSPORT", "auto"),
+                    help="N>1 fetch/release path: auto (default) = in-kernel P2P over our CUDA-IPC mappings when every "
+                         "peer GPU is reachable, else NCCL; nccl = NCCL collectives + K3; ipc / ipc-ce = K2 on SMs / "
+                         "copy engines over IPC mappings; p2p = over torch symmetric memory")
     args = ap.parse_args()
     if args.deterministic:
         os.environ.setdefault("CUBLAS_WORKSPACE_CONFIG", ":4096:8")
@@ -639,10 +747,8 @@ def main():
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
-    elif args.sweep:
-        run_sweep(args)
     else:
-        run_ours(args)
+        run_sweep(args) if args.sweep else run_ours(args)
         import torch.distributed as dist
         if dist.is_available() and dist.is_initialized():
             # no rank exits (releasing the CUDA-IPC memory it exported) while a peer still maps it

@@ -175,6 +175,16 @@ int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int3
  * context reports an error) instead of hanging. */
 int elx_device_barrier(int32_t* const* pads, int32_t world, int32_t rank, int32_t epoch, void* stream);
 
+/* Map a peer process's device allocation into the CURRENT device's context
+ * (cudaIpcOpenMemHandle with lazy peer access): `handle` is the exporter's
+ * 64-byte cudaIpcMemHandle_t of the allocation; *ptr receives its base in
+ * this process. Opening on the current device (not the exporter's) keeps ONE
+ * CUDA context per rank process on an 8-GPU node: the peer's HBM is reached
+ * over NVLink through peer access, the mapping used by K2/K3 and the device
+ * barrier's signal pads (the in-kernel P2P path, transport.IpcTransport). */
+int elx_ipc_open(const void* handle, void** ptr);
+int elx_ipc_close(void* ptr);
+
 /* dst[i] = sum_{r = 0..world-1, in order} peers[r][i] for i < count (fp64,
  * count <= 1024): the N-scalar all-reduce of the step scalars over peer
  * memory (call between two device barriers), deterministic in rank order. */

@@ -97,6 +97,8 @@ _SIGNATURES = {
     "elx_device_barrier": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_vp]),
     "elx_peer_sum_f64": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
     "elx_enable_peer_access": (ctypes.c_int, [c_i32]),
+    "elx_ipc_open": (ctypes.c_int, [c_vp, c_vp]),
+    "elx_ipc_close": (ctypes.c_int, [c_vp]),
     "elx_release": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_f32, c_vp, c_vp]),
     "elx_release_batch": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_f32, c_vp, c_vp]),
     "elx_release_geometry": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_vp, c_vp]),

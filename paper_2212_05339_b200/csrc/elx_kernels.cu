@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <type_traits>
 
@@ -1510,6 +1511,32 @@ int elx_enable_peer_access(int32_t peer_device) {
     return ELX_OK;
   }
   if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "enable peer access %d: %s", peer_device, cudaGetErrorString(e));
+  return ELX_OK;
+}
+
+int elx_ipc_open(const void* handle, void** ptr) {
+  elx::clear_error();
+  if (!handle || !ptr) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  void* p = nullptr;
+  cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return elx::fail(ELX_ERR_CUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+  }
+  *ptr = p;
+  return ELX_OK;
+}
+
+int elx_ipc_close(void* ptr) {
+  elx::clear_error();
+  if (!ptr) return ELX_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(ptr);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return elx::fail(ELX_ERR_CUDA, "cudaIpcCloseMemHandle: %s", cudaGetErrorString(e));
+  }
   return ELX_OK;
 }
 

@@ -112,6 +112,21 @@ def enable_peer_access(peer_device: int) -> None:
     _lib.check(_lib.load().elx_enable_peer_access(int(peer_device)), "elx_enable_peer_access")
 
 
+def ipc_open(handle: bytes) -> int:
+    """Map a peer process's allocation (64-byte cudaIpcMemHandle_t) into the
+    current device's context; returns its base pointer here."""
+    if len(handle) != 64:
+        raise ValidationError("a CUDA IPC handle is 64 bytes")
+    buf = ctypes.create_string_buffer(bytes(handle), 64)
+    out = ctypes.c_void_p()
+    _lib.check(_lib.load().elx_ipc_open(buf, ctypes.byref(out)), "elx_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(ptr: int) -> None:
+    _lib.check(_lib.load().elx_ipc_close(ctypes.c_void_p(ptr)), "elx_ipc_close")
+
+
 def device_barrier(pad_ptrs: Sequence[int], rank: int, epoch: int, stream=None) -> None:
     """Stream-ordered cross-rank barrier over peer-mapped int32[world] signal
     pads (pad_ptrs[r] = rank r's pad as a pointer usable on this device)."""

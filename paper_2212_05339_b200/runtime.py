@@ -366,6 +366,7 @@ class ChunkFetcher:
         self.inv_scale = inv_scale
         self.time_release = False     # bench: CUDA events around each release / offload copy
         self.release_events: list = []
+        self.fetch_events: list = []      # (start, end, block elements) per GPU-home gather at N > 1
         self.copy_events: list = []
         self.optimizer = None         # HybridAdam whose per-chunk updates gate our reads
         self._fenced = False
@@ -515,6 +516,9 @@ class ChunkFetcher:
             if mgr.p2p and b in self._dirty:
                 self._barrier()  # peers may still be reading block b's gradients (released since the last barrier)
             seg = block[mgr.rank * mgr.S:(mgr.rank + 1) * mgr.S]
+            if self.time_release and not cpu and mgr.world > 1:
+                f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                f0.record(comm)
             if mgr.p2p and not cpu:
                 # K2 over NVLink: read every rank's shard of c straight from its HBM
                 es = block.element_size()
@@ -542,6 +546,9 @@ class ChunkFetcher:
                     mgr.transport.gather(block, seg)
             else:
                 mgr.transport.gather(block, mgr.p16[mgr.row[c]])
+            if self.time_release and not cpu and mgr.world > 1:
+                f1.record(comm)
+                self.fetch_events.append((f0, f1, mgr.P))
             if mgr.world > 1:
                 self.bytes_moved["gather"] += (mgr.world - 1) * mgr.S * block.element_size()
             ev = torch.cuda.Event()
@@ -595,11 +602,11 @@ class ChunkFetcher:
             if not self._fenced and opt is not None and opt.done_event is not None:
                 comm.wait_event(opt.done_event)  # g32 / step scalars free again
                 self._fenced = True
-            if self.time_release:
-                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                t0.record(comm)
             if mgr.p2p:
                 self._barrier()
+            if self.time_release:  # after the barrier: the K3 launch itself (bus/HBM rate), not the wait
+                t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                t0.record(comm)
             segs = []
             for c in batch:
                 if mgr.valid(c) > 0:

@@ -198,3 +198,29 @@ def test_multiprocess_steps_without_host_sync(cuda, tmp_path, path):
         assert list(got[r]["losses"]) == want[r][0], r
         for pid, (off, ref_vals) in want[r][1].items():
             assert np.array_equal(got[r][f"val::{pid}"], ref_vals), (r, pid)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sweep_real_peer_pointers_oversubscribed(cuda, world):
+    """bench.py --sweep under torchrun: every rank maps its peers' shards and
+    blocks (our CUDA-IPC mappings) and K2 (SMs and copy engines), K3 and K4
+    run on the real peer pointers between device barriers; one JSON line per
+    (size, N, engine) with busBW; the NCCL bar lines say why they are absent
+    when ranks share the GPU; each rank holds a context on its device only."""
+    p = _torchrun(world, ["bench.py", "--sweep", "--gpus", str(world), "--sweep-sizes", "4,32", "--steps", "3"],
+                  timeout=600)
+    lines = [json.loads(ln) for ln in p.stdout.splitlines() if ln.startswith("{")]
+    recs = [r for r in lines if r.get("sweep") == "chunk"]
+    got = {(r["chunk_mb"], r["engine"]) for r in recs}
+    for mb in (4, 32):
+        for eng in ("k2_fetch_sm", "k2_fetch_ce", "k3_release", "k4_adam", "nccl_all_gather",
+                    "nccl_reduce_scatter_bf16", "nccl_reduce_scatter_f32"):
+            assert (mb, eng) in got, (mb, eng)
+    for r in recs:
+        assert r["world"] == world and r["peers"] == "ipc" and "oversubscribed" in r
+        if r["engine"].startswith("k2") or r["engine"].startswith("k3"):
+            assert r["ms"] > 0 and r["bus_gbs"] > 0
+        if r["engine"].startswith("nccl"):
+            assert "unavailable" in r
+    ctx = [r for r in lines if r.get("sweep") == "contexts"]
+    assert ctx and ctx[0]["cuda_contexts_on_devices"] == [0]
