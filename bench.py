@@ -462,6 +462,20 @@ def run_ours(args):
     if world == 1 and model.manager.gpu_ids:
         rel_alone = _release_alone(model, dev, cur)
 
+    # ---- parity (the checker, after every timed region): one more eager step of the SAME model on the same
+    # batch, its K3 launches logged and the K4 inputs snapshotted on the device; the C oracle recomputes the
+    # sum of squares in each launch's fixed order and AdamW over every element (oracle/parity.py)
+    parity = None
+    if not args.no_parity and rank == 0:
+        if world == 1:
+            from oracle.parity import check_step
+            t0 = time.perf_counter()
+            parity = check_step(model, tok, tgt)
+            parity["seconds"] = round(time.perf_counter() - t0, 1)
+        else:
+            parity = {"checked": False, "reason": "N > 1: the multi-rank parity tests cover it "
+                                                  "(tests/test_multiprocess_gpu.py, tests/test_multirank_gpu.py)"}
+
     if rank != 0:
         return
     peak, peak_src = _peaks()
@@ -560,6 +574,7 @@ def run_ours(args):
                 "api": ("ElixirGPT2.graph_step (the captured train_step)" if use_graph else "ElixirGPT2.train_step")
                        + " on tokens copied from pinned host memory, loss read back"},
         "checkpointed": checkpointed,
+        "parity": parity,
         "chunk_runtime": offload,
         "gpu_launches": launches,
         "gpu_launches_per_step": launches / args.steps,
@@ -720,6 +735,7 @@ def main():
     ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
                     "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-parity", action="store_true", help="skip the post-timing parity check against the oracle")
     ap.add_argument("--cpu-update", choices=["split", "host", "stream"], default="split",
                     help="CPU-home chunk update: host threads, GPU-streamed, or split by measured rate")
     ap.add_argument("--recompute", choices=["auto", "on", "off"], default="auto",

@@ -200,8 +200,13 @@ int elx_enable_peer_access(int32_t peer_device);
  * with loss-scale unscale, fp32 cast, the sum of squares and the overflow
  * flag (rcache_sim.py:160-167 fires it at reduce_after[c]):
  *   g[i] = (sum_{r=0..world-1, in order} float(src[r][i])) * inv_scale
- *   step_scalars[0] += sum_i g[i]^2   (fp64, fixed order, see below)
- *   step_scalars[1]  = 1.0 if any g[i] is not finite
+ *   step_scalars[0] += sum_k q_k      (fp64, fixed order, see below), where
+ *       q_k = ((g[4k]^2 + g[4k+1]^2) + g[4k+2]^2) + g[4k+3]^2 is an fp32
+ *       partial (separately rounded multiplies/adds; zero past n): exact for
+ *       bf16 squares, <= ~4 * 2^-24 relative error overall, one fp64
+ *       conversion per four elements
+ *   step_scalars[1]  = 1.0 if any g[i] is not finite (or |g[i]| >~ 9e18, whose
+ *       quad partial overflows fp32: treated as an overflow too)
  * src[r] points at rank r's copy of THIS rank's segment (peer block + rank*S,
  * or a local all-to-all staging buffer). n = valid elements (padding
  * excluded). dtype is BF16 or F16. g may be NULL: only the sum of squares and
@@ -246,8 +251,9 @@ int elx_release_batch(const elx_release_seg* segs, int32_t nseg, int32_t world, 
  * lengths n[0..nseg) (nseg <= ELX_RELEASE_MAX_SEGS): *ctas = grid size G (0
  * if empty), *tile_vecs = 8-element vectors per tile (threads * unroll). Tile
  * k of the batch (segments' tiles concatenated) goes to CTA k % G; thread t
- * of a tile takes vectors t, t + 256, ...; a thread sums its squares in that
- * order, then CTA and grid reductions as described above. */
+ * of a tile takes vectors t, t + 256, ...; a thread adds each vector's two
+ * quad partials (elements 0-3, then 4-7) in that order, then CTA and grid
+ * reductions as described above. */
 int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t dtype, int32_t* ctas,
                          int32_t* tile_vecs);
 

@@ -101,10 +101,56 @@ def release(srcs, inv_scale: float, dtype: str = "bf16"):
         x = to_f32(np.asarray(s).reshape(-1), dtype)
         acc = x.copy() if acc is None else (acc + x).astype(np.float32)
     g = (acc * F32(inv_scale)).astype(np.float32)
-    g64 = g.astype(np.float64)
+    return g, sumsq(g), bool(not np.isfinite(g).all())
+
+
+def quad_sq(a: np.ndarray) -> np.ndarray:
+    """The release kernel's sum-of-squares unit over the last axis (length 4):
+    q = ((a0*a0 + a1*a1) + a2*a2) + a3*a3 in float32, every multiply and add
+    separately rounded (include/elixir_b200.h, K3). Exact for bf16 values'
+    squares; <= ~4 * 2^-24 relative error otherwise."""
+    a = np.asarray(a, np.float32)
     with np.errstate(over="ignore", invalid="ignore"):
-        sq = float(np.dot(g64, g64))
-    return g, sq, bool(not np.isfinite(g).all())
+        q = a[..., 0] * a[..., 0]
+        for e in (1, 2, 3):
+            q = (q + a[..., e] * a[..., e]).astype(np.float32)
+    return q
+
+
+def sumsq(g) -> float:
+    """Sum of squares of one released segment in K3's units: quads of
+    consecutive elements from element 0 (zero-padded), each an fp32 partial
+    (quad_sq), added in float64 (the order of the fp64 additions is the
+    kernel's launch geometry: release_norm_ordered; here numpy's)."""
+    g = np.asarray(g, np.float32).reshape(-1)
+    pad = np.zeros(-(-g.size // 4) * 4, np.float32)
+    pad[:g.size] = g
+    with np.errstate(over="ignore", invalid="ignore"):
+        return float(np.sum(quad_sq(pad.reshape(-1, 4)).astype(np.float64)))
+
+
+def sumsq_chunked(rel: dict, members: dict) -> float:
+    """Sum of squares of a whole step's released gradients as K3 forms it: the
+    quad units run over each CHUNK's elements from the chunk's offset 0 (the
+    members packed at their layout offsets, pack_chunks' contiguous order,
+    chunking.py:113-131), and over each parameter outside the chunks (the
+    shared wte) from its own element 0. rel: pid -> released fp32 gradient;
+    members: pid -> (chunk id, offset, numel) for chunk members."""
+    chunks: dict = {}
+    sq = 0.0
+    for pid, g in rel.items():
+        if pid in members:
+            c, off, n = members[pid]
+            chunks.setdefault(c, []).append((off, np.asarray(g, np.float32).reshape(-1)))
+        else:
+            sq += sumsq(g)
+    for c in sorted(chunks):
+        parts = sorted(chunks[c], key=lambda t: t[0])
+        flat = np.zeros(max(o + a.size for o, a in parts), np.float32)
+        for o, a in parts:
+            flat[o:o + a.size] = a
+        sq += sumsq(flat)
+    return sq
 
 
 def _block_sum_fixed(x: np.ndarray) -> np.ndarray:
@@ -127,9 +173,9 @@ def release_norm_ordered(gs, ctas: int, tile_vecs: int) -> float:
     exact fp64 order (include/elixir_b200.h, K3; elx_release_geometry gives
     ctas/tile_vecs): the segments' tiles of `tile_vecs` 8-element vectors
     concatenated, tile k to CTA k % ctas, thread t of 256 taking vectors t,
-    t+256, ... of a tile; per thread a sequential sum of squares (d*d is exact
-    in fp64, so numpy's multiply then add equals the kernel's DFMA; np.cumsum
-    is sequential), elements past a segment's end +0.0; per CTA the fixed block
+    t+256, ... of a tile; per thread a sequential fp64 sum of its vectors' two
+    fp32 quad partials (quad_sq; np.cumsum is sequential), elements past a
+    segment's end +0.0; per CTA the fixed block
     reduction; the partials summed per thread in slot order, then reduced the
     same way. Vectorised over CTAs and threads."""
     T = 256
@@ -139,7 +185,7 @@ def release_norm_ordered(gs, ctas: int, tile_vecs: int) -> float:
         g = np.asarray(g, np.float32).reshape(-1)
         te = tile_vecs * 8
         nt = -(-g.size // te)
-        pad = np.zeros(nt * te, np.float64)
+        pad = np.zeros(nt * te, np.float32)
         pad[:g.size] = g
         tiles.append(pad.reshape(nt, U, T, 8))
     if not tiles or sum(t.shape[0] for t in tiles) == 0 or ctas <= 0:
@@ -147,11 +193,13 @@ def release_norm_ordered(gs, ctas: int, tile_vecs: int) -> float:
     allt = np.concatenate(tiles)                    # [tiles, U, T, 8]
     nt = allt.shape[0]
     k = -(-nt // ctas)
-    full = np.zeros((k * ctas, U, T, 8), np.float64)
+    full = np.zeros((k * ctas, U, T, 8), np.float32)
     full[:nt] = allt
-    # [k, ctas, U, T, 8] -> per (cta, thread): sequence over (k, U, 8)
-    seq = full.reshape(k, ctas, U, T, 8).transpose(1, 3, 0, 2, 4).reshape(ctas, T, -1)
-    sq = np.cumsum(seq * seq, axis=-1)[..., -1]      # [ctas, T]
+    q = quad_sq(full.reshape(k * ctas, U, T, 2, 4)).astype(np.float64)   # [tiles, U, T, 2]
+    # [k, ctas, U, T, 2] -> per (cta, thread): sequence over (k, U, 2)
+    seq = q.reshape(k, ctas, U, T, 2).transpose(1, 3, 0, 2, 4).reshape(ctas, T, -1)
+    with np.errstate(over="ignore", invalid="ignore"):
+        sq = np.cumsum(seq, axis=-1)[..., -1]        # [ctas, T]
     part = _block_sum_fixed(sq)                       # [ctas]
     rows = -(-ctas // T)
     slots = np.zeros(rows * T, np.float64)

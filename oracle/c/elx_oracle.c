@@ -28,19 +28,42 @@ static inline uint16_t f32_to_bf16(float x) {
   return (uint16_t)(u >> 16);
 }
 
-/* g[i] = (sum_r bf16(src[r][i])) * inv_scale ; returns sum g^2, sets *bad. */
+/* The sum-of-squares unit of the release kernel (include/elixir_b200.h, K3):
+ * four consecutive released values a0..a3 give the fp32 partial
+ * q = ((a0*a0 + a1*a1) + a2*a2) + a3*a3 (separately rounded multiplies and
+ * adds, no fusion), and q is added to the fp64 running sum. Exact for bf16
+ * inputs' squares; relative error of the total <= ~4 * 2^-24 (all terms >= 0). */
+static inline float quad_sq(const float* a) {
+  float q = a[0] * a[0];
+  q = q + a[1] * a[1];
+  q = q + a[2] * a[2];
+  q = q + a[3] * a[3];
+  return q;
+}
+
+/* g[i] = (sum_r bf16(src[r][i])) * inv_scale ; returns sum g^2 (quads from
+ * element 0, zero-padded; fp64 accumulation order free), sets *bad. */
 double oracle_release_bf16(float* g, const uint16_t* const* src, int world, int64_t n, float inv_scale,
                            int* bad, int threads) {
   double sq = 0.0;
   int b = 0;
-#pragma omp parallel for num_threads(threads) reduction(+ : sq) reduction(| : b) schedule(static)
+#pragma omp parallel for num_threads(threads) schedule(static)
   for (int64_t i = 0; i < n; ++i) {
     float a = bf16_to_f32(src[0][i]);
     for (int r = 1; r < world; ++r) a = a + bf16_to_f32(src[r][i]);
     a = a * inv_scale;
     g[i] = a;
-    b |= !isfinite(a);
-    sq += (double)a * (double)a;
+  }
+  const int64_t nq = (n + 3) / 4;
+#pragma omp parallel for num_threads(threads) reduction(+ : sq) reduction(| : b) schedule(static)
+  for (int64_t k = 0; k < nq; ++k) {
+    float a[4];
+    for (int e = 0; e < 4; ++e) {
+      const int64_t i = k * 4 + e;
+      a[e] = i < n ? g[i] : 0.0f;
+      b |= !isfinite(a[e]);
+    }
+    sq += (double)quad_sq(a);
   }
   *bad = b;
   return sq;
@@ -111,8 +134,8 @@ static double block_sum_fixed(const double* x) {
  * in the kernel's order (include/elixir_b200.h, K3): the segments' tiles of
  * tile_vecs 8-element vectors are concatenated; tile k goes to CTA k % ctas;
  * thread t (of 256) takes vectors t, t+256, ... of its tiles; each thread
- * accumulates a*a in fp64 (d*d is exact, so a multiply then one rounded add
- * equals the kernel's DFMA), elements past a segment's end count as +0.0;
+ * adds, per 8-element vector, the fp32 partials of its two quads (quad_sq) to
+ * its fp64 sum in order, elements past a segment's end counting as +0.0;
  * per-CTA block_sum_fixed into a partial; the partials summed per thread in
  * slot order (thread t: slots t, t+256, ...) and reduced by block_sum_fixed.
  * Returns that total (the kernel adds it to step_scalars[0]). */
@@ -139,11 +162,13 @@ double oracle_release_norm_ordered(const float* const* g, const int64_t* n, int 
         double acc = sq[t];
         for (int u = 0; u < U; ++u) {
           const int64_t v = v0 + (int64_t)u * T + t;
+          float a[8];
           for (int e = 0; e < 8; ++e) {
             const int64_t i = v * 8 + e;
-            const double d = i < n[s] ? (double)g[s][i] : 0.0;
-            acc = acc + d * d;
+            a[e] = i < n[s] ? g[s][i] : 0.0f;
           }
+          acc = acc + (double)quad_sq(a);
+          acc = acc + (double)quad_sq(a + 4);
         }
         sq[t] = acc;
       }

@@ -216,6 +216,11 @@ def chunk_footprint(chunk_length, gpus, compute_bytes=2, optimizer_state_bytes=1
     return -(-(compute_bytes * chunk_length + optimizer_state_bytes * chunk_length) // gpus)
 
 
+def mixed_precision_states(model_elements, compute_bytes=2, optimizer_state_bytes=12):
+    """cost_model.py:156-167: (Lc*M, Lc*M, Los*Fos*M)."""
+    return (compute_bytes * model_elements, compute_bytes * model_elements, optimizer_state_bytes * model_elements)
+
+
 def shared_state_bytes(shared_elements, gpus, compute_bytes=2, optimizer_state_bytes=12):
     """search.py:116-126."""
     if shared_elements <= 0:

@@ -1,0 +1,164 @@
+"""Whole-step arithmetic parity of a live trainer against the C oracle — TEST
+INFRASTRUCTURE ONLY (the checker; bench.py's `parity` field and
+tests/test_fullsize_gpu.py call it after their timed regions).
+
+`check_step(model, tokens, targets)` runs ONE eager training step of an
+ElixirGPT2 (world 1, every chunk GPU-home: BASELINE.json configs[0]/[1] at
+N = 1) with two observation hooks and no change to what executes:
+  * every K3 launch the step issues is logged in issue order (the runtime
+    calls `kernels.release_batch` / `kernels.release` — the log wraps them and
+    forwards the call unchanged);
+  * right before HybridAdam's update (after the backward has written every
+    gradient into its chunk and the releases are done) the update's inputs
+    are snapshotted on the device: the fp32 master / m / v and the bf16
+    gradient of every segment of the K4 table.
+The oracle then recomputes, from the snapshot, (a) the sum of squares launch
+by launch in each launch's fixed order (elx_release_geometry;
+oracle/c/elx_oracle.c oracle_release_norm_bf16_ordered), added in issue order
+as the kernel adds them to step_scalars[0], and (b) AdamW with that norm's
+clip coefficient over every element (oracle_adamw_bf16), and compares with
+what the GPU produced: the sum of squares' bits, and per array the share of
+bit-identical elements and the max relative error.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+import numpy as np
+import torch
+
+from . import arith
+
+LIB = Path(__file__).resolve().parent / "_build" / "liboracle.so"
+
+
+def _lib():
+    lib = ctypes.CDLL(str(LIB))
+    lib.oracle_release_norm_bf16_ordered.restype = ctypes.c_double
+    lib.oracle_release_norm_bf16_ordered.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_float,
+                                                     ctypes.c_int, ctypes.c_int, ctypes.c_int]
+    lib.oracle_adamw_bf16.argtypes = [ctypes.c_void_p] * 5 + [ctypes.c_int64, ctypes.c_void_p, ctypes.c_float,
+                                                             ctypes.c_int, ctypes.c_int]
+    return lib
+
+
+def _bits(t: torch.Tensor) -> np.ndarray:
+    return t.contiguous().view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def _compare(got: torch.Tensor, want: np.ndarray, bf16: bool = False) -> tuple[int, float]:
+    """(bit-identical elements, max relative error) of a device array vs the
+    oracle's, compared on the device."""
+    w = torch.from_numpy(want.view(np.int16) if bf16 else want).to(got.device)
+    if bf16:
+        same = int((got.view(torch.int16) == w).sum())
+        a, b = got.float(), w.view(torch.bfloat16).float()
+    else:
+        same = int((got.view(torch.int32) == w.view(torch.int32)).sum())
+        a, b = got, w
+    den = b.abs().clamp_min(torch.finfo(torch.float32).tiny)
+    rel = float(((a - b).abs() / den).max()) if a.numel() else 0.0
+    return same, rel
+
+
+def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int | None = None) -> dict:
+    from paper_2212_05339_b200 import kernels
+
+    mgr, opt = model.manager, model.optimizer
+    if mgr.world != 1 or mgr.cpu_ids or not mgr.fused_w1:
+        return {"checked": False, "reason": "the full-step check covers world 1 with every chunk GPU-home"}
+    threads = threads or max(1, len(os.sched_getaffinity(0)))
+    dev = mgr.device
+    segs = opt.gpu_segments                    # [(key, (p32, m, v, g, p16, n))], the K4 table's order
+    by_grad_ptr = {seg[3].data_ptr(): key for key, seg in segs}
+    launches: list[list[tuple[object, int]]] = []
+    snap: dict = {}
+    real_batch, real_one, real_step = kernels.release_batch, kernels.release, opt.step
+
+    def log_batch(ss, dtype, inv_scale, step_scalars, stream=None):
+        if step_scalars is mgr.step_scalars:
+            launches.append(([(by_grad_ptr[ptrs[0]], n) for _, ptrs, n in ss if n > 0], float(inv_scale)))
+        return real_batch(ss, dtype, inv_scale, step_scalars, stream=stream)
+
+    def log_one(g, ptrs, n, dtype, inv_scale, step_scalars, stream=None):
+        return log_batch([(g, ptrs, n)], dtype, inv_scale, step_scalars, stream=stream)
+
+    def snapshot_then_step(releases_done=None, grad_scale=1.0):
+        cur = torch.cuda.current_stream(dev)
+        if releases_done is not None:
+            cur.wait_event(releases_done)
+        for key, (p32, m, v, g, _, n) in segs:
+            snap[key] = (p32[:n].clone(), m[:n].clone(), v[:n].clone(), g[:n].clone())
+        snap["__grad_scale__"] = float(grad_scale)
+        return real_step(releases_done, grad_scale)
+
+    model.synchronize()
+    torch.cuda.synchronize(dev)
+    completed = int(mgr.step_scalars[2].item())
+    kernels.release_batch, kernels.release, opt.step = log_batch, log_one, snapshot_then_step
+    try:
+        model.train_step(tokens, targets)
+    finally:
+        kernels.release_batch, kernels.release = real_batch, real_one
+        del opt.step                           # the bound method again
+    model.synchronize()
+    stats = opt.last_stats
+    sq_gpu, flag = stats.scalars()
+    torch.cuda.synchronize(dev)
+
+    lib = _lib()
+    grads = {key: _bits(snap[key][3]) for key, _ in segs}
+    sq = 0.0
+    for grp, inv_scale in launches:
+        ns = [n for _, n in grp]
+        ctas, tv = kernels.release_geometry(ns, 1)
+        ptrs = (ctypes.c_void_p * len(grp))(*[grads[k].ctypes.data for k, _ in grp])
+        nn = (ctypes.c_int64 * len(grp))(*ns)
+        sq = sq + lib.oracle_release_norm_bf16_ordered(ptrs, nn, len(grp), ctypes.c_float(inv_scale), ctas, tv,
+                                                      threads)
+    covered = sorted(str(k) for grp, _ in launches for k, _ in grp)
+    assert covered == sorted(str(k) for k, _ in segs), "every K4 segment is released exactly once"
+
+    hp = opt.hp
+    skip = bool(flag) or not np.isfinite(sq)
+    step = completed + (0 if skip else 1)
+    coef = arith.clip_coef(sq, hp["max_norm"])
+    k = arith.adam_consts(max(step, 1), hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"])
+    kv = np.array([k["decay"], k["omb1"], k["b2"], k["omb2"], k["bc2_sqrt"], k["neg_step"], k["eps"]], np.float32)
+    gs = np.float32(snap["__grad_scale__"])
+    totals = {name: [0, 0.0] for name in ("p32", "m", "v", "p16")}
+    elements = 0
+    for key, (p32, m, v, _, p16, n) in segs:
+        sp, sm, sv, _ = snap[key]
+        P, M, V = sp.cpu().numpy(), sm.cpu().numpy(), sv.cpu().numpy()
+        G = arith.bf16_bits_to_f32(grads[key])
+        if gs != np.float32(1.0):
+            G = (G * gs).astype(np.float32)
+        out16 = np.empty(n, np.uint16)
+        lib.oracle_adamw_bf16(P.ctypes.data, M.ctypes.data, V.ctypes.data, G.ctypes.data, out16.ctypes.data, n,
+                              kv.ctypes.data, ctypes.c_float(coef), int(skip), threads)
+        for name, got, want, bf in (("p32", p32[:n], P, False), ("m", m[:n], M, False), ("v", v[:n], V, False),
+                                    ("p16", p16[:n], out16, True)):
+            same, rel = _compare(got, want, bf)
+            totals[name][0] += same
+            totals[name][1] = max(totals[name][1], rel)
+        elements += n
+        del snap[key]
+    torch.cuda.empty_cache()
+    return {
+        "checked": True,
+        "elements": elements,
+        "segments": len(segs),
+        "release_launches": len(launches),
+        "sumsq_bit_identical": sq_gpu == sq,
+        "sumsq_rel_err": abs(sq_gpu - sq) / sq if sq else 0.0,
+        "bit_identical_frac": {name: t[0] / elements for name, t in totals.items()},
+        "max_rel_err": {name: t[1] for name, t in totals.items()},
+        "tolerance": "north_star: 1e-6 relative for fp32 Adam and reduced gradients; bit-exact for bytes",
+        "within_tolerance": all(t[1] <= 1e-6 for t in totals.values()) and abs(sq_gpu - sq) <= 1e-6 * abs(sq),
+        "oracle": "oracle/c/elx_oracle.c (ordered sum of squares per K3 launch, AdamW), "
+                  f"{threads} host threads",
+    }

@@ -16,6 +16,7 @@ from .errors import (ChunkTooSmallError, ElixirCudaError, ExtensionMissingError,
 from .layout import Chunk, ChunkLayout, ChunkMember, ChunkTrace, build_chunk_trace, pack_chunks, waste_rate, working_set_blocks
 from .profiles import (AccessTrace, ModelProfile, OperatorNode, ParameterSpec, PrecisionSpec, coarsen_graph,
                        partition_multiuse, synthesize_transformer_profile)
+from .memory import chunk_footprint, mixed_precision_states, shared_state_bytes
 from .schedule import Device, Plan, Schedule, SimReport, compile_schedule, load_plan, simulate
 
 __all__ = [
@@ -25,7 +26,8 @@ __all__ = [
     "working_set_blocks", "AccessTrace", "ModelProfile", "OperatorNode", "ParameterSpec", "PrecisionSpec",
     "coarsen_graph", "partition_multiuse", "synthesize_transformer_profile", "Device", "Plan", "Schedule",
     "SimReport", "compile_schedule", "load_plan", "simulate", "ChunkManager", "ChunkFetcher", "HybridAdam",
-    "LossScaler", "ElixirGPT2", "GPT2Config", "PRESETS",
+    "LossScaler", "ElixirGPT2", "GPT2Config", "PRESETS", "chunk_footprint", "mixed_precision_states",
+    "shared_state_bytes",
 ]
 
 __version__ = "0.1.0"

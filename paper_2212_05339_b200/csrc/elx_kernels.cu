@@ -317,14 +317,13 @@ __global__ void peer_sum_f64_kernel(double* dst, const PtrBatch peers, int count
 // One launch reduces a batch of segments (every chunk due at one reduce
 // position, plus the shared parameter at the last one):
 //   g[i] = (sum_{r in rank order} float(src_r[i])) * inv_scale   (fp32)
-//   sq  += g[i]^2  (fp64)        flag |= !isfinite(g[i])
+//   sq  += fp32 quad partial of g[4k..4k+3] (fp64)   flag |= !isfinite(sq)
 // The elements of the batch are cut into tiles of kRelThreads * kU vectors of
 // 8 (16-byte loads per rank); CTA b of a G-CTA grid takes tiles b, b+G, ...,
 // and thread t of a tile handles vectors t, t+256, ... (kU of them, all loads
 // of a tile issued before any is reduced: kU * world 16-byte loads in flight
-// per thread). Each thread accumulates its elements' squares in fp64 in that
-// order (one DFMA each: d*d is exact in fp64, so it rounds like the oracle's
-// multiply-then-add); the CTA reduces its 256 values with a fixed butterfly
+// per thread). Each thread adds its vectors' two quad partials (sq_acc8) to
+// an fp64 sum in that order; the CTA reduces its 256 values with a fixed butterfly
 // (warps, then warp 0 over the 8 warp sums) into partial slot b of the step
 // scalar block; the LAST CTA to finish (arrival ticket) adds the G partials in
 // slot order with the same butterfly and adds the total to step_scalars[0].
@@ -386,14 +385,29 @@ __device__ __forceinline__ void publish_partial(double sq, int bad, double* sc) 
   }
 }
 
-__device__ __forceinline__ double sq_acc(double sq, float a) {
-  const double d = (double)a;
-  return __fma_rn(d, d, sq);
+// The sum-of-squares unit: four consecutive values a0..a3 give the fp32
+// partial q = ((a0*a0 + a1*a1) + a2*a2) + a3*a3 (separately rounded, no FMA),
+// added to the fp64 running sum. A bf16 value's square is exact in fp32, and
+// with every term >= 0 the total's relative error is <= ~4 * 2^-24 — far
+// inside the 1e-6 bar — while the kernel needs one fp32->fp64 conversion per
+// FOUR elements instead of one each (the conversions run on the XU pipe, which
+// per element capped the world-1 norm pass below the HBM rate at power-capped
+// clocks). Restated by oracle/arith.py quad_sq and oracle/c/elx_oracle.c.
+__device__ __forceinline__ float quad_sq(float a0, float a1, float a2, float a3) {
+  float q = __fmul_rn(a0, a0);
+  q = __fadd_rn(q, __fmul_rn(a1, a1));
+  q = __fadd_rn(q, __fmul_rn(a2, a2));
+  return __fadd_rn(q, __fmul_rn(a3, a3));
+}
+__device__ __forceinline__ double sq_acc8(double sq, const float* a) {
+  sq = __dadd_rn(sq, (double)quad_sq(a[0], a[1], a[2], a[3]));
+  return __dadd_rn(sq, (double)quad_sq(a[4], a[5], a[6], a[7]));
 }
 
-// Overflow flag from the accumulated sum of squares: a finite float squares
-// to a finite double (<= 1.2e77) and no sum of < 2^60 of them overflows fp64,
-// so sq is non-finite exactly when some element was inf/nan.
+// Overflow flag from the accumulated sum of squares: sq is non-finite exactly
+// when some element was inf/nan, or finite but so large (|g| >~ 9e18) that its
+// quad's fp32 partial overflows — a gradient no training step can use, treated
+// as an overflow (skip) too. No sum of < 2^60 finite partials overflows fp64.
 __device__ __forceinline__ int bad_of(double sq) { return !isfinite(sq); }
 
 template <typename T16>
@@ -423,30 +437,6 @@ __device__ __forceinline__ uint4 ld_src(const void* p) {
   return ld_rel(p);
 }
 
-// The thread's world-1 sum of squares through the conversion path only, in the
-// kernel's order (subnormal / inf / nan inputs seen by the integer path).
-template <int kU>
-__device__ __noinline__ double thread_sq_exact_bf16(const RelBatch& b) {
-  constexpr int64_t kTileVecs = (int64_t)kRelThreads * kU;
-  const int64_t ntiles = b.tile0[b.nseg];
-  double sq = 0.0;
-  int s = 0;
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
-    const int64_t n = b.n[s];
-    const int64_t v0 = (t - b.tile0[s]) * kTileVecs + threadIdx.x;
-    const __nv_bfloat16* p = static_cast<const __nv_bfloat16*>(b.src[s][0]);
-    for (int u = 0; u < kU; ++u) {
-      const int64_t v = v0 + (int64_t)u * kRelThreads;
-      for (int e = 0; e < 8; ++e) {
-        const int64_t i = v * 8 + e;
-        sq = sq_acc(sq, i < n ? __bfloat162float(p[i]) : 0.f);
-      }
-    }
-  }
-  return sq;
-}
-
 // kScaleOne: inv_scale == 1 (bf16 training), the multiply is an exact identity and is skipped.
 template <typename T16, int kWorld, int kU, bool kScaleOne>
 __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid_constant__ RelBatch b, int world_rt,
@@ -454,10 +444,8 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
   constexpr int kR = kWorld > 0 ? kWorld : 1;
   const int world = kWorld > 0 ? kWorld : world_rt;
   constexpr int64_t kTileVecs = (int64_t)kRelThreads * kU;
-  constexpr bool kIntCvt = kWorld == 1 && kScaleOne && std::is_same<T16, __nv_bfloat16>::value;
   const int64_t ntiles = b.tile0[b.nseg];
   double sq = 0.0;
-  uint32_t mx = 0u, mn = 0xFFFFFFFFu;
   int s = 0;
   for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
     while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
@@ -490,31 +478,11 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
         }
-        if (kIntCvt) {
-          // world-1 bf16 norm pass: the F2F.F64 conversions run on the XU pipe at ~8/clk/SM, below the
-          // HBM rate (11.5 bf16/clk/SM). Half of them are replaced by an exact integer construction of
-          // the same double: the high bf16 of a 32-bit word IS the float's bits, |x| as a double is
-          // hi = (a >> 3) + (1023 - 127) << 20, lo = 0 for a normal x, 0 for zero. Same values, same
-          // DFMA order as the conversion path: bit-identical sums. Subnormal / inf / nan high halves are
-          // tracked (mx, mn) and make the thread recompute its sum through the conversion path.
-          const uint32_t* w = reinterpret_cast<const uint32_t*>(&raw[u][0]);
+        if (!kScaleOne) {
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            sq = sq_acc(sq, __uint_as_float(w[j] << 16));
-            const uint32_t a = w[j] & 0x7FFF0000u;
-            mx = max(mx, a);
-            mn = min(mn, a - 1u);
-            const uint32_t hi = a ? (a >> 3) + 0x38000000u : 0u;
-            const double d = __hiloint2double((int)hi, 0);
-            sq = __fma_rn(d, d, sq);
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            if (!kScaleOne) acc[e] = __fmul_rn(acc[e], inv_scale);
-            sq = sq_acc(sq, acc[e]);
-          }
+          for (int e = 0; e < 8; ++e) acc[e] = __fmul_rn(acc[e], inv_scale);
         }
+        sq = sq_acc8(sq, acc);
         if (g != nullptr && v < nvec) {
           if (v < nfull) {
             float4* d = reinterpret_cast<float4*>(g + v * 8);
@@ -542,10 +510,8 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
           for (int e = 0; e < 8; ++e) acc[e] = r == 0 ? x[e] : __fadd_rn(acc[e], x[e]);
         }
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          acc[e] = __fmul_rn(acc[e], inv_scale);
-          sq = sq_acc(sq, acc[e]);
-        }
+        for (int e = 0; e < 8; ++e) acc[e] = __fmul_rn(acc[e], inv_scale);
+        sq = sq_acc8(sq, acc);
         if (g != nullptr && v < nvec) {
 #pragma unroll
           for (int e = 0; e < 8; ++e)
@@ -554,13 +520,13 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
       }
     }
   }
-  if (kIntCvt && (mx >= 0x7F800000u || mn < 0x007FFFFFu)) sq = thread_sq_exact_bf16<kU>(b);
   publish_partial(sq, bad_of(sq), sc);
 }
 
-// Unaligned sources or destination (not 16/32-byte aligned): one element per
-// thread-step, same partial/ticket reduction. Element i of segment s belongs
-// to CTA (i / kRelThreads) % G... (the elements of the batch flattened, grid-stride).
+// Unaligned sources or destination (not 16-byte aligned): scalar loads, one
+// quad of 4 consecutive elements per thread-step (the same quad partials as the
+// vector path; only the fp64 order of their sum follows this grid-stride
+// walk), same partial/ticket reduction.
 template <typename T16>
 __global__ void __launch_bounds__(kRelThreads) release_batch_scalar_kernel(const __grid_constant__ RelBatch b,
                                                                            int world, float inv_scale,
@@ -568,15 +534,24 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_scalar_kernel(const
   double sq = 0.0;
   for (int s = 0; s < b.nseg; ++s) {
     const int64_t n = b.n[s];
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-      float a = 0.f;
-      for (int r = 0; r < world; ++r) {
-        const float x = to_f32<T16>(static_cast<const T16*>(b.src[s][r])[i]);
-        a = r == 0 ? x : __fadd_rn(a, x);
+    const int64_t nq = (n + 3) >> 2;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nq; k += (int64_t)gridDim.x * blockDim.x) {
+      float a[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int64_t i = k * 4 + e;
+        float x = 0.f;
+        if (i < n) {
+          for (int r = 0; r < world; ++r) {
+            const float y = to_f32<T16>(static_cast<const T16*>(b.src[s][r])[i]);
+            x = r == 0 ? y : __fadd_rn(x, y);
+          }
+          x = __fmul_rn(x, inv_scale);
+          if (b.g[s]) b.g[s][i] = x;
+        }
+        a[e] = x;
       }
-      a = __fmul_rn(a, inv_scale);
-      sq = sq_acc(sq, a);
-      if (b.g[s]) b.g[s][i] = a;
+      sq = __dadd_rn(sq, (double)quad_sq(a[0], a[1], a[2], a[3]));
     }
   }
   publish_partial(sq, bad_of(sq), sc);
@@ -644,7 +619,7 @@ int run_release_batch(RelBatch& b, int world, float inv_scale, double* sc, cudaS
   } else {
     int64_t mx = 0;
     for (int i = 0; i < b.nseg; ++i) mx = std::max(mx, b.n[i]);
-    work = (mx + kRelThreads - 1) / kRelThreads;
+    work = ((mx + 3) / 4 + kRelThreads - 1) / kRelThreads;  // quads per thread-step
     b.tile0[0] = 0;
   }
   if (work == 0) return ELX_OK;

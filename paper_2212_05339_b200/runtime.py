@@ -256,6 +256,21 @@ class ChunkManager:
                                 for s in self.shared.values()),
         }
 
+    def memory_ledger(self) -> dict:
+        """This rank's share of the whole-model states in the contract's terms
+        (mixed_precision_states, cost_model.py:156-167): the compute-dtype
+        parameter bytes it owns, the gradient bytes (the gradient overwrites
+        the parameter's slot in the chunk, so it occupies the
+        same bytes; at N > 1 the reduced fp32 shard is extra and listed
+        separately) and the fp32 master/m/v bytes. Summed over ranks, every
+        element is owned exactly once: params/grads = Lc*M, optimizer =
+        Los*Fos*M, the contract's triple."""
+        lc = torch.tensor([], dtype=self.dtype).element_size()
+        owned = sum(self.valid(c) for c in range(self.n_chunks)) + \
+            sum(sp.valid(self.rank) for sp in self.shared.values())
+        return {"param_bytes": lc * owned, "grad_bytes": lc * owned, "optimizer_bytes": 12 * owned,
+                "reduced_grad_shard_bytes": 0 if self.world == 1 else 4 * owned, "owned_elements": owned}
+
     # ------------------------------------------------------------ init
     def load_params(self, tensors: Mapping[str, torch.Tensor]) -> None:
         """Pack initial parameters into chunks (K1) and seed the fp32 masters."""
@@ -738,7 +753,10 @@ class HybridAdam:
     def __init__(self, manager: ChunkManager, *, lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8,
                  weight_decay: float = 0.01, max_norm: float | None = 1.0, cpu_threads: int | None = None,
                  overlap: bool = False, device_step: bool = True, cpu_update: str = "split",
-                 update_rates: tuple[float, float] | None = None, stream_tile: int = 32 * 2 ** 20):
+                 update_rates: tuple[float, float] | None = None, stream_tile: int = 32 * 2 ** 20,
+                 max_grad_norm: float | None = None):
+        if max_grad_norm is not None:  # SURVEY.md §8b's name for max_norm
+            max_norm = max_grad_norm
         self.mgr = manager
         self.hp = dict(lr=lr, beta1=betas[0], beta2=betas[1], eps=eps, weight_decay=weight_decay,
                        max_norm=max_norm or 0.0)
@@ -748,11 +766,13 @@ class HybridAdam:
         # groups in forward-use order: shared params (used by the first node), then chunks by id
         self.groups: list[tuple[object, kernels.AdamTable]] = []
         all_segs = []
+        self.gpu_segments: list[tuple[object, tuple]] = []  # (shared pid or chunk id, K4 segment), table order
         for pid, sp in m.shared.items():
             n = sp.valid(m.rank)
             if n > 0:
                 seg = (sp.p32, sp.m, sp.v, sp.grad if m.fused_w1 else sp.g32, sp.p16, n)
                 all_segs.append(seg)
+                self.gpu_segments.append((pid, seg))
                 self.groups.append((pid, kernels.AdamTable([seg], m.device)))
         for c in m.gpu_ids:
             r = m.row[c]
@@ -762,6 +782,7 @@ class HybridAdam:
                 # overwritten in place by the new parameter
                 seg = (m.p32[r], m.m[r], m.v[r], m.p16[r] if m.fused_w1 else m.g32[r], m.p16[r], n)
                 all_segs.append(seg)
+                self.gpu_segments.append((c, seg))
                 self.groups.append((c, kernels.AdamTable([seg], m.device)))
         self.table = kernels.AdamTable(all_segs, m.device)  # single-launch form (overlap=False)
         all_cpu = {}
@@ -975,8 +996,14 @@ class HybridAdam:
         torch.cuda.synchronize(m.device)
 
     # ------------------------------------------------------------ step
-    def step(self, releases_done: torch.cuda.Event | None = None, grad_scale: float = 1.0) -> "StepStats":
+    def step(self, releases_done: "torch.cuda.Event | float | None" = None, grad_scale: float = 1.0, *,
+             loss_scale: float | None = None) -> "StepStats":
         """All-reduce norm/overflow, then update every shard.
+
+        SURVEY.md §8b's form `step(loss_scale) -> (found_inf, grad_norm)` is
+        accepted too: a number in the first position (or `loss_scale=`) is the
+        loss scale, and grad_scale = 1 / loss_scale (the releases are then
+        waited for by synchronising the device).
 
         Device-step mode (default): no host synchronisation — the overflow
         skip, the clip coefficient and the step number (step_scalars[2]) are
@@ -985,6 +1012,12 @@ class HybridAdam:
         only when read. `releases_done` is the event ChunkFetcher.finish()
         returns (None: synchronise the device); `grad_scale` = 1/loss_scale,
         applied in-register to compute-dtype gradients (world 1)."""
+        if isinstance(releases_done, (int, float)):
+            releases_done, loss_scale = None, float(releases_done)
+        if loss_scale is not None:
+            if not loss_scale > 0:
+                raise ValidationError("loss_scale must be > 0")
+            grad_scale = 1.0 / loss_scale
         with _nvtx("elx.adam"):
             return self._step_impl(releases_done, grad_scale)
 

@@ -80,8 +80,10 @@ class ReferenceStep:
         for pid in per_rank[0][1]:
             srcs = [g[pid].detach().reshape(-1).cpu().view(torch.int16).numpy().view(np.uint16)
                     for _, g in per_rank]
-            r, s, b = arith.release(srcs, 1.0 / scale, name)
-            rel[pid], sq, bad = r, sq + s, bad or b
+            r, _, b = arith.release(srcs, 1.0 / scale, name)
+            rel[pid], bad = r, bad or b
+        # K3's sum-of-squares units run over each chunk from its offset 0 (oracle/arith.py quad_sq)
+        sq = arith.sumsq_chunked(rel, self.m.manager.members)
         hp = self.hp
         coef = arith.clip_coef(sq, hp["max_norm"])
         t = self.t if bad else self.t + 1

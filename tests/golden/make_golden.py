@@ -153,6 +153,32 @@ def make_layouts(ref):
     print("layouts.json:", (GOLDEN / "layouts.json").stat().st_size, "bytes")
 
 
+def make_memory(ref):
+    """The memory contracts (cost_model.py:147-167, search.py:116-126) at the
+    BASELINE model sizes and edge cases, with default and custom widths."""
+    sizes = [1, 7, 124439808, 1313626112, 3782697984, 9876287488]
+    precs = [(2, 4, 3), (4, 4, 3), (2, 4, 2)]
+    out = {"mixed_precision_states": [], "chunk_footprint": [], "shared_state_bytes": []}
+    for lc, ob, of in precs:
+        P = ref.PrecisionSpec(compute_bytes=lc, optimizer_bytes=ob, optimizer_factor=of)
+        for M in sizes:
+            out["mixed_precision_states"].append([M, [lc, ob, of], list(ref.mixed_precision_states(M, P))])
+        for C in (1, 7, 16 * MI, 84182029, 100 * MI):
+            for n in (1, 2, 3, 8):
+                out["chunk_footprint"].append([C, n, [lc, ob, of], ref.chunk_footprint(C, n, P)])
+        for S in (0, 38597376, 102926336):
+            for n in (1, 2, 8):
+                out["shared_state_bytes"].append([S, n, [lc, ob, of], ref.shared_state_bytes(S, n, P)])
+    for bad in (0, -1):
+        try:
+            ref.mixed_precision_states(bad, ref.PrecisionSpec())
+            raise SystemExit("expected ValidationError")
+        except ref.ValidationError:
+            out.setdefault("mixed_precision_states_invalid", []).append(bad)
+    (GOLDEN / "memory.json").write_text(json.dumps(out, separators=(",", ":")))
+    print("memory.json:", (GOLDEN / "memory.json").stat().st_size, "bytes")
+
+
 def make_adamw():
     import torch
 
@@ -254,6 +280,7 @@ def main():
 
     GOLDEN.mkdir(parents=True, exist_ok=True)
     make_layouts(ref)
+    make_memory(ref)
     make_adamw()
     make_plans(ref)
 

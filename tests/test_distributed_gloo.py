@@ -100,7 +100,7 @@ def _release_case(rank):
     # norm all-reduce across ranks == single-process norm
     tot = torch.tensor([sq, float(bad)], dtype=torch.float64)
     t.all_reduce_sum(tot)
-    want = float(np.dot(full.astype(np.float64), full))
+    want = arith.sumsq(full)  # the same quad partials; only the fp64 order differs
     assert tot[0].item() == pytest.approx(want, rel=1e-12)
     assert tot[1].item() == 0.0
 

@@ -207,3 +207,31 @@ def test_gpt2_small_full_step_equals_reference(cuda, deterministic_library):
     live = model.fetcher.counters()
     for k in ("gather_ops", "replaced_ops", "reduce_ops"):
         assert live[k] == sim[k], (k, live, sim)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_gpt2_small_trainer_step_checked_by_oracle_parity(cuda, graph):
+    """The bench's `parity` field on BASELINE configs[0] (GPT-2 small, plan
+    gpt2-small_n1.json, the trainer's own state after real steps, eager or
+    after CUDA-graph replays): one more step's K3 launches and K4 update
+    recomputed by the C oracle from the update's own inputs — the sum of
+    squares and every p32 / m / v / bf16 element bit-identical."""
+    from oracle.parity import check_step
+    cfg = PRESETS["gpt2-small"]
+    plan = (ROOT / "plans" / "gpt2-small_n1.json").read_text()
+    model = ElixirGPT2(cfg, plan, device=cuda, **HP)
+    gen = torch.Generator(device=cuda).manual_seed(5)
+    t = torch.randint(0, cfg.vocab, (cfg.batch, cfg.seq_len + 1), generator=gen, device=cuda)
+    tok, tgt = t[:, :-1].contiguous(), t[:, 1:].contiguous()
+    model.train_step(tok, tgt)
+    if graph:
+        model.capture(tok, tgt, warmup=1)
+        model.graph_step(tok, tgt)
+        model._graph = None
+    else:
+        model.train_step(tok, tgt)
+    rep = check_step(model, tok, tgt)
+    assert rep["checked"] and rep["elements"] == 124_439_808
+    assert rep["sumsq_bit_identical"], rep
+    assert all(f == 1.0 for f in rep["bit_identical_frac"].values()), rep
+    assert rep["within_tolerance"]

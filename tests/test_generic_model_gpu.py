@@ -117,7 +117,8 @@ class OracleTrainer:
     """Standalone bf16 parameters, the same block function, the CPU oracle's
     release / clip / AdamW (oracle/arith.py)."""
 
-    def __init__(self, init):
+    def __init__(self, init, members):
+        self.members = members  # pid -> (chunk, offset, numel) of the layout the runtime uses
         self.p16 = {k: v.clone() for k, v in init.items()}
         self.master = {k: v.float().cpu().numpy().reshape(-1).copy() for k, v in init.items()}
         self.m = {k: np.zeros_like(v) for k, v in self.master.items()}
@@ -144,10 +145,12 @@ class OracleTrainer:
                     gs = torch.autograd.grad(out, [xin] + ps, grad_outputs=grad)
             grad = gs[0]
             grads.update({p: g for p, g in zip(names[i], gs[1:])})
-        rel, sq, bad = {}, 0.0, False
+        rel, bad = {}, False
         for p, g in grads.items():
-            r, s, b = arith.release([g.detach().reshape(-1).cpu().view(torch.int16).numpy().view(np.uint16)], 1.0)
-            rel[p], sq, bad = r, sq + s, bad or b
+            r, _, b = arith.release([g.detach().reshape(-1).cpu().view(torch.int16).numpy().view(np.uint16)], 1.0)
+            rel[p], bad = r, bad or b
+        # the chunk store's norm units: quads over each chunk from its offset 0 (oracle/arith.py sumsq_chunked)
+        sq = arith.sumsq_chunked(rel, self.members)
         coef = arith.clip_coef(sq, HP["max_norm"])
         self.t += 0 if bad else 1
         for p in rel:
@@ -172,7 +175,7 @@ def test_generic_model_through_public_api(cuda, kind):
             "half-offload": Plan(C, ws + 1, {c: ("cpu" if c % 2 else "gpu") for c in range(n)})}[kind]
     init = _init(shapes, cuda)
     ours = Trainer(profile, shapes, plan, init, cuda)
-    ref = OracleTrainer(init)
+    ref = OracleTrainer(init, ours.mgr.members)
     for s in range(3):
         x, y = _data(cuda, s)
         lo = ours.step(x, y)

@@ -261,7 +261,7 @@ def test_release_accumulates_norm_and_flags_overflow(cuda):
     kernels.release(out, [bb.data_ptr()], n, torch.bfloat16, 1.0, sc)
     torch.cuda.synchronize()
     assert sc[1].item() == 1.0
-    assert first == pytest.approx(float((a.double() ** 2).sum()), rel=1e-12)
+    assert first == pytest.approx(arith.sumsq(a.float().numpy()), rel=1e-12)
     kernels.step_reset(sc)
     torch.cuda.synchronize()
     assert sc[0].item() == 0.0 and sc[1].item() == 0.0
@@ -469,7 +469,7 @@ def test_adam_compute_dtype_grads_equal_released_path(cuda):
         if j % 2 == 0:
             kernels.release(None, [g.data_ptr()], n, torch.bfloat16, inv_scale, sc2)
     torch.cuda.synchronize()
-    want_even = sum(float(np.dot(h[3].astype(np.float64), h[3])) for j, h in enumerate(host) if j % 2 == 0)
+    want_even = sum(arith.sumsq(h[3]) for j, h in enumerate(host) if j % 2 == 0)
     assert sc2[0].item() == pytest.approx(want_even, rel=1e-12)
     tab = kernels.AdamTable(segs, cuda)
     kernels.adam(tab, HP, 2, sc, torch.bfloat16, grad_scale=inv_scale)

@@ -48,7 +48,9 @@ def _torchrun(world: int, args: list[str], timeout: int = 600) -> subprocess.Com
            "--master-addr", "127.0.0.1", "--master-port", str(_port())] + args
     env = dict(os.environ, OMP_NUM_THREADS="4")
     p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=timeout)
-    assert p.returncode == 0, p.stdout[-3000:] + p.stderr[-3000:]
+    if p.returncode != 0:  # the first failing rank's own lines, not just the launcher's tail
+        r0 = [ln for ln in p.stderr.splitlines() if ln.startswith("[rank0]")]
+        raise AssertionError("\n".join(r0[-60:]) + "\n----\n" + p.stdout[-2000:] + p.stderr[-3000:])
     return p
 
 

@@ -280,6 +280,29 @@ def test_memory_contract_chunk_footprint(cuda, world):
         assert rep["shared_bytes"] - contract == ledger, (rep["shared_bytes"], contract, ledger)
 
 
+@pytest.mark.parametrize("world", [1, 2, 3])
+def test_memory_ledger_partitions_mixed_precision_states(cuda, world):
+    """Summed over ranks, the elements each rank owns give exactly the
+    reference's whole-model states mixed_precision_states(M) =
+    (2M, 2M, 12M) (cost_model.py:156-167): every parameter element is owned
+    by one rank, with offloaded plans too."""
+    from _refstep import run_ranks
+    from paper_2212_05339_b200 import mixed_precision_states
+    for name in ("all-gpu-max", "offload-half"):
+        plan = dict(_plans(CFG))[name]
+
+        def rank_fn(r, transport):
+            model = ElixirGPT2(CFG, plan, device=cuda, transport=transport, **HP)
+            return model.manager.memory_ledger(), model.profile.total_elements
+
+        res = [rank_fn(0, None)] if world == 1 else run_ranks(world, rank_fn)
+        total = res[0][1]  # M: every parameter element of the model, chunk members and the shared wte
+        want = mixed_precision_states(total)
+        got = [sum(led[k] for led, _ in res) for k in ("param_bytes", "grad_bytes", "optimizer_bytes")]
+        assert tuple(got) == want, (name, got, want)
+        assert all(led["reduced_grad_shard_bytes"] == (0 if world == 1 else 2 * led["grad_bytes"]) for led, _ in res)
+
+
 def test_cuda_graph_checkpoint_round_trip(cuda):
     """A trainer stepping by graph replays checkpoints like an eager one: its
     state_dict (step count from the device counter) restores into a fresh
