@@ -54,6 +54,12 @@ const char* elx_last_error(void);
 /* Number of kernels this library launched in this process (all streams).
  * bench.py reports the delta over its timed region as `gpu_launches`. */
 int64_t elx_launch_count(void);
+/* Record a (timing) cudaEvent_t on a stream. Outside a capture this is
+ * cudaEventRecord; while the stream is being captured into a CUDA graph the
+ * record is EXTERNAL (an event-record node), so every replay of the graph
+ * re-records the event and kernels inside a replayed step can be timed
+ * (bench.py times K4 inside its timed graph replays this way). */
+int elx_event_record(void* event, void* stream);
 /* sizeof of the ABI structs, for binding checks: 0 elx_event, 1
  * elx_sim_counters, 2 elx_member, 3 elx_adam_seg, 4 elx_adam_hp,
  * 5 elx_cpu_seg; -1 for an unknown id. */

@@ -87,6 +87,7 @@ _SIGNATURES = {
     "elx_abi_version": (c_i32, []),
     "elx_last_error": (ctypes.c_char_p, []),
     "elx_launch_count": (c_i64, []),
+    "elx_event_record": (ctypes.c_int, [c_vp, c_vp]),
     "elx_sizeof": (c_i64, [c_i32]),
     "elx_layout_pack": (ctypes.c_int, [c_vp, c_i32, c_i64, c_vp, c_vp, c_vp]),
     "elx_schedule": (ctypes.c_int, [c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp]),

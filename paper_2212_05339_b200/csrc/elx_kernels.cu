@@ -1472,6 +1472,19 @@ int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int3
   return ELX_OK;
 }
 
+int elx_event_record(void* event, void* stream) {
+  elx::clear_error();
+  if (!event) return elx::fail(ELX_ERR_VALIDATION, "null event");
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaError_t e = cudaStreamIsCapturing((cudaStream_t)stream, &cs);
+  if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_event_record: %s", cudaGetErrorString(e));
+  // inside a capture an EXTERNAL record becomes an event-record node: every replay re-records the event
+  e = cudaEventRecordWithFlags((cudaEvent_t)event, (cudaStream_t)stream,
+                               cs == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault);
+  if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_event_record: %s", cudaGetErrorString(e));
+  return ELX_OK;
+}
+
 int elx_enable_peer_access(int32_t peer_device) {
   elx::clear_error();
   int cur = 0;

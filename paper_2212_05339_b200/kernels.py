@@ -35,6 +35,15 @@ def _stream(stream) -> int:
     return s.cuda_stream
 
 
+def event_record(event: torch.cuda.Event, stream=None) -> None:
+    """Record `event` on `stream`; inside a CUDA-graph capture as an external
+    event-record node that every replay re-records (elx_event_record). The
+    event must already exist (torch creates it on its first record)."""
+    if not event.cuda_event:
+        raise ValidationError("event_record needs an event that was recorded once before (created)")
+    _lib.check(_lib.load().elx_event_record(event.cuda_event, _stream(stream)), "elx_event_record")
+
+
 def _cuda(t: torch.Tensor, what: str) -> None:
     if not t.is_cuda:
         raise ValidationError(f"{what} must be a CUDA tensor")

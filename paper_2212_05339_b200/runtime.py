@@ -623,8 +623,17 @@ class ChunkFetcher:
                 t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 t0.record(comm)
             segs = []
+            exchange = mgr.world > 1 and not mgr.p2p
             for c in batch:
-                if mgr.valid(c) > 0:
+                if exchange:
+                    # the all-to-all lands every rank's copy of our segment in the ONE receive buffer, so each
+                    # chunk's K3 runs before the next chunk's exchange; and every rank joins every collective,
+                    # also for a chunk whose tail leaves this rank no valid elements
+                    srcs = self._release_srcs(c)
+                    if mgr.valid(c) > 0:
+                        kernels.release_batch([(mgr.g32[mgr.row[c]], srcs, mgr.valid(c))], mgr.dtype,
+                                              self.inv_scale, mgr.step_scalars, stream=comm)
+                elif mgr.valid(c) > 0:
                     segs.append((None if mgr.fused_w1 else mgr.g32[mgr.row[c]], self._release_srcs(c), mgr.valid(c)))
             if segs:
                 kernels.release_batch(segs, mgr.dtype, self.inv_scale, mgr.step_scalars, stream=comm)
@@ -637,11 +646,15 @@ class ChunkFetcher:
                 if mgr.p2p:
                     self._dirty.add(self.block_of[c])
                 n = mgr.valid(c)
-                if mgr.homes[c] is not Device.CPU or n == 0:
+                if mgr.homes[c] is not Device.CPU:
                     continue
                 if c in staged:  # CPU-home at N > 1: reduce into the fp32 staging shard, then D2H it
-                    kernels.release(mgr.stage32, self._release_srcs(c), n, mgr.dtype, self.inv_scale,
-                                    mgr.step_scalars, stream=comm)
+                    srcs = self._release_srcs(c)  # a collective on the exchange path: joined even when n == 0
+                    if n > 0:
+                        kernels.release(mgr.stage32, srcs, n, mgr.dtype, self.inv_scale, mgr.step_scalars,
+                                        stream=comm)
+                if n == 0:
+                    continue
                 src = mgr.storage(c) if mgr.fused_w1 else mgr.stage32
                 nbytes = n * src.element_size()
                 if self.time_release:
@@ -824,6 +837,7 @@ class HybridAdam:
         self.cpu_update_s = 0.0    # host time spent in CPU-home updates (on their thread)
         self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
         self.time_adam = False
+        self._cap_events: tuple[torch.cuda.Event, torch.cuda.Event] | None = None
         self.done_event: torch.cuda.Event | None = None
         self.grad_scale = 1.0
         self.pending: dict[object, torch.cuda.Event] = {}     # key -> GPU update done
@@ -1053,9 +1067,16 @@ class HybridAdam:
         if opt is not cur:
             opt.wait_stream(cur)
         tabs = self.tables if self.device_step else None
+        capturing = torch.cuda.is_current_stream_capturing()
         if self.time_adam:
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(opt)
+            if capturing:  # graph-internal K4 timing: the pair prepared by prepare_graph_timing()
+                if self._cap_events is None:
+                    raise ValidationError("time_adam under capture needs prepare_graph_timing() first")
+                e0, e1 = self._cap_events
+                kernels.event_record(e0, opt)
+            else:
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(opt)
         self.pending = {}
         with torch.cuda.stream(opt):
             if self.overlap:
@@ -1073,7 +1094,10 @@ class HybridAdam:
                 for sp in m.shared.values():
                     m.gather_shared(sp)
             if self.time_adam:
-                e1.record(opt)
+                if capturing:
+                    kernels.event_record(e1, opt)
+                else:
+                    e1.record(opt)
                 self.adam_events.append((e0, e1))
             if self.device_step:
                 kernels.step_advance(m.step_scalars, stream=opt)
@@ -1091,6 +1115,17 @@ class HybridAdam:
             self._cpu_thread.start()
         self.last_stats = stats
         return stats
+
+    def prepare_graph_timing(self) -> tuple[torch.cuda.Event, torch.cuda.Event]:
+        """Create the timing-event pair a captured step records around K4 (as
+        event-record nodes: each replay re-records them, so
+        `e0.elapsed_time(e1)` after a replay is that replay's K4 time)."""
+        cur = torch.cuda.current_stream(self.mgr.device)
+        pair = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+        for e in pair:
+            e.record(cur)  # creates the CUDA events before any capture starts
+        self._cap_events = pair
+        return pair
 
     @property
     def last(self) -> dict:

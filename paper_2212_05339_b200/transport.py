@@ -136,11 +136,14 @@ def _ipc_handle(t: torch.Tensor) -> tuple[bytes, int]:
     st = t.untyped_storage()
     _, handle, _, storage_off, *_ = st._share_cuda_()
     h = bytes(handle)
-    if len(h) == 65 and h[:1] == b"c":     # torch's tagged form: 'c' + cudaIpcMemHandle_t
-        h = h[1:]
+    # torch's shareable form: [format version byte] + segment type ('c' = cudaMalloc, 'e' = expandable
+    # segment) + the 64-byte cudaIpcMemHandle_t for 'c'; a bare 64-byte handle on older versions
+    if len(h) > 64 and h[-65:-64] == b"c":
+        h = h[-64:]
     if len(h) != 64:
-        raise ValidationError("IpcTransport needs cudaMalloc-backed segments (unset expandable_segments in "
-                              "PYTORCH_CUDA_ALLOC_CONF)")
+        kind = "expandable segment" if b"e" in h[:2] else f"{len(h)}-byte handle {h[:2]!r}"
+        raise ValidationError(f"IpcTransport needs cudaMalloc-backed segments, got a {kind} (unset "
+                              "expandable_segments in PYTORCH_CUDA_ALLOC_CONF)")
     return h, int(storage_off) + t.storage_offset() * t.element_size()
 
 

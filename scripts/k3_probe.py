@@ -58,3 +58,14 @@ for world in (2, 4, 8):
     nbytes = 2 * world * S + 4 * S
     print(json.dumps({"k3": f"world{world} reduce", "segment_elems": S, "ms": ms,
                       "local_hbm_gbs": nbytes / ms / 1e6}), flush=True)
+# K2: the all-gather of one 32 MB chunk from world local shards (HBM stand-ins for peers), SMs vs copy engines
+for world in (2, 4, 8):
+    S = 16 * 2 ** 20 // world
+    shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(world)]
+    block = torch.empty(world * S, dtype=torch.bfloat16, device=dev)
+    ptrs = [s.data_ptr() for s in shards]
+    for engine in ("sm", "ce"):
+        ms = timeit(lambda: kernels.fetch(block, ptrs, S, engine=engine))
+        nbytes = 2 * 2 * world * S
+        print(json.dumps({"k2": f"world{world} gather 32MB", "engine": engine, "ms": ms,
+                          "local_hbm_gbs": nbytes / ms / 1e6, "frac": nbytes / ms / 1e6 / peak}), flush=True)

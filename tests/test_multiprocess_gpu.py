@@ -226,3 +226,33 @@ def test_sweep_real_peer_pointers_oversubscribed(cuda, world):
             assert "unavailable" in r
     ctx = [r for r in lines if r.get("sweep") == "contexts"]
     assert ctx and ctx[0]["cuda_contexts_on_devices"] == [0]
+
+
+def test_hardware_profiler_under_torchrun_oversubscribed(cuda, tmp_path):
+    """scripts/profile_hw.py under torchrun (§8f row 2 at n > 1): every rank
+    measures K6 / K4 / host Adam concurrently and K2's all-gather over real
+    peer pointers; rank 0 prints the n = 2 row in the reference's format. With
+    the ranks sharing a GPU the row is flagged oversubscribed and NOT written
+    unless asked; written on request, it merges into the profile file with
+    per-row provenance and derived rows for the rest, loadable by the
+    reference's rate-table rules (every rate > 0; b_g2g > 0 for n > 1)."""
+    out = tmp_path / "hw.json"
+    p = _torchrun(2, ["scripts/profile_hw.py", "--out", str(out), "--gpus", "4"], timeout=600)
+    rec = [json.loads(ln) for ln in p.stdout.splitlines() if ln.startswith("{")][0]
+    assert rec["n"] == 2 and rec["oversubscribed"] and not out.exists()
+    for k in ("b_c2g", "b_g2c", "v_g", "v_c", "b_g2g"):
+        assert rec["row"][k] > 0, (k, rec)
+    # n = 1 measured, then the n = 2 row merged on request
+    subprocess.run([sys.executable, "scripts/profile_hw.py", "--out", str(out), "--gpus", "4"], cwd=ROOT,
+                   check=True, capture_output=True, text=True, timeout=600)
+    _torchrun(2, ["scripts/profile_hw.py", "--out", str(out), "--gpus", "4", "--write-oversubscribed"], timeout=600)
+    doc = json.loads(out.read_text())
+    assert sorted(doc["tables"], key=int) == ["1", "2", "3", "4"] and doc["gpu_count"] == 4
+    rows = doc["meta"]["rows"]
+    assert rows["1"]["measured"] and not rows["1"]["oversubscribed"]
+    assert rows["2"]["measured"] and rows["2"]["oversubscribed"]
+    assert not rows["3"]["measured"] and not rows["4"]["measured"]
+    assert doc["tables"]["1"]["b_g2g"] is None
+    for n in ("2", "3", "4"):
+        t = doc["tables"][n]
+        assert all(t[k] > 0 for k in ("b_c2g", "b_g2c", "v_g", "v_c", "b_g2g")), (n, t)
