@@ -313,6 +313,39 @@ __global__ void peer_sum_f64_kernel(double* dst, const PtrBatch peers, int count
   }
 }
 
+// ------------------------------------------- mbarrier / TMA bulk-copy helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 // ============================================================== K3 release
 // One launch reduces a batch of segments (every chunk due at one reduce
 // position, plus the shared parameter at the last one):
@@ -361,8 +394,11 @@ __device__ __forceinline__ double block_sum_fixed(double x, double* s_w) {
 }
 
 // Per-CTA partial -> slot; the last CTA folds the slots in order into sc[0].
+// Blocks of more than kRelThreads threads (the TMA kernel's producer warp) pass
+// sq = 0 from the extra threads: +0.0 lanes leave both butterflies' results
+// unchanged, and the slot fold keeps the kRelThreads stride of the oracle.
 __device__ __forceinline__ void publish_partial(double sq, int bad, double* sc) {
-  __shared__ double s_w[kRelThreads / 32];
+  __shared__ double s_w[32];
   __shared__ int s_last;
   const int any_bad = __syncthreads_or(bad);
   const double part = block_sum_fixed(sq, s_w);
@@ -377,7 +413,8 @@ __device__ __forceinline__ void publish_partial(double sq, int bad, double* sc) 
   if (!s_last) return;
   __threadfence();
   double x = 0.0;
-  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) x += __ldcg(sc + ELX_SC_PARTIALS + i);
+  if (threadIdx.x < kRelThreads)
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += kRelThreads) x += __ldcg(sc + ELX_SC_PARTIALS + i);
   const double tot = block_sum_fixed(x, s_w);
   if (threadIdx.x == 0) {
     sc[0] = sc[0] + tot;
@@ -523,6 +560,110 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
   publish_partial(sq, bad_of(sq), sc);
 }
 
+// World 1 (the norm pass over a rank's own chunks, or a release into fp32
+// shards): the same tiles, the same per-thread order and so the same sums as
+// release_batch_kernel<T16, 1, 4> — but the bytes arrive by TMA. One producer
+// warp streams each tile's whole 16-byte vectors (16 KB) into a shared-memory
+// stage with cp.async.bulk completing on an mbarrier, kRelStages tiles in
+// flight per CTA; the eight consumer warps take their four vectors from the
+// stage (thread t: vectors t + 256u, as before), hand the stage back and
+// reduce. The register-staged kernel kept only its own four loads in flight
+// between two rounds of arithmetic and topped out near 0.75 of the HBM peak;
+// the bulk copies keep 64 KB per CTA in flight regardless of the math.
+constexpr int kRelStages = 4;
+constexpr int kRelU1 = 4;                                   // == rel_unroll(1)
+constexpr int kRelTileVecs1 = kRelThreads * kRelU1;         // 16-byte vectors per tile
+constexpr int kRelTmaThreads = kRelThreads + 32;            // + the producer warp
+constexpr size_t kRelTmaSmem = (size_t)kRelStages * kRelTileVecs1 * 16;
+
+template <typename T16, bool kScaleOne>
+__global__ void __launch_bounds__(kRelTmaThreads, 1)
+    release_w1_tma_kernel(const __grid_constant__ RelBatch b, float inv_scale, double* __restrict__ sc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  uint4* stages = reinterpret_cast<uint4*>(smem_raw);
+  __shared__ __align__(8) uint64_t full[kRelStages];
+  __shared__ __align__(8) uint64_t empty[kRelStages];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kRelStages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], kRelThreads / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ntiles = b.tile0[b.nseg];
+  double sq = 0.0;
+  if (warp == kRelThreads / 32) {  // ---------------- producer warp
+    if (lane == 0) {
+      int s = 0;
+      int64_t q = 0;
+      for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
+        const int64_t v0 = (t - b.tile0[s]) * kRelTileVecs1;
+        const int64_t nv = min((int64_t)kRelTileVecs1, (b.n[s] >> 3) - v0);  // whole vectors in the tile
+        if (nv <= 0) continue;
+        const int st = (int)(q % kRelStages);
+        mbar_wait(&empty[st], (uint32_t)((q / kRelStages) & 1) ^ 1u);
+        mbar_expect_tx(&full[st], (uint32_t)(nv * 16));
+        tma_load_1d(stages + (size_t)st * kRelTileVecs1, static_cast<const uint4*>(b.src[s][0]) + v0,
+                    (uint32_t)(nv * 16), &full[st]);
+        ++q;
+      }
+    }
+  } else {  // ---------------------------------------- consumer warps
+    int s = 0;
+    int64_t q = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
+      const int64_t n = b.n[s];
+      const int64_t nvec = (n + 7) >> 3;
+      const int64_t v0 = (t - b.tile0[s]) * kRelTileVecs1;
+      const int64_t nv = min((int64_t)kRelTileVecs1, (n >> 3) - v0);
+      const void* src = b.src[s][0];
+      const int st = (int)(q % kRelStages);
+      if (nv > 0) mbar_wait(&full[st], (uint32_t)((q / kRelStages) & 1));
+      uint4 raw[kRelU1];
+#pragma unroll
+      for (int u = 0; u < kRelU1; ++u) {
+        const int j = u * kRelThreads + threadIdx.x;
+        const int64_t v = v0 + j;
+        raw[u] = j < nv ? stages[(size_t)st * kRelTileVecs1 + j]
+                        : (v < nvec ? ld_tail(src, v, n) : make_uint4(0, 0, 0, 0));
+      }
+      if (nv > 0) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);  // the stage may be refilled: the vectors are in registers
+        ++q;
+      }
+      float* __restrict__ g = b.g[s];
+#pragma unroll
+      for (int u = 0; u < kRelU1; ++u) {
+        const int64_t v = v0 + u * kRelThreads + threadIdx.x;
+        float acc[8];
+        unpack8<T16>(raw[u], acc);
+        if (!kScaleOne) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = __fmul_rn(acc[e], inv_scale);
+        }
+        sq = sq_acc8(sq, acc);
+        if (g != nullptr && v < nvec) {
+          if (v < (n >> 3)) {
+            float4* d = reinterpret_cast<float4*>(g + v * 8);
+            d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              if (v * 8 + e < n) g[v * 8 + e] = acc[e];
+          }
+        }
+      }
+    }
+  }
+  publish_partial(sq, bad_of(sq), sc);
+}
+
 // Unaligned sources or destination (not 16-byte aligned): scalar loads, one
 // quad of 4 consecutive elements per thread-step (the same quad partials as the
 // vector path; only the fp64 order of their sum follows this grid-stride
@@ -609,9 +750,39 @@ bool rel_vec_ok(const RelBatch& b, int world) {
   return true;
 }
 
+// Grid of the world-1 TMA kernel: resident CTAs per SM (shared-memory bound) x SMs.
+template <typename T16>
+int rel_w1_grid(int64_t work) {
+  const void* kern = (const void*)release_w1_tma_kernel<T16, false>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute((const void*)release_w1_tma_kernel<T16, false>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRelTmaSmem);
+    cudaFuncSetAttribute((const void*)release_w1_tma_kernel<T16, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRelTmaSmem);
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelTmaThreads, kRelTmaSmem);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = std::min<int64_t>((int64_t)sm_count() * per_sm, ELX_RELEASE_MAX_CTAS);
+  return (int)std::max<int64_t>(1, std::min<int64_t>(work, cap));
+}
+
 template <typename T16>
 int run_release_batch(RelBatch& b, int world, float inv_scale, double* sc, cudaStream_t st) {
   const bool vec = rel_vec_ok(b, world);
+  if (vec && world == 1) {
+    const int64_t work = rel_tiles(b, kRelU1);
+    if (work == 0) return ELX_OK;
+    const int grid = rel_w1_grid<T16>(work);
+    const void* kern = inv_scale == 1.0f ? (const void*)release_w1_tma_kernel<T16, true>
+                                         : (const void*)release_w1_tma_kernel<T16, false>;
+    void* args[] = {(void*)&b, (void*)&inv_scale, (void*)&sc};
+    cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(kRelTmaThreads), args, kRelTmaSmem, st);
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_release: %s", cudaGetErrorString(e));
+    return check_launch("elx_release");
+  }
   const RelLaunch L = rel_kernel<T16>(world, vec, inv_scale == 1.0f);
   int64_t work;
   if (vec) {
@@ -809,38 +980,6 @@ __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
 // Shape parameters: kTile elements per tile (one stage = 16*kTile bytes for
 // four fp32 arrays), kCW consumer warps (kTile / (32*kCW) elements per
 // consumer thread, a multiple of 4), kStages stages in flight.
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst_smem)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
 struct TileRef {
   int seg;
@@ -1619,6 +1758,12 @@ int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t 
   for (int i = 0; i < nseg; ++i)
     if (n[i] > 0) b.n[b.nseg++] = n[i];
   // the geometry depends on the tile shape only (the same for scale 1 or not) and the grid
+  if (world == 1) {  // the TMA kernel (release_w1_tma_kernel)
+    const int64_t work = rel_tiles(b, kRelU1);
+    *ctas = work == 0 ? 0 : (dtype == ELX_BF16 ? rel_w1_grid<__nv_bfloat16>(work) : rel_w1_grid<__half>(work));
+    *tile_vecs = kRelTileVecs1;
+    return ELX_OK;
+  }
   const RelLaunch L = dtype == ELX_BF16 ? rel_kernel<__nv_bfloat16>(world, true, false)
                                         : rel_kernel<__half>(world, true, false);
   const int64_t work = rel_tiles(b, L.u);
