@@ -148,14 +148,16 @@ def _barrier(world):
 
 # ---------------------------------------------------------------- CPU baseline
 
-def cpu_baseline(model_name: str, layers_sample: int = 1, threads: int | None = None):
+def cpu_baseline(model_name: str, layers_sample: int = 2, threads: int | None = None, reps: int = 3):
     """Oracle-port CPU training step on a bounded sample, scaled to samples/s.
 
     Sample: ONE sequence (1024 tokens) through `layers_sample` transformer
     layers (forward + AC recompute + backward, torch CPU fp32) plus the tied
     lm_head/loss, and the C oracle's release + AdamW over those layers' chunk
-    elements. Scaled: per-layer time x L, optimizer time x (M / sampled
-    elements), giving seconds per sequence of the full model.
+    elements; the median of `reps` repetitions of each part (the host is
+    shared: single samples spread by tens of percent). Scaled: per-layer time
+    x L, optimizer time x (M / sampled elements), giving seconds per sequence
+    of the full model.
     """
     import numpy as np
     from oracle.gpt2_ref import block as _block
@@ -187,19 +189,24 @@ def cpu_baseline(model_name: str, layers_sample: int = 1, threads: int | None = 
         gr = torch.autograd.grad(out, [xi] + q, torch.ones_like(out))
         return gr[0]
 
-    t0 = time.perf_counter()
-    x = x0
-    for ps in layer_params:
-        layer_pass(ps, x)
-    t_layers = (time.perf_counter() - t0) / layers_sample
-    t0 = time.perf_counter()
-    w = wte.clone().requires_grad_(True)
-    xi = x0.clone().requires_grad_(True)
-    with torch.no_grad():
-        F.cross_entropy(F.linear(x0, wte).view(-1, V), tgt.view(-1))
-    loss = F.cross_entropy(F.linear(xi, w).view(-1, V), tgt.view(-1))
-    torch.autograd.grad(loss, [xi, w])
-    t_head = time.perf_counter() - t0
+    def layers_once():
+        t0 = time.perf_counter()
+        for ps in layer_params:
+            layer_pass(ps, x0)
+        return (time.perf_counter() - t0) / layers_sample
+
+    def head_once():
+        t0 = time.perf_counter()
+        w = wte.clone().requires_grad_(True)
+        xi = x0.clone().requires_grad_(True)
+        with torch.no_grad():
+            F.cross_entropy(F.linear(x0, wte).view(-1, V), tgt.view(-1))
+        loss = F.cross_entropy(F.linear(xi, w).view(-1, V), tgt.view(-1))
+        torch.autograd.grad(loss, [xi, w])
+        return time.perf_counter() - t0
+
+    t_layers = statistics.median(layers_once() for _ in range(reps))
+    t_head = statistics.median(head_once() for _ in range(reps))
 
     # optimizer: C oracle release (world 1) + AdamW over the sampled layers' elements
     lib = ctypes.CDLL(str(ROOT / "oracle" / "_build" / "liboracle.so"))
@@ -218,11 +225,14 @@ def cpu_baseline(model_name: str, layers_sample: int = 1, threads: int | None = 
     ptrs = (ctypes.c_void_p * 1)(gb.ctypes.data)
     bad = ctypes.c_int(0)
     k = np.array([1 - 1e-5, 0.1, 0.999, 0.001, 0.0316, -0.01, 1e-8], np.float32)
-    t0 = time.perf_counter()
-    lib.oracle_release_bf16(g32.ctypes.data, ptrs, 1, n, ctypes.c_float(1.0), ctypes.byref(bad), threads)
-    lib.oracle_adamw_bf16(p.ctypes.data, m.ctypes.data, v.ctypes.data, g32.ctypes.data, p16.ctypes.data, n,
-                          k.ctypes.data, ctypes.c_float(1.0), 0, threads)
-    t_opt = time.perf_counter() - t0
+    def opt_once():
+        t0 = time.perf_counter()
+        lib.oracle_release_bf16(g32.ctypes.data, ptrs, 1, n, ctypes.c_float(1.0), ctypes.byref(bad), threads)
+        lib.oracle_adamw_bf16(p.ctypes.data, m.ctypes.data, v.ctypes.data, g32.ctypes.data, p16.ctypes.data, n,
+                              k.ctypes.data, ctypes.c_float(1.0), 0, threads)
+        return time.perf_counter() - t0
+
+    t_opt = statistics.median(opt_once() for _ in range(reps))
     total = 12 * h * h * cfg.layers + 13 * h * cfg.layers + V * h + T * h + 2 * h
     sec_per_seq = t_head + cfg.layers * t_layers + t_opt * total / n
     return {
@@ -231,9 +241,9 @@ def cpu_baseline(model_name: str, layers_sample: int = 1, threads: int | None = 
         "cores": threads,
         "kind": "port",
         "sample": (f"1 sequence x {T} tokens through {layers_sample} of {cfg.layers} layers + tied lm_head "
-                   f"(torch CPU fp32, fwd+recompute+bwd) and C-oracle release+AdamW over {n} elements; "
-                   f"scaled to the full {total}-parameter model"),
-        "seconds_measured": round(t_layers * layers_sample + t_head + t_opt, 3),
+                   f"(torch CPU fp32, fwd+recompute+bwd) and C-oracle release+AdamW over {n} elements, median of "
+                   f"{reps} repetitions each; scaled to the full {total}-parameter model"),
+        "seconds_measured": round(reps * (t_layers * layers_sample + t_head + t_opt), 3),
         "breakdown_s_per_seq": {"layers": cfg.layers * t_layers, "head": t_head, "optimizer": t_opt * total / n},
     }
 
@@ -245,7 +255,7 @@ def run_reference(args):
     vals = []
     cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(args.model)
+        cb = cpu_baseline(args.model, reps=1)  # one sample per step: the median is over the steps
         if i >= args.warmup:
             vals.append(cb["value"])
     value = statistics.median(vals)
@@ -723,14 +733,16 @@ def run_sweep(args):
             g32 = torch.empty(S, device=dev)
             t_f = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S), None)
             t_fc = timeit(lambda: kernels.fetch(block, [s.data_ptr() for s in shards], S, engine="ce"), None)
-            t_r = timeit(lambda: kernels.release(g32, [s.data_ptr() for s in shards], S, torch.bfloat16, 1.0, sc),
-                         None)
+            # world 1 is the runtime's norm pass (the gradient stays in the chunk: no fp32 output)
+            t_r = timeit(lambda: kernels.release(g32 if w > 1 else None, [s.data_ptr() for s in shards], S,
+                                                 torch.bfloat16, 1.0, sc), None)
             p32, m, v = (torch.zeros(S, device=dev) for _ in range(3))
             p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
             tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
             t_a = timeit(lambda: kernels.adam(tab, hp, 1, sc, torch.bfloat16), None)
             for engine, ms, nbytes in (("k2_fetch_sm", t_f, 2 * 2 * w * S), ("k2_fetch_ce", t_fc, 2 * 2 * w * S),
-                                       ("k3_release", t_r, 2 * w * S + 4 * S), ("k4_adam", t_a, 30 * S)):
+                                       ("k3_release", t_r, 2 * w * S + (4 * S if w > 1 else 0)),
+                                       ("k4_adam", t_a, 30 * S)):
                 emit({"chunk_mb": mb, "emulated_world": w, "engine": engine, "shard_elems": S, "ms": ms,
                       "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "frac": nbytes / (ms * 1e-3) / 1e9 / peak})
             del shards, block, g32, p32, m, v, p16, tab

@@ -561,24 +561,20 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
 }
 
 // World 1 (the norm pass over a rank's own chunks, or a release into fp32
-// shards): the same tiles, the same per-thread order and so the same sums as
-// release_batch_kernel<T16, 1, 4> — but the bytes arrive by TMA. One producer
-// warp streams each tile's whole 16-byte vectors (16 KB) into a shared-memory
-// stage with cp.async.bulk completing on an mbarrier, kRelStages tiles in
-// flight per CTA; the eight consumer warps take their four vectors from the
-// stage (thread t: vectors t + 256u, as before), hand the stage back and
-// reduce. The register-staged kernel kept only its own four loads in flight
+// shards): tiles of 256 x kU 16-byte vectors, thread t of a tile taking
+// vectors t + 256u (the order of release_batch_kernel), but the bytes arrive
+// by TMA. One producer warp streams each tile's whole vectors into a
+// shared-memory stage with cp.async.bulk completing on an mbarrier, kStages
+// tiles in flight per CTA; the eight consumer warps take their vectors from
+// the stage, hand the stage back and reduce. The register-staged kernel kept only its own four loads in flight
 // between two rounds of arithmetic and topped out near 0.75 of the HBM peak;
 // the bulk copies keep 64 KB per CTA in flight regardless of the math.
-constexpr int kRelStages = 4;
-constexpr int kRelU1 = 4;                                   // == rel_unroll(1)
-constexpr int kRelTileVecs1 = kRelThreads * kRelU1;         // 16-byte vectors per tile
 constexpr int kRelTmaThreads = kRelThreads + 32;            // + the producer warp
-constexpr size_t kRelTmaSmem = (size_t)kRelStages * kRelTileVecs1 * 16;
 
-template <typename T16, bool kScaleOne>
+template <typename T16, bool kScaleOne, int kRelU1, int kRelStages>
 __global__ void __launch_bounds__(kRelTmaThreads, 1)
     release_w1_tma_kernel(const __grid_constant__ RelBatch b, float inv_scale, double* __restrict__ sc) {
+  constexpr int kRelTileVecs1 = kRelThreads * kRelU1;  // 16-byte vectors per tile
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint4* stages = reinterpret_cast<uint4*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kRelStages];
@@ -624,12 +620,17 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
       const int st = (int)(q % kRelStages);
       if (nv > 0) mbar_wait(&full[st], (uint32_t)((q / kRelStages) & 1));
       uint4 raw[kRelU1];
+      const uint4* stage = stages + (size_t)st * kRelTileVecs1 + threadIdx.x;
+      if (nv == kRelTileVecs1) {  // a whole tile (all but a segment's last): straight from the stage
 #pragma unroll
-      for (int u = 0; u < kRelU1; ++u) {
-        const int j = u * kRelThreads + threadIdx.x;
-        const int64_t v = v0 + j;
-        raw[u] = j < nv ? stages[(size_t)st * kRelTileVecs1 + j]
-                        : (v < nvec ? ld_tail(src, v, n) : make_uint4(0, 0, 0, 0));
+        for (int u = 0; u < kRelU1; ++u) raw[u] = stage[u * kRelThreads];
+      } else {
+#pragma unroll
+        for (int u = 0; u < kRelU1; ++u) {
+          const int j = u * kRelThreads + threadIdx.x;
+          const int64_t v = v0 + j;
+          raw[u] = j < nv ? stage[u * kRelThreads] : (v < nvec ? ld_tail(src, v, n) : make_uint4(0, 0, 0, 0));
+        }
       }
       if (nv > 0) {
         __syncwarp();
@@ -637,6 +638,19 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
         ++q;
       }
       float* __restrict__ g = b.g[s];
+      if (g == nullptr) {  // the norm pass: no released output
+#pragma unroll
+        for (int u = 0; u < kRelU1; ++u) {
+          float acc[8];
+          unpack8<T16>(raw[u], acc);
+          if (!kScaleOne) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = __fmul_rn(acc[e], inv_scale);
+          }
+          sq = sq_acc8(sq, acc);
+        }
+        continue;
+      }
 #pragma unroll
       for (int u = 0; u < kRelU1; ++u) {
         const int64_t v = v0 + u * kRelThreads + threadIdx.x;
@@ -750,20 +764,48 @@ bool rel_vec_ok(const RelBatch& b, int world) {
   return true;
 }
 
+// World-1 TMA variants (tile = 256 x kU vectors, kStages stages): the tile
+// shape is part of the summation order, which elx_release_geometry reports.
+// ELX_K3_TMA selects one for experiments (scripts/k3_probe.py); 0 is the default.
+struct RelTma {
+  const void* kern[2];  // [scale != 1, scale == 1]
+  int u;
+  size_t smem;
+};
+
+template <typename T16, int kU, int kS>
+RelTma rel_tma_make() {
+  RelTma r{{(const void*)release_w1_tma_kernel<T16, false, kU, kS>,
+            (const void*)release_w1_tma_kernel<T16, true, kU, kS>},
+           kU, (size_t)kS * kRelThreads * kU * 16};
+  for (const void* k : r.kern) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);
+  return r;
+}
+
+inline int rel_tma_variant() {
+  static const int v = [] {
+    const char* e = getenv("ELX_K3_TMA");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
+template <typename T16>
+const RelTma& rel_tma() {
+  // 0: 32 KB tiles x 4 stages, one CTA per SM — the fastest in scripts/k3_variants.py
+  // (profiles/r02g_k3_variants.jsonl: 0.365 ms for the 1.3B plan's chunks vs 0.386-0.72 for the others)
+  static const RelTma table[] = {rel_tma_make<T16, 8, 4>(), rel_tma_make<T16, 4, 4>(), rel_tma_make<T16, 4, 8>(),
+                                 rel_tma_make<T16, 4, 6>(), rel_tma_make<T16, 2, 8>(), rel_tma_make<T16, 8, 3>()};
+  const int v = rel_tma_variant();
+  return table[(v >= 0 && v < (int)(sizeof(table) / sizeof(table[0]))) ? v : 0];
+}
+
 // Grid of the world-1 TMA kernel: resident CTAs per SM (shared-memory bound) x SMs.
 template <typename T16>
 int rel_w1_grid(int64_t work) {
-  const void* kern = (const void*)release_w1_tma_kernel<T16, false>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute((const void*)release_w1_tma_kernel<T16, false>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRelTmaSmem);
-    cudaFuncSetAttribute((const void*)release_w1_tma_kernel<T16, true>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRelTmaSmem);
-    attr = true;
-  }
+  const RelTma& L = rel_tma<T16>();
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kRelTmaThreads, kRelTmaSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.kern[0], kRelTmaThreads, L.smem);
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = std::min<int64_t>((int64_t)sm_count() * per_sm, ELX_RELEASE_MAX_CTAS);
   return (int)std::max<int64_t>(1, std::min<int64_t>(work, cap));
@@ -773,13 +815,12 @@ template <typename T16>
 int run_release_batch(RelBatch& b, int world, float inv_scale, double* sc, cudaStream_t st) {
   const bool vec = rel_vec_ok(b, world);
   if (vec && world == 1) {
-    const int64_t work = rel_tiles(b, kRelU1);
+    const RelTma& L = rel_tma<T16>();
+    const int64_t work = rel_tiles(b, L.u);
     if (work == 0) return ELX_OK;
     const int grid = rel_w1_grid<T16>(work);
-    const void* kern = inv_scale == 1.0f ? (const void*)release_w1_tma_kernel<T16, true>
-                                         : (const void*)release_w1_tma_kernel<T16, false>;
     void* args[] = {(void*)&b, (void*)&inv_scale, (void*)&sc};
-    cudaError_t e = cudaLaunchKernel(kern, dim3(grid), dim3(kRelTmaThreads), args, kRelTmaSmem, st);
+    cudaError_t e = cudaLaunchKernel(L.kern[inv_scale == 1.0f], dim3(grid), dim3(kRelTmaThreads), args, L.smem, st);
     if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_release: %s", cudaGetErrorString(e));
     return check_launch("elx_release");
   }
@@ -1759,9 +1800,10 @@ int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t 
     if (n[i] > 0) b.n[b.nseg++] = n[i];
   // the geometry depends on the tile shape only (the same for scale 1 or not) and the grid
   if (world == 1) {  // the TMA kernel (release_w1_tma_kernel)
-    const int64_t work = rel_tiles(b, kRelU1);
+    const int u = dtype == ELX_BF16 ? rel_tma<__nv_bfloat16>().u : rel_tma<__half>().u;
+    const int64_t work = rel_tiles(b, u);
     *ctas = work == 0 ? 0 : (dtype == ELX_BF16 ? rel_w1_grid<__nv_bfloat16>(work) : rel_w1_grid<__half>(work));
-    *tile_vecs = kRelTileVecs1;
+    *tile_vecs = kRelThreads * u;
     return ELX_OK;
   }
   const RelLaunch L = dtype == ELX_BF16 ? rel_kernel<__nv_bfloat16>(world, true, false)

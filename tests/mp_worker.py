@@ -47,9 +47,15 @@ def main():
     kind, out = sys.argv[1], Path(sys.argv[2])
     path = sys.argv[3] if len(sys.argv) > 3 else "exchange"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(0)
-    dev = torch.device("cuda", 0)
-    dist.init_process_group("gloo")
+    # one GPU per rank when the node has them (tests/test_multigpu.py), else every rank on GPU 0
+    ndev = torch.cuda.device_count()
+    local = int(os.environ.get("LOCAL_RANK", rank)) % ndev if ndev >= world else 0
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    nccl = path.startswith("nccl")
+    if nccl:  # the library exchange on distinct GPUs (NCCL refuses ranks that share one)
+        path = "exchange" + path[len("nccl"):]
+    dist.init_process_group("nccl" if nccl else "gloo", **({"device_id": dev} if nccl else {}))
     plan, _, _ = _plan(kind)
     init = gpt2.init_params(CFG, dev, seed=11)
     if path.startswith("ipc"):  # "ipc": K2 kernel, "ipc-ce": K2 on the copy engines, "ipc-graph": captured step
