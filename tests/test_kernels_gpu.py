@@ -185,10 +185,11 @@ def test_release_norm_only_world1(cuda, dtype, inv_scale, n, bad):
 
 @pytest.mark.parametrize("where", ["even", "odd", "both", "zeros"])
 def test_release_norm_subnormal_and_zero_elements_exact(cuda, where):
-    """The world-1 bf16 norm pass converts half of the elements to double with
-    integer ops (exact for normal values and zero); subnormal elements make the
-    thread recompute through the conversion path. The sum stays bit-exact to
-    the oracle's fixed order whatever the element classes and positions."""
+    """The world-1 bf16 norm pass (TMA-staged) squares in fp32: a subnormal
+    element's square underflows to a subnormal or zero, -0.0 squares to +0.0,
+    with IEEE gradual underflow on both sides (no flush-to-zero in the kernel
+    or the oracle). The sum stays bit-exact to the oracle's fixed order
+    whatever the element classes and positions."""
     n = 3 * 2 ** 20 + 5
     rng = np.random.default_rng(11)
     x = arith.f32_to_bf16_bits((rng.standard_normal(n) * 1e-3).astype(np.float32))
