@@ -259,7 +259,11 @@ int elx_release_batch(const elx_release_seg* segs, int32_t nseg, int32_t world, 
  * k of the batch (segments' tiles concatenated) goes to CTA k % G; thread t
  * of a tile takes vectors t, t + 256, ...; a thread adds each vector's two
  * quad partials (elements 0-3, then 4-7) in that order, then CTA and grid
- * reductions as described above. */
+ * reductions as described above. World 1 runs a TMA-staged kernel (a producer
+ * warp streams 32 KB tiles into shared-memory stages with cp.async.bulk; one
+ * CTA per SM): tile_vecs = 2048 and ctas = min(tiles, SMs); world > 1 the
+ * register-staged kernel (tile_vecs = 256 * unroll, ctas = min(tiles,
+ * resident CTAs)). */
 int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t dtype, int32_t* ctas,
                          int32_t* tile_vecs);
 
