@@ -726,6 +726,29 @@ def run_sweep(args):
                   "hbm_gbs": 30 * S / (ms * 1e-3) / 1e9, "frac": 30 * S / (ms * 1e-3) / 1e9 / peak})
             del shard, block, g32, p32, m, v, p16, tab
             continue
+        # K1: pack a chunk from its members (a GPT-2 layer's 12 parameters in order, cycled, greedy like
+        # pack_chunks; 1.3B widths, GPT-2 small's below 24 MB chunks; the unused tail zero-filled) —
+        # 2*sum(numel) read + 2*C write
+        h = 2048 if C >= 3 * 2048 * 2048 else 768
+        layer = [h, h, 3 * h * h, 3 * h, h * h, h, h, h, 4 * h * h, 4 * h, 4 * h * h, h]
+        members, off, i = [], 0, 0
+        while off + layer[i % 12] <= C and i < 10_000:
+            members.append(off)
+            off += layer[i % 12]
+            i += 1
+        if not members:  # the chunk is smaller than a layer's first weight: split the chunk evenly
+            members, off = [0], C
+            sizes = [C]
+        else:
+            sizes = [layer[j % 12] for j in range(len(members))]
+        pk_src = [torch.randn(n, device=dev).to(torch.bfloat16) for n in sizes]
+        pk_dst = torch.empty(C, dtype=torch.bfloat16, device=dev)
+        pk = [(t, o) for t, o in zip(pk_src, members)]
+        t_k1 = timeit(lambda: kernels.chunk_pack(pk_dst, pk, used_len=off), None)
+        k1_bytes = 2 * off + 2 * C
+        emit({"chunk_mb": mb, "emulated_world": 1, "engine": "k1_pack", "shard_elems": C, "members": len(pk),
+              "ms": t_k1, "hbm_gbs": k1_bytes / (t_k1 * 1e-3) / 1e9, "frac": k1_bytes / (t_k1 * 1e-3) / 1e9 / peak})
+        del pk_src, pk_dst, pk
         for w in (1, 2, 4, 8):
             S = shard_length(C, w)
             shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(w)]

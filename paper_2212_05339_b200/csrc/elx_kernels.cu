@@ -119,7 +119,8 @@ __device__ __forceinline__ uint4 ld_rel(const void* p) {
 // ================================================================ K1 pack
 constexpr int kPackBatch = 48;
 constexpr int kPackThreads = 256;
-constexpr int64_t kPackTile = kPackThreads * 8 * 2;  // elements per tile
+constexpr int kPackUnroll = 4;                                   // 16-byte loads in flight per thread
+constexpr int64_t kPackTile = kPackThreads * 8 * kPackUnroll;    // elements per tile (bf16: one pass)
 
 struct PackBatch {
   const void* ext[kPackBatch];
@@ -145,9 +146,15 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(void* chunk, int chu
     const void* ext = b.ext[j];
     const int edt = b.ext_dtype[j];
     char* cptr = static_cast<char*>(chunk) + coff * csz;
-    if (ext == nullptr) {  // zero fill (pack only)
+    if (ext == nullptr) {  // zero fill (pack only): 16-byte stores when the range allows
       if (kDir == 0) {
-        for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) st_from_f32(chunk, coff + i, chunk_dt, 0.f);
+        const int ve = 16 / csz;
+        if (aligned16(cptr) && (cnt % ve) == 0) {
+          uint4* d = reinterpret_cast<uint4*>(cptr);
+          for (int64_t i = threadIdx.x; i < cnt / ve; i += blockDim.x) d[i] = make_uint4(0, 0, 0, 0);
+        } else {
+          for (int64_t i = threadIdx.x; i < cnt; i += blockDim.x) st_from_f32(chunk, coff + i, chunk_dt, 0.f);
+        }
       }
       continue;
     }
@@ -157,14 +164,21 @@ __global__ void __launch_bounds__(kPackThreads) pack_kernel(void* chunk, int chu
     const int vec_elems = 16 / csz;
     if (edt == chunk_dt && aligned16(cptr) && aligned16(eptr) && (cnt % vec_elems) == 0) {
       const int64_t nv = cnt / vec_elems;
-      if (kDir == 0) {
-        const uint4* s = reinterpret_cast<const uint4*>(eptr);
-        uint4* d = reinterpret_cast<uint4*>(cptr);
-        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = ld_stream(s + i);
-      } else {
-        const uint4* s = reinterpret_cast<const uint4*>(cptr);
-        uint4* d = reinterpret_cast<uint4*>(const_cast<char*>(eptr));
-        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) d[i] = ld_stream(s + i);
+      const uint4* __restrict__ s = reinterpret_cast<const uint4*>(kDir == 0 ? eptr : cptr);
+      uint4* __restrict__ d = reinterpret_cast<uint4*>(kDir == 0 ? cptr : const_cast<char*>(eptr));
+      // every load of the pass issued before any store: kPackUnroll 16-byte loads in flight per thread
+      for (int64_t i0 = threadIdx.x; i0 < nv; i0 += (int64_t)blockDim.x * kPackUnroll) {
+        uint4 r[kPackUnroll];
+#pragma unroll
+        for (int u = 0; u < kPackUnroll; ++u) {
+          const int64_t i = i0 + (int64_t)u * blockDim.x;
+          if (i < nv) r[u] = ld_stream(s + i);
+        }
+#pragma unroll
+        for (int u = 0; u < kPackUnroll; ++u) {
+          const int64_t i = i0 + (int64_t)u * blockDim.x;
+          if (i < nv) d[i] = r[u];
+        }
       }
       continue;
     }

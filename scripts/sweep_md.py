@@ -26,7 +26,7 @@ def main():
     for r in recs:
         key = (r["chunk_mb"], r.get("emulated_world", r.get("world")))
         table[key][r["engine"]] = r
-    engines = ["k2_fetch_sm", "k2_fetch_ce", "k3_release", "k4_adam"]
+    engines = ["k1_pack", "k2_fetch_sm", "k2_fetch_ce", "k3_release", "k4_adam"]
     lines = [f"# {title}", "",
              f"`python bench.py --sweep`: standalone K2 (SM kernel / copy engines), K3 and K4 on one rank's share of "
              f"one chunk; N local HBM buffers stand in for the N ranks (one GPU). Median of the launches after "
