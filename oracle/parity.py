@@ -3,21 +3,26 @@ INFRASTRUCTURE ONLY (the checker; bench.py's `parity` field and
 tests/test_fullsize_gpu.py call it after their timed regions).
 
 `check_step(model, tokens, targets)` runs ONE eager training step of an
-ElixirGPT2 (world 1, every chunk GPU-home: BASELINE.json configs[0]/[1] at
-N = 1) with two observation hooks and no change to what executes:
-  * every K3 launch the step issues is logged in issue order (the runtime
-    calls `kernels.release_batch` / `kernels.release` — the log wraps them and
-    forwards the call unchanged);
-  * right before HybridAdam's update (after the backward has written every
-    gradient into its chunk and the releases are done) the update's inputs
-    are snapshotted on the device: the fp32 master / m / v and the bf16
-    gradient of every segment of the K4 table.
-The oracle then recomputes, from the snapshot, (a) the sum of squares launch
+ElixirGPT2 at world 1 — every BASELINE.json configuration that fits one GPU:
+all chunks GPU-home (configs[0]/[1]) or partly CPU-home (configs[2]/[3],
+updated on host threads or streamed through HBM) — with two observation hooks
+and no change to what executes:
+  * every K3 launch the step issues is logged in issue order, and the
+    gradient segments it reads are copied on the launch's own stream right
+    before it (the runtime calls `kernels.release_batch` / `kernels.release`;
+    the wrapper forwards the call unchanged). A CPU-home chunk's gradient sits
+    in an rCache block that a later gather may reuse, so it is captured there;
+  * right before HybridAdam's update the update's other inputs are copied to
+    host memory: the fp32 master / m / v of the GPU-home segments (device)
+    and of the CPU-home chunks (pinned host), in update order up to
+    `host_budget` bytes (the 10B configuration is checked on its first
+    segments; the sum of squares always covers every element).
+The oracle then recomputes, from those copies, (a) the sum of squares launch
 by launch in each launch's fixed order (elx_release_geometry;
 oracle/c/elx_oracle.c oracle_release_norm_bf16_ordered), added in issue order
-as the kernel adds them to step_scalars[0], and (b) AdamW with that norm's
-clip coefficient over every element (oracle_adamw_bf16), and compares with
-what the GPU produced: the sum of squares' bits, and per array the share of
+as the kernels add them to step_scalars[0], and (b) AdamW with that norm's clip
+coefficient over every checked element (oracle_adamw_bf16), and compares with
+what the step produced: the sum of squares' bits, and per array the share of
 bit-identical elements and the max relative error.
 """
 
@@ -50,8 +55,8 @@ def _bits(t: torch.Tensor) -> np.ndarray:
 
 
 def _compare(got: torch.Tensor, want: np.ndarray, bf16: bool = False) -> tuple[int, float]:
-    """(bit-identical elements, max relative error) of a device array vs the
-    oracle's, compared on the device."""
+    """(bit-identical elements, max relative error) of an array (device or
+    host) vs the oracle's, compared where `got` lives."""
     w = torch.from_numpy(want.view(np.int16) if bf16 else want).to(got.device)
     if bf16:
         same = int((got.view(torch.int16) == w).sum())
@@ -64,23 +69,52 @@ def _compare(got: torch.Tensor, want: np.ndarray, bf16: bool = False) -> tuple[i
     return same, rel
 
 
-def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int | None = None) -> dict:
+def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int | None = None,
+               host_budget: float = 48e9, device_budget: float = 24e9) -> dict:
     from paper_2212_05339_b200 import kernels
 
     mgr, opt = model.manager, model.optimizer
-    if mgr.world != 1 or mgr.cpu_ids or not mgr.fused_w1:
-        return {"checked": False, "reason": "the full-step check covers world 1 with every chunk GPU-home"}
+    if mgr.world != 1:
+        return {"checked": False, "reason": "the whole-step check runs at world 1 (the multi-rank parity tests "
+                                            "cover N > 1)"}
+    total = sum(mgr.valid(c) for c in range(mgr.n_chunks)) + sum(sp.numel for sp in mgr.shared.values())
+    if 2 * total > device_budget:
+        return {"checked": False, "reason": f"{2 * total / 1e9:.1f} GB of gradient copies exceed the "
+                                            f"{device_budget / 1e9:.0f} GB device budget"}
     threads = threads or max(1, len(os.sched_getaffinity(0)))
     dev = mgr.device
-    segs = opt.gpu_segments                    # [(key, (p32, m, v, g, p16, n))], the K4 table's order
-    by_grad_ptr = {seg[3].data_ptr(): key for key, seg in segs}
-    launches: list[list[tuple[object, int]]] = []
+    # every updated segment: GPU-home (the K4 table's order), then CPU-home chunks in forward order; the
+    # Adam check covers them in that order up to `host_budget` bytes of host copies (12 B per element)
+    host_all = sorted({**opt.cpu_segs, **opt.stream_segs}.items())
+    updated = list(opt.gpu_segments) + host_all
+    checked, budget = [], host_budget
+    for key, seg in updated:
+        if 12 * seg[5] > budget:
+            break
+        checked.append((key, seg))
+        budget -= 12 * seg[5]
+    launches: list = []
+    grads: dict = {}
     snap: dict = {}
     real_batch, real_one, real_step = kernels.release_batch, kernels.release, opt.step
 
+    def resolve():
+        m = {st.data_ptr(): (c, st) for c, st in mgr._bound.items()}
+        m.update({sp.grad.data_ptr(): (pid, sp.grad) for pid, sp in mgr.shared.items()})
+        return m
+
     def log_batch(ss, dtype, inv_scale, step_scalars, stream=None):
         if step_scalars is mgr.step_scalars:
-            launches.append(([(by_grad_ptr[ptrs[0]], n) for _, ptrs, n in ss if n > 0], float(inv_scale)))
+            where = resolve()
+            grp = []
+            with torch.cuda.stream(stream if stream is not None else torch.cuda.current_stream(dev)):
+                for _, ptrs, n in ss:
+                    if n <= 0:
+                        continue
+                    key, src = where[ptrs[0]]
+                    grads[key] = src[:n].clone()   # on the release's stream: after the gradient, before reuse
+                    grp.append((key, n))
+            launches.append((grp, float(inv_scale)))
         return real_batch(ss, dtype, inv_scale, step_scalars, stream=stream)
 
     def log_one(g, ptrs, n, dtype, inv_scale, step_scalars, stream=None):
@@ -90,8 +124,8 @@ def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int 
         cur = torch.cuda.current_stream(dev)
         if releases_done is not None:
             cur.wait_event(releases_done)
-        for key, (p32, m, v, g, _, n) in segs:
-            snap[key] = (p32[:n].clone(), m[:n].clone(), v[:n].clone(), g[:n].clone())
+        for key, (p32, m, v, _, _, n) in checked:   # to host memory (K4 and the host update come after)
+            snap[key] = tuple(t[:n].cpu() if t.is_cuda else t[:n].clone() for t in (p32, m, v))
         snap["__grad_scale__"] = float(grad_scale)
         return real_step(releases_done, grad_scale)
 
@@ -110,17 +144,19 @@ def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int 
     torch.cuda.synchronize(dev)
 
     lib = _lib()
-    grads = {key: _bits(snap[key][3]) for key, _ in segs}
+    released = sorted(str(k) for grp, _ in launches for k, _ in grp)
+    want_keys = sorted(str(k) for k, _ in updated)
+    assert released == want_keys, "every updated segment is released exactly once"
+    gbits = {key: _bits(t) for key, t in grads.items()}
+    grads.clear()
     sq = 0.0
     for grp, inv_scale in launches:
         ns = [n for _, n in grp]
         ctas, tv = kernels.release_geometry(ns, 1)
-        ptrs = (ctypes.c_void_p * len(grp))(*[grads[k].ctypes.data for k, _ in grp])
+        ptrs = (ctypes.c_void_p * len(grp))(*[gbits[k].ctypes.data for k, _ in grp])
         nn = (ctypes.c_int64 * len(grp))(*ns)
         sq = sq + lib.oracle_release_norm_bf16_ordered(ptrs, nn, len(grp), ctypes.c_float(inv_scale), ctas, tv,
                                                       threads)
-    covered = sorted(str(k) for grp, _ in launches for k, _ in grp)
-    assert covered == sorted(str(k) for k, _ in segs), "every K4 segment is released exactly once"
 
     hp = opt.hp
     skip = bool(flag) or not np.isfinite(sq)
@@ -131,10 +167,9 @@ def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int 
     gs = np.float32(snap["__grad_scale__"])
     totals = {name: [0, 0.0] for name in ("p32", "m", "v", "p16")}
     elements = 0
-    for key, (p32, m, v, _, p16, n) in segs:
-        sp, sm, sv, _ = snap[key]
-        P, M, V = sp.cpu().numpy(), sm.cpu().numpy(), sv.cpu().numpy()
-        G = arith.bf16_bits_to_f32(grads[key])
+    for key, (p32, m, v, _, p16, n) in checked:
+        P, M, V = (t.numpy() for t in snap.pop(key))
+        G = arith.bf16_bits_to_f32(gbits[key])
         if gs != np.float32(1.0):
             G = (G * gs).astype(np.float32)
         out16 = np.empty(n, np.uint16)
@@ -146,12 +181,15 @@ def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int 
             totals[name][0] += same
             totals[name][1] = max(totals[name][1], rel)
         elements += n
-        del snap[key]
     torch.cuda.empty_cache()
     return {
         "checked": True,
         "elements": elements,
-        "segments": len(segs),
+        "model_elements": total,
+        "segments_checked": len(checked),
+        "segments": len(updated),
+        "cpu_home_chunks": len(host_all),
+        "cpu_home_chunks_checked": sum(1 for key, _ in checked if key in dict(host_all)),
         "release_launches": len(launches),
         "sumsq_bit_identical": sq_gpu == sq,
         "sumsq_rel_err": abs(sq_gpu - sq) / sq if sq else 0.0,

@@ -235,3 +235,26 @@ def test_gpt2_small_trainer_step_checked_by_oracle_parity(cuda, graph):
     assert rep["sumsq_bit_identical"], rep
     assert all(f == 1.0 for f in rep["bit_identical_frac"].values()), rep
     assert rep["within_tolerance"]
+
+
+@pytest.mark.parametrize("cpu_update", ["host", "stream", "split"])
+@pytest.mark.parametrize("plan_name", ["offload-half", "offload-all", "all-gpu-min"])
+def test_offloaded_trainer_step_checked_by_oracle_parity(cuda, plan_name, cpu_update):
+    """The bench's `parity` check on plans with CPU-home chunks (configs[2]/[3]'s
+    regime) and evictions: the CPU-home chunks' gradients are captured from
+    their rCache blocks at release time, their fp32 state from pinned host
+    memory, and the host-thread, GPU-streamed or split update is recomputed by
+    the C oracle — every element bit-identical, the sum of squares too."""
+    from oracle.parity import check_step
+    from test_runtime_gpu import CFG as TOY, _batch, _plans
+    plan = dict(_plans(TOY))[plan_name]
+    model = ElixirGPT2(TOY, plan, device=cuda, cpu_update=cpu_update, **HP)
+    if model.optimizer.stream_segs:
+        model.optimizer._init_stream_update(1000)  # tiny tiles: several per chunk, both slots
+    tok, tgt = _batch(TOY, cuda, 1)
+    model.train_step(tok, tgt)
+    rep = check_step(model, tok, tgt)
+    assert rep["checked"] and rep["elements"] == rep["model_elements"], rep
+    assert rep["cpu_home_chunks_checked"] == rep["cpu_home_chunks"] == len(model.manager.cpu_ids)
+    assert rep["sumsq_bit_identical"], rep
+    assert all(f == 1.0 for f in rep["bit_identical_frac"].values()), rep
