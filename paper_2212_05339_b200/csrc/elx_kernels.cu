@@ -574,21 +574,28 @@ __global__ void __launch_bounds__(kRelThreads) release_batch_kernel(const __grid
   publish_partial(sq, bad_of(sq), sc);
 }
 
-// World 1 (the norm pass over a rank's own chunks, or a release into fp32
-// shards): tiles of 256 x kU 16-byte vectors, thread t of a tile taking
-// vectors t + 256u (the order of release_batch_kernel), but the bytes arrive
-// by TMA. One producer warp streams each tile's whole vectors into a
-// shared-memory stage with cp.async.bulk completing on an mbarrier, kStages
-// tiles in flight per CTA; the eight consumer warps take their vectors from
-// the stage, hand the stage back and reduce. The register-staged kernel kept only its own four loads in flight
-// between two rounds of arithmetic and topped out near 0.75 of the HBM peak;
-// the bulk copies keep 64 KB per CTA in flight regardless of the math.
+// TMA-staged release (world 1: the norm pass over a rank's own chunks, or a
+// release into fp32 shards; world 2/4/8: the fused reduce-scatter over peer
+// pointers). Tiles of 256 x kU 16-byte vectors PER RANK, thread t of a tile
+// taking vectors t + 256u (the order of release_batch_kernel), but the bytes
+// arrive by TMA. One producer thread streams each tile's whole vectors — one
+// bulk copy per rank, all completing on the stage's mbarrier — into a
+// shared-memory stage, kStages tiles in flight per CTA; the eight consumer
+// warps take their vectors from the stage, hand the stage back and reduce the
+// ranks in rank order. The register-staged kernel kept only its own loads in
+// flight between two rounds of arithmetic and topped out near 0.75 of the HBM
+// peak; the bulk copies keep kStages x 32 KB per CTA in flight regardless of
+// the math — over NVLink, whose latency is several times HBM's, that depth is
+// what the fetch of a peer's slice needs. Peer sources are UVA addresses of
+// peer-mapped memory (CUDA IPC / symmetric memory); the bulk-copy engine reads
+// them like local global memory.
 constexpr int kRelTmaThreads = kRelThreads + 32;            // + the producer warp
 
-template <typename T16, bool kScaleOne, int kRelU1, int kRelStages>
+template <typename T16, int kWorld, bool kScaleOne, int kRelU1, int kRelStages>
 __global__ void __launch_bounds__(kRelTmaThreads, 1)
-    release_w1_tma_kernel(const __grid_constant__ RelBatch b, float inv_scale, double* __restrict__ sc) {
-  constexpr int kRelTileVecs1 = kRelThreads * kRelU1;  // 16-byte vectors per tile
+    release_tma_kernel(const __grid_constant__ RelBatch b, float inv_scale, double* __restrict__ sc) {
+  constexpr int kRelTileVecs1 = kRelThreads * kRelU1;  // 16-byte vectors per tile per rank
+  constexpr int kStageVecs = kRelTileVecs1 * kWorld;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint4* stages = reinterpret_cast<uint4*>(smem_raw);
   __shared__ __align__(8) uint64_t full[kRelStages];
@@ -615,9 +622,11 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
         if (nv <= 0) continue;
         const int st = (int)(q % kRelStages);
         mbar_wait(&empty[st], (uint32_t)((q / kRelStages) & 1) ^ 1u);
-        mbar_expect_tx(&full[st], (uint32_t)(nv * 16));
-        tma_load_1d(stages + (size_t)st * kRelTileVecs1, static_cast<const uint4*>(b.src[s][0]) + v0,
-                    (uint32_t)(nv * 16), &full[st]);
+        mbar_expect_tx(&full[st], (uint32_t)(nv * 16 * kWorld));
+#pragma unroll
+        for (int r = 0; r < kWorld; ++r)
+          tma_load_1d(stages + (size_t)st * kStageVecs + r * kRelTileVecs1,
+                      static_cast<const uint4*>(b.src[s][r]) + v0, (uint32_t)(nv * 16), &full[st]);
         ++q;
       }
     }
@@ -630,20 +639,24 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
       const int64_t nvec = (n + 7) >> 3;
       const int64_t v0 = (t - b.tile0[s]) * kRelTileVecs1;
       const int64_t nv = min((int64_t)kRelTileVecs1, (n >> 3) - v0);
-      const void* src = b.src[s][0];
       const int st = (int)(q % kRelStages);
       if (nv > 0) mbar_wait(&full[st], (uint32_t)((q / kRelStages) & 1));
-      uint4 raw[kRelU1];
-      const uint4* stage = stages + (size_t)st * kRelTileVecs1 + threadIdx.x;
+      uint4 raw[kRelU1][kWorld];
+      const uint4* stage = stages + (size_t)st * kStageVecs + threadIdx.x;
       if (nv == kRelTileVecs1) {  // a whole tile (all but a segment's last): straight from the stage
 #pragma unroll
-        for (int u = 0; u < kRelU1; ++u) raw[u] = stage[u * kRelThreads];
+        for (int u = 0; u < kRelU1; ++u)
+#pragma unroll
+          for (int r = 0; r < kWorld; ++r) raw[u][r] = stage[r * kRelTileVecs1 + u * kRelThreads];
       } else {
 #pragma unroll
         for (int u = 0; u < kRelU1; ++u) {
           const int j = u * kRelThreads + threadIdx.x;
           const int64_t v = v0 + j;
-          raw[u] = j < nv ? stage[u * kRelThreads] : (v < nvec ? ld_tail(src, v, n) : make_uint4(0, 0, 0, 0));
+#pragma unroll
+          for (int r = 0; r < kWorld; ++r)
+            raw[u][r] = j < nv ? stage[r * kRelTileVecs1 + u * kRelThreads]
+                               : (v < nvec ? ld_tail(b.src[s][r], v, n) : make_uint4(0, 0, 0, 0));
         }
       }
       if (nv > 0) {
@@ -652,11 +665,11 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
         ++q;
       }
       float* __restrict__ g = b.g[s];
-      if (g == nullptr) {  // the norm pass: no released output
+      if (kWorld == 1 && g == nullptr) {  // the norm pass: no released output
 #pragma unroll
         for (int u = 0; u < kRelU1; ++u) {
           float acc[8];
-          unpack8<T16>(raw[u], acc);
+          unpack8<T16>(raw[u][0], acc);
           if (!kScaleOne) {
 #pragma unroll
             for (int e = 0; e < 8; ++e) acc[e] = __fmul_rn(acc[e], inv_scale);
@@ -669,7 +682,14 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
       for (int u = 0; u < kRelU1; ++u) {
         const int64_t v = v0 + u * kRelThreads + threadIdx.x;
         float acc[8];
-        unpack8<T16>(raw[u], acc);
+        unpack8<T16>(raw[u][0], acc);
+#pragma unroll
+        for (int r = 1; r < kWorld; ++r) {
+          float x[8];
+          unpack8<T16>(raw[u][r], x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
+        }
         if (!kScaleOne) {
 #pragma unroll
           for (int e = 0; e < 8; ++e) acc[e] = __fmul_rn(acc[e], inv_scale);
@@ -778,46 +798,80 @@ bool rel_vec_ok(const RelBatch& b, int world) {
   return true;
 }
 
-// World-1 TMA variants (tile = 256 x kU vectors, kStages stages): the tile
+// TMA variants (tile = 256 x kU vectors per rank, kStages stages): the tile
 // shape is part of the summation order, which elx_release_geometry reports.
-// ELX_K3_TMA selects one for experiments (scripts/k3_probe.py); 0 is the default.
+// ELX_K3_TMA selects one for experiments (scripts/k3_probe.py); 0 is the
+// default. ELX_K3_PEER_TMA=0 sends world > 1 back to the register-staged
+// kernel (A/B on a multi-GPU node).
 struct RelTma {
   const void* kern[2];  // [scale != 1, scale == 1]
   int u;
   size_t smem;
 };
 
-template <typename T16, int kU, int kS>
+template <typename T16, int kWorld, int kU, int kS>
 RelTma rel_tma_make() {
-  RelTma r{{(const void*)release_w1_tma_kernel<T16, false, kU, kS>,
-            (const void*)release_w1_tma_kernel<T16, true, kU, kS>},
-           kU, (size_t)kS * kRelThreads * kU * 16};
+  RelTma r{{(const void*)release_tma_kernel<T16, kWorld, false, kU, kS>,
+            (const void*)release_tma_kernel<T16, kWorld, true, kU, kS>},
+           kU, (size_t)kS * kWorld * kRelThreads * kU * 16};
   for (const void* k : r.kern) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);
   return r;
 }
 
+inline int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
 inline int rel_tma_variant() {
-  static const int v = [] {
-    const char* e = getenv("ELX_K3_TMA");
-    return e ? atoi(e) : 0;
-  }();
+  static const int v = env_int("ELX_K3_TMA", 0);
   return v;
 }
-
-template <typename T16>
-const RelTma& rel_tma() {
-  // 0: 32 KB tiles x 4 stages, one CTA per SM — the fastest in scripts/k3_variants.py
-  // (profiles/r02g_k3_variants.jsonl: 0.365 ms for the 1.3B plan's chunks vs 0.386-0.72 for the others)
-  static const RelTma table[] = {rel_tma_make<T16, 8, 4>(), rel_tma_make<T16, 4, 4>(), rel_tma_make<T16, 4, 8>(),
-                                 rel_tma_make<T16, 4, 6>(), rel_tma_make<T16, 2, 8>(), rel_tma_make<T16, 8, 3>()};
-  const int v = rel_tma_variant();
-  return table[(v >= 0 && v < (int)(sizeof(table) / sizeof(table[0]))) ? v : 0];
+inline bool rel_peer_tma() {
+  static const bool on = env_int("ELX_K3_PEER_TMA", 1) != 0;
+  return on;
 }
 
-// Grid of the world-1 TMA kernel: resident CTAs per SM (shared-memory bound) x SMs.
+template <typename T16, int kWorld, size_t kN>
+const RelTma& rel_tma_pick(const RelTma (&table)[kN]) {
+  const int v = rel_tma_variant();
+  return table[(v >= 0 && v < (int)kN) ? v : 0];
+}
+
+// The TMA launch for this world, or nullptr (worlds other than 1/2/4/8, or
+// peer TMA switched off): those run release_batch_kernel.
 template <typename T16>
-int rel_w1_grid(int64_t work) {
-  const RelTma& L = rel_tma<T16>();
+const RelTma* rel_tma(int world) {
+  switch (world) {
+    case 1: {
+      // 0: 32 KB tiles x 4 stages, one CTA per SM — the fastest in scripts/k3_variants.py
+      // (profiles/r02g_k3_variants.jsonl: 0.365 ms for the 1.3B plan's chunks vs 0.386-0.72 for the others)
+      static const RelTma t[] = {rel_tma_make<T16, 1, 8, 4>(), rel_tma_make<T16, 1, 4, 4>(),
+                                 rel_tma_make<T16, 1, 4, 8>(), rel_tma_make<T16, 1, 4, 6>(),
+                                 rel_tma_make<T16, 1, 2, 8>(), rel_tma_make<T16, 1, 8, 3>()};
+      return &rel_tma_pick<T16, 1>(t);
+    }
+    // world N: 32 KB stages (N slices of 32/N KB) x 4, or 64 KB x 3 (variant 1)
+    case 2: {
+      if (!rel_peer_tma()) return nullptr;
+      static const RelTma t[] = {rel_tma_make<T16, 2, 4, 4>(), rel_tma_make<T16, 2, 8, 3>()};
+      return &rel_tma_pick<T16, 2>(t);
+    }
+    case 4: {
+      if (!rel_peer_tma()) return nullptr;
+      static const RelTma t[] = {rel_tma_make<T16, 4, 2, 4>(), rel_tma_make<T16, 4, 4, 3>()};
+      return &rel_tma_pick<T16, 4>(t);
+    }
+    case 8: {
+      if (!rel_peer_tma()) return nullptr;
+      static const RelTma t[] = {rel_tma_make<T16, 8, 1, 4>(), rel_tma_make<T16, 8, 2, 3>()};
+      return &rel_tma_pick<T16, 8>(t);
+    }
+    default: return nullptr;
+  }
+}
+
+// Grid of a TMA release: resident CTAs per SM (shared-memory bound) x SMs.
+inline int rel_tma_grid(const RelTma& L, int64_t work) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.kern[0], kRelTmaThreads, L.smem);
   if (per_sm < 1) per_sm = 1;
@@ -828,11 +882,12 @@ int rel_w1_grid(int64_t work) {
 template <typename T16>
 int run_release_batch(RelBatch& b, int world, float inv_scale, double* sc, cudaStream_t st) {
   const bool vec = rel_vec_ok(b, world);
-  if (vec && world == 1) {
-    const RelTma& L = rel_tma<T16>();
+  const RelTma* T = vec ? rel_tma<T16>(world) : nullptr;
+  if (T) {
+    const RelTma& L = *T;
     const int64_t work = rel_tiles(b, L.u);
     if (work == 0) return ELX_OK;
-    const int grid = rel_w1_grid<T16>(work);
+    const int grid = rel_tma_grid(L, work);
     void* args[] = {(void*)&b, (void*)&inv_scale, (void*)&sc};
     cudaError_t e = cudaLaunchKernel(L.kern[inv_scale == 1.0f], dim3(grid), dim3(kRelTmaThreads), args, L.smem, st);
     if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_release: %s", cudaGetErrorString(e));
@@ -1592,6 +1647,78 @@ __global__ void __cluster_dims__(1, kCcCluster, 1) __launch_bounds__(kCcThreads,
 }  // namespace
 
 // ======================================================================= ABI
+// ============================================================ K2 fetch, TMA
+// The all-gather of one chunk as bulk copies: the concatenated rank shards
+// are cut into tiles of kTile bytes (the last tile of a shard shorter, always
+// a multiple of 16 bytes); CTA b takes tiles b, b+G, ... One thread per CTA
+// runs a kStages-deep pipeline: bulk-load tile k+kStages-1 from the (peer)
+// shard into a shared-memory stage (complete_tx on the stage's mbarrier)
+// while the bulk store of tile k drains the stage before it to the rCache
+// block; a stage is reloaded only once the store that read it has finished
+// reading (wait_group.read). No registers carry data, so the bytes in flight
+// per SM are the stages' (kStages x kTile) whatever the latency of the source
+// — HBM for a local shard, NVLink for a peer's.
+template <int kTile, int kStages>
+__global__ void __launch_bounds__(32, 1) fetch_tma_kernel(char* __restrict__ block,
+                                                           const __grid_constant__ PtrBatch src,
+                                                           int64_t shard_bytes, int64_t tiles_per_rank,
+                                                           int64_t ntiles) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ __align__(8) uint64_t full[kStages];
+  if (threadIdx.x != 0) return;
+  for (int i = 0; i < kStages; ++i) mbar_init(&full[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int64_t G = gridDim.x;
+  const int64_t K = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;  // tiles of this CTA
+  auto issue = [&](int64_t k) {
+    const int64_t t = blockIdx.x + k * G;
+    const int r = (int)(t / tiles_per_rank);
+    const int64_t off = (t - (int64_t)r * tiles_per_rank) * kTile;
+    const uint32_t bytes = (uint32_t)min((int64_t)kTile, shard_bytes - off);
+    const int st = (int)(k % kStages);
+    mbar_expect_tx(&full[st], bytes);
+    tma_load_1d(smem_raw + (size_t)st * kTile, static_cast<const char*>(src.p[r]) + off, bytes, &full[st]);
+  };
+  for (int64_t k = 0; k < K && k < kStages - 1; ++k) issue(k);
+  for (int64_t k = 0; k < K; ++k) {
+    const int st = (int)(k % kStages);
+    mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));
+    const int64_t t = blockIdx.x + k * G;
+    const int r = (int)(t / tiles_per_rank);
+    const int64_t off = (t - (int64_t)r * tiles_per_rank) * kTile;
+    const uint32_t bytes = (uint32_t)min((int64_t)kTile, shard_bytes - off);
+    tma_store_1d(block + (int64_t)r * shard_bytes + off, smem_raw + (size_t)st * kTile, bytes);
+    tma_store_commit();
+    if (k + kStages - 1 < K) {
+      tma_store_wait_read<1>();  // the store of tile k-1 has read the stage tile k+kStages-1 goes into
+      issue(k + kStages - 1);
+    }
+  }
+  tma_store_wait_all();
+}
+
+struct FetchTma {
+  const void* kern;
+  int tile;
+  size_t smem;
+};
+
+template <int kTile, int kStages>
+FetchTma fetch_tma_make() {
+  FetchTma f{(const void*)fetch_tma_kernel<kTile, kStages>, kTile, (size_t)kTile * kStages};
+  cudaFuncSetAttribute(f.kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f.smem);
+  return f;
+}
+
+// ELX_K2_TMA: -1 = the register-copy fetch_kernel; 0 (default) .. 3 = tile x stages below.
+const FetchTma* fetch_tma() {
+  static const int v = env_int("ELX_K2_TMA", 0);
+  if (v < 0) return nullptr;
+  static const FetchTma t[] = {fetch_tma_make<32768, 4>(), fetch_tma_make<16384, 4>(),
+                               fetch_tma_make<65536, 3>(), fetch_tma_make<16384, 8>()};
+  return &t[v < 4 ? v : 0];
+}
+
 extern "C" {
 
 int elx_chunk_pack(void* chunk, int32_t chunk_dtype, int64_t phys_len, int64_t used_len,
@@ -1635,6 +1762,19 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
     pb.p[r] = shards[r];
   }
   if (shard_len == 0) return ELX_OK;
+  if (const FetchTma* F = fetch_tma()) {
+    const int64_t bytes = shard_len * 2;
+    const int64_t tpr = (bytes + F->tile - 1) / F->tile;
+    const int64_t ntiles = tpr * world;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, F->kern, 32, F->smem);
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(per_sm, 1)));
+    char* blk = static_cast<char*>(block);
+    void* args[] = {(void*)&blk, (void*)&pb, (void*)&bytes, (void*)&tpr, (void*)&ntiles};
+    cudaError_t e = cudaLaunchKernel(F->kern, dim3(grid), dim3(32), args, F->smem, (cudaStream_t)stream);
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_fetch: %s", cudaGetErrorString(e));
+    return check_launch("elx_fetch");
+  }
   const int64_t vecs = shard_len / 8;
   const int64_t per_cta = (int64_t)kCopyThreads * kCopyUnroll;
   const int gx = (int)std::max<int64_t>(
@@ -1813,11 +1953,11 @@ int elx_release_geometry(const int64_t* n, int32_t nseg, int32_t world, int32_t 
   for (int i = 0; i < nseg; ++i)
     if (n[i] > 0) b.n[b.nseg++] = n[i];
   // the geometry depends on the tile shape only (the same for scale 1 or not) and the grid
-  if (world == 1) {  // the TMA kernel (release_w1_tma_kernel)
-    const int u = dtype == ELX_BF16 ? rel_tma<__nv_bfloat16>().u : rel_tma<__half>().u;
-    const int64_t work = rel_tiles(b, u);
-    *ctas = work == 0 ? 0 : (dtype == ELX_BF16 ? rel_w1_grid<__nv_bfloat16>(work) : rel_w1_grid<__half>(work));
-    *tile_vecs = kRelThreads * u;
+  const RelTma* T = dtype == ELX_BF16 ? rel_tma<__nv_bfloat16>(world) : rel_tma<__half>(world);
+  if (T) {  // the TMA kernel (release_tma_kernel)
+    const int64_t work = rel_tiles(b, T->u);
+    *ctas = work == 0 ? 0 : rel_tma_grid(*T, work);
+    *tile_vecs = kRelThreads * T->u;
     return ELX_OK;
   }
   const RelLaunch L = dtype == ELX_BF16 ? rel_kernel<__nv_bfloat16>(world, true, false)

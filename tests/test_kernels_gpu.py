@@ -80,7 +80,7 @@ def test_pack_validation(cuda):
 # ------------------------------------------------------------------ K2 fetch
 
 @pytest.mark.parametrize("world", [1, 2, 3, 4, 8])
-@pytest.mark.parametrize("shard", [8, 4096, 1_000_008])
+@pytest.mark.parametrize("shard", [8, 4096, 16_384, 1_000_008, 3_000_000])
 def test_fetch_gathers_shards_in_rank_order(cuda, world, shard):
     g = torch.Generator().manual_seed(world * 7 + shard)
     shards = [torch.randint(-32768, 32767, (shard,), generator=g, dtype=torch.int16).view(torch.bfloat16).to(cuda)
@@ -104,6 +104,53 @@ def test_fetch_copy_engine_equals_kernel(cuda, world):
     assert np.array_equal(_bits(block), arith.gather([_bits(s) for s in shards]))
     with pytest.raises(errors.ValidationError):
         kernels.fetch(block, [s.data_ptr() + 2 for s in shards], 8, engine="ce")
+
+
+_K2K3_VARIANT_SCRIPT = r"""
+import sys
+sys.path.insert(0, sys.argv[1])
+import numpy as np, torch
+from paper_2212_05339_b200 import kernels
+from oracle import arith
+dev = torch.device("cuda", 0)
+bits = lambda t: t.cpu().view(torch.int16).numpy().view(np.uint16)
+for world in (1, 2, 3, 4, 8):
+    for n in (8, 4104, 1_000_008, 2_500_000):
+        g = torch.Generator().manual_seed(n + world)
+        srcs = [(torch.randn(n, generator=g) * 3.0).to(torch.bfloat16) for _ in range(world)]
+        dsrc = [s.to(dev) for s in srcs]
+        block = torch.zeros(world * n, dtype=torch.bfloat16, device=dev)
+        kernels.fetch(block, [t.data_ptr() for t in dsrc], n)
+        torch.cuda.synchronize()
+        assert np.array_equal(bits(block), arith.gather([bits(s) for s in srcs])), (world, n)
+        for scale in (1.0, 1.0 / 64):
+            out = torch.full((n,), -1.0, device=dev)
+            sc = kernels.new_step_scalars(dev)
+            kernels.release(out, [t.data_ptr() for t in dsrc], n, torch.bfloat16, scale, sc)
+            torch.cuda.synchronize()
+            wg, wsq, wbad = arith.release([bits(s) for s in srcs], scale, "bf16")
+            assert np.array_equal(out.cpu().numpy(), wg), (world, n, scale)
+            ctas, tv = kernels.release_geometry([n], world)
+            assert sc[0].item() == arith.release_norm_ordered([wg], ctas, tv), (world, n, scale, ctas, tv)
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("env", [{"ELX_K2_TMA": "-1", "ELX_K3_PEER_TMA": "0"}, {"ELX_K2_TMA": "1", "ELX_K3_TMA": "1"},
+                                 {"ELX_K2_TMA": "2"}, {"ELX_K2_TMA": "3"}])
+def test_fetch_release_variants_bit_exact(cuda, env):
+    """Every K2 shape (register copy, TMA tiles x stages) gathers the oracle's bytes, and K3 at world 1-8 with
+    the TMA stages off (register-staged peer loads) or in their other shape equals the oracle: the reduced
+    fp32 bits, and the sum of squares in the order elx_release_geometry reports."""
+    import os
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = str(Path(__file__).resolve().parents[1])
+    out = subprocess.run([sys.executable, "-c", _K2K3_VARIANT_SCRIPT, root], env=dict(os.environ, **env),
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
 
 
 def test_fetch_rejects_unaligned(cuda):
