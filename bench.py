@@ -24,6 +24,7 @@ from __future__ import annotations
 import argparse
 import ctypes
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -440,15 +441,27 @@ def run_ours(args):
     # ---- end to end through the public API with host buffers
     host_ids = torch.randint(0, cfg.vocab, (B, T + 1), generator=torch.Generator().manual_seed(99 + rank)).pin_memory()
     dev_ids = torch.empty_like(host_ids, device=dev)
-    loss_host = torch.zeros(1, dtype=torch.float32).pin_memory()
+    loss_host = torch.zeros(2, dtype=torch.float32).pin_memory()   # one slot per step in flight
+    e2e_losses = []
     _barrier(world)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     f0.record(cur)
-    for _ in range(args.steps):
+    # a non-blocking training loop: step i's tokens go up and its loss comes back on the compute stream;
+    # the host reads step i's loss once step i+1 is enqueued (one step in flight), so the GPU never idles
+    # on the host's wake-up and the next launch
+    pending = None
+    for i in range(args.steps):
         dev_ids.copy_(host_ids, non_blocking=True)
         lo = step_fn(dev_ids[:, :-1], dev_ids[:, 1:])
-        loss_host.copy_(lo.reshape(1), non_blocking=True)
-        cur.synchronize()
+        loss_host[i % 2].copy_(lo.reshape(()), non_blocking=True)
+        done = torch.cuda.Event()
+        done.record(cur)
+        if pending is not None:
+            pending[0].synchronize()
+            e2e_losses.append(float(loss_host[pending[1]]))
+        pending = (done, i % 2)
+    pending[0].synchronize()
+    e2e_losses.append(float(loss_host[pending[1]]))
     model.synchronize()
     f1.record(cur)
     torch.cuda.synchronize(dev)
@@ -598,9 +611,11 @@ def run_ours(args):
                      "algorithmic_bytes_per_launch": bpe * adam_elems, "bytes_per_element": bpe},
         "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s",
                 "h2d_bytes_per_step": host_ids.numel() * host_ids.element_size(),
-                "d2h_bytes_per_step": loss_host.numel() * loss_host.element_size(),
+                "d2h_bytes_per_step": loss_host.element_size(),
                 "api": ("ElixirGPT2.graph_step (the captured train_step)" if use_graph else "ElixirGPT2.train_step")
-                       + " on tokens copied from pinned host memory, loss read back"},
+                       + " on tokens copied from pinned host memory every step, every step's loss read back "
+                         "on the host (one step in flight)",
+                "losses_read": len(e2e_losses), "all_finite": all(math.isfinite(x) for x in e2e_losses)},
         "checkpointed": checkpointed,
         "parity": parity,
         "chunk_runtime": offload,
@@ -613,6 +628,71 @@ def run_ours(args):
 
 
 # ---------------------------------------------------------------- kernel sweep
+
+def _sweep_graph_stream(mb, w, S, dev, reps, flush, flush_sink, hp, peak, emit):
+    """The sweep's kernels as the step issues them: R back-to-back launches,
+    each on its OWN buffers (R x the per-launch bytes >= 512 MB, four times
+    the L2, so no launch reads what an earlier one left in L2), captured as
+    one CUDA graph and replayed; ms per launch = replay time / R. A single
+    cold launch of a few-MB chunk is dominated by launch latency and the DRAM
+    ramp (the plain sweep lines); this is the per-chunk cost inside a step."""
+    from paper_2212_05339_b200 import kernels
+
+    sc = kernels.new_step_scalars(dev)
+    engines = {
+        "k2_fetch_sm": 2 * 2 * w * S,
+        "k2_fetch_ce": 2 * 2 * w * S,
+        "k3_release": 2 * w * S + (4 * S if w > 1 else 0),
+        "k4_adam": 30 * S,
+    }
+    for engine, nbytes in engines.items():
+        R = max(1, min(64, -(-(512 * 2 ** 20) // nbytes)))
+        launches = []
+        for _ in range(R):
+            if engine.startswith("k2"):
+                shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(w)]
+                block = torch.empty(w * S, dtype=torch.bfloat16, device=dev)
+                ce = "ce" if engine.endswith("ce") else "sm"
+                launches.append((lambda b=block, ps=[t.data_ptr() for t in shards], e=ce:
+                                 kernels.fetch(b, ps, S, engine=e), (shards, block)))
+            elif engine == "k3_release":
+                shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(w)]
+                g32 = torch.empty(S, device=dev) if w > 1 else None
+                launches.append((lambda g=g32, ps=[t.data_ptr() for t in shards]:
+                                 kernels.release(g, ps, S, torch.bfloat16, 1.0, sc), (shards, g32)))
+            else:
+                p32, m, v, g32 = (torch.zeros(S, device=dev) for _ in range(4))
+                p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+                tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
+                launches.append((lambda t=tab: kernels.adam(t, hp, 1, sc, torch.bfloat16), (p32, m, v, g32, p16)))
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream(dev))
+        with torch.cuda.stream(side):
+            for f, _ in launches:
+                f()
+        torch.cuda.current_stream(dev).wait_stream(side)
+        torch.cuda.synchronize(dev)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            for f, _ in launches:
+                f()
+        ts = []
+        for i in range(reps + 2):
+            torch.sum(flush, dim=0, out=flush_sink)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            graph.replay()
+            b.record()
+            torch.cuda.synchronize(dev)
+            if i >= 2:
+                ts.append(a.elapsed_time(b))
+        ms = statistics.median(ts) / R
+        emit({"chunk_mb": mb, "emulated_world": w, "engine": engine, "shard_elems": S, "mode": "graph_stream",
+              "launches_per_graph": R, "ms": ms, "hbm_gbs": nbytes / (ms * 1e-3) / 1e9,
+              "frac": nbytes / (ms * 1e-3) / 1e9 / peak})
+        del graph, launches
+        torch.cuda.empty_cache()
+
 
 def run_sweep(args):
     """configs[4]: the chunk sweep — K2 fetch (SMs and copy engines), K3
@@ -751,6 +831,9 @@ def run_sweep(args):
         del pk_src, pk_dst, pk
         for w in (1, 2, 4, 8):
             S = shard_length(C, w)
+            if args.sweep_graph:
+                _sweep_graph_stream(mb, w, S, dev, reps, flush, flush_sink, hp, peak, emit)
+                continue
             shards = [torch.randn(S, device=dev).to(torch.bfloat16) for _ in range(w)]
             block = torch.empty(w * S, dtype=torch.bfloat16, device=dev)
             g32 = torch.empty(S, device=dev)
@@ -785,6 +868,9 @@ def main():
     ap.add_argument("--model", default="gpt2-1.3b")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--sweep-sizes", default="4,8,16,32,64,128,256", help="chunk sizes in MB for --sweep")
+    ap.add_argument("--sweep-graph", action="store_true",
+                    help="--sweep at N=1: time each kernel as R back-to-back launches on distinct buffers in one "
+                         "CUDA graph (the step's issue pattern) instead of single cold launches")
     ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
                     "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")

@@ -360,6 +360,25 @@ __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src, uin
       : "memory");
 }
 
+// bulk stores (shared -> global) and the consumer-warp named barrier
+__device__ __forceinline__ void bar_consumers(int n) {
+  asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ void tma_store_1d(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int kN>
+__device__ __forceinline__ void tma_store_wait_read() {
+  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kN) : "memory");
+}
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // ============================================================== K3 release
 // One launch reduces a batch of segments (every chunk due at one reduce
 // position, plus the shared parameter at the last one):
@@ -596,8 +615,10 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
     release_tma_kernel(const __grid_constant__ RelBatch b, float inv_scale, double* __restrict__ sc) {
   constexpr int kRelTileVecs1 = kRelThreads * kRelU1;  // 16-byte vectors per tile per rank
   constexpr int kStageVecs = kRelTileVecs1 * kWorld;
+  constexpr bool kBulkOut = kWorld > 1;  // fp32 output through two shared-memory stages and bulk stores
   extern __shared__ __align__(128) unsigned char smem_raw[];
   uint4* stages = reinterpret_cast<uint4*>(smem_raw);
+  float* ostage = reinterpret_cast<float*>(stages + (size_t)kRelStages * kStageVecs);
   __shared__ __align__(8) uint64_t full[kRelStages];
   __shared__ __align__(8) uint64_t empty[kRelStages];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -632,7 +653,7 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
     }
   } else {  // ---------------------------------------- consumer warps
     int s = 0;
-    int64_t q = 0;
+    int64_t q = 0, oq = 0;
     for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
       while (s + 1 < b.nseg && b.tile0[s + 1] <= t) ++s;
       const int64_t n = b.n[s];
@@ -665,6 +686,43 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
         ++q;
       }
       float* __restrict__ g = b.g[s];
+      if (kBulkOut && g != nullptr && nv == kRelTileVecs1) {
+        // a whole tile's fp32 output: into output stage oq&1 (the same bytes, in the same order, as the
+        // global tile), then one bulk store. The stage was last read by the store of tile oq-2: the storer
+        // (thread 0) waits for that read before the consumers write, and issues this tile's store once all
+        // of them have written.
+        float* ob = ostage + (size_t)(oq & 1) * kRelTileVecs1 * 8;
+        if (threadIdx.x == 0) tma_store_wait_read<1>();
+        bar_consumers(kRelThreads);
+#pragma unroll
+        for (int u = 0; u < kRelU1; ++u) {
+          float acc[8];
+          unpack8<T16>(raw[u][0], acc);
+#pragma unroll
+          for (int r = 1; r < kWorld; ++r) {
+            float x[8];
+            unpack8<T16>(raw[u][r], x);
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = __fadd_rn(acc[e], x[e]);
+          }
+          if (!kScaleOne) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] = __fmul_rn(acc[e], inv_scale);
+          }
+          sq = sq_acc8(sq, acc);
+          float4* d = reinterpret_cast<float4*>(ob + (size_t)(u * kRelThreads + threadIdx.x) * 8);
+          d[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          d[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        }
+        fence_proxy_async_smem();  // generic-proxy smem writes -> visible to the bulk copy engine
+        bar_consumers(kRelThreads);
+        if (threadIdx.x == 0) {
+          tma_store_1d(g + v0 * 8, ob, (uint32_t)kRelTileVecs1 * 32);
+          tma_store_commit();
+        }
+        ++oq;
+        continue;
+      }
       if (kWorld == 1 && g == nullptr) {  // the norm pass: no released output
 #pragma unroll
         for (int u = 0; u < kRelU1; ++u) {
@@ -708,6 +766,7 @@ __global__ void __launch_bounds__(kRelTmaThreads, 1)
         }
       }
     }
+    if (kBulkOut && threadIdx.x == 0) tma_store_wait_all();  // the released shards are written at kernel end
   }
   publish_partial(sq, bad_of(sq), sc);
 }
@@ -813,7 +872,7 @@ template <typename T16, int kWorld, int kU, int kS>
 RelTma rel_tma_make() {
   RelTma r{{(const void*)release_tma_kernel<T16, kWorld, false, kU, kS>,
             (const void*)release_tma_kernel<T16, kWorld, true, kU, kS>},
-           kU, (size_t)kS * kWorld * kRelThreads * kU * 16};
+           kU, (size_t)kS * kWorld * kRelThreads * kU * 16 + (kWorld > 1 ? (size_t)2 * kRelThreads * kU * 32 : 0)};
   for (const void* k : r.kern) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)r.smem);
   return r;
 }
@@ -850,20 +909,21 @@ const RelTma* rel_tma(int world) {
                                  rel_tma_make<T16, 1, 2, 8>(), rel_tma_make<T16, 1, 8, 3>()};
       return &rel_tma_pick<T16, 1>(t);
     }
-    // world N: 32 KB stages (N slices of 32/N KB) x 4, or 64 KB x 3 (variant 1)
+    // world N: 32 KB stages (N slices of 32/N KB) x 4, or x 3 (variant 1); plus two output stages of the
+    // tile's fp32 results (2 x 64/N KB)
     case 2: {
       if (!rel_peer_tma()) return nullptr;
-      static const RelTma t[] = {rel_tma_make<T16, 2, 4, 4>(), rel_tma_make<T16, 2, 8, 3>()};
+      static const RelTma t[] = {rel_tma_make<T16, 2, 4, 4>(), rel_tma_make<T16, 2, 4, 3>()};
       return &rel_tma_pick<T16, 2>(t);
     }
     case 4: {
       if (!rel_peer_tma()) return nullptr;
-      static const RelTma t[] = {rel_tma_make<T16, 4, 2, 4>(), rel_tma_make<T16, 4, 4, 3>()};
+      static const RelTma t[] = {rel_tma_make<T16, 4, 2, 4>(), rel_tma_make<T16, 4, 2, 3>()};
       return &rel_tma_pick<T16, 4>(t);
     }
     case 8: {
       if (!rel_peer_tma()) return nullptr;
-      static const RelTma t[] = {rel_tma_make<T16, 8, 1, 4>(), rel_tma_make<T16, 8, 2, 3>()};
+      static const RelTma t[] = {rel_tma_make<T16, 8, 1, 4>(), rel_tma_make<T16, 8, 1, 3>()};
       return &rel_tma_pick<T16, 8>(t);
     }
     default: return nullptr;
@@ -1233,23 +1293,6 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1)
 // group) and hands the stage back to the producer once those stores have
 // READ shared memory (wait_group.read, one tile behind so the stores of
 // tile q overlap the math of tile q+1). Warps issue no global stores at all.
-__device__ __forceinline__ void bar_consumers(int n) {
-  asm volatile("bar.sync 1, %0;" ::"r"(n) : "memory");
-}
-__device__ __forceinline__ void fence_proxy_async_smem() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-__device__ __forceinline__ void tma_store_1d(void* dst, const void* src_smem, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-template <int kN>
-__device__ __forceinline__ void tma_store_wait_read() {
-  asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(kN) : "memory");
-}
-__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 template <typename T16, int kStages, int kTile, int kCW>
 __global__ void __launch_bounds__(kCW * 32 + 32, 1)

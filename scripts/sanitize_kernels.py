@@ -55,6 +55,21 @@ torch.cuda.synchronize()
 want, _, _ = arith.release([bits(s)[:39_997] for s in shards], 0.5)
 assert np.array_equal(out[:39_997].cpu().numpy(), want)
 
+# K3 at world 2 and 8 over several tiles per CTA (TMA stages wrap, the two fp32 output stages alternate
+# with their bulk stores) plus a partial tile; K2 over several tiles per CTA (stages reused)
+for w, n in ((2, 1_300_003), (8, 700_005)):
+    big = [torch.randn(n + 5, device=dev, generator=g).to(bf) for _ in range(w)]
+    outw = torch.empty(n, device=dev)
+    kernels.release(outw, [t.data_ptr() for t in big], n, bf, 1.0, sc)
+    torch.cuda.synchronize()
+    want, _, _ = arith.release([bits(t)[:n] for t in big], 1.0)
+    assert np.array_equal(outw.cpu().numpy(), want)
+    L = (n + 5) // 8 * 8
+    blk = torch.empty(w * L, dtype=bf, device=dev)
+    kernels.fetch(blk, [t.data_ptr() for t in big], L)
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(blk), arith.gather([bits(t)[:L] for t in big]))
+
 # K4 Adam: every variant family (TMA in/out default, TMA in, register-staged) over a tail + misaligned segment
 sizes = [4096 * 3 + 5, 2048, 777]
 segs = []
