@@ -661,7 +661,8 @@ def _sweep_graph_stream(mb, w, S, dev, reps, flush, flush_sink, hp, peak, emit):
                 launches.append((lambda g=g32, ps=[t.data_ptr() for t in shards]:
                                  kernels.release(g, ps, S, torch.bfloat16, 1.0, sc), (shards, g32)))
             else:
-                p32, m, v, g32 = (torch.zeros(S, device=dev) for _ in range(4))
+                p32, m, v = (torch.zeros(S, device=dev) for _ in range(3))
+                g32 = torch.randn(S, device=dev)
                 p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
                 tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
                 launches.append((lambda t=tab: kernels.adam(t, hp, 1, sc, torch.bfloat16), (p32, m, v, g32, p16)))
@@ -844,6 +845,8 @@ def run_sweep(args):
                                                  torch.bfloat16, 1.0, sc), None)
             p32, m, v = (torch.zeros(S, device=dev) for _ in range(3))
             p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+            if w == 1:
+                g32.normal_()   # (at N > 1 K3 wrote it)
             tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
             t_a = timeit(lambda: kernels.adam(tab, hp, 1, sc, torch.bfloat16), None)
             for engine, ms, nbytes in (("k2_fetch_sm", t_f, 2 * 2 * w * S), ("k2_fetch_ce", t_fc, 2 * 2 * w * S),

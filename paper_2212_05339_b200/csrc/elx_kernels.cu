@@ -1026,14 +1026,58 @@ __device__ __forceinline__ float4 cvt4_grad(uint2 raw, float gs) {
 
 // One element of the update; every operation is a single IEEE rounding in
 // the order of the oracle (oracle/arith.py: adamw_step).
-__device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float g, float coef,
-                                          const AdamK& k) {
+__device__ __forceinline__ void adam_moments(float& p, float& m, float& v, float g, float coef,
+                                             const AdamK& k) {
   g = __fmul_rn(g, coef);
   p = __fmul_rn(p, k.decay);
   m = __fadd_rn(m, __fmul_rn(k.omb1, __fsub_rn(g, m)));
   v = __fadd_rn(__fmul_rn(v, k.b2), __fmul_rn(__fmul_rn(k.omb2, g), g));
+}
+// p += -lr/bc1 * m / (sqrt(v)/sqrt(bc2) + eps), every operation IEEE round-to-nearest.
+__device__ __forceinline__ void adam_apply(float& p, float m, float v, const AdamK& k) {
   const float denom = __fadd_rn(__fdiv_rn(__fsqrt_rn(v), k.bc2_sqrt), k.eps);
   p = __fadd_rn(p, __fdiv_rn(__fmul_rn(k.neg_step, m), denom));
+}
+// The same with exact zeros routed around sqrt.rn / div.rn: a zero operand sends them to their
+// out-of-line slow paths, and an element whose gradient has been exactly 0 at every step so far (a
+// never-seen token's embedding row: m = v = 0) made K4 run at 0.62 of the HBM peak instead of 0.97
+// (scripts/k4_graph_probe.py). sqrt(+0) = +0 and (+-0)/x = +-0 for x > 0 exactly, so a safe operand (1)
+// feeds the fast path and the exact zero is selected back: bits unchanged for every input.
+__device__ __forceinline__ void adam_apply_zero_safe(float& p, float m, float v, const AdamK& k) {
+  const bool v0 = v == 0.f;
+  float r = __fsqrt_rn(v0 ? 1.f : v);
+  r = v0 ? v : __fdiv_rn(r, k.bc2_sqrt);
+  const float denom = __fadd_rn(r, k.eps);
+  const float num = __fmul_rn(k.neg_step, m);
+  const bool n0 = num == 0.f;
+  const float q = __fdiv_rn(n0 ? 1.f : num, denom);
+  p = __fadd_rn(p, n0 ? num : q);
+}
+__device__ __forceinline__ void adam_elem(float& p, float& m, float& v, float g, float coef,
+                                          const AdamK& k) {
+  adam_moments(p, m, v, g, coef, k);
+  adam_apply_zero_safe(p, m, v, k);
+}
+// Four elements: the guarded form only when one of their new second moments is 0 (v >= 0 or NaN, so
+// the min is 0 exactly then) — one compare per element on dense data. (m = 0 with v != 0 only costs
+// the slow path; the bits are the same either way.)
+__device__ __forceinline__ void adam4(float4& P, float4& M, float4& V, const float4& G, float coef,
+                                      const AdamK& k) {
+  adam_moments(P.x, M.x, V.x, G.x, coef, k);
+  adam_moments(P.y, M.y, V.y, G.y, coef, k);
+  adam_moments(P.z, M.z, V.z, G.z, coef, k);
+  adam_moments(P.w, M.w, V.w, G.w, coef, k);
+  if (fminf(fminf(V.x, V.y), fminf(V.z, V.w)) == 0.f) {
+    adam_apply_zero_safe(P.x, M.x, V.x, k);
+    adam_apply_zero_safe(P.y, M.y, V.y, k);
+    adam_apply_zero_safe(P.z, M.z, V.z, k);
+    adam_apply_zero_safe(P.w, M.w, V.w, k);
+  } else {
+    adam_apply(P.x, M.x, V.x, k);
+    adam_apply(P.y, M.y, V.y, k);
+    adam_apply(P.z, M.z, V.z, k);
+    adam_apply(P.w, M.w, V.w, k);
+  }
 }
 
 __device__ __forceinline__ float clip_coef(const double* sc, double max_norm) {
@@ -1111,10 +1155,7 @@ __global__ void __launch_bounds__(kAdamThreads, kMinBlocks)
         }
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-          adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
-          adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
-          adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
-          adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
+          adam4(P[u], M[u], V[u], G[u], coef, k);
           const int64_t j = j0 + u * kAdamThreads;
           reinterpret_cast<float4*>(p32 + base)[j] = P[u];
           reinterpret_cast<float4*>(m + base)[j] = M[u];
@@ -1272,10 +1313,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1)
     for (int u = 0; u < kU; ++u) {
       const int j = u * kCons + threadIdx.x;
       if (!skip) {
-        adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
-        adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
-        adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
-        adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
+        adam4(P[u], M[u], V[u], G[u], coef, k);
         reinterpret_cast<float4*>(p32)[j] = P[u];
         reinterpret_cast<float4*>(m)[j] = M[u];
         reinterpret_cast<float4*>(v)[j] = V[u];
@@ -1400,10 +1438,7 @@ __global__ void __launch_bounds__(kCW * 32 + 32, 1)
     for (int u = 0; u < kU; ++u) {
       const int j = u * kCons + threadIdx.x;
       if (!skip) {
-        adam_elem(P[u].x, M[u].x, V[u].x, G[u].x, coef, k);
-        adam_elem(P[u].y, M[u].y, V[u].y, G[u].y, coef, k);
-        adam_elem(P[u].z, M[u].z, V[u].z, G[u].z, coef, k);
-        adam_elem(P[u].w, M[u].w, V[u].w, G[u].w, coef, k);
+        adam4(P[u], M[u], V[u], G[u], coef, k);
         reinterpret_cast<float4*>(stg)[j] = P[u];
         reinterpret_cast<float4*>(stg + kTile)[j] = M[u];
         reinterpret_cast<float4*>(stg + 2 * kTile)[j] = V[u];

@@ -360,6 +360,40 @@ def test_adam_bit_exact_multi_segment_multi_step(cuda, misalign):
             h[0], h[1], h[2] = rp, rm, rv
 
 
+def test_adam_zero_state_and_zero_gradients_bit_exact(cuda):
+    """K4 routes exact zeros around the slow sqrt/div paths (a never-seen embedding row: m = v = 0, g = 0);
+    the bits equal the oracle's for zero state, zero gradients, signed zeros, and mixed elements, across
+    steps, in every K4 variant family reached by the default launch."""
+    rng = np.random.default_rng(5)
+    n = 200_003
+    p = (rng.standard_normal(n) * 0.02).astype(np.float32)
+    p[::7] = 0.0
+    p[1::7] = -0.0
+    m = np.zeros(n, np.float32)
+    v = np.zeros(n, np.float32)
+    g = (rng.standard_normal(n) * 1e-3).astype(np.float32)
+    g[: n // 2] = 0.0                 # half the elements never get a gradient
+    g[n // 2::5] = -0.0
+    host = [p, m, v, g]
+    ts = [torch.from_numpy(a.copy()).to(cuda) for a in host]
+    p16 = torch.zeros(n, dtype=torch.bfloat16, device=cuda)
+    table = kernels.AdamTable([(*ts, p16, n)], cuda)
+    sc = kernels.new_step_scalars(cuda)
+    for step in range(1, 4):
+        sq = float(np.dot(host[3].astype(np.float64), host[3]))
+        sc[0] = sq
+        sc[1] = 0.0
+        kernels.adam(table, HP, step, sc, torch.bfloat16)
+        torch.cuda.synchronize()
+        coef = arith.clip_coef(sq, HP["max_norm"])
+        rp, rm, rv, r16 = arith.adamw(host[0], host[1], host[2], host[3], step, HP["lr"], HP["beta1"],
+                                      HP["beta2"], HP["eps"], HP["weight_decay"], coef)
+        for got, want in ((ts[0], rp), (ts[1], rm), (ts[2], rv)):
+            assert np.array_equal(got.cpu().numpy().view(np.uint32), want.view(np.uint32))
+        assert np.array_equal(_bits(p16), r16)
+        host[0], host[1], host[2] = rp, rm, rv
+
+
 def test_adam_skips_on_overflow_and_restores_compute_copy(cuda):
     host, dev = _segments(cuda, [5000, 77], 12)
     for d in dev:
