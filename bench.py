@@ -501,16 +501,19 @@ def run_ours(args):
     # ---- parity (the checker, after every timed region): one more eager step of the SAME model on the same
     # batch, its K3 launches logged and the K4 inputs snapshotted on the device; the C oracle recomputes the
     # sum of squares in each launch's fixed order and AdamW over every element (oracle/parity.py)
+    # (N > 1: every rank checks its own shards, oracle/parity.check_step_multirank, merged on every rank)
     parity = None
-    if not args.no_parity and rank == 0:
+    if not args.no_parity:
+        if use_graph:
+            model.release_graph()   # the eager checked step runs in the captured step's memory (N ranks per GPU)
+        t0 = time.perf_counter()
         if world == 1:
             from oracle.parity import check_step
-            t0 = time.perf_counter()
             parity = check_step(model, tok, tgt)
-            parity["seconds"] = round(time.perf_counter() - t0, 1)
         else:
-            parity = {"checked": False, "reason": "N > 1: the multi-rank parity tests cover it "
-                                                  "(tests/test_multiprocess_gpu.py, tests/test_multirank_gpu.py)"}
+            from oracle.parity import check_step_multirank
+            parity = check_step_multirank(model, tok, tgt)
+        parity["seconds"] = round(time.perf_counter() - t0, 1)
 
     if rank != 0:
         return
@@ -775,8 +778,8 @@ def run_sweep(args):
             segs = [p + rank * S * 2 for p in pb]
             bar = transport.device_barrier
             bus = (world - 1) / world * 2 * P      # bytes: the gathered block / the bf16 reduce-scatter input
-            for engine, fn in (("k2_fetch_sm", lambda: kernels.fetch(block, ps, S)),
-                               ("k2_fetch_ce", lambda: kernels.fetch(block, ps, S, engine="ce")),
+            for engine, fn in (("k2_fetch_sm", lambda: kernels.fetch(block, ps, S, rank=rank)),
+                               ("k2_fetch_ce", lambda: kernels.fetch(block, ps, S, engine="ce", rank=rank)),
                                ("k3_release", lambda: kernels.release(g32, segs, S, torch.bfloat16, 1.0, sc))):
                 ms = timeit(fn, bar)
                 emit({"chunk_mb": mb, "engine": engine, "shard_elems": S, "ms": ms,

@@ -166,6 +166,19 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
 int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int32_t world,
                  int32_t dtype, void* stream);
 
+/* K2 with the calling rank known (SURVEY.md §8b's elx_fetch(block, peer_shards,
+ * shard_len, rank, world, dtype, stream)): the same gather, engine
+ * ELX_FETCH_SM (kernel) or ELX_FETCH_CE (copy engines), with the order of the
+ * peer reads rotated to start at rank+1 (own shard last): the copy engines
+ * read peer rank+1, rank+2, ... in turn and the kernel's tiles interleave the
+ * ranks from rank+1, so the N ranks of one all-gather never all pull from the
+ * same peer's NVLink egress at once. elx_fetch / elx_fetch_ce are this with
+ * rank 0. */
+#define ELX_FETCH_SM 0
+#define ELX_FETCH_CE 1
+int elx_fetch_ranked(void* block, const void* const* shards, int64_t shard_len, int32_t rank,
+                     int32_t world, int32_t dtype, int32_t engine, void* stream);
+
 /* Stream-ordered barrier across ranks over peer-mapped memory (the ordering
  * the in-kernel P2P fetch/release needs: every rank's earlier work on its
  * stream is visible to every peer before any rank's later work starts).

@@ -200,3 +200,179 @@ def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int 
         "oracle": "oracle/c/elx_oracle.c (ordered sum of squares per K3 launch, AdamW), "
                   f"{threads} host threads",
     }
+
+
+def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int | None = None) -> dict:
+    """The whole-step check at N > 1 (every rank calls it; the ranks' results
+    are merged and every rank gets the same dict). One eager step of the
+    trainer, unchanged, observed at the same two points as `check_step`:
+      * every K3 launch is logged in issue order and, on its own stream right
+        before it (after the release's device barrier on the P2P path; after
+        the exchange on the NCCL path), the N bf16 gradient slices it reads —
+        segment `rank` of every rank's copy of the chunk, peers' through their
+        mapped pointers — are copied to pinned host memory;
+      * right before HybridAdam's update, the fp32 master / m / v of every
+        GPU-home segment and this rank's local sum of squares (step_scalars[0]
+        before the cross-rank reduction) are copied to the host.
+    The oracle recomputes per rank (a) the reduced gradient of every segment,
+    the rank-ordered fp32 sum times inv_scale (oracle_release_bf16), compared
+    bit for bit with the fp32 shard K3 wrote; (b) the rank's sum of squares
+    launch by launch in each launch's fixed order; (c) the global sum — the
+    ranks' sums added in rank order from 0.0, as the P2P scalar reduction
+    reads them (elx_peer_sum_f64; NCCL's all-reduce on the exchange path
+    follows its own order, so there the global sum is compared to 1e-12) —
+    and (d) AdamW with the resulting clip coefficient over every element of
+    the rank's shards. Plans with CPU-home chunks are not covered here (their
+    N > 1 release goes through the fp32 staging shard): checked=False."""
+    import torch.distributed as dist
+
+    from paper_2212_05339_b200 import _lib as elx_lib
+    from paper_2212_05339_b200 import kernels
+
+    mgr, opt = model.manager, model.optimizer
+    world, rank = mgr.world, mgr.rank
+    if world == 1:
+        return check_step(model, tokens, targets, threads)
+    if mgr.cpu_ids:
+        return {"checked": False, "reason": "N > 1 check covers all-GPU-home plans"}
+    threads = threads or max(1, len(os.sched_getaffinity(0)) // world)   # the ranks share the host's cores
+    dev = mgr.device
+    lib_elx = elx_lib.load()
+    segs = list(opt.gpu_segments)
+    key_of = {seg[3].data_ptr(): key for key, seg in segs}          # K4's gradient input = K3's fp32 output
+    host = {key: torch.empty((world, seg[5]), dtype=torch.int16, pin_memory=True) for key, seg in segs}
+    launches: list = []
+    snap: dict = {}
+    real_batch, real_one, real_step = kernels.release_batch, kernels.release, opt.step
+
+    def log_batch(ss, dtype, inv_scale, step_scalars, stream=None):
+        if step_scalars is mgr.step_scalars:
+            st = stream if stream is not None else torch.cuda.current_stream(dev)
+            grp = []
+            for g, ptrs, n in ss:
+                if n <= 0:
+                    continue
+                key = key_of[g.data_ptr()]
+                for r in range(world):
+                    rc = lib_elx.elx_copy_d2h(host[key][r].data_ptr(), int(ptrs[r]), 2 * n, st.cuda_stream, None)
+                    elx_lib.check(rc, "parity copy of a K3 source")
+                grp.append((key, n))
+            launches.append((grp, float(inv_scale)))
+        return real_batch(ss, dtype, inv_scale, step_scalars, stream=stream)
+
+    def log_one(g, ptrs, n, dtype, inv_scale, step_scalars, stream=None):
+        return log_batch([(g, ptrs, n)], dtype, inv_scale, step_scalars, stream=stream)
+
+    def snapshot_then_step(releases_done=None, grad_scale=1.0):
+        cur = torch.cuda.current_stream(dev)
+        if releases_done is not None:
+            cur.wait_event(releases_done)
+        snap["__sq_local__"] = float(mgr.step_scalars[0].item())
+        snap["__flag_local__"] = float(mgr.step_scalars[1].item())
+        for key, (p32, m, v, _, _, n) in segs:
+            snap[key] = tuple(t[:n].cpu() for t in (p32, m, v))
+        return real_step(releases_done, grad_scale)
+
+    model.synchronize()
+    torch.cuda.synchronize(dev)
+    completed = int(mgr.step_scalars[2].item())
+    kernels.release_batch, kernels.release, opt.step = log_batch, log_one, snapshot_then_step
+    try:
+        model.train_step(tokens, targets)
+    finally:
+        kernels.release_batch, kernels.release = real_batch, real_one
+        del opt.step
+    model.synchronize()
+    sq_gpu, flag = opt.last_stats.scalars()
+    torch.cuda.synchronize(dev)
+
+    lib = _lib()
+    lib.oracle_release_bf16.restype = ctypes.c_double
+    lib.oracle_release_bf16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_float, ctypes.c_void_p, ctypes.c_int]
+    lib.oracle_release_norm_ordered.restype = ctypes.c_double
+    lib.oracle_release_norm_ordered.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int]
+    released = sorted(str(k) for grp, _ in launches for k, _ in grp)
+    assert released == sorted(str(k) for k, _ in segs), "every GPU-home segment is released exactly once"
+    gref: dict = {}
+    g_same = g_total = 0
+    g_rel = 0.0
+    sq_local = 0.0
+    for grp, inv_scale in launches:
+        for key, n in grp:
+            src = host[key].numpy().view(np.uint16)
+            ptrs = (ctypes.c_void_p * world)(*[src[r].ctypes.data for r in range(world)])
+            out = np.empty(n, np.float32)
+            bad = ctypes.c_int(0)
+            lib.oracle_release_bf16(out.ctypes.data, ptrs, world, n, ctypes.c_float(inv_scale), ctypes.byref(bad),
+                                    threads)
+            gref[key] = out
+            seg = dict(segs)[key]
+            same, rel = _compare(seg[3][:n], out)
+            g_same += same
+            g_total += n
+            g_rel = max(g_rel, rel)
+        ns = [n for _, n in grp]
+        ctas, tv = kernels.release_geometry(ns, world)
+        gp = (ctypes.c_void_p * len(grp))(*[gref[k].ctypes.data for k, _ in grp])
+        nn = (ctypes.c_int64 * len(grp))(*ns)
+        sq_local = sq_local + lib.oracle_release_norm_ordered(gp, nn, len(grp), ctas, tv, threads)
+    host.clear()
+    everyone = [None] * world
+    dist.all_gather_object(everyone, sq_local)
+    sq = 0.0
+    for s in everyone:
+        sq = sq + s
+    exact_order = bool(mgr.p2p)
+    sq_ok = (sq_gpu == sq) if exact_order else abs(sq_gpu - sq) <= 1e-12 * abs(sq)
+    # the exchange path's all-reduce adds in the library's order: once the global sum is within 1e-12, the
+    # update is checked with the value the step used (its clip coefficient), so AdamW stays a bit-exact test
+    sq_adam = sq if exact_order or not sq_ok else sq_gpu
+    hp = opt.hp
+    skip = bool(flag) or not np.isfinite(sq_adam)
+    step = completed + (0 if skip else 1)
+    coef = arith.clip_coef(sq_adam, hp["max_norm"])
+    k = arith.adam_consts(max(step, 1), hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"])
+    kv = np.array([k["decay"], k["omb1"], k["b2"], k["omb2"], k["bc2_sqrt"], k["neg_step"], k["eps"]], np.float32)
+    totals = {name: [0, 0.0] for name in ("p32", "m", "v", "p16")}
+    elements = 0
+    for key, (p32, m, v, _, p16, n) in segs:
+        P, M, V = (t.numpy() for t in snap.pop(key))
+        out16 = np.empty(n, np.uint16)
+        lib.oracle_adamw_bf16(P.ctypes.data, M.ctypes.data, V.ctypes.data, gref[key].ctypes.data,
+                              out16.ctypes.data, n, kv.ctypes.data, ctypes.c_float(coef), int(skip), threads)
+        for name, got, want, bf in (("p32", p32[:n], P, False), ("m", m[:n], M, False), ("v", v[:n], V, False),
+                                    ("p16", p16[:n], out16, True)):
+            same, rel = _compare(got, want, bf)
+            totals[name][0] += same
+            totals[name][1] = max(totals[name][1], rel)
+        elements += n
+    mine = {"elements": elements, "g_same": g_same, "g_total": g_total, "g_rel": g_rel,
+            "sq_local_gpu": snap["__sq_local__"], "sq_local_oracle": sq_local,
+            "totals": totals, "launches": len(launches)}
+    allr = [None] * world
+    dist.all_gather_object(allr, mine)
+    torch.cuda.empty_cache()
+    elements = sum(r["elements"] for r in allr)
+    merged = {name: [sum(r["totals"][name][0] for r in allr), max(r["totals"][name][1] for r in allr)]
+              for name in totals}
+    g_total = sum(r["g_total"] for r in allr)
+    return {
+        "checked": True,
+        "world": world,
+        "transport": type(mgr.transport).__name__,
+        "elements": elements,
+        "release_launches_per_rank": [r["launches"] for r in allr],
+        "reduced_grad_bit_identical_frac": sum(r["g_same"] for r in allr) / max(1, g_total),
+        "reduced_grad_max_rel_err": max(r["g_rel"] for r in allr),
+        "sumsq_local_bit_identical": all(r["sq_local_gpu"] == r["sq_local_oracle"] for r in allr),
+        "sumsq_global_bit_identical" if exact_order else "sumsq_global_within_1e-12": sq_ok,
+        "bit_identical_frac": {name: t[0] / elements for name, t in merged.items()},
+        "max_rel_err": {name: t[1] for name, t in merged.items()},
+        "tolerance": "north_star: 1e-6 relative for fp32 Adam and reduced gradients; bit-exact for bytes",
+        "within_tolerance": all(t[1] <= 1e-6 for t in merged.values()) and max(r["g_rel"] for r in allr) <= 1e-6
+                            and (sq_ok or abs(sq_gpu - sq) <= 1e-6 * abs(sq)),
+        "oracle": "oracle/c/elx_oracle.c (rank-ordered release, ordered sum of squares per K3 launch, AdamW), "
+                  f"{threads} host threads per rank",
+    }

@@ -95,6 +95,7 @@ _SIGNATURES = {
     "elx_chunk_unpack": (ctypes.c_int, [c_vp, c_i32, c_vp, c_i32, c_vp]),
     "elx_fetch": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]),
     "elx_fetch_ce": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp]),
+    "elx_fetch_ranked": (ctypes.c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp]),
     "elx_device_barrier": (ctypes.c_int, [c_vp, c_i32, c_i32, c_i32, c_vp]),
     "elx_peer_sum_f64": (ctypes.c_int, [c_vp, c_vp, c_i32, c_i32, c_vp]),
     "elx_enable_peer_access": (ctypes.c_int, [c_i32]),

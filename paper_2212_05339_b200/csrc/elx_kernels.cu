@@ -1739,7 +1739,7 @@ __global__ void __cluster_dims__(1, kCcCluster, 1) __launch_bounds__(kCcThreads,
 template <int kTile, int kStages>
 __global__ void __launch_bounds__(32, 1) fetch_tma_kernel(char* __restrict__ block,
                                                            const __grid_constant__ PtrBatch src,
-                                                           int64_t shard_bytes, int64_t tiles_per_rank,
+                                                           int64_t shard_bytes, int world, int rot,
                                                            int64_t ntiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[kStages];
@@ -1748,10 +1748,18 @@ __global__ void __launch_bounds__(32, 1) fetch_tma_kernel(char* __restrict__ blo
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   const int64_t G = gridDim.x;
   const int64_t K = ntiles > blockIdx.x ? (ntiles - blockIdx.x + G - 1) / G : 0;  // tiles of this CTA
+  // tile t: rank (t + rot) mod world, the (t / world)-th tile of that shard — consecutive tiles (and so
+  // the CTAs of a wave) spread over every rank's shard, and with rot = this rank + 1 each rank starts on
+  // a different peer: no peer's NVLink egress serves every reader at once
+  auto locate = [&](int64_t t, int& r, int64_t& off) {
+    r = (int)((t + rot) % world);
+    off = (t / world) * kTile;
+  };
   auto issue = [&](int64_t k) {
     const int64_t t = blockIdx.x + k * G;
-    const int r = (int)(t / tiles_per_rank);
-    const int64_t off = (t - (int64_t)r * tiles_per_rank) * kTile;
+    int r;
+    int64_t off;
+    locate(t, r, off);
     const uint32_t bytes = (uint32_t)min((int64_t)kTile, shard_bytes - off);
     const int st = (int)(k % kStages);
     mbar_expect_tx(&full[st], bytes);
@@ -1762,8 +1770,9 @@ __global__ void __launch_bounds__(32, 1) fetch_tma_kernel(char* __restrict__ blo
     const int st = (int)(k % kStages);
     mbar_wait(&full[st], (uint32_t)((k / kStages) & 1));
     const int64_t t = blockIdx.x + k * G;
-    const int r = (int)(t / tiles_per_rank);
-    const int64_t off = (t - (int64_t)r * tiles_per_rank) * kTile;
+    int r;
+    int64_t off;
+    locate(t, r, off);
     const uint32_t bytes = (uint32_t)min((int64_t)kTile, shard_bytes - off);
     tma_store_1d(block + (int64_t)r * shard_bytes + off, smem_raw + (size_t)st * kTile, bytes);
     tma_store_commit();
@@ -1823,10 +1832,12 @@ int elx_chunk_unpack(const void* chunk, int32_t chunk_dtype, const elx_member* m
   return run_pack<1>(const_cast<void*>(chunk), chunk_dtype, members, n, 0, 0, (cudaStream_t)stream);
 }
 
-int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t world, int32_t dtype,
-              void* stream) {
+int elx_fetch_ranked(void* block, const void* const* shards, int64_t shard_len, int32_t rank, int32_t world,
+                     int32_t dtype, int32_t engine, void* stream) {
   elx::clear_error();
   if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
+  if (rank < 0 || rank >= world) return elx::fail(ELX_ERR_VALIDATION, "rank %d out of range", rank);
+  if (engine != ELX_FETCH_SM && engine != ELX_FETCH_CE) return elx::fail(ELX_ERR_VALIDATION, "bad engine %d", engine);
   if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "fetch dtype must be bf16/f16");
   if (shard_len < 0 || (shard_len % 8) != 0)
     return elx::fail(ELX_ERR_VALIDATION, "shard_len %lld must be a non-negative multiple of 8",
@@ -1840,15 +1851,26 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
     pb.p[r] = shards[r];
   }
   if (shard_len == 0) return ELX_OK;
+  const int rot = (rank + 1) % world;  // start on the next rank's shard, own shard last
+  if (engine == ELX_FETCH_CE) {
+    const size_t bytes = (size_t)shard_len * 2;
+    for (int i = 0; i < world; ++i) {
+      const int r = (rot + i) % world;
+      cudaError_t e = cudaMemcpyAsync(static_cast<char*>(block) + r * bytes, shards[r], bytes, cudaMemcpyDefault,
+                                      (cudaStream_t)stream);
+      if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_fetch_ce rank %d: %s", r, cudaGetErrorString(e));
+    }
+    return ELX_OK;
+  }
   if (const FetchTma* F = fetch_tma()) {
     const int64_t bytes = shard_len * 2;
-    const int64_t tpr = (bytes + F->tile - 1) / F->tile;
-    const int64_t ntiles = tpr * world;
+    const int64_t ntiles = (bytes + F->tile - 1) / F->tile * world;
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, F->kern, 32, F->smem);
     const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(ntiles, (int64_t)sm_count() * std::max(per_sm, 1)));
     char* blk = static_cast<char*>(block);
-    void* args[] = {(void*)&blk, (void*)&pb, (void*)&bytes, (void*)&tpr, (void*)&ntiles};
+    int w = world, rt = rot;
+    void* args[] = {(void*)&blk, (void*)&pb, (void*)&bytes, (void*)&w, (void*)&rt, (void*)&ntiles};
     cudaError_t e = cudaLaunchKernel(F->kern, dim3(grid), dim3(32), args, F->smem, (cudaStream_t)stream);
     if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_fetch: %s", cudaGetErrorString(e));
     return check_launch("elx_fetch");
@@ -1862,26 +1884,14 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
   return check_launch("elx_fetch");
 }
 
+int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t world, int32_t dtype,
+              void* stream) {
+  return elx_fetch_ranked(block, shards, shard_len, 0, world, dtype, ELX_FETCH_SM, stream);
+}
+
 int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int32_t world, int32_t dtype,
                  void* stream) {
-  elx::clear_error();
-  if (world < 1 || world > ELX_MAX_WORLD) return elx::fail(ELX_ERR_VALIDATION, "world %d out of range", world);
-  if (dtype != ELX_BF16 && dtype != ELX_F16) return elx::fail(ELX_ERR_VALIDATION, "fetch dtype must be bf16/f16");
-  if (shard_len < 0 || (shard_len % 8) != 0)
-    return elx::fail(ELX_ERR_VALIDATION, "shard_len %lld must be a non-negative multiple of 8",
-                     (long long)shard_len);
-  if (!block || !shards) return elx::fail(ELX_ERR_VALIDATION, "null pointer");
-  if (!aligned16(block)) return elx::fail(ELX_ERR_VALIDATION, "block must be 16-byte aligned");
-  for (int r = 0; r < world; ++r)
-    if (!shards[r] || !aligned16(shards[r]))
-      return elx::fail(ELX_ERR_VALIDATION, "shard %d null or not 16-byte aligned", r);
-  const size_t bytes = (size_t)shard_len * 2;
-  for (int r = 0; r < world && bytes > 0; ++r) {
-    cudaError_t e = cudaMemcpyAsync(static_cast<char*>(block) + r * bytes, shards[r], bytes, cudaMemcpyDefault,
-                                    (cudaStream_t)stream);
-    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_fetch_ce rank %d: %s", r, cudaGetErrorString(e));
-  }
-  return ELX_OK;
+  return elx_fetch_ranked(block, shards, shard_len, 0, world, dtype, ELX_FETCH_CE, stream);
 }
 
 int elx_event_record(void* event, void* stream) {

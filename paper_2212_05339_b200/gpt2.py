@@ -700,6 +700,15 @@ class ElixirGPT2:
         self.last_loss = self._g_loss
         return self._g_loss
 
+    def release_graph(self) -> None:
+        """Drop the captured step (its private memory pool: the kept
+        activations and workspaces of one step) so an eager step can run in
+        that memory; graph_step needs capture() again afterwards."""
+        torch.cuda.synchronize(self.device)
+        self._graph = self._g_loss = None
+        self.last_loss = None if not isinstance(self.last_loss, torch.Tensor) else self.last_loss.clone()
+        torch.cuda.empty_cache()
+
     # -------------------------------------------------------------- misc
     @property
     def n_params(self) -> int:

@@ -98,10 +98,13 @@ def _ptr_array(ptrs: Sequence[int]):
     return arr
 
 
-def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream=None, engine: str = "sm") -> None:
+def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream=None, engine: str = "sm",
+          rank: int = 0) -> None:
     """K2: block[r*S:(r+1)*S] <- shard r (device pointers, local or peer-mapped).
     engine "sm": the fetch kernel; "ce": the copy engines (cudaMemcpyAsync per
-    rank), leaving every SM to the compute stream."""
+    rank), leaving every SM to the compute stream. `rank` (the caller's) rotates
+    the order of the peer reads to start at rank+1 (elx_fetch_ranked), so the
+    ranks of one all-gather do not all read the same peer at once."""
     lib = _lib.load()
     _cuda(block, "block")
     if block.numel() < len(shard_ptrs) * shard_len:
@@ -109,9 +112,8 @@ def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream
     if engine not in ("sm", "ce"):
         raise ValidationError(f"fetch engine must be 'sm' or 'ce', not {engine!r}")
     arr = _ptr_array(shard_ptrs)
-    fn = lib.elx_fetch if engine == "sm" else lib.elx_fetch_ce
-    rc = fn(block.data_ptr(), ctypes.addressof(arr), int(shard_len), len(shard_ptrs), elx_dtype(block.dtype),
-            _stream(stream))
+    rc = lib.elx_fetch_ranked(block.data_ptr(), ctypes.addressof(arr), int(shard_len), int(rank), len(shard_ptrs),
+                              elx_dtype(block.dtype), 0 if engine == "sm" else 1, _stream(stream))
     _lib.check(rc, "elx_fetch" if engine == "sm" else "elx_fetch_ce")
 
 

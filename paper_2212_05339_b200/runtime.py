@@ -237,7 +237,7 @@ class ChunkManager:
             self.transport.gather(sp.full[:sp.shard * self.world], sp.p16)
             return
         self.transport.device_barrier()  # every rank's K4 has written its shard
-        kernels.fetch(sp.full, self.peer_shared[sp.pid][0], sp.shard)
+        kernels.fetch(sp.full, self.peer_shared[sp.pid][0], sp.shard, rank=self.rank)
 
     # ------------------------------------------------------------ sizes
     def valid(self, c: int, rank: int | None = None) -> int:
@@ -539,7 +539,7 @@ class ChunkFetcher:
                 es = block.element_size()
                 off = mgr.row[c] * mgr.S * es
                 kernels.fetch(block, [p + off for p in mgr.peer_p16], mgr.S, stream=comm,
-                              engine=getattr(mgr.transport, "fetch_engine", "sm"))
+                              engine=getattr(mgr.transport, "fetch_engine", "sm"), rank=mgr.rank)
             elif cpu:
                 if self.time_release:
                     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -555,7 +555,7 @@ class ChunkFetcher:
                     off = b * mgr.P * es
                     self._barrier()
                     kernels.fetch(block, [p + off + r * mgr.S * es for r, p in enumerate(mgr.peer_blocks)], mgr.S,
-                                  stream=comm, engine=getattr(mgr.transport, "fetch_engine", "sm"))
+                                  stream=comm, engine=getattr(mgr.transport, "fetch_engine", "sm"), rank=mgr.rank)
                     self._barrier()  # peers may reuse block b (its gradients, later) only after every rank read it
                 elif mgr.world > 1:
                     mgr.transport.gather(block, seg)

@@ -161,7 +161,7 @@ def measure(world, rank, oversub, n_elems=64 * 2 ** 20, cpu_elems=32 * 2 ** 20, 
         ptrs = tr.peer_ptrs(shard)
         bus = (world - 1) / world * 2 * world * S
         # timed after a device barrier on the same stream: every rank's K2 starts together
-        t_k2 = _max(_time(lambda: kernels.fetch(block, ptrs, S), world, pre=tr.device_barrier), world)
+        t_k2 = _max(_time(lambda: kernels.fetch(block, ptrs, S, rank=rank), world, pre=tr.device_barrier), world)
         row["b_g2g"] = bus / t_k2 / GB
         detail.update({"b_g2g_engine": "K2 (elx_fetch) over CUDA-IPC peer mappings", "fetch_chunk_mb": fetch_mb,
                        "k2_ms": t_k2 * 1e3})

@@ -53,6 +53,8 @@ def test_gpu_entry_points_validate_before_launch():
     lib = _lib.load()
     assert lib.elx_fetch(None, None, 8, 0, _lib.BF16, None) == _lib.ERR_VALIDATION
     assert lib.elx_fetch(None, None, 7, 1, _lib.BF16, None) == _lib.ERR_VALIDATION
+    assert lib.elx_fetch_ranked(None, None, 8, 2, 2, _lib.BF16, 0, None) == _lib.ERR_VALIDATION  # rank >= world
+    assert lib.elx_fetch_ranked(None, None, 8, 0, 2, _lib.BF16, 7, None) == _lib.ERR_VALIDATION  # bad engine
     assert lib.elx_release(None, None, 8, 1, _lib.BF16, ctypes.c_float(1.0), None, None) == _lib.ERR_VALIDATION
     assert lib.elx_adam(None, 1, 1, None, 1, None, None) == _lib.ERR_VALIDATION
     hp = _lib.AdamHP(1e-3, 0.9, 0.999, 1e-8, 0.0, 0.0, 1.0, _lib.BF16, 0)

@@ -153,6 +153,21 @@ def test_fetch_release_variants_bit_exact(cuda, env):
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
 
 
+@pytest.mark.parametrize("engine", ["sm", "ce"])
+@pytest.mark.parametrize("world,rank", [(2, 1), (4, 3), (8, 0), (8, 5), (3, 2)])
+def test_fetch_rank_rotation_gathers_the_same_bytes(cuda, engine, world, rank):
+    """elx_fetch_ranked: the peer reads start at rank+1 (tiles interleaved over the ranks / copy-engine order
+    rotated), the gathered block is the same rank-ordered concatenation."""
+    g = torch.Generator().manual_seed(world * 31 + rank)
+    shard = 600_008
+    shards = [torch.randint(-32768, 32767, (shard,), generator=g, dtype=torch.int16).view(torch.bfloat16).to(cuda)
+              for _ in range(world)]
+    block = torch.zeros(world * shard, dtype=torch.bfloat16, device=cuda)
+    kernels.fetch(block, [s.data_ptr() for s in shards], shard, engine=engine, rank=rank)
+    torch.cuda.synchronize()
+    assert np.array_equal(_bits(block), arith.gather([_bits(s) for s in shards]))
+
+
 def test_fetch_rejects_unaligned(cuda):
     block = torch.zeros(64, dtype=torch.bfloat16, device=cuda)
     s = torch.zeros(16, dtype=torch.bfloat16, device=cuda)
