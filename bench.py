@@ -345,6 +345,9 @@ def run_ours(args):
         raise SystemExit("--transport p2p needs one GPU per rank (symmetric memory refuses a shared device)")
     dev = torch.device("cuda", local)
     cfg = PRESETS[args.model]
+    if args.batch:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, batch=args.batch)
     plan_path = ROOT / "plans" / (args.plan.format(n=world) if args.plan else f"{args.model}_n{world}.json")
     plan_text = plan_path.read_text()
     from paper_2212_05339_b200.transport import make_transport, primary_contexts, resolve_kind
@@ -879,6 +882,9 @@ def main():
                          "CUDA graph (the step's issue pattern) instead of single cold launches")
     ap.add_argument("--plan", default=None, help="plan file under plans/, {n} = world size "
                     "(default <model>_n<N>.json), e.g. gpt2-4b_offload_n{n}.json")
+    ap.add_argument("--batch", type=int, default=0,
+                    help="per-rank micro-batch (default: the preset's 8, BASELINE.json's configuration); a smaller "
+                         "one only for functional runs of many ranks on one GPU")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-parity", action="store_true", help="skip the post-timing parity check against the oracle")
     ap.add_argument("--cpu-update", choices=["split", "host", "stream"], default="split",
