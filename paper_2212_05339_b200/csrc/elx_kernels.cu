@@ -931,11 +931,15 @@ const RelTma* rel_tma(int world) {
 }
 
 // Grid of a TMA release: resident CTAs per SM (shared-memory bound) x SMs.
+// ELX_K3_MAX_CTAS > 0 caps it (experiments: a release sharing the SMs with the backward's GEMMs); the cap
+// is part of the geometry elx_release_geometry reports, so the order stays restated.
 inline int rel_tma_grid(const RelTma& L, int64_t work) {
+  static const int env_cap = env_int("ELX_K3_MAX_CTAS", 0);
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, L.kern[0], kRelTmaThreads, L.smem);
   if (per_sm < 1) per_sm = 1;
-  const int64_t cap = std::min<int64_t>((int64_t)sm_count() * per_sm, ELX_RELEASE_MAX_CTAS);
+  int64_t cap = std::min<int64_t>((int64_t)sm_count() * per_sm, ELX_RELEASE_MAX_CTAS);
+  if (env_cap > 0) cap = std::min<int64_t>(cap, env_cap);
   return (int)std::max<int64_t>(1, std::min<int64_t>(work, cap));
 }
 
