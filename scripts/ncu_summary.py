@@ -51,7 +51,7 @@ def launches(tag: str, path: Path) -> None:
     total = sum(tot.values())
     ours = {k: v for k, v in tot.items() if any(s in k for s in ("adam_kernel", "adam_tma_kernel", "adam_tma_st_kernel", "device_barrier", "release_kernel", "xent_fwd_kernel",
                                                                   "xent_bwd_kernel", "ln_param_grad_kernel", "ln_fwd_kernel", "ln_bwd_dx_kernel", "gelu_fwd_kernel", "gelu_bwd_kernel", "embedding_bwd_kernel", "release_norm_kernel", "::norm_kernel<",
-                                                                  "pack_kernel", "fetch_kernel", "colsum_", "release_batch", "release_w1_tma", "peer_sum",
+                                                                  "pack_kernel", "fetch_kernel", "colsum_", "release_batch", "release_w1_tma", "release_tma", "fetch_tma", "peer_sum",
                                                                   "norm_finalize", "step_reset", "step_advance"))}
     lines = [f"# {tag}: kernel launch list of one training step (ncu gpu__time_duration.sum, cold, serialised)",
              "", f"Total device time {total:.3f} ms over {sum(cnt.values())} launches; "
