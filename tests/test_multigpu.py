@@ -11,7 +11,8 @@ what the one-GPU box can only run oversubscribed:
    pointers beside NCCL's all-gather / reduce-scatter on the same buffers, and
    every rank holding a CUDA context on its own device only.
 3. bench.py --gpus N with no transport flag: the default is the P2P path with
-   the step captured as a CUDA graph, counters equal to simulate.
+   the step captured as a CUDA graph, counters equal to simulate, and the
+   bench's whole-step parity check bit-identical on every rank.
 """
 
 from __future__ import annotations
@@ -95,3 +96,8 @@ def test_bench_default_transport_is_p2p_graph(cuda):
     assert line["config"]["transport"] == "ipc" and line["config"]["cuda_graph"]
     assert line["config"]["cuda_contexts_on_devices"] == [0]
     assert line["kernels"]["fetch"]["bus_gbs"] > 0
+    # whole-step parity on distinct GPUs: peers' gradients read over NVLink, every element vs the C oracle
+    par = line["parity"]
+    assert par["checked"] and par["within_tolerance"] and par["sumsq_global_bit_identical"], par
+    assert par["reduced_grad_bit_identical_frac"] == 1.0, par
+    assert all(v == 1.0 for v in par["bit_identical_frac"].values()), par
