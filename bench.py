@@ -614,7 +614,9 @@ def run_ours(args):
         },
         "roofline": {"bound": "hbm", "kernel": "elx_adam (K4)", "achieved": adam_gbs, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": adam_gbs / peak, "traffic": traffic,
-                     "algorithmic_bytes_per_launch": bpe * adam_elems, "bytes_per_element": bpe},
+                     "algorithmic_bytes_per_launch": bpe * adam_elems, "bytes_per_element": bpe,
+                     # also against the nominal HBM3e rate (HGX B200, B200_PROFILING.md)
+                     "nominal_peak": 7700.0, "frac_of_nominal": adam_gbs / 7700.0},
         "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s",
                 "h2d_bytes_per_step": host_ids.numel() * host_ids.element_size(),
                 "d2h_bytes_per_step": loss_host.element_size(),
