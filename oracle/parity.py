@@ -222,8 +222,11 @@ def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, thr
     reads them (elx_peer_sum_f64; NCCL's all-reduce on the exchange path
     follows its own order, so there the global sum is compared to 1e-12) —
     and (d) AdamW with the resulting clip coefficient over every element of
-    the rank's shards. Plans with CPU-home chunks are not covered here (their
-    N > 1 release goes through the fp32 staging shard): checked=False."""
+    the rank's shards. CPU-home chunks are covered too: their K3 writes the
+    shared fp32 staging shard (the chunk is identified through the release
+    sources the fetcher computed for it), the reduced gradient is compared
+    with the host shard it was copied to, and the host-thread or streamed
+    update with the host state after the step."""
     import torch.distributed as dist
 
     from paper_2212_05339_b200 import _lib as elx_lib
@@ -233,17 +236,26 @@ def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, thr
     world, rank = mgr.world, mgr.rank
     if world == 1:
         return check_step(model, tokens, targets, threads)
-    if mgr.cpu_ids:
-        return {"checked": False, "reason": "N > 1 check covers all-GPU-home plans"}
     threads = threads or max(1, len(os.sched_getaffinity(0)) // world)   # the ranks share the host's cores
     dev = mgr.device
     lib_elx = elx_lib.load()
-    segs = list(opt.gpu_segments)
-    key_of = {seg[3].data_ptr(): key for key, seg in segs}          # K4's gradient input = K3's fp32 output
+    # GPU-home segments (K4's table order), then CPU-home chunks (host-thread or streamed update)
+    host_all = sorted({**opt.cpu_segs, **opt.stream_segs}.items())
+    segs = list(opt.gpu_segments) + host_all
+    key_of = {seg[3].data_ptr(): key for key, seg in opt.gpu_segments}   # K4's gradient input = K3's output
     host = {key: torch.empty((world, seg[5]), dtype=torch.int16, pin_memory=True) for key, seg in segs}
     launches: list = []
     snap: dict = {}
     real_batch, real_one, real_step = kernels.release_batch, kernels.release, opt.step
+    # a CPU-home chunk's K3 writes the shared fp32 staging shard (then D2H to its host gradient shard): the
+    # chunk is the one whose release sources the fetcher computed last
+    fetcher = model.fetcher
+    real_srcs = fetcher._release_srcs
+    last_chunk = [None]
+
+    def srcs_noted(c):
+        last_chunk[0] = c
+        return real_srcs(c)
 
     def log_batch(ss, dtype, inv_scale, step_scalars, stream=None):
         if step_scalars is mgr.step_scalars:
@@ -252,7 +264,7 @@ def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, thr
             for g, ptrs, n in ss:
                 if n <= 0:
                     continue
-                key = key_of[g.data_ptr()]
+                key = key_of[g.data_ptr()] if g is not None and g.data_ptr() in key_of else last_chunk[0]
                 for r in range(world):
                     rc = lib_elx.elx_copy_d2h(host[key][r].data_ptr(), int(ptrs[r]), 2 * n, st.cuda_stream, None)
                     elx_lib.check(rc, "parity copy of a K3 source")
@@ -269,19 +281,21 @@ def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, thr
             cur.wait_event(releases_done)
         snap["__sq_local__"] = float(mgr.step_scalars[0].item())
         snap["__flag_local__"] = float(mgr.step_scalars[1].item())
-        for key, (p32, m, v, _, _, n) in segs:
-            snap[key] = tuple(t[:n].cpu() for t in (p32, m, v))
+        for key, (p32, m, v, _, _, n) in segs:   # (the host-home state: no update runs before real_step)
+            snap[key] = tuple(t[:n].cpu() if t.is_cuda else t[:n].clone() for t in (p32, m, v))
         return real_step(releases_done, grad_scale)
 
     model.synchronize()
     torch.cuda.synchronize(dev)
     completed = int(mgr.step_scalars[2].item())
     kernels.release_batch, kernels.release, opt.step = log_batch, log_one, snapshot_then_step
+    fetcher._release_srcs = srcs_noted
     try:
         model.train_step(tokens, targets)
     finally:
         kernels.release_batch, kernels.release = real_batch, real_one
         del opt.step
+        del fetcher._release_srcs
     model.synchronize()
     sq_gpu, flag = opt.last_stats.scalars()
     torch.cuda.synchronize(dev)
@@ -294,7 +308,7 @@ def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, thr
     lib.oracle_release_norm_ordered.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
                                                 ctypes.c_int, ctypes.c_int]
     released = sorted(str(k) for grp, _ in launches for k, _ in grp)
-    assert released == sorted(str(k) for k, _ in segs), "every GPU-home segment is released exactly once"
+    assert released == sorted(str(k) for k, _ in segs), "every updated segment is released exactly once"
     gref: dict = {}
     g_same = g_total = 0
     g_rel = 0.0
@@ -348,7 +362,7 @@ def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, thr
             totals[name][0] += same
             totals[name][1] = max(totals[name][1], rel)
         elements += n
-    mine = {"elements": elements, "g_same": g_same, "g_total": g_total, "g_rel": g_rel,
+    mine = {"elements": elements, "g_same": g_same, "g_total": g_total, "g_rel": g_rel, "cpu_home": len(host_all),
             "sq_local_gpu": snap["__sq_local__"], "sq_local_oracle": sq_local,
             "totals": totals, "launches": len(launches)}
     allr = [None] * world
@@ -363,6 +377,7 @@ def check_step_multirank(model, tokens: torch.Tensor, targets: torch.Tensor, thr
         "world": world,
         "transport": type(mgr.transport).__name__,
         "elements": elements,
+        "cpu_home_chunks_per_rank": [r["cpu_home"] for r in allr],
         "release_launches_per_rank": [r["launches"] for r in allr],
         "reduced_grad_bit_identical_frac": sum(r["g_same"] for r in allr) / max(1, g_total),
         "reduced_grad_max_rel_err": max(r["g_rel"] for r in allr),

@@ -172,15 +172,16 @@ def test_bench_two_ranks_one_gpu(cuda, plan, transport):
     assert line["config"]["cuda_graph"] == (transport == "ipc" and plan == "gpt2-small_n2.json")
     # whole-step parity at N = 2 (oracle/parity.check_step_multirank): the reduced fp32 gradients, the sums
     # of squares and AdamW over both ranks' shards against the C oracle
+    # (the rcache plan: evictions, re-gathers and 5 CPU-home chunks, their K3 into the fp32 staging shard and
+    # their host-thread / streamed updates)
     par = line["parity"]
-    if plan == "gpt2-small_n2.json":
-        assert par["checked"] and par["within_tolerance"], par
-        assert par["reduced_grad_bit_identical_frac"] == 1.0 and par["sumsq_local_bit_identical"], par
-        assert all(v == 1.0 for v in par["bit_identical_frac"].values()), par
-        if transport == "ipc":
-            assert par["sumsq_global_bit_identical"], par
-    else:
-        assert not par["checked"]
+    assert par["checked"] and par["within_tolerance"], par
+    assert par["reduced_grad_bit_identical_frac"] == 1.0 and par["sumsq_local_bit_identical"], par
+    assert all(v == 1.0 for v in par["bit_identical_frac"].values()), par
+    if transport == "ipc":
+        assert par["sumsq_global_bit_identical"], par
+    if plan == "gpt2-small_rcache_n2.json":
+        assert sum(par["cpu_home_chunks_per_rank"]) > 0, par
 
 
 @pytest.mark.parametrize("path", ["exchange-nosync", "ipc-nosync"])
