@@ -453,12 +453,16 @@ def run_ours(args):
     # the host reads step i's loss once step i+1 is enqueued (one step in flight), so the GPU never idles
     # on the host's wake-up and the next launch
     pending = None
+    step_marks = []   # (start, done) per step: device time of the step vs the gaps between steps
     for i in range(args.steps):
+        start = torch.cuda.Event(enable_timing=True)
+        start.record(cur)
         dev_ids.copy_(host_ids, non_blocking=True)
         lo = step_fn(dev_ids[:, :-1], dev_ids[:, 1:])
         loss_host[i % 2].copy_(lo.reshape(()), non_blocking=True)
-        done = torch.cuda.Event()
+        done = torch.cuda.Event(enable_timing=True)
         done.record(cur)
+        step_marks.append((start, done))
         if pending is not None:
             pending[0].synchronize()
             e2e_losses.append(float(loss_host[pending[1]]))
@@ -469,6 +473,9 @@ def run_ours(args):
     f1.record(cur)
     torch.cuda.synchronize(dev)
     e2e_ms = _max_over_ranks(f0.elapsed_time(f1), world)
+    e2e_step_ms = statistics.median(a.elapsed_time(b) for a, b in step_marks)
+    e2e_gap_ms = (statistics.median(step_marks[i][1].elapsed_time(step_marks[i + 1][0])
+                                    for i in range(len(step_marks) - 1)) if len(step_marks) > 1 else 0.0)
 
     # ---- the same step with the reference's per-layer checkpointing (world 1, graph mode): the model keeps
     # training, its step is re-captured with the recompute on and timed the same way (reported beside the
@@ -623,7 +630,8 @@ def run_ours(args):
                 "api": ("ElixirGPT2.graph_step (the captured train_step)" if use_graph else "ElixirGPT2.train_step")
                        + " on tokens copied from pinned host memory every step, every step's loss read back "
                          "on the host (one step in flight)",
-                "losses_read": len(e2e_losses), "all_finite": all(math.isfinite(x) for x in e2e_losses)},
+                "losses_read": len(e2e_losses), "all_finite": all(math.isfinite(x) for x in e2e_losses),
+                "device_ms_per_step": e2e_step_ms, "gap_ms_between_steps": e2e_gap_ms},
         "checkpointed": checkpointed,
         "parity": parity,
         "chunk_runtime": offload,
