@@ -27,12 +27,16 @@ def main():
         key = (r["chunk_mb"], r.get("emulated_world", r.get("world")))
         table[key][r["engine"]] = r
     engines = ["k1_pack", "k2_fetch_sm", "k2_fetch_ce", "k3_release", "k4_adam"]
+    graph = any(r.get("mode") == "graph_stream" for r in recs)
     lines = [f"# {title}", "",
              f"`python bench.py --sweep`: standalone K2 (SM kernel / copy engines), K3 and K4 on one rank's share of "
              f"one chunk; N local HBM buffers stand in for the N ranks (one GPU). Median of the launches after "
              f"warm-up, L2 flushed (256 MB read) before each. GB/s = algorithmic bytes / time; fraction of the "
              f"measured {peak} GB/s copy peak (MEASURED_PEAKS.json; a read-only stream such as the N = 1 K3 norm "
-             f"pass can exceed it). N = 1 K3 is the runtime's norm pass (2 B/element read, no fp32 output).", "",
+             f"pass can exceed it). N = 1 K3 is the runtime's norm pass (2 B/element read, no fp32 output)."
+             + (" GRAPH-STREAMED (`--sweep-graph`): K2/K3/K4 as R back-to-back launches on distinct buffers "
+                "(R x bytes >= 512 MB) captured in one CUDA graph, ms per launch = replay time / R — the issue "
+                "pattern of a step; K1 (run once per plan) stays a single launch." if graph else ""), "",
              "| chunk MB | N | shard elems | " + " | ".join(f"{e} ms | {e} GB/s | frac" for e in engines) + " |",
              "|---:|---:|---:|" + "---:|---:|---:|" * len(engines)]
     for (mb, n) in sorted(table):
