@@ -175,8 +175,10 @@ def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int 
         out16 = np.empty(n, np.uint16)
         lib.oracle_adamw_bf16(P.ctypes.data, M.ctypes.data, V.ctypes.data, G.ctypes.data, out16.ctypes.data, n,
                               kv.ctypes.data, ctypes.c_float(coef), int(skip), threads)
+        # a resident streamed chunk's new parameters are in its rCache block (HybridAdam.attach_fetcher)
+        p16_home = opt.resident[key] if key in getattr(opt, "resident", {}) else p16
         for name, got, want, bf in (("p32", p32[:n], P, False), ("m", m[:n], M, False), ("v", v[:n], V, False),
-                                    ("p16", p16[:n], out16, True)):
+                                    ("p16", p16_home[:n], out16, True)):
             same, rel = _compare(got, want, bf)
             totals[name][0] += same
             totals[name][1] = max(totals[name][1], rel)
@@ -186,6 +188,7 @@ def check_step(model, tokens: torch.Tensor, targets: torch.Tensor, threads: int 
         "checked": True,
         "elements": elements,
         "model_elements": total,
+        "resident_streamed_chunks": len(getattr(opt, "resident", {})),
         "segments_checked": len(checked),
         "segments": len(updated),
         "cpu_home_chunks": len(host_all),

@@ -453,7 +453,7 @@ class ElixirGPT2:
         self.optimizer = HybridAdam(self.manager, lr=lr, betas=betas, eps=eps, weight_decay=weight_decay,
                                     max_norm=max_norm, cpu_threads=cpu_threads, overlap=overlap_update,
                                     cpu_update=cpu_update)
-        self.fetcher.optimizer = self.optimizer
+        self.optimizer.attach_fetcher(self.fetcher)
         # coarse node -> its chunk parameters, in declaration order
         order = {p.id: i for i, p in enumerate(self.profile.parameters)}
         self.node_params = [sorted(node, key=order.__getitem__) for node in self.access.coarse_ops]

@@ -390,6 +390,10 @@ class ChunkFetcher:
         self.due = [[] for _ in range(W)]
         self.early = [[] for _ in range(W)]
         self.reduces = [[] for _ in range(W)]
+        # no eviction anywhere in the program: every chunk is gathered into the same block each step and that
+        # block holds nothing else (HybridAdam.attach_fetcher keeps streamed chunks' state there between steps)
+        self.stable_blocks = all(int(e["victim"]) < 0 for e in ev if int(e["kind"]) != _lib.EV_REDUCE)
+        self.block_for = {int(e["chunk"]): int(e["block"]) for e in ev if int(e["kind"]) != _lib.EV_REDUCE}
         for e in ev:
             rec = (int(e["chunk"]), int(e["block"]), int(e["victim"]), int(e["pos"]))
             if int(e["kind"]) == _lib.EV_REDUCE:
@@ -540,6 +544,8 @@ class ChunkFetcher:
                 off = mgr.row[c] * mgr.S * es
                 kernels.fetch(block, [p + off for p in mgr.peer_p16], mgr.S, stream=comm,
                               engine=getattr(mgr.transport, "fetch_engine", "sm"), rank=mgr.rank)
+            elif cpu and opt is not None and c in opt.in_block:
+                pass  # the streamed update wrote this chunk's parameters into its block (attach_fetcher)
             elif cpu:
                 if self.time_release:
                     c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -655,6 +661,8 @@ class ChunkFetcher:
                                         stream=comm)
                 if n == 0:
                     continue
+                if opt is not None and c in opt.resident:
+                    continue  # its streamed update reads the gradient from the block itself
                 src = mgr.storage(c) if mgr.fused_w1 else mgr.stage32
                 nbytes = n * src.element_size()
                 if self.time_release:
@@ -808,20 +816,14 @@ class HybridAdam:
         # v_c) and a GPU-streamed update (H2D p32/m/v/g -> K4 -> D2H
         # p32/m/v/p16 over PCIe) by measured rate: chunks in forward order go
         # to the worker that would finish them first (§8f row 4).
-        host_rate, stream_rate = update_rates or DEFAULT_UPDATE_RATES
-        self.cpu_segs, self.stream_segs = {}, {}
-        t_host = t_stream = 0.0
-        for c in sorted(all_cpu):
-            n = all_cpu[c][5]
-            use_stream = (cpu_update == "stream" or
-                          (cpu_update == "split" and t_stream + n / stream_rate < t_host + n / host_rate))
-            if use_stream:
-                self.stream_segs[c] = all_cpu[c]
-                t_stream += n / stream_rate
-            else:
-                self.cpu_segs[c] = all_cpu[c]
-                t_host += n / host_rate
-        self._init_stream_update(stream_tile)
+        self._all_cpu, self._cpu_update_mode = all_cpu, cpu_update
+        self._rates = update_rates or DEFAULT_UPDATE_RATES
+        self._stream_tile = stream_tile
+        # streamed chunks whose gradient and parameters stay in their rCache block between steps
+        # (attach_fetcher): chunk -> block tensor; in_block: the block holds the chunk's current parameters
+        self.resident: dict[int, torch.Tensor] = {}
+        self.in_block: set[int] = set()
+        self._assign_cpu_updates(self._rates[0], self._rates[1])
         self.stream = torch.cuda.Stream(device=m.device) if overlap else None
         pin = torch.cuda.is_available()
         # ring of pinned snapshots of the step scalars (read lazily by StepStats / the CPU thread)
@@ -841,11 +843,62 @@ class HybridAdam:
         self.done_event: torch.cuda.Event | None = None
         self.grad_scale = 1.0
         self.pending: dict[object, torch.cuda.Event] = {}     # key -> GPU update done
+        self._cpu_thread: threading.Thread | None = None
+        self._cpu_error: BaseException | None = None
+
+    def _assign_cpu_updates(self, host_rate: float, stream_rate: float) -> None:
+        self.cpu_segs, self.stream_segs = {}, {}
+        t_host = t_stream = 0.0
+        for c in sorted(self._all_cpu):
+            n = self._all_cpu[c][5]
+            mode = self._cpu_update_mode
+            use_stream = mode == "stream" or (mode == "split" and t_stream + n / stream_rate < t_host + n / host_rate)
+            if use_stream:
+                self.stream_segs[c] = self._all_cpu[c]
+                t_stream += n / stream_rate
+            else:
+                self.cpu_segs[c] = self._all_cpu[c]
+                t_host += n / host_rate
         self.cpu_ready: dict[int, threading.Event] = {c: threading.Event() for c in self.cpu_segs}
         for ev in self.cpu_ready.values():
             ev.set()
-        self._cpu_thread: threading.Thread | None = None
-        self._cpu_error: BaseException | None = None
+        self._init_stream_update(self._stream_tile)
+
+    def attach_fetcher(self, fetcher: "ChunkFetcher") -> None:
+        """Pair with the fetcher whose releases feed this optimizer (and whose
+        gathers wait on its updates). At world 1 with a schedule that never
+        evicts (`fetcher.stable_blocks`: each chunk keeps one rCache block,
+        gathered into it every step), a streamed CPU-home chunk keeps its
+        gradient and its parameters in that block: its release skips the D2H of
+        the gradient, the streamed K4 reads the gradient from the block and
+        writes the new bf16 parameters over it (as the GPU-home update does in
+        the chunk itself), only p32/m/v cross PCIe (12 B each way per element
+        instead of 14), and the next gather of the chunk copies nothing. The
+        host memory traffic of such an element drops from 32 to 24 B per step
+        — host DRAM is the offload path's bound — so the split
+        between host threads and the streamed update is re-planned with that
+        rate. The chunk's host parameter copy (h_p16) is then not kept current;
+        `host_params_current()` writes it back on demand."""
+        fetcher.optimizer = self
+        m = self.mgr
+        if not (m.fused_w1 and fetcher.stable_blocks and self._all_cpu and self._cpu_update_mode != "host"):
+            return
+        if os.environ.get("ELX_RESIDENT_STREAM", "1") == "0":  # A/B switch: the round-trip form
+            return
+        host_rate, stream_rate = self._rates
+        self._assign_cpu_updates(host_rate, stream_rate * 14.0 / 12.0)
+        self.resident = {c: m.blocks[fetcher.block_for[c]] for c in self.stream_segs if c in fetcher.block_for}
+
+    def host_params_current(self) -> None:
+        """Copy the parameters of resident streamed chunks from their blocks
+        back to the host copies (h_p16), after the pending updates."""
+        if not self.in_block:
+            return
+        self.synchronize()
+        torch.cuda.synchronize(self.mgr.device)
+        for c in sorted(self.in_block):
+            n = self.stream_segs[c][5]
+            self.stream_segs[c][4][:n].copy_(self.resident[c][:n])
 
     def _init_stream_update(self, tile: int) -> None:
         m = self.mgr
@@ -866,6 +919,16 @@ class HybridAdam:
         self.xfer_stream = torch.cuda.Stream(device=dev)
         self.sc_stream = torch.zeros(4, dtype=torch.float64, device=dev)  # K4 reads [0..2] only
 
+    def _resident_table(self, s: int, cnt: int, c: int, a: int) -> kernels.AdamTable:
+        """K4 over slot s's p32/m/v with the gradient read from (and the bf16
+        parameters written over) elements [a, a+cnt) of chunk c's block."""
+        key = ("res", s, cnt, c, a)
+        if key not in self._slot_tables:
+            sl, blk = self._slots[s], self.resident[c][a:a + cnt]
+            self._slot_tables[key] = kernels.AdamTable(
+                [(sl["p32"][:cnt], sl["m"][:cnt], sl["v"][:cnt], blk, blk, cnt)], self.mgr.device)
+        return self._slot_tables[key]
+
     def _slot_table(self, s: int, cnt: int) -> kernels.AdamTable:
         key = (s, cnt)
         if key not in self._slot_tables:
@@ -885,6 +948,7 @@ class HybridAdam:
         k = 0
         for c in sorted(self.stream_segs):
             p32, mm, vv, g, p16, n = self.stream_segs[c]
+            blk = self.resident.get(c)
             for a in range(0, n, self._tile):
                 cnt = min(self._tile, n - a)
                 s = k % 2
@@ -892,16 +956,19 @@ class HybridAdam:
                 with torch.cuda.stream(h2d):
                     if sl["free"] is not None:
                         h2d.wait_event(sl["free"])
-                    for src, dst in ((p32, sl["p32"]), (mm, sl["m"]), (vv, sl["v"]), (g, sl["g"])):
+                    moves = ((p32, sl["p32"]), (mm, sl["m"]), (vv, sl["v"])) + (((g, sl["g"]),) if blk is None else ())
+                    for src, dst in moves:
                         kernels.copy_h2d(dst, src[a:a + cnt], stream=h2d)
                     loaded = torch.cuda.Event()
                     loaded.record(h2d)
                 with torch.cuda.stream(xfer):
                     xfer.wait_event(loaded)
-                    kernels.adam(self._slot_table(s, cnt), self.hp, 0 if tabs is not None else self._kstep,
+                    tab = self._slot_table(s, cnt) if blk is None else self._resident_table(s, cnt, c, a)
+                    kernels.adam(tab, self.hp, 0 if tabs is not None else self._kstep,
                                  self.sc_stream, m.dtype, stream=xfer, grad_scale=self.grad_scale,
                                  bias_tables=tabs)
-                    for src, dst in ((sl["p32"], p32), (sl["m"], mm), (sl["v"], vv), (sl["p16"], p16)):
+                    backs = ((sl["p32"], p32), (sl["m"], mm), (sl["v"], vv)) + (((sl["p16"], p16),) if blk is None else ())
+                    for src, dst in backs:
                         kernels.copy_d2h(dst[a:a + cnt], src, cnt * src.element_size(), stream=xfer)
                     free = torch.cuda.Event()
                     free.record(xfer)
@@ -910,6 +977,8 @@ class HybridAdam:
             ev = torch.cuda.Event()
             ev.record(xfer)
             self.xfer_done[c] = ev
+            if blk is not None:
+                self.in_block.add(c)   # the next gather finds the new parameters in the block
         self.stream_done = torch.cuda.Event()
         self.stream_done.record(xfer)
 
