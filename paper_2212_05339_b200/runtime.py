@@ -210,6 +210,9 @@ class ChunkManager:
             self.step_scalars = kernels.new_step_scalars(dev)
             self.peer_scalars = None
         self._bound: dict[int, torch.Tensor] = {}   # chunk -> storage it is bound to
+        # CPU-home chunks whose rCache block holds their current parameters (the resident streamed update,
+        # HybridAdam.attach_fetcher): their gather copies nothing; cleared whenever the host copies are rewritten
+        self.in_block: set[int] = set()
         self._views: dict[str, torch.Tensor] = {}
 
     def all_reduce_scalars(self) -> None:
@@ -274,6 +277,7 @@ class ChunkManager:
     # ------------------------------------------------------------ init
     def load_params(self, tensors: Mapping[str, torch.Tensor]) -> None:
         """Pack initial parameters into chunks (K1) and seed the fp32 masters."""
+        self.in_block.clear()
         dev = self.device
         tmp16 = torch.empty(self.P, dtype=self.dtype, device=dev)
         tmp32 = torch.empty(self.P, dtype=torch.float32, device=dev)
@@ -544,7 +548,7 @@ class ChunkFetcher:
                 off = mgr.row[c] * mgr.S * es
                 kernels.fetch(block, [p + off for p in mgr.peer_p16], mgr.S, stream=comm,
                               engine=getattr(mgr.transport, "fetch_engine", "sm"), rank=mgr.rank)
-            elif cpu and opt is not None and c in opt.in_block:
+            elif cpu and c in mgr.in_block:
                 pass  # the streamed update wrote this chunk's parameters into its block (attach_fetcher)
             elif cpu:
                 if self.time_release:
@@ -820,9 +824,8 @@ class HybridAdam:
         self._rates = update_rates or DEFAULT_UPDATE_RATES
         self._stream_tile = stream_tile
         # streamed chunks whose gradient and parameters stay in their rCache block between steps
-        # (attach_fetcher): chunk -> block tensor; in_block: the block holds the chunk's current parameters
+        # (attach_fetcher): chunk -> block tensor (mgr.in_block: the block holds the current parameters)
         self.resident: dict[int, torch.Tensor] = {}
-        self.in_block: set[int] = set()
         self._assign_cpu_updates(self._rates[0], self._rates[1])
         self.stream = torch.cuda.Stream(device=m.device) if overlap else None
         pin = torch.cuda.is_available()
@@ -892,11 +895,11 @@ class HybridAdam:
     def host_params_current(self) -> None:
         """Copy the parameters of resident streamed chunks from their blocks
         back to the host copies (h_p16), after the pending updates."""
-        if not self.in_block:
+        if not self.mgr.in_block:
             return
         self.synchronize()
         torch.cuda.synchronize(self.mgr.device)
-        for c in sorted(self.in_block):
+        for c in sorted(self.mgr.in_block):
             n = self.stream_segs[c][5]
             self.stream_segs[c][4][:n].copy_(self.resident[c][:n])
 
@@ -978,7 +981,7 @@ class HybridAdam:
             ev.record(xfer)
             self.xfer_done[c] = ev
             if blk is not None:
-                self.in_block.add(c)   # the next gather finds the new parameters in the block
+                self.mgr.in_block.add(c)   # the next gather finds the new parameters in the block
         self.stream_done = torch.cuda.Event()
         self.stream_done.record(xfer)
 
@@ -1064,6 +1067,7 @@ class HybridAdam:
             for pid, sp in m.shared.items():
                 getattr(sp, k).copy_(state["shared"][pid][k])
         steps = int(state["step"])
+        m.in_block.clear()  # the host copies are rebuilt below: the next gathers read them
         self._host_steps = self._cpu_steps = steps
         self._issued = 0
         self._step0 = steps

@@ -238,7 +238,7 @@ def test_gpt2_small_trainer_step_checked_by_oracle_parity(cuda, graph):
 
 
 @pytest.mark.parametrize("cpu_update", ["host", "stream", "split"])
-@pytest.mark.parametrize("plan_name", ["offload-half", "offload-all", "all-gpu-min"])
+@pytest.mark.parametrize("plan_name", ["offload-half", "offload-all", "all-gpu-min", "offload-resident"])
 def test_offloaded_trainer_step_checked_by_oracle_parity(cuda, plan_name, cpu_update):
     """The bench's `parity` check on plans with CPU-home chunks (configs[2]/[3]'s
     regime) and evictions: the CPU-home chunks' gradients are captured from

@@ -43,6 +43,8 @@ def _plans(cfg):
         ("all-gpu-min", Plan(C, ws, {c: "gpu" for c in range(n)})),
         ("offload-half", Plan(C, ws + 1, {c: ("cpu" if c % 2 else "gpu") for c in range(n)})),
         ("offload-all", Plan(C, ws, {c: "cpu" for c in range(n)})),
+        # every chunk keeps a block (no eviction), half CPU-home: the resident streamed update
+        ("offload-resident", Plan(C, n, {c: ("cpu" if c % 2 else "gpu") for c in range(n)})),
     ]
 
 
@@ -78,7 +80,7 @@ def test_counters_equal_simulate(cuda, plan_name):
 
 
 @pytest.mark.parametrize("overlap", [True, False])
-@pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min", "offload-half", "offload-all"])
+@pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min", "offload-half", "offload-all", "offload-resident"])
 def test_step_parity_bit_exact(cuda, plan_name, overlap):
     plan = dict(_plans(CFG))[plan_name]
     init = gpt2.init_params(CFG, cuda, seed=5)
@@ -152,12 +154,15 @@ def test_checkpoint_round_trip(cuda):
         assert np.array_equal(ma[k], mb[k]), k
 
 
+@pytest.mark.parametrize("plan_name", ["offload-all", "offload-resident"])
 @pytest.mark.parametrize("cpu_update", ["host", "stream", "split"])
-def test_offloaded_update_modes_bit_exact(cuda, cpu_update):
+def test_offloaded_update_modes_bit_exact(cuda, cpu_update, plan_name):
     """CPU-home chunks updated on host threads, by the GPU-streamed update
     (H2D -> K4 -> D2H in double-buffered tiles), or split between them: all
-    bit-exact against the oracle; also across an fp16 overflow skip."""
-    plan = dict(_plans(CFG))["offload-all"]
+    bit-exact against the oracle; also across an fp16 overflow skip. On the
+    never-evicting plan the streamed chunks are resident (gradient and
+    parameters kept in their block between steps)."""
+    plan = dict(_plans(CFG))[plan_name]
     init = gpt2.init_params(CFG, cuda, seed=12)
     model = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()},
                        cpu_update=cpu_update, **HP)
@@ -168,6 +173,7 @@ def test_offloaded_update_modes_bit_exact(cuda, cpu_update):
         assert opt.stream_segs and not opt.cpu_segs
     else:
         assert opt.cpu_segs and opt.stream_segs
+    assert bool(opt.resident) == (plan_name == "offload-resident" and cpu_update != "host")
     opt._init_stream_update(1000) if opt.stream_segs else None  # tiny tiles: several per chunk, both slots
     ref = ReferenceStep(model, init, HP)
     for s in range(3):
@@ -178,6 +184,33 @@ def test_offloaded_update_modes_bit_exact(cuda, cpu_update):
         got = _masters(model)
         for pid, want in ref.master.items():
             assert np.array_equal(got[pid], want), (s, pid)
+
+
+def test_resident_checkpoint_reload_into_trained_model(cuda):
+    """A resident streamed chunk's current parameters live in its block; a checkpoint loaded into a model that
+    has trained since must not be shadowed by them: the reloaded model continues exactly like a fresh one."""
+    plan = dict(_plans(CFG))["offload-resident"]
+    init = gpt2.init_params(CFG, cuda, seed=8)
+    a = ElixirGPT2(CFG, plan, device=cuda, init={k: v.clone() for k, v in init.items()}, cpu_update="stream", **HP)
+    assert a.optimizer.resident
+    tok, tgt = _batch(CFG, cuda, 4)
+    a.train_step(tok, tgt)
+    st = a.optimizer.state_dict()
+    a.train_step(tok, tgt)
+    a.train_step(tok, tgt)
+    assert a.manager.in_block
+    a.optimizer.load_state_dict(st)
+    b = ElixirGPT2(CFG, plan, device=cuda, init=gpt2.init_params(CFG, cuda, seed=99), cpu_update="stream", **HP)
+    b.optimizer.load_state_dict(st)
+    assert a.train_step(tok, tgt).item() == b.train_step(tok, tgt).item()
+    ma, mb = _masters(a), _masters(b)
+    for k in ma:
+        assert np.array_equal(ma[k], mb[k]), k
+    # the host copies written back on demand equal the parameters in the blocks
+    a.optimizer.host_params_current()
+    for c, blk in a.optimizer.resident.items():
+        n = a.optimizer.stream_segs[c][5]
+        assert torch.equal(a.optimizer.stream_segs[c][4][:n], blk[:n].cpu())
 
 
 @pytest.mark.parametrize("plan_name", ["all-gpu-max", "all-gpu-min"])
