@@ -888,8 +888,12 @@ class HybridAdam:
             return
         if os.environ.get("ELX_RESIDENT_STREAM", "1") == "0":  # A/B switch: the round-trip form
             return
+        # planning rate of the resident streamed worker: 12 instead of 14 B each way per element, times 0.8 —
+        # calibrated on the box (4B offload: 4 streamed chunks 14.5-14.6 samples/s vs 5 at 13.3-13.8; 10B: equal
+        # at 0.8 and 1.0; 1.3/1.6 worse on both — profiles/r02aj_split_scale.txt); ELX_STREAM_RATE_SCALE overrides
         host_rate, stream_rate = self._rates
-        self._assign_cpu_updates(host_rate, stream_rate * 14.0 / 12.0)
+        scale = float(os.environ.get("ELX_STREAM_RATE_SCALE", "0.8"))
+        self._assign_cpu_updates(host_rate, stream_rate * 14.0 / 12.0 * scale)
         self.resident = {c: m.blocks[fetcher.block_for[c]] for c in self.stream_segs if c in fetcher.block_for}
 
     def host_params_current(self) -> None:
