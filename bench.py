@@ -645,6 +645,70 @@ def run_ours(args):
 
 # ---------------------------------------------------------------- kernel sweep
 
+def _sweep_parity(mb, w, S, shards, block, dev, hp):
+    """--sweep-check: the sweep's kernels at this chunk size against the C
+    oracle (the checker, after the timed launches): K2's gathered bytes; K3's
+    rank-ordered fp32 reduction (N > 1) and its sum of squares in the launch's
+    fixed order; K4 over one rank's shard from fresh state."""
+    import ctypes
+
+    import numpy as np
+
+    from oracle import arith, parity
+    from paper_2212_05339_b200 import kernels
+
+    lib = parity._lib()
+    lib.oracle_release_bf16.restype = ctypes.c_double
+    lib.oracle_release_bf16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_float, ctypes.c_void_p, ctypes.c_int]
+    lib.oracle_release_norm_ordered.restype = ctypes.c_double
+    lib.oracle_release_norm_ordered.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int]
+    threads = len(os.sched_getaffinity(0))
+    hp = dict(hp, max_norm=1.0)   # with clipping: K4 reads the sum of squares K3 left in the step scalars
+    t0 = time.perf_counter()
+    hs = [t.view(torch.int16).cpu().numpy().view(np.uint16) for t in shards]
+    kernels.fetch(block, [t.data_ptr() for t in shards], S)
+    torch.cuda.synchronize(dev)
+    k2 = bool(np.array_equal(block.view(torch.int16).cpu().numpy().view(np.uint16), np.concatenate(hs)))
+    # K3: release into a fresh fp32 shard and fresh step scalars, scale 1/8
+    g32 = torch.empty(S, device=dev)
+    sc = kernels.new_step_scalars(dev)
+    kernels.release(g32, [t.data_ptr() for t in shards], S, torch.bfloat16, 0.125, sc)
+    torch.cuda.synchronize(dev)
+    want = np.empty(S, np.float32)
+    bad = ctypes.c_int(0)
+    ptrs = (ctypes.c_void_p * w)(*[h.ctypes.data for h in hs])
+    lib.oracle_release_bf16(want.ctypes.data, ptrs, w, S, ctypes.c_float(0.125), ctypes.byref(bad), threads)
+    k3_g = bool(np.array_equal(g32.cpu().numpy().view(np.uint32), want.view(np.uint32)))
+    ctas, tv = kernels.release_geometry([S], w)
+    gp = (ctypes.c_void_p * 1)(want.ctypes.data)
+    nn = (ctypes.c_int64 * 1)(S)
+    sq = lib.oracle_release_norm_ordered(gp, nn, 1, ctas, tv, threads)
+    k3_sq = float(sc[0].item()) == sq
+    # K4 from fresh state on the released gradient
+    gen = torch.Generator(device=dev).manual_seed(mb * 10 + w)
+    p32 = torch.randn(S, device=dev, generator=gen) * 0.02
+    m = torch.randn(S, device=dev, generator=gen) * 1e-3
+    v = torch.rand(S, device=dev, generator=gen) * 1e-6
+    P, M, V = (t.cpu().numpy() for t in (p32, m, v))
+    p16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
+    tab = kernels.AdamTable([(p32, m, v, g32, p16, S)], dev)
+    kernels.adam(tab, hp, 1, sc, torch.bfloat16)
+    torch.cuda.synchronize(dev)
+    coef = arith.clip_coef(sq, hp["max_norm"])
+    k = arith.adam_consts(1, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"], hp["weight_decay"])
+    kv = np.array([k["decay"], k["omb1"], k["b2"], k["omb2"], k["bc2_sqrt"], k["neg_step"], k["eps"]], np.float32)
+    out16 = np.empty(S, np.uint16)
+    lib.oracle_adamw_bf16(P.ctypes.data, M.ctypes.data, V.ctypes.data, want.ctypes.data, out16.ctypes.data, S,
+                          kv.ctypes.data, ctypes.c_float(coef), 0, threads)
+    k4 = all(np.array_equal(a.cpu().numpy().view(np.uint32), b.view(np.uint32)) for a, b in ((p32, P), (m, M), (v, V)))
+    k4 = k4 and bool(np.array_equal(p16.view(torch.int16).cpu().numpy().view(np.uint16), out16))
+    return {"chunk_mb": mb, "emulated_world": w, "engine": "parity", "shard_elems": S,
+            "k2_bytes_identical": k2, "k3_grad_bit_identical": k3_g, "k3_sumsq_bit_identical": k3_sq,
+            "k4_bit_identical": bool(k4), "oracle": "oracle/c/elx_oracle.c", "seconds": round(time.perf_counter() - t0, 1)}
+
+
 def _sweep_graph_stream(mb, w, S, dev, reps, flush, flush_sink, hp, peak, emit):
     """The sweep's kernels as the step issues them: R back-to-back launches,
     each on its OWN buffers (R x the per-launch bytes >= 512 MB, four times
@@ -870,6 +934,8 @@ def run_sweep(args):
                                        ("k4_adam", t_a, 30 * S)):
                 emit({"chunk_mb": mb, "emulated_world": w, "engine": engine, "shard_elems": S, "ms": ms,
                       "hbm_gbs": nbytes / (ms * 1e-3) / 1e9, "frac": nbytes / (ms * 1e-3) / 1e9 / peak})
+            if args.sweep_check:
+                emit(_sweep_parity(mb, w, S, shards, block, dev, hp))
             del shards, block, g32, p32, m, v, p16, tab
     if world > 1:
         torch.cuda.synchronize()
@@ -887,6 +953,8 @@ def main():
     ap.add_argument("--model", default="gpt2-1.3b")
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--sweep-sizes", default="4,8,16,32,64,128,256", help="chunk sizes in MB for --sweep")
+    ap.add_argument("--sweep-check", action="store_true",
+                    help="--sweep at N=1: also check each size's K2/K3/K4 outputs against the C oracle")
     ap.add_argument("--sweep-graph", action="store_true",
                     help="--sweep at N=1: time each kernel as R back-to-back launches on distinct buffers in one "
                          "CUDA graph (the step's issue pattern) instead of single cold launches")
