@@ -258,3 +258,23 @@ def test_offloaded_trainer_step_checked_by_oracle_parity(cuda, plan_name, cpu_up
     assert rep["cpu_home_chunks_checked"] == rep["cpu_home_chunks"] == len(model.manager.cpu_ids)
     assert rep["sumsq_bit_identical"], rep
     assert all(f == 1.0 for f in rep["bit_identical_frac"].values()), rep
+
+
+def test_sweep_parity_check(cuda):
+    """bench.py --sweep --sweep-check (configs[4]): every emulated world's K2/K3/K4 outputs equal the C oracle
+    (the same checker that produced profiles/r02am_sweep_parity.jsonl at 4-256 MB), here at 8 and 32 MB."""
+    import json
+    import subprocess
+    import sys
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    out = subprocess.run([sys.executable, "bench.py", "--sweep", "--sweep-check", "--sweep-sizes", "8,32",
+                          "--steps", "2"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-3000:]
+    recs = [json.loads(ln) for ln in out.stdout.splitlines() if ln.startswith("{")]
+    par = [r for r in recs if r.get("engine") == "parity"]
+    assert len(par) == 8, par
+    for r in par:
+        assert r["k2_bytes_identical"] and r["k3_grad_bit_identical"] and r["k3_sumsq_bit_identical"], r
+        assert r["k4_bit_identical"], r
