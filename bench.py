@@ -377,6 +377,7 @@ def run_ours(args):
             model.fetcher.fetch_events.clear()
             model.fetcher.copy_events.clear()
             opt.cpu_wait_s = opt.cpu_update_s = 0.0
+            opt.stream_events.clear()
 
     # CUDA graph: the whole step as one graph launch (every chunk GPU-home; world 1, or N ranks on the
     # IPC P2P transport, whose exchanges are our kernels between device-numbered barriers). The per-kernel
@@ -438,6 +439,8 @@ def run_ours(args):
         copies[kind] = (ms_ + a.elapsed_time(b), nb0 + nb)
     cpu_wait_ms = opt.cpu_wait_s * 1e3 / probe_steps
     cpu_update_ms = opt.cpu_update_s * 1e3 / probe_steps
+    stream_update_ms = (statistics.mean(a.elapsed_time(b) for a, b in opt.stream_events)
+                        if opt.stream_events else 0.0)
     timing(False)
     loss = float(model.last_loss)
 
@@ -559,6 +562,7 @@ def run_ours(args):
                                                "gbs": v[1] / (v[0] * 1e-3) / 1e9 if v[0] else None}
                                            for k, v in copies.items()},
                "cpu_update_ms_per_step": cpu_update_ms, "host_wait_on_cpu_update_ms_per_step": cpu_wait_ms,
+               "stream_update_ms_per_step": stream_update_ms,
                "cpu_update_mode": args.cpu_update,
                "host_updated_chunks": sorted(opt.cpu_segs), "stream_updated_chunks": sorted(opt.stream_segs)}
     flops = model.flops_per_step()

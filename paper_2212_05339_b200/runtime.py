@@ -841,6 +841,7 @@ class HybridAdam:
         self.cpu_wait_s = 0.0      # host time the runtime blocked on CPU-home updates
         self.cpu_update_s = 0.0    # host time spent in CPU-home updates (on their thread)
         self.adam_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []
+        self.stream_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] = []  # streamed update spans
         self.time_adam = False
         self._cap_events: tuple[torch.cuda.Event, torch.cuda.Event] | None = None
         self.done_event: torch.cuda.Event | None = None
@@ -952,6 +953,9 @@ class HybridAdam:
         h2d, xfer = self.h2d_stream, self.xfer_stream
         h2d.wait_stream(cur)
         xfer.wait_stream(cur)
+        if self.time_adam:  # the streamed worker's span: its first H2D can start here
+            t0 = torch.cuda.Event(enable_timing=True)
+            t0.record(h2d)
         k = 0
         for c in sorted(self.stream_segs):
             p32, mm, vv, g, p16, n = self.stream_segs[c]
@@ -986,8 +990,10 @@ class HybridAdam:
             self.xfer_done[c] = ev
             if blk is not None:
                 self.mgr.in_block.add(c)   # the next gather finds the new parameters in the block
-        self.stream_done = torch.cuda.Event()
+        self.stream_done = torch.cuda.Event(enable_timing=self.time_adam)
         self.stream_done.record(xfer)
+        if self.time_adam:
+            self.stream_events.append((t0, self.stream_done))
 
     def wait_offloaded(self, c: int, stream: torch.cuda.Stream) -> None:
         """Before touching chunk c's host shards: its previous update must be done
