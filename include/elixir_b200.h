@@ -173,7 +173,8 @@ int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int3
  * read peer rank+1, rank+2, ... in turn and the kernel's tiles interleave the
  * ranks from rank+1, so the N ranks of one all-gather never all pull from the
  * same peer's NVLink egress at once. elx_fetch / elx_fetch_ce are this with
- * rank 0. */
+ * rank 0. Replaces the gather of PAPER.md:176-181 ("gather them into rCache
+ * before compute operators"), volume gather_bytes (rcache_sim.py:189). */
 #define ELX_FETCH_SM 0
 #define ELX_FETCH_CE 1
 int elx_fetch_ranked(void* block, const void* const* shards, int64_t shard_len, int32_t rank,
