@@ -1788,6 +1788,32 @@ __global__ void __launch_bounds__(32, 1) fetch_tma_kernel(char* __restrict__ blo
   tma_store_wait_all();
 }
 
+// Copy-engine lanes of elx_fetch_ce: side streams (one set per device, created on first use) and the
+// events that fork them from the caller's stream and join them back.
+constexpr int kCeLanes = 4;
+struct CeLanes {
+  cudaStream_t s[kCeLanes];
+  cudaEvent_t fork;
+  cudaEvent_t join[kCeLanes];
+};
+CeLanes* ce_lanes() {
+  static CeLanes* per_dev[64] = {nullptr};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return nullptr;
+  if (!per_dev[dev]) {
+    CeLanes* L = new CeLanes{};
+    bool ok = cudaEventCreateWithFlags(&L->fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int j = 0; j < kCeLanes && ok; ++j) {
+      ok = cudaStreamCreateWithFlags(&L->s[j], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&L->join[j], cudaEventDisableTiming) == cudaSuccess;
+    }
+    if (!ok) return nullptr;
+    per_dev[dev] = L;
+  }
+  return per_dev[dev];
+}
+
 struct FetchTma {
   const void* kern;
   int tile;
@@ -1857,13 +1883,25 @@ int elx_fetch_ranked(void* block, const void* const* shards, int64_t shard_len, 
   if (shard_len == 0) return ELX_OK;
   const int rot = (rank + 1) % world;  // start on the next rank's shard, own shard last
   if (engine == ELX_FETCH_CE) {
+    // The N copies go to up to kCeLanes streams forked from `stream` and joined back (event fork/join, also
+    // inside a CUDA graph capture), so several copy engines move shards at once instead of one after another.
     const size_t bytes = (size_t)shard_len * 2;
-    for (int i = 0; i < world; ++i) {
+    CeLanes* L = ce_lanes();
+    if (!L) return elx::fail(ELX_ERR_CUDA, "elx_fetch_ce: cannot create copy lanes");
+    const int lanes = std::min(world, env_int("ELX_CE_LANES", kCeLanes));
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = lanes > 1 ? cudaEventRecord(L->fork, st) : cudaSuccess;
+    for (int j = 1; j < lanes && e == cudaSuccess; ++j) e = cudaStreamWaitEvent(L->s[j], L->fork, 0);
+    for (int i = 0; i < world && e == cudaSuccess; ++i) {
       const int r = (rot + i) % world;
-      cudaError_t e = cudaMemcpyAsync(static_cast<char*>(block) + r * bytes, shards[r], bytes, cudaMemcpyDefault,
-                                      (cudaStream_t)stream);
-      if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_fetch_ce rank %d: %s", r, cudaGetErrorString(e));
+      const cudaStream_t lane = (i % lanes) == 0 ? st : L->s[i % lanes];
+      e = cudaMemcpyAsync(static_cast<char*>(block) + r * bytes, shards[r], bytes, cudaMemcpyDefault, lane);
     }
+    for (int j = 1; j < lanes && e == cudaSuccess; ++j) {
+      e = cudaEventRecord(L->join[j], L->s[j]);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(st, L->join[j], 0);
+    }
+    if (e != cudaSuccess) return elx::fail(ELX_ERR_CUDA, "elx_fetch_ce: %s", cudaGetErrorString(e));
     return ELX_OK;
   }
   if (const FetchTma* F = fetch_tma()) {
