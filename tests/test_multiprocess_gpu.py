@@ -145,7 +145,8 @@ def test_multiprocess_gloo_equals_loopback(cuda, tmp_path, world, kind, path):
 
 
 @pytest.mark.parametrize("plan,transport", [("gpt2-small_n2.json", "nccl"), ("gpt2-small_rcache_n2.json", "nccl"),
-                                            ("gpt2-small_rcache_n2.json", "ipc"), ("gpt2-small_n2.json", "ipc")])
+                                            ("gpt2-small_rcache_n2.json", "ipc"), ("gpt2-small_n2.json", "ipc"),
+                                            ("gpt2-small_n2.json", "ipc-ce")])
 def test_bench_two_ranks_one_gpu(cuda, plan, transport):
     """transport "nccl" falls back to gloo on a shared GPU (same TorchDistTransport code)."""
     p = _torchrun(2, ["bench.py", "--gpus", "2", "--model", "gpt2-small", "--plan", plan, "--steps", "2",
@@ -169,7 +170,7 @@ def test_bench_two_ranks_one_gpu(cuda, plan, transport):
     if plan == "gpt2-small_rcache_n2.json":
         assert sim["replaced_ops"] > 0 and sim["c2g_units"] > 0
     # the IPC transport with every chunk GPU-home runs the step as CUDA graphs on both ranks
-    assert line["config"]["cuda_graph"] == (transport == "ipc" and plan == "gpt2-small_n2.json")
+    assert line["config"]["cuda_graph"] == (transport in ("ipc", "ipc-ce") and plan == "gpt2-small_n2.json")
     # whole-step parity at N = 2 (oracle/parity.check_step_multirank): the reduced fp32 gradients, the sums
     # of squares and AdamW over both ranks' shards against the C oracle
     # (the rcache plan: evictions, re-gathers and 5 CPU-home chunks, their K3 into the fp32 staging shard and
