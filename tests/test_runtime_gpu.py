@@ -98,8 +98,9 @@ def test_step_parity_bit_exact(cuda, plan_name, overlap):
             assert np.array_equal(got[pid], want), (s, pid, np.abs(got[pid] - want).max())
 
 
-def test_fp16_loss_scale_and_overflow_skip(cuda):
-    plan = dict(_plans(CFG))["offload-half"]
+@pytest.mark.parametrize("plan_name", ["offload-half", "offload-resident"])
+def test_fp16_loss_scale_and_overflow_skip(cuda, plan_name):
+    plan = dict(_plans(CFG))[plan_name]
     init = gpt2.init_params(CFG, cuda, seed=6, dtype=torch.float16)
     model = ElixirGPT2(CFG, plan, device=cuda, dtype=torch.float16, loss_scale=1024.0,
                        init={k: v.clone() for k, v in init.items()}, **HP)
