@@ -434,9 +434,9 @@ def run_ours(args):
     rel = [(a.elapsed_time(b), n) for a, b, n in model.fetcher.release_events]
     fet = [(a.elapsed_time(b), n) for a, b, n in model.fetcher.fetch_events]
     copies = {}
-    for kind, a, b, nb in model.fetcher.copy_events:
-        ms_, nb0 = copies.get(kind, (0.0, 0))
-        copies[kind] = (ms_ + a.elapsed_time(b), nb0 + nb)
+    for ckind, a, b, nb in model.fetcher.copy_events:
+        ms_, nb0 = copies.get(ckind, (0.0, 0))
+        copies[ckind] = (ms_ + a.elapsed_time(b), nb0 + nb)
     cpu_wait_ms = opt.cpu_wait_s * 1e3 / probe_steps
     cpu_update_ms = opt.cpu_update_s * 1e3 / probe_steps
     stream_update_ms = (statistics.mean(a.elapsed_time(b) for a, b in opt.stream_events)
