@@ -297,7 +297,7 @@ __device__ __forceinline__ int32_t ld_acquire_sys(const int32_t* p) {
 // stores; the acquire loads order the peers' writes before everything this
 // stream runs next. Bounded: ~20 s of polling, then trap (a loud error, never
 // a silent hang).
-__global__ void device_barrier_kernel(const PadBatch pads, int world, int rank, int32_t epoch) {
+__global__ void device_barrier_kernel(const __grid_constant__ PadBatch pads, int world, int rank, int32_t epoch) {
   if (epoch <= 0) {  // device-numbered barrier: the count lives in our own pad (graph-replayable)
     int32_t* counter = pads.p[rank] + world;
     epoch = *counter + 1;
@@ -319,7 +319,7 @@ __global__ void device_barrier_kernel(const PadBatch pads, int world, int rank, 
 // dst[i] = sum over ranks, in rank order, of peers[r][i] (fp64): the N-scalar
 // all-reduce of the step scalars (sum of squares, overflow flag) over peer
 // memory — deterministic, unlike a ring all-reduce.
-__global__ void peer_sum_f64_kernel(double* dst, const PtrBatch peers, int count, int world) {
+__global__ void peer_sum_f64_kernel(double* dst, const __grid_constant__ PtrBatch peers, int count, int world) {
   for (int i = threadIdx.x; i < count; i += blockDim.x) {
     double a = 0.0;
     for (int r = 0; r < world; ++r) a += static_cast<const volatile double*>(peers.p[r])[i];
@@ -1666,7 +1666,7 @@ struct ColsumBatch {
 
 template <typename T16>
 __global__ void __cluster_dims__(1, kCcCluster, 1) __launch_bounds__(kCcThreads, 1)
-    colsum_cluster_kernel(const ColsumBatch batch, int64_t rows, int64_t cols, int out_dt) {
+    colsum_cluster_kernel(const __grid_constant__ ColsumBatch batch, int64_t rows, int64_t cols, int out_dt) {
   const T16* __restrict__ in = static_cast<const T16*>(batch.in[blockIdx.z]);
   void* out = batch.out[blockIdx.z];
   __shared__ float part[kCcWarps][kCcStrip];
