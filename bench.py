@@ -649,6 +649,60 @@ def run_ours(args):
 
 # ---------------------------------------------------------------- kernel sweep
 
+def _sweep_parity_peers(mb, world, rank, S, block, pb, sc, dev, bar):
+    """--sweep-check at N > 1 (real peer pointers): after the timed launches
+    every rank's block holds the gathered shards (K2 last wrote them). Each
+    rank regenerates every rank's shard from its seed and checks (a) its block's
+    bytes == their concatenation, (b) K3 over segment `rank` of every peer's
+    block — fresh step scalars, scale 1/8 — against the C oracle: the fp32
+    reduction bit for bit and the sum of squares in the launch's order. Merged
+    over ranks (every rank runs it; rank 0 prints)."""
+    import ctypes
+
+    import numpy as np
+    import torch.distributed as dist
+
+    from oracle import parity
+    from paper_2212_05339_b200 import kernels
+
+    lib = parity._lib()
+    lib.oracle_release_bf16.restype = ctypes.c_double
+    lib.oracle_release_bf16.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int64,
+                                        ctypes.c_float, ctypes.c_void_p, ctypes.c_int]
+    lib.oracle_release_norm_ordered.restype = ctypes.c_double
+    lib.oracle_release_norm_ordered.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int,
+                                                ctypes.c_int, ctypes.c_int]
+    threads = max(1, len(os.sched_getaffinity(0)) // world)
+    shards = []
+    for r in range(world):  # the shards exactly as run_sweep made them (seed 77 + r, first draw)
+        g = torch.Generator(device=dev).manual_seed(77 + r)
+        shards.append(torch.randn(S, generator=g, device=dev).to(torch.bfloat16).view(torch.int16).cpu()
+                      .numpy().view(np.uint16))
+    torch.cuda.synchronize(dev)
+    k2 = bool(np.array_equal(block.view(torch.int16).cpu().numpy().view(np.uint16), np.concatenate(shards)))
+    bar()
+    g32 = torch.empty(S, device=dev)
+    sc.zero_()
+    kernels.release(g32, [p + rank * S * 2 for p in pb], S, torch.bfloat16, 0.125, sc)
+    bar()  # peers' blocks are read before anyone moves on
+    torch.cuda.synchronize(dev)
+    mine = shards[rank]   # segment `rank` of every rank's block is this rank's shard
+    ptrs = (ctypes.c_void_p * world)(*([mine.ctypes.data] * world))
+    want = np.empty(S, np.float32)
+    bad = ctypes.c_int(0)
+    lib.oracle_release_bf16(want.ctypes.data, ptrs, world, S, ctypes.c_float(0.125), ctypes.byref(bad), threads)
+    k3_g = bool(np.array_equal(g32.cpu().numpy().view(np.uint32), want.view(np.uint32)))
+    ctas, tv = kernels.release_geometry([S], world)
+    gp = (ctypes.c_void_p * 1)(want.ctypes.data)
+    nn = (ctypes.c_int64 * 1)(S)
+    k3_sq = float(sc[0].item()) == lib.oracle_release_norm_ordered(gp, nn, 1, ctas, tv, threads)
+    allr = [None] * world
+    dist.all_gather_object(allr, (k2, k3_g, k3_sq))
+    return {"chunk_mb": mb, "engine": "parity", "shard_elems": S, "ranks": world,
+            "k2_bytes_identical": all(a for a, _, _ in allr), "k3_grad_bit_identical": all(b for _, b, _ in allr),
+            "k3_sumsq_bit_identical": all(c for _, _, c in allr), "oracle": "oracle/c/elx_oracle.c"}
+
+
 def _sweep_parity(mb, w, S, shards, block, dev, hp):
     """--sweep-check: the sweep's kernels at this chunk size against the C
     oracle (the checker, after the timed launches): K2's gathered bytes; K3's
@@ -865,6 +919,8 @@ def run_sweep(args):
                 ms = timeit(fn, bar)
                 emit({"chunk_mb": mb, "engine": engine, "shard_elems": S, "ms": ms,
                       "bus_gbs": bus / (ms * 1e-3) / 1e9, "frac_of_900": bus / (ms * 1e-3) / 1e9 / 900})
+            if args.sweep_check:
+                emit(_sweep_parity_peers(mb, world, rank, S, block, pb, sc, dev, bar))
             if nccl_ok:
                 out16 = torch.empty(S, dtype=torch.bfloat16, device=dev)
                 blk32 = block.float()
@@ -958,7 +1014,7 @@ def main():
     ap.add_argument("--sweep", action="store_true")
     ap.add_argument("--sweep-sizes", default="4,8,16,32,64,128,256", help="chunk sizes in MB for --sweep")
     ap.add_argument("--sweep-check", action="store_true",
-                    help="--sweep at N=1: also check each size's K2/K3/K4 outputs against the C oracle")
+                    help="--sweep: also check each size's K2/K3 (and at N=1 K4) outputs against the C oracle")
     ap.add_argument("--sweep-graph", action="store_true",
                     help="--sweep at N=1: time each kernel as R back-to-back launches on distinct buffers in one "
                          "CUDA graph (the step's issue pattern) instead of single cold launches")

@@ -222,10 +222,14 @@ def test_sweep_real_peer_pointers_oversubscribed(cuda, world):
     run on the real peer pointers between device barriers; one JSON line per
     (size, N, engine) with busBW; the NCCL bar lines say why they are absent
     when ranks share the GPU; each rank holds a context on its device only."""
-    p = _torchrun(world, ["bench.py", "--sweep", "--gpus", str(world), "--sweep-sizes", "4,32", "--steps", "3"],
-                  timeout=600)
+    p = _torchrun(world, ["bench.py", "--sweep", "--gpus", str(world), "--sweep-sizes", "4,32", "--steps", "3",
+                          "--sweep-check"], timeout=600)
     lines = [json.loads(ln) for ln in p.stdout.splitlines() if ln.startswith("{")]
-    recs = [r for r in lines if r.get("sweep") == "chunk"]
+    # --sweep-check: K2's gathered bytes and K3 over the peers' blocks equal the C oracle on every rank
+    par = [r for r in lines if r.get("engine") == "parity"]
+    assert len(par) == 2 and all(r["k2_bytes_identical"] and r["k3_grad_bit_identical"] and
+                                 r["k3_sumsq_bit_identical"] for r in par), par
+    recs = [r for r in lines if r.get("sweep") == "chunk" and r.get("engine") != "parity"]
     got = {(r["chunk_mb"], r["engine"]) for r in recs}
     for mb in (4, 32):
         for eng in ("k2_fetch_sm", "k2_fetch_ce", "k3_release", "k4_adam", "nccl_all_gather",
