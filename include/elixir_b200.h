@@ -160,9 +160,11 @@ int elx_fetch(void* block, const void* const* shards, int64_t shard_len, int32_t
               int32_t dtype, void* stream);
 
 /* K2 on the copy engines instead of SMs: the same gather (same arguments,
- * same validation, same bytes) as `world` cudaMemcpyAsync calls on `stream`
- * (peer shards over NVLink through the DMA engines), so a fetch overlapped
- * with the compute stream's GEMMs takes no SM time from them. */
+ * same validation, same bytes) as `world` cudaMemcpyAsync calls (peer shards
+ * over NVLink through the DMA engines), spread over up to four streams forked
+ * from `stream` by an event and joined back to it (graph-capturable), so
+ * several copy engines run at once and a fetch overlapped with the compute
+ * stream's GEMMs takes no SM time from them. */
 int elx_fetch_ce(void* block, const void* const* shards, int64_t shard_len, int32_t world,
                  int32_t dtype, void* stream);
 

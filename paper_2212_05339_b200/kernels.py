@@ -101,10 +101,12 @@ def _ptr_array(ptrs: Sequence[int]):
 def fetch(block: torch.Tensor, shard_ptrs: Sequence[int], shard_len: int, stream=None, engine: str = "sm",
           rank: int = 0) -> None:
     """K2: block[r*S:(r+1)*S] <- shard r (device pointers, local or peer-mapped).
-    engine "sm": the fetch kernel; "ce": the copy engines (cudaMemcpyAsync per
-    rank), leaving every SM to the compute stream. `rank` (the caller's) rotates
-    the order of the peer reads to start at rank+1 (elx_fetch_ranked), so the
-    ranks of one all-gather do not all read the same peer at once."""
+    engine "sm": the fetch kernel (TMA bulk copies); "ce": the copy engines
+    (one cudaMemcpyAsync per rank, spread over up to four streams forked from
+    `stream` and joined back), leaving every SM to the compute stream. `rank`
+    (the caller's) rotates the order of the peer reads to start at rank+1
+    (elx_fetch_ranked), so the ranks of one all-gather do not all read the
+    same peer at once."""
     lib = _lib.load()
     _cuda(block, "block")
     if block.numel() < len(shard_ptrs) * shard_len:
